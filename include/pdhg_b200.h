@@ -1,0 +1,158 @@
+/*
+ * pdhg_b200.h -- C ABI of the B200-native PDHG engine (libpdhg_b200.so).
+ *
+ * This is the drop-in boundary for the reference package's hot path,
+ * `hybridlp.pdhg.run_pdhg` (/root/reference/pkg/src/hybridlp/pdhg.py:162-258).
+ * The Python host (paper_2603_03150_b200/engine.py) keeps the reference's
+ * Python signature and control flow and calls down through this ABI for all
+ * arithmetic; a C/C++ caller can drive it the same way.
+ *
+ * Conventions
+ *   - Every function returns 0 on success and a negative code on failure;
+ *     pdhg_last_error() returns a thread-local message.  No C++ exception
+ *     crosses this boundary.
+ *   - The library never allocates device memory.  The caller owns every
+ *     device buffer (the Python host allocates them as torch tensors) and
+ *     passes raw device pointers; sizes come from pdhg_workspace_bytes().
+ *   - All work is enqueued on the cudaStream_t given to pdhg_ctx_create;
+ *     functions that return host scalars synchronise that stream.
+ *   - fp64 values, int32 column indices and row offsets (nnz < 2^31).
+ *   - Results are bitwise reproducible run to run for a fixed layout
+ *     (fixed-order reductions, no floating-point atomics).
+ */
+#ifndef PDHG_B200_H
+#define PDHG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDHG_ABI_VERSION 1
+
+/* Error codes. */
+#define PDHG_OK 0
+#define PDHG_ERR_ARG (-1)
+#define PDHG_ERR_CUDA (-2)
+#define PDHG_ERR_STATE (-3)
+
+/* Which iterate a call refers to. */
+#define PDHG_PT_CUR 0  /* (x, y)            -- state.x / state.y      pdhg.py:55-56 */
+#define PDHG_PT_AVG 1  /* (avg_x, avg_y)    -- state.avg_x / avg_y    pdhg.py:57-58 */
+#define PDHG_PT_BEST 2 /* best point so far -- best_pt               pdhg.py:180,231-232 */
+
+/* Number of doubles pdhg_check writes per scored point (see PDHG_Q_*). */
+#define PDHG_NQ 8
+#define PDHG_Q_RP2 0   /* sum r_p^2        -> ||r_p||_2^2   lp_core.py:436,458 */
+#define PDHG_Q_RPMAX 1 /* max |r_p|        -> primal_inf    lp_core.py:476 */
+#define PDHG_Q_BY 2    /* b'y              -> dual_obj      lp_core.py:442 */
+#define PDHG_Q_RD2 3   /* sum r_d^2        -> ||r_d||_2^2   lp_core.py:437,459 */
+#define PDHG_Q_RDMAX 4 /* max |r_d|        -> dual_inf      lp_core.py:477 */
+#define PDHG_Q_CX 5    /* c'x              -> primal_obj    lp_core.py:441 */
+#define PDHG_Q_XZ 6    /* x'z              -> comp          lp_core.py:443 */
+#define PDHG_Q_RSV 7   /* reserved (0) */
+
+/*
+ * Problem on the device: the standard-form LP min c'x, Ax=b, x>=0 of
+ * StandardLp (lp_core.py:106-142) in a dual layout -- A as CSR (rows i,
+ * drives A@x) and A' as CSR (= CSC of A, drives A'y = StandardLp.at_y,
+ * lp_core.py:140-142).  Rows longer than `heavy_threshold` are listed in
+ * the heavy-row arrays and get a whole thread block each.
+ */
+typedef struct pdhg_problem {
+  int32_t m, n;
+  int64_t nnz;
+  const int32_t* a_ptr;   /* m+1 */
+  const int32_t* a_col;   /* nnz */
+  const double* a_val;    /* nnz */
+  const int32_t* at_ptr;  /* n+1 */
+  const int32_t* at_col;  /* nnz */
+  const double* at_val;   /* nnz */
+  const double* b;        /* m */
+  const double* c;        /* n */
+  int32_t a_lanes;        /* lanes per row for A rows: 1,2,4,8,16,32 (0 = auto from mean row length) */
+  int32_t at_lanes;       /* same for A' rows */
+  int32_t heavy_threshold;/* rows with more entries are processed block-per-row */
+  int32_t a_n_heavy, at_n_heavy;
+  const int32_t* a_heavy;  /* device list of heavy rows of A */
+  const int32_t* at_heavy; /* device list of heavy rows of A' */
+} pdhg_problem;
+
+typedef struct pdhg_ctx pdhg_ctx;
+
+int pdhg_abi_version(void);
+const char* pdhg_last_error(void);
+
+/* Device workspace the caller must provide for a problem of size m x n. */
+size_t pdhg_workspace_bytes(int32_t m, int32_t n);
+
+/* Create / destroy an engine context bound to `stream` (a cudaStream_t). */
+int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_bytes,
+                    void* stream, pdhg_ctx** out);
+int pdhg_ctx_destroy(pdhg_ctx* ctx);
+
+/* out = A @ in (transpose=0) or A' @ in (transpose=1); device pointers.
+ * Replaces scipy csr_matvec behind `p.A @ x` and `p.at_y(y)` (lp_core.py:140-142). */
+int pdhg_spmv(pdhg_ctx* ctx, int transpose, const double* in, double* out);
+
+/* Power iteration on A'A (estimate_opnorm, pdhg.py:80-109).  v0 (host, n)
+ * is the caller's normalised start vector (numpy default_rng(seed), pdhg.py:89-91). */
+int pdhg_opnorm(pdhg_ctx* ctx, const double* v0_host, double tol, int32_t max_iters,
+                double* lam_out, int32_t* iters_out);
+
+/* x = y = avg_x = avg_y = 0 (initial_state, pdhg.py:120-127). */
+int pdhg_reset(pdhg_ctx* ctx);
+
+/* Run `iters` PDHG steps (pdhg_step, pdhg.py:140-151) starting at global
+ * iteration `iter0` with steps tau/omega, sigma*omega and average weight w0
+ * (integer-valued).  Steps after the first non-finite iterate are skipped
+ * (pdhg.py:194-196); *fail_iter_out receives that iteration or -1. */
+int pdhg_run_period(pdhg_ctx* ctx, int32_t iters, int64_t iter0, double tau_over_omega,
+                    double sigma_omega, double w0, int64_t* fail_iter_out);
+
+/* Score points.  specs[k] selects point k's (x, y) source (PDHG_PT_*) and,
+ * with PDHG_SPEC_BEST_Z, takes z from the stored best z instead of
+ * z = max(0, c - A'y) (pdhg.py:112-114).  The stored-z form is how the
+ * reference re-checks best_pt with the z it was scored with (pdhg.py:249).
+ * Writes PDHG_NQ doubles per point, in spec order, to out_host. */
+#define PDHG_SPEC_BEST_Z 16
+int pdhg_check(pdhg_ctx* ctx, int32_t npts, const int32_t* specs, double* out_host);
+
+/* Restart at point `which` (CUR or AVG): x, y, avg_x, avg_y <- that point
+ * (pdhg.py:235-238). */
+int pdhg_restart(pdhg_ctx* ctx, int32_t which);
+
+/* Best-point bookkeeping (pdhg.py:231-232).  With PDHG_BEST_Z the stored
+ * best z <- max(0, c - A'y_which); with PDHG_BEST_XY best x,y <- point
+ * `which`.  The split lets the host mirror the reference's aliasing: a
+ * best point taken from the running average keeps its check-time z while
+ * its x,y follow the average until the next restart (pdhg.py:147-148,237-238). */
+#define PDHG_BEST_XY 1
+#define PDHG_BEST_Z 2
+int pdhg_save_best(pdhg_ctx* ctx, int32_t which, int32_t flags);
+
+/* Copy point spec (as in pdhg_check) to host arrays (any may be NULL).
+ * z is max(0, c - A'y) unless PDHG_SPEC_BEST_Z selects the stored best z. */
+int pdhg_fetch(pdhg_ctx* ctx, int32_t spec, double* x_host, double* y_host, double* z_host);
+
+/* Average device time (ms) of one launch of kernel `which` (0 = primal
+ * step over A' rows, 1 = dual step over A rows) over `reps` launches,
+ * CUDA events on the context stream.  The iterate is advanced. */
+int pdhg_time_kernel(pdhg_ctx* ctx, int32_t which, int32_t reps, double tau_over_omega,
+                     double sigma_omega, double* avg_ms_out);
+
+/* Layout helper: A' (CSR of the transpose, = CSC of A with rows ascending
+ * in each column, as scipy's tocsc) from CSR A, all on the device.
+ * tmp must hold pdhg_transpose_tmp_bytes(nnz, m, n) bytes. */
+size_t pdhg_transpose_tmp_bytes(int64_t nnz, int32_t m, int32_t n);
+int pdhg_transpose_csr(int32_t m, int32_t n, int64_t nnz, const int32_t* a_ptr,
+                       const int32_t* a_col, const double* a_val, int32_t* at_ptr,
+                       int32_t* at_col, double* at_val, void* tmp, size_t tmp_bytes,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDHG_B200_H */

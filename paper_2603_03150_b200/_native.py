@@ -1,0 +1,99 @@
+"""ctypes binding of libpdhg_b200.so (declared in include/pdhg_b200.h).
+
+There is no fallback: if the library is missing or fails to load, every
+entry point raises.  The product path has exactly one implementation, the
+sm_100a kernels behind this ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libpdhg_b200.so"
+
+PT_CUR, PT_AVG, PT_BEST = 0, 1, 2
+SPEC_BEST_Z = 16
+BEST_XY, BEST_Z = 1, 2
+NQ = 8
+Q_RP2, Q_RPMAX, Q_BY, Q_RD2, Q_RDMAX, Q_CX, Q_XZ = range(7)
+
+# every symbol include/pdhg_b200.h declares (checked by tests/test_native_abi.py)
+EXPORTS = (
+    "pdhg_abi_version", "pdhg_last_error", "pdhg_workspace_bytes", "pdhg_ctx_create",
+    "pdhg_ctx_destroy", "pdhg_spmv", "pdhg_opnorm", "pdhg_reset", "pdhg_run_period",
+    "pdhg_check", "pdhg_restart", "pdhg_save_best", "pdhg_fetch", "pdhg_time_kernel",
+    "pdhg_transpose_tmp_bytes", "pdhg_transpose_csr",
+)
+
+
+class Problem(C.Structure):
+    """struct pdhg_problem."""
+
+    _fields_ = [
+        ("m", C.c_int32), ("n", C.c_int32), ("nnz", C.c_int64),
+        ("a_ptr", C.c_void_p), ("a_col", C.c_void_p), ("a_val", C.c_void_p),
+        ("at_ptr", C.c_void_p), ("at_col", C.c_void_p), ("at_val", C.c_void_p),
+        ("b", C.c_void_p), ("c", C.c_void_p),
+        ("a_lanes", C.c_int32), ("at_lanes", C.c_int32), ("heavy_threshold", C.c_int32),
+        ("a_n_heavy", C.c_int32), ("at_n_heavy", C.c_int32),
+        ("a_heavy", C.c_void_p), ("at_heavy", C.c_void_p),
+    ]
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def _sig(lib, name, restype, *argtypes):
+    f = getattr(lib, name)
+    f.restype = restype
+    f.argtypes = list(argtypes)
+
+
+def load():
+    """Load (once) and type the native library; raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise NativeError(
+                f"{LIB_PATH} not found: build it with `python -m paper_2603_03150_b200.build` "
+                "(there is no CPU fallback)")
+        lib = C.CDLL(str(LIB_PATH))
+        vp, i32, i64, dbl, szt = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_size_t
+        P = C.POINTER
+        _sig(lib, "pdhg_abi_version", C.c_int)
+        _sig(lib, "pdhg_last_error", C.c_char_p)
+        _sig(lib, "pdhg_workspace_bytes", szt, i32, i32)
+        _sig(lib, "pdhg_ctx_create", C.c_int, P(Problem), vp, szt, vp, P(vp))
+        _sig(lib, "pdhg_ctx_destroy", C.c_int, vp)
+        _sig(lib, "pdhg_spmv", C.c_int, vp, C.c_int, vp, vp)
+        _sig(lib, "pdhg_opnorm", C.c_int, vp, vp, dbl, i32, P(dbl), P(i32))
+        _sig(lib, "pdhg_reset", C.c_int, vp)
+        _sig(lib, "pdhg_run_period", C.c_int, vp, i32, i64, dbl, dbl, dbl, P(i64))
+        _sig(lib, "pdhg_check", C.c_int, vp, i32, P(i32), P(dbl))
+        _sig(lib, "pdhg_restart", C.c_int, vp, i32)
+        _sig(lib, "pdhg_save_best", C.c_int, vp, i32, i32)
+        _sig(lib, "pdhg_fetch", C.c_int, vp, i32, vp, vp, vp)
+        _sig(lib, "pdhg_time_kernel", C.c_int, vp, i32, i32, dbl, dbl, P(dbl))
+        _sig(lib, "pdhg_transpose_tmp_bytes", szt, i64, i32, i32)
+        _sig(lib, "pdhg_transpose_csr", C.c_int, i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, szt, vp)
+        if lib.pdhg_abi_version() != 1:
+            raise NativeError("libpdhg_b200.so ABI version mismatch")
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = _lib.pdhg_last_error().decode(errors="replace") if _lib is not None else "?"
+        raise NativeError(f"libpdhg_b200 error {rc}: {msg}")

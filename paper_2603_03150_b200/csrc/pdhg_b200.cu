@@ -1,0 +1,894 @@
+// pdhg_b200.cu -- sm_100a kernels and the C ABI of the B200 PDHG engine.
+//
+// Hot path replaced: hybridlp.pdhg.run_pdhg and what it calls
+// (/root/reference/pkg/src/hybridlp/pdhg.py:80-258, lp_core.py:106-142,430-485).
+// The arithmetic runs on fp64 CSR layouts of A and A' (dual layout); every
+// elementwise epilogue uses explicitly rounded operations (__dmul_rn etc.,
+// no FMA contraction) in the reference's operation order so that, given
+// the same SpMV results, iterates are bit-identical to numpy's.  SpMV and
+// reduction sums use fixed-order warp/block trees (no float atomics), so
+// results are bitwise reproducible run to run.
+//
+// Kernels
+//   k_primal_step   pdhg.py:142,146-147 (+194): A'y SpMV over rows of A' fused
+//                   with x+ = max(0, x - tau/omega (c - A'y)), xe = 2x+ - x,
+//                   avg_x += (x+ - avg_x)/w, non-finite flag.
+//   k_dual_step     pdhg.py:143,148 (+194): A xe SpMV over rows of A fused with
+//                   y+ = y + sigma*omega (b - A xe), avg_y += (y+ - avg_y)/w.
+//   k_check_primal  lp_core.py:436,441-443,458,476 for 1-2 points: A x with
+//                   r_p = b - Ax, sum r_p^2, max|r_p|, b'y (fixed-order partials).
+//   k_check_dual    pdhg.py:114 + lp_core.py:437,459,477: A'y with
+//                   z = max(0, c - A'y), r_d = c - A'y - z, sum r_d^2, max|r_d|,
+//                   c'x, x'z.
+//   k_reduce        fixed-order combine of the per-block partials.
+//   k_spmv / k_div  power iteration (pdhg.py:80-109) and the 1e-12 SpMV gate.
+#include "../../include/pdhg_b200.h"
+
+#include <cuda_runtime.h>
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(PDHG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kBlock = 256;
+constexpr int kWarps = kBlock / 32;
+constexpr int kCheckBlocks = 148 * 4;  // fixed grid => fixed reduction order
+constexpr int kMaxQ = 2 * PDHG_NQ;
+
+// ---------------------------------------------------------------- device utils
+
+__device__ __forceinline__ double np_max0(double d) {
+  // np.maximum(0.0, d): returns d unless 0.0 > d (NaN propagates, -0.0 kept)
+  return (0.0 > d) ? 0.0 : d;
+}
+
+__device__ __forceinline__ double nan_max(double a, double b) {
+  // np.max semantics: any NaN wins
+  return (a != a || a > b) ? a : b;
+}
+
+__device__ __forceinline__ bool finite(double v) { return isfinite(v); }
+
+template <int V>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = V / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum; result valid in every thread.  Fixed tree order.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = group_sum<32>(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double t = (l < kWarps) ? red[l] : 0.0;
+  t = group_sum<32>(t);
+  return t;
+}
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = nan_max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double t = (l < kWarps) ? red[l] : -1.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t = nan_max(t, __shfl_xor_sync(0xffffffffu, t, o));
+  return t;
+}
+
+struct RowSet {
+  const int* __restrict__ ptr;
+  const int* __restrict__ col;
+  const double* __restrict__ val;
+  int rows;
+  int heavy_threshold;
+  int n_heavy;
+  const int* __restrict__ heavy;
+};
+
+// Partial dot of one row over lanes [lane, lane+V, ...]; NR right-hand sides
+// share one pass over the row's values and indices.
+template <int V, int NR>
+__device__ __forceinline__ void row_dot(const RowSet& A, int s, int e, int lane,
+                                        const double* const* __restrict__ xin, double* acc) {
+#pragma unroll
+  for (int r = 0; r < NR; ++r) acc[r] = 0.0;
+  for (int k = s + lane; k < e; k += V) {
+    const double a = __ldcs(A.val + k);
+    const int j = __ldcs(A.col + k);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[r] = fma(a, __ldg(xin[r] + j), acc[r]);
+  }
+}
+
+// Device-resident per-period parameters (updated by one H2D copy per period
+// so the captured CUDA graph of a period can be replayed unchanged).
+struct StepParams {
+  double tau_w;    // tau / omega      (pdhg.py:142)
+  double sigma_w;  // sigma * omega    (pdhg.py:143)
+  double w0;       // avg_weight at period start (integer valued)
+  long long iter0; // state.iterations at period start
+  long long fail_iter;  // first iteration with a non-finite iterate (LLONG_MAX = none)
+};
+
+// ------------------------------------------------------------------- steps
+
+// Epilogue of the primal step for row j of A' (= column j of A).
+__device__ __forceinline__ void primal_epi(int j, double aty, const double* __restrict__ c,
+                                           double* __restrict__ x, double* __restrict__ xe,
+                                           double* __restrict__ xbar, double tau_w, double w,
+                                           long long iter, StepParams* P) {
+  const double xj = x[j];
+  const double g = __dsub_rn(c[j], aty);                       // c - A'y
+  const double xn = np_max0(__dsub_rn(xj, __dmul_rn(tau_w, g)));  // max(0, x - t g)
+  const double xb = xbar[j];
+  x[j] = xn;
+  xe[j] = __dsub_rn(__dmul_rn(2.0, xn), xj);                  // 2 x+ - x
+  xbar[j] = __dadd_rn(xb, __ddiv_rn(__dsub_rn(xn, xb), w));    // avg += (x+ - avg)/w
+  if (!finite(xn)) atomicMin(&P->fail_iter, iter);
+}
+
+__device__ __forceinline__ void dual_epi(int i, double ax, const double* __restrict__ b,
+                                         double* __restrict__ y, double* __restrict__ ybar,
+                                         double sigma_w, double w, long long iter, StepParams* P) {
+  const double yi = y[i];
+  const double yn = __dadd_rn(yi, __dmul_rn(sigma_w, __dsub_rn(b[i], ax)));
+  const double yb = ybar[i];
+  y[i] = yn;
+  ybar[i] = __dadd_rn(yb, __ddiv_rn(__dsub_rn(yn, yb), w));
+  if (!finite(yn)) atomicMin(&P->fail_iter, iter);
+}
+
+struct StepArgs {
+  RowSet rs;
+  const double* __restrict__ gather;  // y (primal) or xe (dual)
+  const double* __restrict__ cb;      // c (primal) or b (dual)
+  double* x;      // x (primal) or y (dual)
+  double* xe;     // xe (primal only)
+  double* xbar;   // avg_x or avg_y
+  StepParams* P;
+};
+
+template <int V, bool PRIMAL>
+__global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
+  __shared__ double red[kWarps];
+  StepParams* P = a.P;
+  const long long iter = P->iter0 + j_in_period + 1;  // state.iterations after this step
+  if (P->fail_iter < iter) return;                    // pdhg.py:194-196: stop after failure
+  const double w = P->w0 + (double)(j_in_period + 1);  // avg_weight + 1 (exact, integer valued)
+  const double step = PRIMAL ? P->tau_w : P->sigma_w;
+  const double* xin[1] = {a.gather};
+
+  if ((int)blockIdx.x < a.rs.n_heavy) {  // one block per heavy row
+    const int row = a.rs.heavy[blockIdx.x];
+    const int s = a.rs.ptr[row], e = a.rs.ptr[row + 1];
+    double acc[1];
+    row_dot<kBlock, 1>(a.rs, s, e, threadIdx.x, xin, acc);
+    const double d = block_sum(acc[0], red);
+    if (threadIdx.x == 0) {
+      if (PRIMAL) primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
+      else dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
+    }
+    return;
+  }
+  const long long gid = (long long)(blockIdx.x - a.rs.n_heavy) * kBlock + threadIdx.x;
+  const int row = (int)(gid / V);
+  const int lane = threadIdx.x % V;
+  bool valid = row < a.rs.rows;
+  int s = 0, e = 0;
+  if (valid) {
+    s = a.rs.ptr[row];
+    e = a.rs.ptr[row + 1];
+    if (e - s > a.rs.heavy_threshold) { valid = false; e = s; }
+  }
+  double acc[1];
+  row_dot<V, 1>(a.rs, s, e, lane, xin, acc);
+  const double d = group_sum<V>(acc[0]);
+  if (valid && lane == 0) {
+    if (PRIMAL) primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
+    else dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
+  }
+}
+
+// ------------------------------------------------------------------ plain SpMV
+
+template <int V>
+__global__ void __launch_bounds__(kBlock) k_spmv(RowSet rs, const double* __restrict__ in,
+                                                 double* __restrict__ out) {
+  __shared__ double red[kWarps];
+  const double* xin[1] = {in};
+  if ((int)blockIdx.x < rs.n_heavy) {
+    const int row = rs.heavy[blockIdx.x];
+    double acc[1];
+    row_dot<kBlock, 1>(rs, rs.ptr[row], rs.ptr[row + 1], threadIdx.x, xin, acc);
+    const double d = block_sum(acc[0], red);
+    if (threadIdx.x == 0) out[row] = d;
+    return;
+  }
+  const long long gid = (long long)(blockIdx.x - rs.n_heavy) * kBlock + threadIdx.x;
+  const int row = (int)(gid / V);
+  const int lane = threadIdx.x % V;
+  bool valid = row < rs.rows;
+  int s = 0, e = 0;
+  if (valid) {
+    s = rs.ptr[row];
+    e = rs.ptr[row + 1];
+    if (e - s > rs.heavy_threshold) { valid = false; e = s; }
+  }
+  double acc[1];
+  row_dot<V, 1>(rs, s, e, lane, xin, acc);
+  const double d = group_sum<V>(acc[0]);
+  if (valid && lane == 0) out[row] = d;
+}
+
+__global__ void k_div(const double* __restrict__ w, double* __restrict__ v, double s, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = __ddiv_rn(w[i], s);  // v = w / norm_w   (pdhg.py:99)
+}
+
+// sum of squares partials (np.linalg.norm), fixed grid
+__global__ void __launch_bounds__(kBlock) k_sumsq(const double* __restrict__ v, int n,
+                                                  double* __restrict__ partials) {
+  __shared__ double red[kWarps];
+  double acc = 0.0;
+  for (long long i = (long long)blockIdx.x * kBlock + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kBlock)
+    acc = fma(v[i], v[i], acc);
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = t;
+}
+
+// ---------------------------------------------------------------- KKT checks
+
+struct CheckPts {
+  const double* x[2];
+  const double* y[2];
+  const double* zin[2];  // nullptr => z = max(0, c - A'y)
+  double* zout[2];       // optional z output
+};
+
+// Per-point primal-side terms over rows of A: r_p = b - A x (lp_core.py:436).
+template <int V, int NP>
+__global__ void __launch_bounds__(kBlock) k_check_primal(RowSet rs, const double* __restrict__ b,
+                                                         CheckPts pts, double* __restrict__ partials) {
+  __shared__ double red[kWarps];
+  double rp2[NP], rpmax[NP], by[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) { rp2[p] = 0.0; rpmax[p] = 0.0; by[p] = 0.0; }
+  const double* xin[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) xin[p] = pts.x[p];
+
+  auto row_terms = [&](int i, const double* d) {
+    const double bi = b[i];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const double r = __dsub_rn(bi, d[p]);
+      rp2[p] = fma(r, r, rp2[p]);
+      rpmax[p] = nan_max(fabs(r), rpmax[p]);
+      by[p] = fma(bi, pts.y[p][i], by[p]);
+    }
+  };
+  // heavy rows: block per row, blocks take them round robin
+  for (int h = blockIdx.x; h < rs.n_heavy; h += gridDim.x) {
+    const int row = rs.heavy[h];
+    double acc[NP], d[NP];
+    row_dot<kBlock, NP>(rs, rs.ptr[row], rs.ptr[row + 1], threadIdx.x, xin, acc);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) d[p] = block_sum(acc[p], red);
+    if (threadIdx.x == 0) row_terms(row, d);
+  }
+  const int lane = threadIdx.x % V;
+  const long long groups = (long long)gridDim.x * (kBlock / V);
+  for (long long g = (long long)blockIdx.x * (kBlock / V) + threadIdx.x / V; g - threadIdx.x / V < rs.rows;
+       g += groups) {
+    const int row = (int)g;
+    bool valid = row < rs.rows;
+    int s = 0, e = 0;
+    if (valid) {
+      s = rs.ptr[row];
+      e = rs.ptr[row + 1];
+      if (e - s > rs.heavy_threshold) { valid = false; e = s; }
+    }
+    double acc[NP], d[NP];
+    row_dot<V, NP>(rs, s, e, lane, xin, acc);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) d[p] = group_sum<V>(acc[p]);
+    if (valid && lane == 0) row_terms(row, d);
+  }
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const double t0 = block_sum(rp2[p], red);
+    const double t1 = block_max(rpmax[p], red);
+    const double t2 = block_sum(by[p], red);
+    if (threadIdx.x == 0) {
+      double* o = partials + (size_t)blockIdx.x * kMaxQ + p * PDHG_NQ;
+      o[PDHG_Q_RP2] = t0;
+      o[PDHG_Q_RPMAX] = t1;
+      o[PDHG_Q_BY] = t2;
+    }
+  }
+}
+
+// Per-point dual-side terms over rows of A' (lp_core.py:437,441,443; pdhg.py:114).
+template <int V, int NP>
+__global__ void __launch_bounds__(kBlock) k_check_dual(RowSet rs, const double* __restrict__ c,
+                                                       CheckPts pts, double* __restrict__ partials) {
+  __shared__ double red[kWarps];
+  double rd2[NP], rdmax[NP], cx[NP], xz[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) { rd2[p] = 0.0; rdmax[p] = 0.0; cx[p] = 0.0; xz[p] = 0.0; }
+  const double* yin[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) yin[p] = pts.y[p];
+
+  auto row_terms = [&](int j, const double* d) {
+    const double cj = c[j];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const double t = __dsub_rn(cj, d[p]);                 // c - A'y
+      const double z = pts.zin[p] ? pts.zin[p][j] : np_max0(t);
+      if (pts.zout[p]) pts.zout[p][j] = z;
+      const double r = __dsub_rn(t, z);                     // r_d = c - A'y - z
+      const double xj = pts.x[p][j];
+      rd2[p] = fma(r, r, rd2[p]);
+      rdmax[p] = nan_max(fabs(r), rdmax[p]);
+      cx[p] = fma(cj, xj, cx[p]);
+      xz[p] = fma(xj, z, xz[p]);
+    }
+  };
+  for (int h = blockIdx.x; h < rs.n_heavy; h += gridDim.x) {
+    const int row = rs.heavy[h];
+    double acc[NP], d[NP];
+    row_dot<kBlock, NP>(rs, rs.ptr[row], rs.ptr[row + 1], threadIdx.x, yin, acc);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) d[p] = block_sum(acc[p], red);
+    if (threadIdx.x == 0) row_terms(row, d);
+  }
+  const int lane = threadIdx.x % V;
+  const long long groups = (long long)gridDim.x * (kBlock / V);
+  for (long long g = (long long)blockIdx.x * (kBlock / V) + threadIdx.x / V; g - threadIdx.x / V < rs.rows;
+       g += groups) {
+    const int row = (int)g;
+    bool valid = row < rs.rows;
+    int s = 0, e = 0;
+    if (valid) {
+      s = rs.ptr[row];
+      e = rs.ptr[row + 1];
+      if (e - s > rs.heavy_threshold) { valid = false; e = s; }
+    }
+    double acc[NP], d[NP];
+    row_dot<V, NP>(rs, s, e, lane, yin, acc);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) d[p] = group_sum<V>(acc[p]);
+    if (valid && lane == 0) row_terms(row, d);
+  }
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const double t0 = block_sum(rd2[p], red);
+    const double t1 = block_max(rdmax[p], red);
+    const double t2 = block_sum(cx[p], red);
+    const double t3 = block_sum(xz[p], red);
+    if (threadIdx.x == 0) {
+      double* o = partials + (size_t)blockIdx.x * kMaxQ + p * PDHG_NQ;
+      o[PDHG_Q_RD2] = t0;
+      o[PDHG_Q_RDMAX] = t1;
+      o[PDHG_Q_CX] = t2;
+      o[PDHG_Q_XZ] = t3;
+    }
+  }
+}
+
+// One block per quantity: combine per-block partials in a fixed order.
+__global__ void __launch_bounds__(kBlock) k_reduce(const double* __restrict__ partials, int nblk,
+                                                   int stride, int nq, double* __restrict__ out) {
+  __shared__ double red[kWarps];
+  const int q = blockIdx.x;
+  const bool is_max = (q % PDHG_NQ) == PDHG_Q_RPMAX || (q % PDHG_NQ) == PDHG_Q_RDMAX;
+  double acc = is_max ? -1.0 : 0.0;
+  for (int bi = threadIdx.x; bi < nblk; bi += kBlock) {
+    const double v = partials[(size_t)bi * stride + q];
+    acc = is_max ? nan_max(v, acc) : acc + v;
+  }
+  const double t = is_max ? block_max(acc, red) : block_sum(acc, red);
+  if (threadIdx.x == 0) out[q] = ((q % PDHG_NQ) == PDHG_Q_RSV) ? 0.0 : t;
+}
+
+// ------------------------------------------------------------- layout helpers
+
+__global__ void k_row_ids(const int* __restrict__ ptr, int rows, int* __restrict__ rid) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) rid[k] = i;
+}
+
+__global__ void k_iota(int* __restrict__ v, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int)i;
+}
+
+__global__ void k_gather_t(const int* __restrict__ perm, const int* __restrict__ rid,
+                           const double* __restrict__ val, int* __restrict__ at_col,
+                           double* __restrict__ at_val, long long nnz) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nnz) return;
+  const int p = perm[k];
+  at_col[k] = rid[p];
+  at_val[k] = val[p];
+}
+
+// at_ptr[j] = first position of key >= j in the sorted column keys
+__global__ void k_col_ptr(const int* __restrict__ keys, long long nnz, int n, int* __restrict__ at_ptr) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > n) return;
+  long long lo = 0, hi = nnz;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (keys[mid] < j) lo = mid + 1; else hi = mid;
+  }
+  at_ptr[j] = (int)lo;
+}
+
+// ---------------------------------------------------------------- dispatch
+
+template <template <int> class F, class... Args>
+int dispatch_lanes(int lanes, Args&&... args) {
+  switch (lanes) {
+    case 1: return F<1>::run(args...);
+    case 2: return F<2>::run(args...);
+    case 4: return F<4>::run(args...);
+    case 8: return F<8>::run(args...);
+    case 16: return F<16>::run(args...);
+    case 32: return F<32>::run(args...);
+    default: return fail(PDHG_ERR_ARG, "lanes must be 1,2,4,8,16 or 32");
+  }
+}
+
+int grid_rows(const RowSet& rs, int lanes) {
+  return rs.n_heavy + (int)(((long long)rs.rows * lanes + kBlock - 1) / kBlock);
+}
+
+template <int V>
+struct StepLaunch {
+  static int run(bool primal, const StepArgs& a, int j, cudaStream_t s) {
+    const int g = grid_rows(a.rs, V);
+    if (g == 0) return 0;
+    if (primal) k_step<V, true><<<g, kBlock, 0, s>>>(a, j);
+    else k_step<V, false><<<g, kBlock, 0, s>>>(a, j);
+    return 0;
+  }
+};
+
+template <int V>
+struct SpmvLaunch {
+  static int run(const RowSet& rs, const double* in, double* out, cudaStream_t s) {
+    const int g = grid_rows(rs, V);
+    if (g > 0) k_spmv<V><<<g, kBlock, 0, s>>>(rs, in, out);
+    return 0;
+  }
+};
+
+template <int V>
+struct CheckLaunch {
+  static int run(bool primal, int np, const RowSet& rs, const double* bc, const CheckPts& pts,
+                 double* partials, cudaStream_t s) {
+    if (primal) {
+      if (np == 1) k_check_primal<V, 1><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
+      else k_check_primal<V, 2><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
+    } else {
+      if (np == 1) k_check_dual<V, 1><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
+      else k_check_dual<V, 2><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
+    }
+    return 0;
+  }
+};
+
+int auto_lanes(long long nnz, int rows) {
+  if (rows <= 0) return 1;
+  const double mean = (double)nnz / rows;
+  int v = 1;
+  while (v < 32 && 4.0 * v * 2 <= mean) v *= 2;  // ~4+ entries per lane
+  return v;
+}
+
+size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
+
+}  // namespace
+
+// ------------------------------------------------------------------ context
+
+struct pdhg_ctx {
+  pdhg_problem prob;
+  RowSet A, At;
+  int a_lanes, at_lanes;
+  cudaStream_t stream;
+  // workspace carve
+  double *x, *xe, *xbar, *xbest, *zbest, *tn1, *tn2;
+  double *y, *ybar, *ybest, *tm1;
+  double* partials;
+  double* scalars;
+  StepParams* P;
+  // pinned host staging
+  StepParams* P_host;
+  double* scal_host;
+  std::map<int, cudaGraphExec_t> graphs;
+};
+
+namespace {
+
+struct Carve {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t count) {
+    T* p = reinterpret_cast<T*>(base + off);
+    off += align_up(count * sizeof(T));
+    return p;
+  }
+};
+
+size_t carve_bytes(int32_t m, int32_t n) {
+  size_t b = 0;
+  b += 7 * align_up((size_t)n * 8);
+  b += 4 * align_up((size_t)m * 8);
+  b += align_up((size_t)kCheckBlocks * kMaxQ * 8);
+  b += align_up(64 * 8);
+  b += align_up(sizeof(StepParams));
+  return b;
+}
+
+int launch_step(pdhg_ctx* c, bool primal, int j) {
+  StepArgs a;
+  if (primal) {
+    a.rs = c->At; a.gather = c->y; a.cb = c->prob.c; a.x = c->x; a.xe = c->xe; a.xbar = c->xbar;
+  } else {
+    a.rs = c->A; a.gather = c->xe; a.cb = c->prob.b; a.x = c->y; a.xe = nullptr; a.xbar = c->ybar;
+  }
+  a.P = c->P;
+  return dispatch_lanes<StepLaunch>(primal ? c->at_lanes : c->a_lanes, primal, a, j, c->stream);
+}
+
+int spmv(pdhg_ctx* c, bool transpose, const double* in, double* out) {
+  return dispatch_lanes<SpmvLaunch>(transpose ? c->at_lanes : c->a_lanes, transpose ? c->At : c->A,
+                                    in, out, c->stream);
+}
+
+void point_xy(pdhg_ctx* c, int which, const double** x, const double** y) {
+  switch (which & 3) {
+    case PDHG_PT_AVG: *x = c->xbar; *y = c->ybar; break;
+    case PDHG_PT_BEST: *x = c->xbest; *y = c->ybest; break;
+    default: *x = c->x; *y = c->y; break;
+  }
+}
+
+// reduce sum of squares of v (length len) into host scalar (syncs)
+int sumsq_host(pdhg_ctx* c, const double* v, int len, double* out) {
+  k_sumsq<<<kCheckBlocks, kBlock, 0, c->stream>>>(v, len, c->partials);
+  k_reduce<<<1, kBlock, 0, c->stream>>>(c->partials, kCheckBlocks, 1, 1, c->scalars);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(c->scal_host, c->scalars, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  *out = c->scal_host[0];
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pdhg_abi_version(void) { return PDHG_ABI_VERSION; }
+
+const char* pdhg_last_error(void) { return g_err.c_str(); }
+
+size_t pdhg_workspace_bytes(int32_t m, int32_t n) { return carve_bytes(m, n); }
+
+int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_bytes, void* stream,
+                    pdhg_ctx** out) {
+  if (!prob || !out) return fail(PDHG_ERR_ARG, "null argument");
+  if (prob->m <= 0 || prob->n <= 0) return fail(PDHG_ERR_ARG, "empty model");
+  if (workspace_bytes < carve_bytes(prob->m, prob->n))
+    return fail(PDHG_ERR_ARG, "workspace too small");
+  pdhg_ctx* c = new pdhg_ctx();
+  c->prob = *prob;
+  c->stream = (cudaStream_t)stream;
+  c->A = RowSet{prob->a_ptr, prob->a_col, prob->a_val, prob->m, prob->heavy_threshold,
+                prob->a_n_heavy, prob->a_heavy};
+  c->At = RowSet{prob->at_ptr, prob->at_col, prob->at_val, prob->n, prob->heavy_threshold,
+                 prob->at_n_heavy, prob->at_heavy};
+  c->a_lanes = prob->a_lanes > 0 ? prob->a_lanes : auto_lanes(prob->nnz, prob->m);
+  c->at_lanes = prob->at_lanes > 0 ? prob->at_lanes : auto_lanes(prob->nnz, prob->n);
+  Carve cv{(char*)workspace};
+  const int n = prob->n, m = prob->m;
+  c->x = cv.take<double>(n); c->xe = cv.take<double>(n); c->xbar = cv.take<double>(n);
+  c->xbest = cv.take<double>(n); c->zbest = cv.take<double>(n);
+  c->tn1 = cv.take<double>(n); c->tn2 = cv.take<double>(n);
+  c->y = cv.take<double>(m); c->ybar = cv.take<double>(m); c->ybest = cv.take<double>(m);
+  c->tm1 = cv.take<double>(m);
+  c->partials = cv.take<double>((size_t)kCheckBlocks * kMaxQ);
+  c->scalars = cv.take<double>(64);
+  c->P = cv.take<StepParams>(1);
+  cudaError_t e1 = cudaMallocHost(&c->P_host, sizeof(StepParams));
+  cudaError_t e2 = cudaMallocHost(&c->scal_host, 64 * sizeof(double));
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    delete c;
+    return fail(PDHG_ERR_CUDA, "cudaMallocHost failed");
+  }
+  *out = c;
+  return 0;
+}
+
+int pdhg_ctx_destroy(pdhg_ctx* c) {
+  if (!c) return 0;
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  cudaFreeHost(c->P_host);
+  cudaFreeHost(c->scal_host);
+  delete c;
+  return 0;
+}
+
+int pdhg_spmv(pdhg_ctx* c, int transpose, const double* in, double* out) {
+  if (!c || !in || !out) return fail(PDHG_ERR_ARG, "null argument");
+  int rc = spmv(c, transpose != 0, in, out);
+  if (rc) return rc;
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int pdhg_opnorm(pdhg_ctx* c, const double* v0_host, double tol, int32_t max_iters, double* lam_out,
+                int32_t* iters_out) {
+  // pdhg.py:80-109.  v (tn1) <- v0; loop: w (tn2) = A'(A v); ||w||; v = w/||w||.
+  if (!c || !v0_host || !lam_out) return fail(PDHG_ERR_ARG, "null argument");
+  const int n = c->prob.n;
+  CUDA_TRY(cudaMemcpyAsync(c->tn1, v0_host, (size_t)n * 8, cudaMemcpyHostToDevice, c->stream));
+  double lam = 0.0;
+  int it = 0;
+  int rc;
+  for (; it < max_iters; ++it) {
+    if ((rc = spmv(c, false, c->tn1, c->tm1))) return rc;
+    if ((rc = spmv(c, true, c->tm1, c->tn2))) return rc;
+    double ss;
+    if ((rc = sumsq_host(c, c->tn2, n, &ss))) return rc;
+    const double norm_w = std::sqrt(ss);
+    if (norm_w == 0.0) break;
+    const double new_lam = std::sqrt(norm_w);
+    k_div<<<(n + kBlock - 1) / kBlock, kBlock, 0, c->stream>>>(c->tn2, c->tn1, norm_w, n);
+    if (lam > 0 && std::fabs(new_lam - lam) <= tol * new_lam) {
+      lam = new_lam;
+      ++it;
+      break;
+    }
+    lam = new_lam;
+  }
+  // safeguard multiply (pdhg.py:104-108)
+  if ((rc = spmv(c, false, c->tn1, c->tm1))) return rc;
+  if ((rc = spmv(c, true, c->tm1, c->tn2))) return rc;
+  double ss;
+  if ((rc = sumsq_host(c, c->tn2, n, &ss))) return rc;
+  const double norm_w = std::sqrt(ss);
+  if (norm_w > 0) lam = std::max(lam, std::sqrt(norm_w));
+  *lam_out = lam;
+  if (iters_out) *iters_out = it;
+  return 0;
+}
+
+int pdhg_reset(pdhg_ctx* c) {
+  if (!c) return fail(PDHG_ERR_ARG, "null ctx");
+  const size_t nb = (size_t)c->prob.n * 8, mb = (size_t)c->prob.m * 8;
+  CUDA_TRY(cudaMemsetAsync(c->x, 0, nb, c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->xe, 0, nb, c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->xbar, 0, nb, c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->y, 0, mb, c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->ybar, 0, mb, c->stream));
+  return 0;
+}
+
+int pdhg_run_period(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_over_omega,
+                    double sigma_omega, double w0, int64_t* fail_iter_out) {
+  if (!c || iters < 0) return fail(PDHG_ERR_ARG, "bad argument");
+  StepParams& h = *c->P_host;
+  h.tau_w = tau_over_omega;
+  h.sigma_w = sigma_omega;
+  h.w0 = w0;
+  h.iter0 = iter0;
+  h.fail_iter = LLONG_MAX;
+  CUDA_TRY(cudaMemcpyAsync(c->P, c->P_host, sizeof(StepParams), cudaMemcpyHostToDevice, c->stream));
+  if (iters > 0) {
+    auto it = c->graphs.find(iters);
+    if (it == c->graphs.end()) {
+      cudaGraph_t g;
+      CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      int rc = 0;
+      for (int j = 0; j < iters && !rc; ++j) {
+        rc = launch_step(c, true, j);
+        if (!rc) rc = launch_step(c, false, j);
+      }
+      cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+      if (rc) return rc;
+      if (ce != cudaSuccess) return fail(PDHG_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
+      cudaGraphExec_t ex;
+      CUDA_TRY(cudaGraphInstantiate(&ex, g, 0));
+      cudaGraphDestroy(g);
+      it = c->graphs.emplace(iters, ex).first;
+    }
+    CUDA_TRY(cudaGraphLaunch(it->second, c->stream));
+  }
+  CUDA_TRY(cudaMemcpyAsync(&c->P_host->fail_iter, &c->P->fail_iter, sizeof(long long),
+                           cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (fail_iter_out) *fail_iter_out = (c->P_host->fail_iter == LLONG_MAX) ? -1 : c->P_host->fail_iter;
+  return 0;
+}
+
+int pdhg_check(pdhg_ctx* c, int32_t npts, const int32_t* specs, double* out_host) {
+  if (!c || !specs || !out_host || npts < 1 || npts > 2) return fail(PDHG_ERR_ARG, "bad argument");
+  CheckPts pts{};
+  for (int p = 0; p < npts; ++p) {
+    point_xy(c, specs[p], &pts.x[p], &pts.y[p]);
+    pts.zin[p] = (specs[p] & PDHG_SPEC_BEST_Z) ? c->zbest : nullptr;
+    pts.zout[p] = nullptr;
+  }
+  CUDA_TRY(cudaMemsetAsync(c->partials, 0, (size_t)kCheckBlocks * kMaxQ * 8, c->stream));
+  int rc = dispatch_lanes<CheckLaunch>(c->a_lanes, true, (int)npts, c->A, c->prob.b, pts, c->partials,
+                                       c->stream);
+  if (rc) return rc;
+  rc = dispatch_lanes<CheckLaunch>(c->at_lanes, false, (int)npts, c->At, c->prob.c, pts, c->partials,
+                                   c->stream);
+  if (rc) return rc;
+  const int nq = npts * PDHG_NQ;
+  k_reduce<<<nq, kBlock, 0, c->stream>>>(c->partials, kCheckBlocks, kMaxQ, nq, c->scalars);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(c->scal_host, c->scalars, nq * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  std::memcpy(out_host, c->scal_host, nq * sizeof(double));
+  return 0;
+}
+
+int pdhg_restart(pdhg_ctx* c, int32_t which) {
+  if (!c) return fail(PDHG_ERR_ARG, "null ctx");
+  const size_t nb = (size_t)c->prob.n * 8, mb = (size_t)c->prob.m * 8;
+  if (which == PDHG_PT_CUR) {
+    CUDA_TRY(cudaMemcpyAsync(c->xbar, c->x, nb, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->ybar, c->y, mb, cudaMemcpyDeviceToDevice, c->stream));
+  } else if (which == PDHG_PT_AVG) {
+    CUDA_TRY(cudaMemcpyAsync(c->x, c->xbar, nb, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->y, c->ybar, mb, cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    return fail(PDHG_ERR_ARG, "restart point must be CUR or AVG");
+  }
+  return 0;
+}
+
+int pdhg_save_best(pdhg_ctx* c, int32_t which, int32_t flags) {
+  if (!c) return fail(PDHG_ERR_ARG, "null ctx");
+  const double *x, *y;
+  point_xy(c, which, &x, &y);
+  if (flags & PDHG_BEST_Z) {
+    CheckPts pts{};
+    pts.x[0] = x; pts.y[0] = y; pts.zin[0] = nullptr; pts.zout[0] = c->zbest;
+    int rc = dispatch_lanes<CheckLaunch>(c->at_lanes, false, 1, c->At, c->prob.c, pts, c->partials,
+                                         c->stream);
+    if (rc) return rc;
+    CUDA_TRY(cudaGetLastError());
+  }
+  if ((flags & PDHG_BEST_XY) && (which & 3) != PDHG_PT_BEST) {
+    CUDA_TRY(cudaMemcpyAsync(c->xbest, x, (size_t)c->prob.n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->ybest, y, (size_t)c->prob.m * 8, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  return 0;
+}
+
+int pdhg_fetch(pdhg_ctx* c, int32_t spec, double* x_host, double* y_host, double* z_host) {
+  if (!c) return fail(PDHG_ERR_ARG, "null ctx");
+  const double *x, *y;
+  point_xy(c, spec, &x, &y);
+  const size_t nb = (size_t)c->prob.n * 8, mb = (size_t)c->prob.m * 8;
+  if (x_host) CUDA_TRY(cudaMemcpyAsync(x_host, x, nb, cudaMemcpyDeviceToHost, c->stream));
+  if (y_host) CUDA_TRY(cudaMemcpyAsync(y_host, y, mb, cudaMemcpyDeviceToHost, c->stream));
+  if (z_host) {
+    if (spec & PDHG_SPEC_BEST_Z) {
+      CUDA_TRY(cudaMemcpyAsync(z_host, c->zbest, nb, cudaMemcpyDeviceToHost, c->stream));
+    } else {
+      CheckPts pts{};
+      pts.x[0] = x; pts.y[0] = y; pts.zin[0] = nullptr; pts.zout[0] = c->tn1;
+      int rc = dispatch_lanes<CheckLaunch>(c->at_lanes, false, 1, c->At, c->prob.c, pts, c->partials,
+                                           c->stream);
+      if (rc) return rc;
+      CUDA_TRY(cudaMemcpyAsync(z_host, c->tn1, nb, cudaMemcpyDeviceToHost, c->stream));
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int pdhg_time_kernel(pdhg_ctx* c, int32_t which, int32_t reps, double tau_over_omega,
+                     double sigma_omega, double* avg_ms_out) {
+  if (!c || reps < 1 || !avg_ms_out) return fail(PDHG_ERR_ARG, "bad argument");
+  StepParams& h = *c->P_host;
+  h.tau_w = tau_over_omega; h.sigma_w = sigma_omega; h.w0 = 0.0; h.iter0 = 0; h.fail_iter = LLONG_MAX;
+  CUDA_TRY(cudaMemcpyAsync(c->P, c->P_host, sizeof(StepParams), cudaMemcpyHostToDevice, c->stream));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  int rc = launch_step(c, which == 0, 0);  // warm
+  if (rc) return rc;
+  CUDA_TRY(cudaEventRecord(e0, c->stream));
+  for (int r = 0; r < reps && !rc; ++r) rc = launch_step(c, which == 0, 0);
+  CUDA_TRY(cudaEventRecord(e1, c->stream));
+  CUDA_TRY(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc) return rc;
+  *avg_ms_out = ms / reps;
+  return 0;
+}
+
+size_t pdhg_transpose_tmp_bytes(int64_t nnz, int32_t m, int32_t n) {
+  size_t cub_bytes = 0;
+  cub::DoubleBuffer<int> k(nullptr, nullptr), v(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, k, v, (int)nnz);
+  (void)m; (void)n;
+  return 5 * align_up((size_t)nnz * 4) + align_up(cub_bytes);
+}
+
+int pdhg_transpose_csr(int32_t m, int32_t n, int64_t nnz, const int32_t* a_ptr, const int32_t* a_col,
+                       const double* a_val, int32_t* at_ptr, int32_t* at_col, double* at_val,
+                       void* tmp, size_t tmp_bytes, void* stream) {
+  if (nnz < 0 || nnz >= INT_MAX) return fail(PDHG_ERR_ARG, "nnz out of int32 range");
+  if (tmp_bytes < pdhg_transpose_tmp_bytes(nnz, m, n)) return fail(PDHG_ERR_ARG, "tmp too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  Carve cv{(char*)tmp};
+  int* k0 = cv.take<int>(nnz);
+  int* k1 = cv.take<int>(nnz);
+  int* v0 = cv.take<int>(nnz);
+  int* v1 = cv.take<int>(nnz);
+  int* rid = cv.take<int>(nnz);
+  size_t cub_bytes = tmp_bytes - cv.off;
+  void* cub_tmp = (char*)tmp + cv.off;
+  if (nnz > 0) {
+    CUDA_TRY(cudaMemcpyAsync(k0, a_col, (size_t)nnz * 4, cudaMemcpyDeviceToDevice, s));
+    k_iota<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(v0, nnz);
+    k_row_ids<<<(m + 255) / 256, 256, 0, s>>>(a_ptr, m, rid);
+    cub::DoubleBuffer<int> kb(k0, k1), vb(v0, v1);
+    int bits = 1;
+    while (bits < 31 && (1LL << bits) <= n) ++bits;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, kb, vb, (int)nnz, 0, bits, s));
+    k_gather_t<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(vb.Current(), rid, a_val, at_col, at_val, nnz);
+    k_col_ptr<<<(n + 1 + 255) / 256, 256, 0, s>>>(kb.Current(), nnz, n, at_ptr);
+  } else {
+    CUDA_TRY(cudaMemsetAsync(at_ptr, 0, (size_t)(n + 1) * 4, s));
+  }
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // extern "C"

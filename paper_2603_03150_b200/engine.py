@@ -1,0 +1,455 @@
+"""Host side of the B200 PDHG engine: the reference's `run_pdhg` control flow
+over the sm_100a kernels of libpdhg_b200.so.
+
+Drop-in for ``hybridlp.pdhg.run_pdhg`` (/root/reference/pkg/src/hybridlp/
+pdhg.py:162-258): same signature, same options object, same result objects,
+same status/raise behaviour.  The loop below follows the reference line by
+line, at the granularity of one *period* (the iterations up to the next KKT
+check, pdhg.py:198-199): the device runs a whole period as one CUDA graph and
+returns ~16 scalars; every decision (termination, candidate, best point,
+restart, primal weight) is taken here from those scalars exactly as the
+reference takes it.
+
+Differences from the reference, all documented in DESIGN.md:
+  * the time limit is tested before every period instead of every step
+    (pdhg.py:188); time_limit_s=0 still returns after 0 iterations;
+  * sums (SpMV rows, norms, dots) run in a different but fixed order, so
+    scores agree to rounding (1e-16 relative), not bit for bit.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+import time
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .lp_types import resolve
+
+_WEIGHT_CLIP = (1e-4, 1e4)  # pdhg.py:28
+
+
+@dataclass
+class GpuOptions:
+    """GPU-only knobs (keyword-only in run_pdhg, never required).
+
+    device:          CUDA device index (default: current device).
+    a_lanes/at_lanes: lanes per row for A / A' rows (0 = auto from the mean row length).
+    heavy_threshold: rows longer than this get a whole thread block.
+    opnorm:          override the power-iteration estimate (parity fallback).
+    cache_layout:    keep the device layout of a model for repeated solves.
+    """
+
+    device: int | None = None
+    a_lanes: int = 0
+    at_lanes: int = 0
+    heavy_threshold: int = 1024
+    opnorm: float | None = None
+    cache_layout: bool = True
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise N.NativeError("paper_2603_03150_b200 needs a CUDA device (B200, sm_100a); "
+                            "there is no CPU fallback")
+    return torch
+
+
+def _as_csr(A):
+    import scipy.sparse as sp
+
+    if not sp.isspmatrix_csr(A) and not isinstance(A, sp.csr_array):
+        A = sp.csr_matrix(A, dtype=float)
+    if A.dtype != np.float64:
+        A = A.astype(np.float64)
+    return A
+
+
+class DeviceLp:
+    """Device-resident dual layout of one StandardLp plus the engine context.
+
+    Owns (as torch tensors) A in CSR, A' in CSR (built on the device, equal to
+    scipy's tocsc arrays), b, c, the heavy-row lists and the workspace the
+    library carves its iterate buffers from.
+    """
+
+    def __init__(self, A, b, c, opts: GpuOptions):
+        torch = _torch()
+        self.lib = N.load()
+        dev = torch.device("cuda", torch.cuda.current_device() if opts.device is None else opts.device)
+        self.device = dev
+        self.lock = threading.Lock()
+        A = _as_csr(A)
+        m, n = A.shape
+        nnz = int(A.nnz)
+        if nnz >= 2**31 - 1:
+            raise ValueError("nnz >= 2^31 is not supported by the int32 layout")
+        self.m, self.n, self.nnz = m, n, nnz
+        with torch.cuda.device(dev):
+            self.stream = torch.cuda.Stream(dev)
+            with torch.cuda.stream(self.stream):
+                t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
+                self.a_ptr = t(A.indptr, np.int32)
+                self.a_col = t(A.indices, np.int32)
+                self.a_val = t(A.data, np.float64)
+                self.b = t(b, np.float64)
+                self.c = t(c, np.float64)
+                self.at_ptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
+                self.at_col = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+                self.at_val = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+                sptr = self.stream.cuda_stream
+                tmp_bytes = self.lib.pdhg_transpose_tmp_bytes(nnz, m, n)
+                tmp = torch.empty(max(tmp_bytes, 1), dtype=torch.uint8, device=dev)
+                N.check(self.lib.pdhg_transpose_csr(
+                    m, n, nnz, self.a_ptr.data_ptr(), self.a_col.data_ptr(), self.a_val.data_ptr(),
+                    self.at_ptr.data_ptr(), self.at_col.data_ptr(), self.at_val.data_ptr(),
+                    tmp.data_ptr(), tmp_bytes, sptr))
+                H = int(opts.heavy_threshold)
+                self.a_heavy = torch.nonzero((self.a_ptr[1:] - self.a_ptr[:-1]) > H).flatten().to(torch.int32)
+                self.at_heavy = torch.nonzero((self.at_ptr[1:] - self.at_ptr[:-1]) > H).flatten().to(torch.int32)
+                ws_bytes = self.lib.pdhg_workspace_bytes(m, n)
+                self.ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+                self.stream.synchronize()
+                del tmp
+        p = N.Problem()
+        p.m, p.n, p.nnz = m, n, nnz
+        p.a_ptr, p.a_col, p.a_val = self.a_ptr.data_ptr(), self.a_col.data_ptr(), self.a_val.data_ptr()
+        p.at_ptr, p.at_col, p.at_val = self.at_ptr.data_ptr(), self.at_col.data_ptr(), self.at_val.data_ptr()
+        p.b, p.c = self.b.data_ptr(), self.c.data_ptr()
+        p.a_lanes, p.at_lanes, p.heavy_threshold = opts.a_lanes, opts.at_lanes, H
+        p.a_n_heavy, p.at_n_heavy = self.a_heavy.numel(), self.at_heavy.numel()
+        p.a_heavy = self.a_heavy.data_ptr() if p.a_n_heavy else None
+        p.at_heavy = self.at_heavy.data_ptr() if p.at_n_heavy else None
+        self._prob = p
+        ctx = C.c_void_p()
+        N.check(self.lib.pdhg_ctx_create(C.byref(p), self.ws.data_ptr(), ws_bytes,
+                                         self.stream.cuda_stream, C.byref(ctx)))
+        self.ctx = ctx
+        self._fin = weakref.finalize(self, self.lib.pdhg_ctx_destroy, ctx)
+        self._scal = (C.c_double * (2 * N.NQ))()
+
+    # --- thin wrappers over the C ABI -------------------------------------
+    def opnorm(self, v0: np.ndarray, tol: float = 1e-4, max_iters: int = 100) -> float:
+        v0 = np.ascontiguousarray(v0, dtype=np.float64)
+        lam, its = C.c_double(), C.c_int32()
+        N.check(self.lib.pdhg_opnorm(self.ctx, v0.ctypes.data, tol, max_iters,
+                                     C.byref(lam), C.byref(its)))
+        return float(lam.value)
+
+    def reset(self):
+        N.check(self.lib.pdhg_reset(self.ctx))
+
+    def run_period(self, iters: int, iter0: int, tau_w: float, sigma_w: float, w0: float) -> int:
+        f = C.c_int64()
+        N.check(self.lib.pdhg_run_period(self.ctx, int(iters), int(iter0), float(tau_w),
+                                         float(sigma_w), float(w0), C.byref(f)))
+        return int(f.value)
+
+    def check(self, *specs: int) -> list[np.ndarray]:
+        arr = (C.c_int32 * len(specs))(*specs)
+        N.check(self.lib.pdhg_check(self.ctx, len(specs), arr, self._scal))
+        flat = np.frombuffer(self._scal, dtype=np.float64, count=len(specs) * N.NQ).copy()
+        return [flat[k * N.NQ:(k + 1) * N.NQ] for k in range(len(specs))]
+
+    def restart(self, which: int):
+        N.check(self.lib.pdhg_restart(self.ctx, which))
+
+    def save_best(self, which: int, flags: int):
+        N.check(self.lib.pdhg_save_best(self.ctx, which, flags))
+
+    def fetch(self, spec: int, want_z: bool = True):
+        x = np.empty(self.n)
+        y = np.empty(self.m)
+        z = np.empty(self.n) if want_z else None
+        N.check(self.lib.pdhg_fetch(self.ctx, spec, x.ctypes.data, y.ctypes.data,
+                                    z.ctypes.data if want_z else None))
+        return x, y, z
+
+    def spmv(self, v: np.ndarray, transpose: bool = False) -> np.ndarray:
+        """A @ v or A' @ v through the device SpMV (the 1e-12 parity gate)."""
+        torch = _torch()
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            vin = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(self.device)
+            out = torch.empty(self.n if transpose else self.m, dtype=torch.float64, device=self.device)
+            N.check(self.lib.pdhg_spmv(self.ctx, 1 if transpose else 0, vin.data_ptr(), out.data_ptr()))
+            self.stream.synchronize()
+            return out.cpu().numpy()
+
+    def time_kernel(self, which: int, reps: int, tau_w: float = 0.0, sigma_w: float = 0.0) -> float:
+        ms = C.c_double()
+        N.check(self.lib.pdhg_time_kernel(self.ctx, which, reps, tau_w, sigma_w, C.byref(ms)))
+        return float(ms.value)
+
+
+# ----------------------------------------------------------------- layout cache
+
+_cache_lock = threading.Lock()
+_cache: dict[int, tuple] = {}
+_CACHE_MAX = 4
+
+
+def _fingerprint(p):
+    A = p.A
+    data = A.data
+    step = max(1, data.size // 65536)
+    return (A.shape, int(A.nnz), data.ctypes.data, A.indices.ctypes.data, A.indptr.ctypes.data,
+            float(np.sum(data[::step])) if data.size else 0.0)
+
+
+def device_lp(p, opts: GpuOptions) -> DeviceLp:
+    """The cached device layout of StandardLp ``p`` (built on first use).
+
+    Cache entries die with ``p`` (weakref) and are rebuilt when A's storage,
+    b or c change.  A GPU-side analogue of StandardLp.A_csc (lp_core.py:133-138).
+    """
+    if not opts.cache_layout:
+        return DeviceLp(p.A, p.b, p.c, opts)
+    key = id(p)
+    fp = _fingerprint(p)
+    b = np.asarray(p.b, dtype=float)
+    c = np.asarray(p.c, dtype=float)
+    with _cache_lock:
+        ent = _cache.get(key)
+        if ent is not None:
+            ref, lay, efp, eb, ec, eopts = ent
+            if (ref() is p and efp == fp and eopts == opts and np.array_equal(eb, b)
+                    and np.array_equal(ec, c)):
+                return lay
+            _cache.pop(key, None)
+    lay = DeviceLp(p.A, b, c, opts)
+    with _cache_lock:
+        while len(_cache) >= _CACHE_MAX:
+            _cache.pop(next(iter(_cache)))
+        try:
+            ref = weakref.ref(p, lambda _r, k=key: _cache.pop(k, None))
+        except TypeError:  # not weak-referenceable: do not cache
+            return lay
+        _cache[key] = (ref, lay, fp, b.copy(), c.copy(), GpuOptions(**vars(opts)))
+    return lay
+
+
+def clear_cache() -> None:
+    with _cache_lock:
+        _cache.clear()
+
+
+# ----------------------------------------------------------------- scores
+
+
+@dataclass
+class _Score:
+    """Scalars of one scored point (what _score + residuals give, pdhg.py:154-159)."""
+
+    rp_norm: float
+    rd_norm: float
+    primal_obj: float
+    dual_obj: float
+    comp: float
+    primal_inf: float
+    dual_inf: float
+    extra: dict = field(default_factory=dict)
+
+
+def _score(q: np.ndarray) -> _Score:
+    return _Score(
+        rp_norm=math.sqrt(q[N.Q_RP2]),   # np.linalg.norm = sqrt(x.x) (lp_core.py:458)
+        rd_norm=math.sqrt(q[N.Q_RD2]),
+        primal_obj=float(q[N.Q_CX]),     # lp_core.py:441
+        dual_obj=float(q[N.Q_BY]),       # lp_core.py:442
+        comp=float(q[N.Q_XZ]),           # lp_core.py:443
+        primal_inf=float(q[N.Q_RPMAX]),  # lp_core.py:476
+        dual_inf=float(q[N.Q_RDMAX]),    # lp_core.py:477
+    )
+
+
+def _summary(T, s: _Score):
+    """violation_summary (lp_core.py:468-485) from device scalars."""
+    rel_gap = s.comp / (1.0 + abs(s.primal_obj))
+    return T.ViolationSummary(
+        primal_inf=s.primal_inf, dual_inf=s.dual_inf, rel_gap=rel_gap,
+        max_violation=max(s.primal_inf, s.dual_inf, rel_gap), comp_negative=s.comp < 0,
+    )
+
+
+def _termination(T, s: _Score, eps_rel: float, norm_b: float, norm_c: float):
+    """check_relative_termination (lp_core.py:447-465) from device scalars."""
+    if eps_rel <= 0:
+        raise ValueError("eps_rel must be positive")
+    p_lhs, d_lhs = s.rp_norm, s.rd_norm
+    p_rhs = eps_rel * (1.0 + norm_b)
+    d_rhs = eps_rel * (1.0 + norm_c)
+    gap_lhs = abs(s.primal_obj - s.dual_obj)
+    gap_rhs = eps_rel * (1.0 + abs(s.primal_obj) + abs(s.dual_obj))
+    ok = p_lhs <= p_rhs and d_lhs <= d_rhs and gap_lhs <= gap_rhs
+    return T.TerminationCheck(ok, p_lhs, p_rhs, d_lhs, d_rhs, gap_lhs, gap_rhs)
+
+
+# ----------------------------------------------------------------- run_pdhg
+
+
+def run_pdhg(p, params=None, seed: int = 0, *, gpu: GpuOptions | None = None):
+    """Iterate to the requested relative tolerance, restarting adaptively.
+
+    Same contract as hybridlp.pdhg.run_pdhg (pdhg.py:162-258): returns
+    (KktPoint, SolveStats); solver outcomes are returned in stats.status,
+    never raised; raises InvalidModelError for an empty model or matrix and
+    ZeroDivisionError when A holds only explicit zeros (pdhg.py:119).
+    """
+    T = resolve()
+    opts = gpu or GpuOptions()
+    if params is None:
+        params = T.PdhgParams()
+    m, n = p.A.shape
+    if m == 0 or n == 0:                                       # pdhg.py:175-176
+        raise T.InvalidModelError("pdhg requires a nonempty model")
+    t0 = time.monotonic()                                      # pdhg.py:177
+    if p.A.nnz == 0:                                           # pdhg.py:87-88
+        raise T.InvalidModelError("cannot estimate the norm of an empty matrix")
+    dev = device_lp(p, opts)
+    with dev.lock:
+        return _run(T, dev, p, params, seed, opts, t0)
+
+
+def _run(T, dev: DeviceLp, p, params, seed, opts, t0):
+    S = T.SolveStatus
+    b = np.asarray(p.b, dtype=float)
+    c = np.asarray(p.c, dtype=float)
+    norm_b = float(np.linalg.norm(b)) if b.size else 0.0       # lp_core.py:460
+    norm_c = float(np.linalg.norm(c)) if c.size else 0.0       # lp_core.py:461
+    eps = params.eps_rel
+
+    # initial_state (pdhg.py:117-137)
+    if opts.opnorm is not None:
+        opnorm = float(opts.opnorm)
+    else:
+        rng = np.random.default_rng(seed)                      # pdhg.py:89-91
+        v = rng.standard_normal(dev.n)
+        v /= np.linalg.norm(v)
+        opnorm = dev.opnorm(v, tol=1e-4, max_iters=100)
+    step = 1.0 / (1.05 * opnorm)                               # pdhg.py:119
+    dev.reset()
+    tau = sigma = step
+    omega = params.primal_weight_init
+    iterations = 0
+    restarts = 0
+    avg_weight = 0.0
+
+    (q0,) = dev.check(N.PT_CUR)
+    zero_sum = _summary(T, _score(q0))
+    restart_score = zero_sum.max_violation                     # pdhg.py:122,136
+    # best_pt = zero point (pdhg.py:180): a frozen snapshot
+    dev.save_best(N.PT_CUR, N.BEST_XY | N.BEST_Z)
+    best_summary = zero_sum
+    best_live_avg = False   # True: best x,y alias the running average (see module doc)
+    status = S.ITERATION_LIMIT
+    history = []
+    check_every = int(params.check_every)
+
+    while True:
+        if iterations >= params.max_kkt_passes:                # pdhg.py:185-187
+            status = S.ITERATION_LIMIT
+            break
+        if time.monotonic() - t0 > params.time_limit_s:        # pdhg.py:188-190
+            status = S.TIME_LIMIT
+            break
+        k = min(check_every - iterations % check_every, int(params.max_kkt_passes) - iterations)
+        fail = dev.run_period(k, iterations, tau / omega, sigma * omega, avg_weight)
+        if fail >= 0:                                          # pdhg.py:194-196
+            avg_weight += fail - iterations
+            iterations = fail
+            status = S.NUMERICAL_FAILURE
+            break
+        iterations += k
+        avg_weight += k
+        if iterations % check_every != 0:                      # pdhg.py:198-199
+            continue
+
+        q_cur, q_avg = dev.check(N.PT_CUR, N.PT_AVG)           # pdhg.py:201-204
+        s_cur, s_avg = _score(q_cur), _score(q_avg)
+        cur_sum, avg_sum = _summary(T, s_cur), _summary(T, s_avg)
+        cur_term = _termination(T, s_cur, eps, norm_b, norm_c)
+        avg_term = _termination(T, s_avg, eps, norm_b, norm_c)
+        rec = {
+            "iteration": iterations, "omega": omega, "restart": False,
+            "cur_max_violation": cur_sum.max_violation, "avg_max_violation": avg_sum.max_violation,
+            "cur_termination": cur_term, "avg_termination": avg_term,
+        }
+        history.append(rec)
+
+        passing = [(which, term, s) for which, term, s in
+                   ((N.PT_CUR, cur_term, cur_sum), (N.PT_AVG, avg_term, avg_sum)) if term.ok]
+        if passing:                                            # pdhg.py:214-224
+            which, term, summ = min(passing, key=lambda t: t[2].max_violation)
+            x, y, z = dev.fetch(which)
+            stats = T.SolveStats(
+                status=S.OPTIMAL, iterations=iterations, restarts=restarts,
+                wall_seconds=time.monotonic() - t0, termination=term,
+                max_violation=summ.max_violation, history=history,
+            )
+            return T.KktPoint(x, y, z), stats
+
+        if avg_sum.max_violation < cur_sum.max_violation:      # pdhg.py:226-229
+            cand, cand_sum, cand_s = N.PT_AVG, avg_sum, s_avg
+        else:
+            cand, cand_sum, cand_s = N.PT_CUR, cur_sum, s_cur
+
+        if cand_sum.max_violation < best_summary.max_violation:  # pdhg.py:231-232
+            best_summary = cand_sum
+            if cand == N.PT_CUR:
+                dev.save_best(N.PT_CUR, N.BEST_XY | N.BEST_Z)
+                best_live_avg = False
+            else:
+                dev.save_best(N.PT_AVG, N.BEST_Z)
+                best_live_avg = True
+
+        if cand_sum.max_violation <= params.restart_beta * restart_score:  # pdhg.py:234-247
+            if best_live_avg:  # the average array best_pt aliases is rebound: freeze it
+                dev.save_best(N.PT_AVG, N.BEST_XY)
+                best_live_avg = False
+            dev.restart(cand)
+            avg_weight = 0.0
+            rp, rd = cand_s.rp_norm, cand_s.rd_norm
+            if rp > 0.0 and rd > 0.0:
+                omega = float(np.clip(rp / rd, *_WEIGHT_CLIP))
+            restart_score = cand_sum.max_violation
+            restarts += 1
+            rec["restart"] = True
+
+    # failure exit (pdhg.py:249-258): best point, re-checked with its own z
+    spec = (N.PT_AVG if best_live_avg else N.PT_BEST) | N.SPEC_BEST_Z
+    (q_best,) = dev.check(spec)
+    termination = _termination(T, _score(q_best), eps, norm_b, norm_c)
+    x, y, z = dev.fetch(spec)
+    stats = T.SolveStats(
+        status=status, iterations=iterations, restarts=restarts,
+        wall_seconds=time.monotonic() - t0, termination=termination,
+        max_violation=best_summary.max_violation, history=history,
+    )
+    return T.KktPoint(x, y, z), stats
+
+
+def estimate_opnorm(A, seed: int = 0, tol: float = 1e-4, max_iters: int = 100,
+                    *, gpu: GpuOptions | None = None) -> float:
+    """Device power iteration with the reference's start vector (pdhg.py:80-109)."""
+    T = resolve()
+    m, n = A.shape
+    if m == 0 or n == 0 or A.nnz == 0:
+        raise T.InvalidModelError("cannot estimate the norm of an empty matrix")
+
+    class _P:  # minimal StandardLp stand-in
+        pass
+
+    q = _P()
+    q.A, q.b, q.c = A, np.zeros(m), np.zeros(n)
+    dev = DeviceLp(A, q.b, q.c, gpu or GpuOptions())
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    return dev.opnorm(v, tol=tol, max_iters=max_iters)
