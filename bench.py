@@ -1,0 +1,366 @@
+"""Benchmark: PDHG iterations/s on BASELINE config 4 (5M x 10M, 200M nnz, fp64).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--scale S] [--ttk]
+
+A *step* is one PDHG period: check_every=64 iterations (pdhg_step,
+pdhg.py:140-151) followed by the KKT scoring of the current and averaged
+iterates (pdhg.py:201-204) -- the unit in which run_pdhg talks to the device.
+``value`` = iterations/s over K timed steps with the LP resident in HBM
+(CUDA events on the engine's stream, max over ranks).  ``e2e`` = the same
+metric through the public drop-in call ``run_pdhg(p, params)`` on host
+arrays: layout upload + device transpose + power iteration + K*64
+iterations + result download, all inside the timed region.
+
+``--impl reference`` times the CPU oracle (oracle/pdhg_port.py: the
+reference's numpy/scipy run_pdhg restated, pinned bit-for-bit against the
+reference in tests/test_oracle_golden.py) on the same instance: per-step
+samples of pdhg_step plus one scored check amortised over 64 iterations.
+The reference path is single-threaded (scipy csr_matvec); BLAS is pinned to
+one thread.
+
+Inputs (4.8 GB of matrix) are far larger than the 126 MB L2, so no L2 flush
+is needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "PDHG iters/s and time-to-1e-4 rel KKT; achieved HBM GB/s vs B200 peak"
+UNIT = "iter/s"
+CHECK_EVERY = 64
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def _peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return None
+
+
+def _instance(scale: float, seed: int):
+    from paper_2603_03150_b200.instances import config4
+
+    return config4(scale=scale, seed=seed)
+
+
+def algorithmic_bytes(m: int, n: int, nnz: int) -> dict:
+    """Bytes one PDHG iteration must move, fp64 values, int32 indices.
+
+    primal step (rows of A'): 12 nnz + 4(n+1) offsets + 8m (y gather, compulsory)
+                              + 24n (c, x, avg_x) + 24n (write x, xe, avg_x)
+    dual step   (rows of A):  12 nnz + 4(m+1) offsets + 8n (xe gather, compulsory)
+                              + 24m (b, y, avg_y) + 16m (write y, avg_y)
+    total = 24 nnz + 60 n + 52 m (+8).
+    check (every 64): A[x,avg_x] + A'[y,avg_y] = 24 nnz + 44 n + 44 m.
+    """
+    primal = 12 * nnz + 4 * (n + 1) + 8 * m + 48 * n
+    dual = 12 * nnz + 4 * (m + 1) + 8 * n + 40 * m
+    check = 24 * nnz + 44 * n + 44 * m
+    return {"primal": primal, "dual": dual, "iter": primal + dual, "check": check}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/bench_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self) -> dict:
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = [r.split(",") for r in self.path.read_text().strip().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) < 9:
+                continue
+            for k, nm in enumerate(names):
+                if r[5 + k].strip().lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_sample(inst, steps: int = 3) -> dict:
+    """Oracle (reference numpy/scipy path, 1 thread) per-iteration time on `inst`."""
+    import numpy as np
+
+    import oracle
+    from oracle.pdhg_port import KktPoint, Model, PdhgState, _score, check_relative_termination
+
+    p = Model(inst.A, inst.b, inst.c)
+    t = time.perf_counter()
+    p.A_csc  # the reference builds the CSC copy lazily on first at_y (lp_core.py:133-138)
+    t_csc = time.perf_counter() - t
+    st = PdhgState(x=np.zeros(p.n), y=np.zeros(p.m), avg_x=np.zeros(p.n), avg_y=np.zeros(p.m),
+                   avg_weight=0.0, tau=0.5 / 40.0, sigma=0.5 / 40.0, omega=1.0, iterations=0,
+                   restarts=0, restart_x=None, restart_y=None, restart_score=1.0)
+    oracle.pdhg_step(st, p)  # warm
+    t = time.perf_counter()
+    for _ in range(steps):
+        oracle.pdhg_step(st, p)
+    t_step = (time.perf_counter() - t) / steps
+    t = time.perf_counter()
+    cur_pt, _, _ = _score(p, st.x, st.y)
+    avg_pt, _, _ = _score(p, st.avg_x, st.avg_y)
+    check_relative_termination(p, cur_pt, 1e-4)
+    check_relative_termination(p, avg_pt, 1e-4)
+    t_check = time.perf_counter() - t
+    per_iter = t_step + t_check / CHECK_EVERY
+    return {"per_iter_s": per_iter, "step_s": t_step, "check_s": t_check, "tocsc_s": t_csc,
+            "steps": steps}
+
+
+def run_reference(args):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return 0
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    inst = _instance(args.scale, args.seed)
+    samples = []
+    import numpy as np
+
+    import oracle
+    from oracle.pdhg_port import Model, PdhgState, _score, check_relative_termination
+
+    p = Model(inst.A, inst.b, inst.c)
+    p.A_csc
+    st = PdhgState(x=np.zeros(p.n), y=np.zeros(p.m), avg_x=np.zeros(p.n), avg_y=np.zeros(p.m),
+                   avg_weight=0.0, tau=0.5 / 40.0, sigma=0.5 / 40.0, omega=1.0, iterations=0,
+                   restarts=0, restart_x=None, restart_y=None, restart_score=1.0)
+    for _ in range(args.warmup):
+        oracle.pdhg_step(st, p)
+    t = time.perf_counter()
+    cur_pt, _, _ = _score(p, st.x, st.y)
+    avg_pt, _, _ = _score(p, st.avg_x, st.avg_y)
+    check_relative_termination(p, cur_pt, 1e-4)
+    check_relative_termination(p, avg_pt, 1e-4)
+    t_check = time.perf_counter() - t
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        oracle.pdhg_step(st, p)
+        samples.append(time.perf_counter() - t)
+    per_iter = sum(samples) / len(samples) + t_check / CHECK_EVERY
+    value = 1.0 / per_iter
+    sample = (f"{args.steps} pdhg_step calls + 1 scored check (2 points, amortised over "
+              f"{CHECK_EVERY} iterations) of the oracle on config4 scale={args.scale}; "
+              "scipy csr_matvec single-threaded, OPENBLAS_NUM_THREADS=1")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_iter * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"config4 (m={inst.m}, n={inst.n}, nnz={inst.nnz}) PDHG iteration",
+                   "scale": args.scale, "seed": args.seed},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_s_samples": samples, "check_s": t_check,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = _env_rank()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    import paper_2603_03150_b200 as eng
+    from paper_2603_03150_b200 import _native as N
+
+    inst = _instance(args.scale, args.seed + rank)  # replicas: one LP per rank (no sharding yet)
+    T = eng.types()
+    m, n, nnz = inst.m, inst.n, inst.nnz
+    ab = algorithmic_bytes(m, n, nnz)
+
+    # ---- device-resident timing: K periods of 64 iterations + check
+    t_setup = time.perf_counter()
+    dev = eng.DeviceLp(inst.A, inst.b, inst.c, eng.GpuOptions(cache_layout=False))
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    rng = np.random.default_rng(0)
+    v = rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    lam = dev.opnorm(v)
+    step = 1.0 / (1.05 * lam)
+    dev.reset()
+    it = 0
+    for _ in range(args.warmup):
+        dev.run_period(CHECK_EVERY, it, step, step, float(it))
+        dev.check(N.PT_CUR, N.PT_AVG)
+        it += CHECK_EVERY
+    s = dev.stream
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(s)
+        for _ in range(args.steps):
+            fail = dev.run_period(CHECK_EVERY, it, step, step, float(it))
+            dev.check(N.PT_CUR, N.PT_AVG)
+            it += CHECK_EVERY
+        ev1.record(s)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    iters = args.steps * CHECK_EVERY
+    value = world * iters / (ms / 1e3)
+    ms_per_step = ms / args.steps
+
+    # ---- per-kernel timing for the roofline (CUDA events on the engine stream)
+    reps = 20
+    tk = {"primal": dev.time_kernel(0, reps, step, step), "dual": dev.time_kernel(1, reps, step, step)}
+    top = max(tk, key=tk.get)
+    peaks = _peaks()
+    peak = peaks["hbm_gbs"] if peaks else 6650.0
+    achieved = ab[top] / (tk[top] * 1e-3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(top)
+        except Exception:
+            traffic = None
+    iter_ms = ms_per_step / CHECK_EVERY
+    roofline = {"bound": "hbm", "kernel": f"k_step<{'primal' if top == 'primal' else 'dual'}>",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
+                "kernels_ms": tk, "algorithmic_bytes": ab,
+                "iteration_gbs": (ab["iter"] + ab["check"] / CHECK_EVERY) / (iter_ms * 1e-3) / 1e9}
+    del dev
+    torch.cuda.empty_cache()
+
+    # ---- e2e through the public drop-in call, host arrays in, host arrays out
+    K = args.steps
+    params = T.PdhgParams(eps_rel=1e-12, max_kkt_passes=K * CHECK_EVERY)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    t0 = time.perf_counter()
+    pt, st = eng.run_pdhg(inst, params, gpu=eng.GpuOptions(cache_layout=False))
+    e1.record()
+    torch.cuda.synchronize()
+    wall_e2e = time.perf_counter() - t0
+    e2e_ms = e0.elapsed_time(e1)
+    e2e_value = world * st.iterations / (e2e_ms / 1e3)
+    h2d = 12 * nnz + 4 * (m + 1) + 8 * (m + n) + 8 * n
+    d2h = 8 * (2 * n + m)
+
+    out = None
+    if args.ttk:
+        pt2, st2 = eng.run_pdhg(inst, T.PdhgParams(eps_rel=1e-4, time_limit_s=args.ttk_limit))
+        out = {"status": st2.status.value, "iterations": st2.iterations, "restarts": st2.restarts,
+               "wall_s": st2.wall_seconds}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+        cs = cpu_sample(inst, steps=args.cpu_steps)
+        cpu = {"value": 1.0 / cs["per_iter_s"], "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": (f"oracle (reference numpy/scipy path) on the same config4 instance: "
+                          f"{cs['steps']} pdhg_step calls ({cs['step_s']:.3f} s each) + one scored "
+                          f"check ({cs['check_s']:.2f} s) amortised over 64 iterations; 1 thread"),
+               "detail": cs}
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config4 (m={m}, n={n}, nnz={nnz}) PDHG period = 64 iterations + KKT check",
+                   "scale": args.scale, "seed": args.seed,
+                   "l2": "no flush: 4.8 GB matrix > 126 MB L2 (inputs larger than L2)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+        "roofline": roofline,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / K,
+                "d2h_bytes_per_step": d2h / K, "iterations": st.iterations,
+                "wall_s": wall_e2e, "note": "run_pdhg(StandardLp on host) incl. upload, transpose, opnorm"},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "gpu_launches": args.steps * (2 * CHECK_EVERY + 3),
+        "setup_s": t_setup,
+        "time_to_1e4": out,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--seed", type=int, default=4)
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ttk", action="store_true", help="also run to eps_rel=1e-4 (time-to-1e-4)")
+    ap.add_argument("--ttk-limit", type=float, default=300.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
