@@ -61,6 +61,26 @@ extern "C" {
  * lp_core.py:140-142).  Rows longer than `heavy_threshold` are listed in
  * the heavy-row arrays and get a whole thread block each.
  */
+/*
+ * Panel-staged rows (PSR) layout of one operator (A or A'), built on the
+ * device by pdhg_psr_plan + pdhg_psr_build (see csrc/psr.cuh for the
+ * format).  Used by the step kernels when the host decides it pays
+ * (enough entries in dense column panels); NULL = CSR-vector kernels.
+ */
+typedef struct pdhg_psr {
+  int32_t rows, cols, R, W, nblk, ntiles;
+  int64_t nent;
+  const int32_t* blk_tile_ptr;  /* nblk+1 */
+  const int32_t* blk_warp_row;  /* nblk*(PDHG_PSR_WARPS+1) */
+  const int32_t* tile_bin;      /* ntiles */
+  const int32_t* tile_ent;      /* ntiles*(PDHG_PSR_WARPS+1) */
+  const double* val;            /* nent */
+  const uint32_t* meta;         /* nent */
+  const int32_t* col;           /* nent */
+  const uint8_t* heavy;         /* rows */
+} pdhg_psr;
+#define PDHG_PSR_WARPS 32
+
 typedef struct pdhg_problem {
   int32_t m, n;
   int64_t nnz;
@@ -78,6 +98,9 @@ typedef struct pdhg_problem {
   int32_t a_n_heavy, at_n_heavy;
   const int32_t* a_heavy;  /* device list of heavy rows of A */
   const int32_t* at_heavy; /* device list of heavy rows of A' */
+  const pdhg_psr* a_psr;   /* optional PSR layout of A  (dual step)   */
+  const pdhg_psr* at_psr;  /* optional PSR layout of A' (primal step) */
+  int32_t l2_persist;      /* 1: pin the gathered vector in L2 (persisting access-policy window) */
 } pdhg_problem;
 
 typedef struct pdhg_ctx pdhg_ctx;
@@ -151,6 +174,25 @@ int pdhg_transpose_csr(int32_t m, int32_t n, int64_t nnz, const int32_t* a_ptr,
                        const int32_t* a_col, const double* a_val, int32_t* at_ptr,
                        int32_t* at_col, double* at_val, void* tmp, size_t tmp_bytes,
                        void* stream);
+
+/* PSR layout build (device).  pdhg_psr_plan fixes the row-block size R and
+ * panel width W from the shape, counts entries per (row block, panel),
+ * marks panels with >= min_staged entries as staged and returns the sizes
+ * the caller must allocate: nblk, ntiles, and the number of entries that
+ * land in staged panels (*staged_out) and in the layout (*nent_out; heavy
+ * rows -- longer than heavy_threshold -- are left to the CSR heavy path).
+ * tmp (pdhg_psr_tmp_bytes) carries the plan into pdhg_psr_build and must
+ * not be touched in between. */
+size_t pdhg_psr_tmp_bytes(int32_t rows, int32_t cols, int64_t nnz);
+int pdhg_psr_plan(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, const int32_t* col,
+                  int32_t heavy_threshold, int32_t min_staged, void* tmp, size_t tmp_bytes,
+                  void* stream, int32_t* R_out, int32_t* W_out, int32_t* nblk_out,
+                  int32_t* ntiles_out, int64_t* staged_out, int64_t* nent_out);
+int pdhg_psr_build(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, const int32_t* col,
+                   const double* val, int32_t heavy_threshold, void* tmp, size_t tmp_bytes,
+                   void* stream, int32_t* blk_tile_ptr, int32_t* blk_warp_row, int32_t* tile_bin,
+                   int32_t* tile_ent, double* val_out, uint32_t* meta_out, int32_t* col_out,
+                   uint8_t* heavy_out);
 
 #ifdef __cplusplus
 }

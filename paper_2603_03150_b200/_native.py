@@ -25,7 +25,23 @@ EXPORTS = (
     "pdhg_ctx_destroy", "pdhg_spmv", "pdhg_opnorm", "pdhg_reset", "pdhg_run_period",
     "pdhg_check", "pdhg_restart", "pdhg_save_best", "pdhg_fetch", "pdhg_time_kernel",
     "pdhg_transpose_tmp_bytes", "pdhg_transpose_csr",
+    "pdhg_psr_tmp_bytes", "pdhg_psr_plan", "pdhg_psr_build",
 )
+
+
+PSR_WARPS = 32
+
+
+class Psr(C.Structure):
+    """struct pdhg_psr (panel-staged rows layout of one operator)."""
+
+    _fields_ = [
+        ("rows", C.c_int32), ("cols", C.c_int32), ("R", C.c_int32), ("W", C.c_int32),
+        ("nblk", C.c_int32), ("ntiles", C.c_int32), ("nent", C.c_int64),
+        ("blk_tile_ptr", C.c_void_p), ("blk_warp_row", C.c_void_p), ("tile_bin", C.c_void_p),
+        ("tile_ent", C.c_void_p), ("val", C.c_void_p), ("meta", C.c_void_p), ("col", C.c_void_p),
+        ("heavy", C.c_void_p),
+    ]
 
 
 class Problem(C.Structure):
@@ -39,6 +55,8 @@ class Problem(C.Structure):
         ("a_lanes", C.c_int32), ("at_lanes", C.c_int32), ("heavy_threshold", C.c_int32),
         ("a_n_heavy", C.c_int32), ("at_n_heavy", C.c_int32),
         ("a_heavy", C.c_void_p), ("at_heavy", C.c_void_p),
+        ("a_psr", C.POINTER(Psr)), ("at_psr", C.POINTER(Psr)),
+        ("l2_persist", C.c_int32),
     ]
 
 
@@ -87,6 +105,11 @@ def load():
         _sig(lib, "pdhg_time_kernel", C.c_int, vp, i32, i32, dbl, dbl, P(dbl))
         _sig(lib, "pdhg_transpose_tmp_bytes", szt, i64, i32, i32)
         _sig(lib, "pdhg_transpose_csr", C.c_int, i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, szt, vp)
+        _sig(lib, "pdhg_psr_tmp_bytes", szt, i32, i32, i64)
+        _sig(lib, "pdhg_psr_plan", C.c_int, i32, i32, i64, vp, vp, i32, i32, vp, szt, vp,
+             P(i32), P(i32), P(i32), P(i32), P(i64), P(i64))
+        _sig(lib, "pdhg_psr_build", C.c_int, i32, i32, i64, vp, vp, vp, i32, vp, szt, vp,
+             vp, vp, vp, vp, vp, vp, vp, vp)
         if lib.pdhg_abi_version() != 1:
             raise NativeError("libpdhg_b200.so ABI version mismatch")
         _lib = lib

@@ -23,6 +23,7 @@
 //   k_reduce        fixed-order combine of the per-block partials.
 //   k_spmv / k_div  power iteration (pdhg.py:80-109) and the 1e-12 SpMV gate.
 #include "../../include/pdhg_b200.h"
+#include "psr.cuh"
 
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
@@ -44,6 +45,17 @@ int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
+
+}  // namespace
+
+namespace pdhg_internal {
+int set_error(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+}  // namespace pdhg_internal
+
+namespace {
 
 #define CUDA_TRY(expr)                                                                \
   do {                                                                                \
@@ -214,6 +226,53 @@ __global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
   if (valid && lane == 0) {
     if (PRIMAL) primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
     else dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
+  }
+}
+
+// PSR step: persistent CTAs (one per SM) walk row blocks; the SpMV lands in
+// shared memory (psr::block_spmv), then the same epilogue as k_step.
+struct PsrStepArgs {
+  psr::Layout L;
+  const double* __restrict__ gather;
+  const double* __restrict__ cb;
+  double* x;
+  double* xe;
+  double* xbar;
+  StepParams* P;
+};
+
+template <bool PRIMAL>
+__global__ void __launch_bounds__(psr::kThreads, 1) k_step_psr(PsrStepArgs a, int j_in_period) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t bars[2];
+  StepParams* P = a.P;
+  const long long iter = P->iter0 + j_in_period + 1;
+  if (P->fail_iter < iter) return;
+  const double w = P->w0 + (double)(j_in_period + 1);
+  const double step = PRIMAL ? P->tau_w : P->sigma_w;
+  const int tid = threadIdx.x;
+  double* panels = reinterpret_cast<double*>(smem_raw);
+  double* acc = panels + 2 * a.L.W;
+  double* prodw = acc + a.L.R + (tid >> 5) * 32;
+  if (tid == 0) {
+    psr::mbar_init(&bars[0], 1);
+    psr::mbar_init(&bars[1], 1);
+    psr::fence_mbar_init();
+  }
+  __syncthreads();
+  psr::Pipe pp{bars, {0u, 0u}};
+  const double* gx[1] = {a.gather};
+  for (int b = blockIdx.x; b < a.L.nblk; b += gridDim.x) {
+    psr::block_spmv<1>(a.L, b, gx, panels, acc, prodw, pp);
+    const int row0 = b * a.L.R;
+    const int rows_b = min(a.L.R, a.L.rows - row0);
+    for (int r = tid; r < rows_b; r += psr::kThreads) {
+      const int row = row0 + r;
+      if (a.L.heavy[row]) continue;
+      if (PRIMAL) primal_epi(row, acc[r], a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
+      else dual_epi(row, acc[r], a.cb, a.x, a.xbar, step, w, iter, P);
+    }
+    __syncthreads();
   }
 }
 
@@ -539,6 +598,10 @@ struct pdhg_ctx {
   StepParams* P_host;
   double* scal_host;
   std::map<int, cudaGraphExec_t> graphs;
+  bool has_psr[2];     // [0] = A (dual), [1] = A' (primal)
+  psr::Layout psr_l[2];
+  size_t psr_smem[2];
+  int l2_persist, l2_maxwin;
 };
 
 namespace {
@@ -549,20 +612,60 @@ struct Carve {
   template <class T>
   T* take(size_t count) {
     T* p = reinterpret_cast<T*>(base + off);
-    off += align_up(count * sizeof(T));
+    off += align_up(count * sizeof(T) + 256);  // +256: bulk copies round up to 16 B
     return p;
   }
 };
 
 size_t carve_bytes(int32_t m, int32_t n) {
   size_t b = 0;
-  b += 7 * align_up((size_t)n * 8);
-  b += 4 * align_up((size_t)m * 8);
-  b += align_up((size_t)kCheckBlocks * kMaxQ * 8);
-  b += align_up(64 * 8);
-  b += align_up(sizeof(StepParams));
+  b += 7 * align_up((size_t)n * 8 + 256);
+  b += 4 * align_up((size_t)m * 8 + 256);
+  b += align_up((size_t)kCheckBlocks * kMaxQ * 8 + 256);
+  b += align_up(64 * 8 + 256);
+  b += align_up(sizeof(StepParams) + 256);
   return b;
 }
+
+cudaAccessPolicyWindow l2_window(const pdhg_ctx* c, const void* base, size_t bytes) {
+  cudaAccessPolicyWindow w{};
+  if (c->l2_persist <= 0 || c->l2_maxwin <= 0) return w;
+  w.base_ptr = const_cast<void*>(base);
+  w.num_bytes = std::min(bytes, (size_t)c->l2_maxwin);
+  w.hitRatio = (float)std::min(1.0, (double)c->l2_persist / (double)w.num_bytes);
+  w.hitProp = cudaAccessPropertyPersisting;
+  w.missProp = cudaAccessPropertyStreaming;
+  return w;
+}
+
+template <class K, class... Args>
+int launch_ex(const pdhg_ctx* c, K kernel, dim3 grid, dim3 block, size_t smem, const void* win_base,
+              size_t win_bytes, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  cfg.attrs = attr;
+  cfg.numAttrs = 0;
+  if (win_base && c->l2_persist > 0) {
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow = l2_window(c, win_base, win_bytes);
+    cfg.numAttrs = 1;
+  }
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, args...));
+  return 0;
+}
+
+template <int V>
+struct StepLaunchEx {
+  static int run(const pdhg_ctx* c, bool primal, const StepArgs& a, int j, int grid, size_t win) {
+    if (grid == 0) return 0;
+    if (primal) return launch_ex(c, k_step<V, true>, dim3(grid), dim3(kBlock), 0, a.gather, win, a, j);
+    return launch_ex(c, k_step<V, false>, dim3(grid), dim3(kBlock), 0, a.gather, win, a, j);
+  }
+};
 
 int launch_step(pdhg_ctx* c, bool primal, int j) {
   StepArgs a;
@@ -572,7 +675,21 @@ int launch_step(pdhg_ctx* c, bool primal, int j) {
     a.rs = c->A; a.gather = c->xe; a.cb = c->prob.b; a.x = c->y; a.xe = nullptr; a.xbar = c->ybar;
   }
   a.P = c->P;
-  return dispatch_lanes<StepLaunch>(primal ? c->at_lanes : c->a_lanes, primal, a, j, c->stream);
+  const size_t win = (size_t)(primal ? c->prob.m : c->prob.n) * 8;
+  const int lanes = primal ? c->at_lanes : c->a_lanes;
+  const int k = primal ? 1 : 0;
+  if (c->has_psr[k]) {
+    PsrStepArgs pa{c->psr_l[k], a.gather, a.cb, a.x, a.xe, a.xbar, a.P};
+    const int grid = std::min(c->psr_l[k].nblk, 148);
+    int rc = primal ? launch_ex(c, k_step_psr<true>, dim3(grid), dim3(psr::kThreads), c->psr_smem[k],
+                                a.gather, win, pa, j)
+                    : launch_ex(c, k_step_psr<false>, dim3(grid), dim3(psr::kThreads), c->psr_smem[k],
+                                a.gather, win, pa, j);
+    if (rc) return rc;
+    // heavy rows: block per row through the CSR kernel (grid = n_heavy => no light rows)
+    return dispatch_lanes<StepLaunchEx>(lanes, c, primal, a, j, a.rs.n_heavy, win);
+  }
+  return dispatch_lanes<StepLaunchEx>(lanes, c, primal, a, j, grid_rows(a.rs, lanes), win);
 }
 
 int spmv(pdhg_ctx* c, bool transpose, const double* in, double* out) {
@@ -634,6 +751,35 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->partials = cv.take<double>((size_t)kCheckBlocks * kMaxQ);
   c->scalars = cv.take<double>(64);
   c->P = cv.take<StepParams>(1);
+  for (int k = 0; k < 2; ++k) {
+    const pdhg_psr* q = k == 0 ? prob->a_psr : prob->at_psr;
+    c->has_psr[k] = q != nullptr;
+    if (q) {
+      if (q->R > psr::kMaxRows || q->W != psr::kPanel || !q->heavy) {
+        delete c;
+        return fail(PDHG_ERR_ARG, "psr layout geometry not supported");
+      }
+      c->psr_l[k] = psr::Layout{q->rows, q->cols, q->R, q->W, q->nblk, q->ntiles, q->blk_tile_ptr,
+                                q->blk_warp_row, q->tile_bin, q->tile_ent, q->val, q->meta, q->col,
+                                q->heavy};
+      c->psr_smem[k] = psr::smem_bytes(q->R, q->W);
+    }
+  }
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int maxp = 0, maxw = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    c->l2_persist = prob->l2_persist ? maxp : 0;
+    c->l2_maxwin = maxw;
+    if (c->l2_persist > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp);
+    cudaGetLastError();
+    const size_t sm = psr::smem_bytes(psr::kMaxRows, psr::kPanel);
+    cudaFuncSetAttribute(k_step_psr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_step_psr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaGetLastError();
+  }
   cudaError_t e1 = cudaMallocHost(&c->P_host, sizeof(StepParams));
   cudaError_t e2 = cudaMallocHost(&c->scal_host, 64 * sizeof(double));
   if (e1 != cudaSuccess || e2 != cudaSuccess) {

@@ -43,6 +43,11 @@ class GpuOptions:
     heavy_threshold: rows longer than this get a whole thread block.
     opnorm:          override the power-iteration estimate (parity fallback).
     cache_layout:    keep the device layout of a model for repeated solves.
+    psr:             "auto" | "on" | "off" -- panel-staged rows layout for the step
+                     kernels (csrc/psr.cuh); auto uses it when >= psr_min_fraction of
+                     the entries fall in staged panels and the operator has enough rows.
+    psr_min_staged:  entries a (row block, panel) needs to be staged in shared memory.
+    l2_persist:      pin the gathered vector in L2 with a persisting access window.
     """
 
     device: int | None = None
@@ -51,6 +56,11 @@ class GpuOptions:
     heavy_threshold: int = 1024
     opnorm: float | None = None
     cache_layout: bool = True
+    psr: str = "auto"
+    psr_min_staged: int = 1024
+    psr_min_fraction: float = 0.3
+    psr_min_rows: int = 148 * 256
+    l2_persist: bool = True
 
 
 def _torch():
@@ -114,6 +124,11 @@ class DeviceLp:
                 H = int(opts.heavy_threshold)
                 self.a_heavy = torch.nonzero((self.a_ptr[1:] - self.a_ptr[:-1]) > H).flatten().to(torch.int32)
                 self.at_heavy = torch.nonzero((self.at_ptr[1:] - self.at_ptr[:-1]) > H).flatten().to(torch.int32)
+                self.psr_info = {}
+                self._psr = {}
+                for key, rows, cols, ptr, col, val in (("A", m, n, self.a_ptr, self.a_col, self.a_val),
+                                                      ("At", n, m, self.at_ptr, self.at_col, self.at_val)):
+                    self._psr[key] = self._build_psr(torch, dev, key, rows, cols, ptr, col, val, H, opts)
                 ws_bytes = self.lib.pdhg_workspace_bytes(m, n)
                 self.ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
                 self.stream.synchronize()
@@ -127,6 +142,9 @@ class DeviceLp:
         p.a_n_heavy, p.at_n_heavy = self.a_heavy.numel(), self.at_heavy.numel()
         p.a_heavy = self.a_heavy.data_ptr() if p.a_n_heavy else None
         p.at_heavy = self.at_heavy.data_ptr() if p.at_n_heavy else None
+        p.a_psr = C.pointer(self._psr["A"][0]) if self._psr["A"] else None
+        p.at_psr = C.pointer(self._psr["At"][0]) if self._psr["At"] else None
+        p.l2_persist = 1 if opts.l2_persist else 0
         self._prob = p
         ctx = C.c_void_p()
         N.check(self.lib.pdhg_ctx_create(C.byref(p), self.ws.data_ptr(), ws_bytes,
@@ -134,6 +152,49 @@ class DeviceLp:
         self.ctx = ctx
         self._fin = weakref.finalize(self, self.lib.pdhg_ctx_destroy, ctx)
         self._scal = (C.c_double * (2 * N.NQ))()
+
+    def _build_psr(self, torch, dev, key, rows, cols, ptr, col, val, H, opts):
+        """Plan + build the PSR layout of one operator on the device (or None)."""
+        if opts.psr == "off" or (opts.psr == "auto" and rows < opts.psr_min_rows):
+            return None
+        lib = self.lib
+        nnz = self.nnz
+        sptr = self.stream.cuda_stream
+        tb = lib.pdhg_psr_tmp_bytes(rows, cols, nnz)
+        tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=dev)
+        R, W, nblk, ntiles = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        staged, nent = C.c_int64(), C.c_int64()
+        N.check(lib.pdhg_psr_plan(rows, cols, nnz, ptr.data_ptr(), col.data_ptr(), H,
+                                  int(opts.psr_min_staged), tmp.data_ptr(), tb, sptr,
+                                  C.byref(R), C.byref(W), C.byref(nblk), C.byref(ntiles),
+                                  C.byref(staged), C.byref(nent)))
+        frac = staged.value / max(1, nnz)
+        self.psr_info[key] = {"R": R.value, "W": W.value, "nblk": nblk.value, "ntiles": ntiles.value,
+                              "staged_fraction": frac, "nent": nent.value}
+        if opts.psr == "auto" and frac < opts.psr_min_fraction:
+            return None
+        i32 = torch.int32
+        bufs = {
+            "blk_tile_ptr": torch.empty(nblk.value + 1, dtype=i32, device=dev),
+            "blk_warp_row": torch.empty(nblk.value * (N.PSR_WARPS + 1), dtype=i32, device=dev),
+            "tile_bin": torch.empty(max(1, ntiles.value), dtype=i32, device=dev),
+            "tile_ent": torch.empty(max(1, ntiles.value) * (N.PSR_WARPS + 1), dtype=i32, device=dev),
+            "val": torch.empty(max(1, nnz), dtype=torch.float64, device=dev),
+            "meta": torch.empty(max(1, nnz), dtype=i32, device=dev),
+            "col": torch.empty(max(1, nnz), dtype=i32, device=dev),
+            "heavy": torch.empty(rows, dtype=torch.uint8, device=dev),
+        }
+        N.check(lib.pdhg_psr_build(
+            rows, cols, nnz, ptr.data_ptr(), col.data_ptr(), val.data_ptr(), H, tmp.data_ptr(), tb,
+            sptr, *(bufs[k].data_ptr() for k in ("blk_tile_ptr", "blk_warp_row", "tile_bin",
+                                                 "tile_ent", "val", "meta", "col", "heavy"))))
+        d = N.Psr()
+        d.rows, d.cols, d.R, d.W = rows, cols, R.value, W.value
+        d.nblk, d.ntiles, d.nent = nblk.value, ntiles.value, nent.value
+        for k in ("blk_tile_ptr", "blk_warp_row", "tile_bin", "tile_ent", "val", "meta", "col", "heavy"):
+            setattr(d, k, bufs[k].data_ptr())
+        self.psr_info[key]["used"] = True
+        return (d, bufs)
 
     # --- thin wrappers over the C ABI -------------------------------------
     def opnorm(self, v0: np.ndarray, tol: float = 1e-4, max_iters: int = 100) -> float:

@@ -29,6 +29,19 @@ def eng():
     return eng
 
 
+# the step kernels have three layouts: CSR-vector, and PSR with every entry
+# staged in shared-memory panels or every entry gathered from global memory
+LAYOUTS = {
+    "csr": dict(psr="off"),
+    "psr_staged": dict(psr="on", psr_min_staged=1),
+    "psr_remote": dict(psr="on", psr_min_staged=10**9),
+}
+
+
+def _opts(eng, layout):
+    return eng.GpuOptions(**LAYOUTS[layout])
+
+
 def _rel(a, b):
     a = np.asarray(a, dtype=float)
     b = np.asarray(b, dtype=float)
@@ -52,8 +65,9 @@ def test_opnorm_matches_reference(eng, name):
     assert lam == pytest.approx(float(gm.g["opnorm_seed0"]), rel=1e-12)
 
 
+@pytest.mark.parametrize("layout", sorted(LAYOUTS))
 @pytest.mark.parametrize("name", GOLDEN_NAMES)
-def test_first_100_iterates_1e9(eng, name):
+def test_first_100_iterates_1e9(eng, name, layout):
     """Run k iterations on the GPU for each captured k and compare the state.
 
     max_kkt_passes=k with eps=1e-12 stops right after step k; the returned
@@ -70,8 +84,11 @@ def test_first_100_iterates_1e9(eng, name):
         # a check at k itself would already have restarted; the reference
         # capture is taken right after the step (before the check)
         ce = 10**6 if k % 64 == 0 else 64
-        eng.run_pdhg(gm, _params(eng, eps_rel=1e-12, max_kkt_passes=k, check_every=ce))
-        dev = eng.device_lp(gm, eng.GpuOptions())
+        opts = _opts(eng, layout)
+        eng.run_pdhg(gm, _params(eng, eps_rel=1e-12, max_kkt_passes=k, check_every=ce), gpu=opts)
+        dev = eng.device_lp(gm, opts)
+        if layout != "csr":
+            assert dev.psr_info["A"].get("used") and dev.psr_info["At"].get("used")
         x, y, _ = dev.fetch(N.PT_CUR, want_z=False)
         ax, ay, _ = dev.fetch(N.PT_AVG, want_z=False)
         assert _rel(x, g["it_x"][j]) <= ITER_RTOL, (name, k)
@@ -84,13 +101,14 @@ def _params(eng, **kw):
     return eng.types().PdhgParams(**kw)
 
 
+@pytest.mark.parametrize("layout", sorted(LAYOUTS))
 @pytest.mark.parametrize("name", GOLDEN_NAMES)
 @pytest.mark.parametrize("tag,eps,limit", [("e4", 1e-4, 200_000), ("e6", 1e-6, 200_000),
                                            ("lim128", 1e-12, 128), ("lim200", 1e-12, 200)])
-def test_full_run_parity(eng, name, tag, eps, limit):
+def test_full_run_parity(eng, name, tag, eps, limit, layout):
     gm = load_golden(name)
     r = gm.run(tag)
-    pt, st = eng.run_pdhg(gm, _params(eng, eps_rel=eps, max_kkt_passes=limit))
+    pt, st = eng.run_pdhg(gm, _params(eng, eps_rel=eps, max_kkt_passes=limit), gpu=_opts(eng, layout))
     assert st.status.value == str(r["status"])
     ref_it = int(r["iterations"])
     if ref_it < 1280:
@@ -118,12 +136,13 @@ def test_full_run_parity(eng, name, tag, eps, limit):
         np.testing.assert_allclose(got, ref_t, rtol=1e-9, atol=1e-14)
 
 
-def test_deterministic_bitwise(eng):
+@pytest.mark.parametrize("layout", sorted(LAYOUTS))
+def test_deterministic_bitwise(eng, layout):
     gm = load_golden("config0_s0")
     eng.clear_cache()
-    pt1, s1 = eng.run_pdhg(gm, _params(eng, eps_rel=1e-4), seed=3)
+    pt1, s1 = eng.run_pdhg(gm, _params(eng, eps_rel=1e-4), seed=3, gpu=_opts(eng, layout))
     eng.clear_cache()
-    pt2, s2 = eng.run_pdhg(gm, _params(eng, eps_rel=1e-4), seed=3)
+    pt2, s2 = eng.run_pdhg(gm, _params(eng, eps_rel=1e-4), seed=3, gpu=_opts(eng, layout))
     np.testing.assert_array_equal(pt1.x, pt2.x)
     np.testing.assert_array_equal(pt1.y, pt2.y)
     assert s1.iterations == s2.iterations
