@@ -1003,7 +1003,7 @@ size_t pdhg_transpose_tmp_bytes(int64_t nnz, int32_t m, int32_t n) {
   cub::DoubleBuffer<int> k(nullptr, nullptr), v(nullptr, nullptr);
   cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, k, v, (int)nnz);
   (void)m; (void)n;
-  return 5 * align_up((size_t)nnz * 4) + align_up(cub_bytes);
+  return 5 * align_up((size_t)nnz * 4 + 256) + align_up(cub_bytes + 256);
 }
 
 int pdhg_transpose_csr(int32_t m, int32_t n, int64_t nnz, const int32_t* a_ptr, const int32_t* a_col,
