@@ -1,0 +1,59 @@
+"""Time the two step kernels on config 4 under each layout/L2 option (dev tool).
+
+    python tools/kernel_matrix.py [--scale 1.0] [--reps 20]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--variants", default="csr,csr_l2,psr,psr_l2")
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+
+    import paper_2603_03150_b200 as eng
+    from bench import algorithmic_bytes
+    from paper_2603_03150_b200.instances import config4
+
+    t = time.time()
+    inst = config4(scale=args.scale, seed=4)
+    print(f"gen {time.time() - t:.1f}s m={inst.m} n={inst.n} nnz={inst.nnz}", flush=True)
+    ab = algorithmic_bytes(inst.m, inst.n, inst.nnz)
+    variants = {
+        "csr": dict(psr="off", l2_persist=False),
+        "csr_l2": dict(psr="off", l2_persist=True),
+        "psr": dict(psr="on", l2_persist=False),
+        "psr_l2": dict(psr="on", l2_persist=True),
+    }
+    out = {}
+    for name in args.variants.split(","):
+        t = time.time()
+        dev = eng.DeviceLp(inst.A, inst.b, inst.c, eng.GpuOptions(cache_layout=False, **variants[name]))
+        torch.cuda.synchronize()
+        build = time.time() - t
+        dev.reset()
+        tp = dev.time_kernel(0, args.reps, 1e-3, 1e-3)
+        td = dev.time_kernel(1, args.reps, 1e-3, 1e-3)
+        out[name] = {"build_s": build, "primal_ms": tp, "dual_ms": td,
+                     "primal_gbs": ab["primal"] / tp / 1e6, "dual_gbs": ab["dual"] / td / 1e6,
+                     "psr": dev.psr_info}
+        print(name, json.dumps(out[name]), flush=True)
+        del dev
+        torch.cuda.empty_cache()
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
