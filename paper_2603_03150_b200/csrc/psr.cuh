@@ -97,48 +97,58 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // Accumulate one warp's entries [e0, e1) of a tile into acc[row_local].
 // STAGED: x from the shared-memory panel; otherwise gathered from global.
+// kUnroll chunks of 32 entries are loaded before any is consumed, so each
+// warp keeps kUnroll x (8+4[+4]) B per lane of streaming loads (and, for the
+// remote tile, kUnroll gathers) in flight -- one CTA of 32 warps per SM
+// needs that memory-level parallelism to cover DRAM latency.
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ void seg_commit(double p, unsigned mt, bool v, double* acc, double* prodw,
+                                           int lane) {
+  const int r = (int)(mt >> 16);
+  const int rp = __shfl_up_sync(0xffffffffu, r, 1);
+  const unsigned hm = __ballot_sync(0xffffffffu, lane == 0 || rp != r);
+  prodw[lane] = p;
+  __syncwarp();
+  const bool tail = v && (lane == 31 || ((hm >> (lane + 1)) & 1u));
+  if (tail) {
+    const unsigned below = (lane == 31) ? hm : (hm & ((2u << lane) - 1u));
+    const int h = 31 - __clz(below);
+    double s = prodw[h];
+    for (int k = h + 1; k <= lane; ++k) s += prodw[k];
+    acc[r] += s;
+  }
+  __syncwarp();
+}
+
 template <bool STAGED, int NR>
 __device__ __forceinline__ void seg_accumulate(const Layout& L, int e0, int e1,
                                                const double* const* px, const double* const* gx,
                                                double* acc, double* prodw, int lane) {
-  for (int base = e0; base < e1; base += 32) {
-    const int e = base + lane;
-    const bool v = e < e1;
-    unsigned mt = 0xFFFF0000u;
-    double p[NR];
+  static_assert(NR == 1, "PSR step kernels take one right-hand side");
+  for (int base = e0; base < e1; base += 32 * kUnroll) {
+    unsigned mt[kUnroll];
+    double a[kUnroll], xv[kUnroll];
+    int cc[kUnroll];
 #pragma unroll
-    for (int q = 0; q < NR; ++q) p[q] = 0.0;
-    if (v) {
-      mt = __ldcs(L.meta + e);
-      const double a = __ldcs(L.val + e);
-      if (STAGED) {
-        const int c = (int)(mt & 0xFFFFu);
-#pragma unroll
-        for (int q = 0; q < NR; ++q) p[q] = a * px[q][c];
-      } else {
-        const int c = __ldcs(L.col + e);
-#pragma unroll
-        for (int q = 0; q < NR; ++q) p[q] = a * __ldg(gx[q] + c);
-      }
+    for (int u = 0; u < kUnroll; ++u) {
+      const int e = base + u * 32 + lane;
+      const bool v = e < e1;
+      mt[u] = v ? __ldcs(L.meta + e) : 0xFFFF0000u;
+      a[u] = v ? __ldcs(L.val + e) : 0.0;
+      if (!STAGED) cc[u] = v ? __ldcs(L.col + e) : -1;
     }
-    const int r = (int)(mt >> 16);
-    const int rp = __shfl_up_sync(0xffffffffu, r, 1);
-    const unsigned hm = __ballot_sync(0xffffffffu, lane == 0 || rp != r);
+    if (!STAGED) {
 #pragma unroll
-    for (int q = 0; q < NR; ++q) prodw[q * 32 + lane] = p[q];
-    __syncwarp();
-    const bool tail = v && (lane == 31 || ((hm >> (lane + 1)) & 1u));
-    if (tail) {
-      const unsigned below = (lane == 31) ? hm : (hm & ((2u << lane) - 1u));
-      const int h = 31 - __clz(below);
-#pragma unroll
-      for (int q = 0; q < NR; ++q) {
-        double s = prodw[q * 32 + h];
-        for (int k = h + 1; k <= lane; ++k) s += prodw[q * 32 + k];
-        acc[q * kMaxRows + r] += s;
-      }
+      for (int u = 0; u < kUnroll; ++u) xv[u] = cc[u] >= 0 ? __ldg(gx[0] + cc[u]) : 0.0;
     }
-    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (base + u * 32 >= e1) break;  // warp-uniform
+      const bool v = base + u * 32 + lane < e1;
+      const double x = STAGED ? (v ? px[0][mt[u] & 0xFFFFu] : 0.0) : xv[u];
+      seg_commit(a[u] * x, mt[u], v, acc, prodw, lane);
+    }
   }
 }
 

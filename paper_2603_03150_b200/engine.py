@@ -60,7 +60,7 @@ class GpuOptions:
     psr_min_staged: int = 1024
     psr_min_fraction: float = 0.3
     psr_min_rows: int = 148 * 256
-    l2_persist: bool = True
+    l2_persist: bool = False
 
 
 def _torch():
