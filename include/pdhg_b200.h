@@ -68,18 +68,17 @@ extern "C" {
  * (enough entries in dense column panels); NULL = CSR-vector kernels.
  */
 typedef struct pdhg_psr {
-  int32_t rows, cols, R, W, nblk, ntiles;
+  int32_t rows, cols, R, W, nblk, ntiles, ngroups;
   int64_t nent;
   const int32_t* blk_tile_ptr;  /* nblk+1 */
-  const int32_t* blk_warp_row;  /* nblk*(PDHG_PSR_WARPS+1) */
-  const int32_t* tile_bin;      /* ntiles */
-  const int32_t* tile_ent;      /* ntiles*(PDHG_PSR_WARPS+1) */
+  const int32_t* tile_bin;      /* ntiles, -1 = remote tile */
+  const int32_t* gstart;        /* ntiles*(ngroups+1) */
+  const uint16_t* goff;         /* ntiles*ngroups*32 */
   const double* val;            /* nent */
-  const uint32_t* meta;         /* nent */
-  const int32_t* col;           /* nent */
+  const uint16_t* col16;        /* nent: column inside the panel */
+  const int32_t* col;           /* nent: global column */
   const uint8_t* heavy;         /* rows */
 } pdhg_psr;
-#define PDHG_PSR_WARPS 32
 
 typedef struct pdhg_problem {
   int32_t m, n;
@@ -187,11 +186,12 @@ size_t pdhg_psr_tmp_bytes(int32_t rows, int32_t cols, int64_t nnz);
 int pdhg_psr_plan(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, const int32_t* col,
                   int32_t heavy_threshold, int32_t min_staged, void* tmp, size_t tmp_bytes,
                   void* stream, int32_t* R_out, int32_t* W_out, int32_t* nblk_out,
-                  int32_t* ntiles_out, int64_t* staged_out, int64_t* nent_out);
+                  int32_t* ngroups_out, int32_t* ntiles_out, int64_t* staged_out,
+                  int64_t* nent_out);
 int pdhg_psr_build(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, const int32_t* col,
                    const double* val, int32_t heavy_threshold, void* tmp, size_t tmp_bytes,
-                   void* stream, int32_t* blk_tile_ptr, int32_t* blk_warp_row, int32_t* tile_bin,
-                   int32_t* tile_ent, double* val_out, uint32_t* meta_out, int32_t* col_out,
+                   void* stream, int32_t* blk_tile_ptr, int32_t* tile_bin, int32_t* gstart,
+                   uint16_t* goff, double* val_out, uint16_t* col16_out, int32_t* col_out,
                    uint8_t* heavy_out);
 
 #ifdef __cplusplus

@@ -29,17 +29,14 @@ EXPORTS = (
 )
 
 
-PSR_WARPS = 32
-
-
 class Psr(C.Structure):
     """struct pdhg_psr (panel-staged rows layout of one operator)."""
 
     _fields_ = [
         ("rows", C.c_int32), ("cols", C.c_int32), ("R", C.c_int32), ("W", C.c_int32),
-        ("nblk", C.c_int32), ("ntiles", C.c_int32), ("nent", C.c_int64),
-        ("blk_tile_ptr", C.c_void_p), ("blk_warp_row", C.c_void_p), ("tile_bin", C.c_void_p),
-        ("tile_ent", C.c_void_p), ("val", C.c_void_p), ("meta", C.c_void_p), ("col", C.c_void_p),
+        ("nblk", C.c_int32), ("ntiles", C.c_int32), ("ngroups", C.c_int32), ("nent", C.c_int64),
+        ("blk_tile_ptr", C.c_void_p), ("tile_bin", C.c_void_p), ("gstart", C.c_void_p),
+        ("goff", C.c_void_p), ("val", C.c_void_p), ("col16", C.c_void_p), ("col", C.c_void_p),
         ("heavy", C.c_void_p),
     ]
 
@@ -107,7 +104,7 @@ def load():
         _sig(lib, "pdhg_transpose_csr", C.c_int, i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, szt, vp)
         _sig(lib, "pdhg_psr_tmp_bytes", szt, i32, i32, i64)
         _sig(lib, "pdhg_psr_plan", C.c_int, i32, i32, i64, vp, vp, i32, i32, vp, szt, vp,
-             P(i32), P(i32), P(i32), P(i32), P(i64), P(i64))
+             P(i32), P(i32), P(i32), P(i32), P(i32), P(i64), P(i64))
         _sig(lib, "pdhg_psr_build", C.c_int, i32, i32, i64, vp, vp, vp, i32, vp, szt, vp,
              vp, vp, vp, vp, vp, vp, vp, vp)
         if lib.pdhg_abi_version() != 1:

@@ -244,35 +244,26 @@ struct PsrStepArgs {
 template <bool PRIMAL>
 __global__ void __launch_bounds__(psr::kThreads, 1) k_step_psr(PsrStepArgs a, int j_in_period) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t bars[2];
+  __shared__ uint64_t bars[psr::kStages];
   StepParams* P = a.P;
   const long long iter = P->iter0 + j_in_period + 1;
   if (P->fail_iter < iter) return;
   const double w = P->w0 + (double)(j_in_period + 1);
   const double step = PRIMAL ? P->tau_w : P->sigma_w;
-  const int tid = threadIdx.x;
   double* panels = reinterpret_cast<double*>(smem_raw);
-  double* acc = panels + 2 * a.L.W;
-  double* prodw = acc + a.L.R + (tid >> 5) * 32;
-  if (tid == 0) {
-    psr::mbar_init(&bars[0], 1);
-    psr::mbar_init(&bars[1], 1);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < psr::kStages; ++k) psr::mbar_init(&bars[k], 1);
     psr::fence_mbar_init();
   }
   __syncthreads();
-  psr::Pipe pp{bars, {0u, 0u}};
-  const double* gx[1] = {a.gather};
+  uint32_t ph[psr::kStages];
+#pragma unroll
+  for (int k = 0; k < psr::kStages; ++k) ph[k] = 0u;
   for (int b = blockIdx.x; b < a.L.nblk; b += gridDim.x) {
-    psr::block_spmv<1>(a.L, b, gx, panels, acc, prodw, pp);
-    const int row0 = b * a.L.R;
-    const int rows_b = min(a.L.R, a.L.rows - row0);
-    for (int r = tid; r < rows_b; r += psr::kThreads) {
-      const int row = row0 + r;
-      if (a.L.heavy[row]) continue;
-      if (PRIMAL) primal_epi(row, acc[r], a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
-      else dual_epi(row, acc[r], a.cb, a.x, a.xbar, step, w, iter, P);
-    }
-    __syncthreads();
+    psr::block_rows(a.L, b, a.gather, panels, bars, ph, [&](int row, double d) {
+      if (PRIMAL) primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
+      else dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
+    });
   }
 }
 
@@ -755,14 +746,14 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
     const pdhg_psr* q = k == 0 ? prob->a_psr : prob->at_psr;
     c->has_psr[k] = q != nullptr;
     if (q) {
-      if (q->R > psr::kMaxRows || q->W != psr::kPanel || !q->heavy) {
+      if (q->R > psr::kMaxRows || q->W != psr::kPanel || !q->heavy || q->ngroups != (q->R + 31) / 32) {
         delete c;
         return fail(PDHG_ERR_ARG, "psr layout geometry not supported");
       }
-      c->psr_l[k] = psr::Layout{q->rows, q->cols, q->R, q->W, q->nblk, q->ntiles, q->blk_tile_ptr,
-                                q->blk_warp_row, q->tile_bin, q->tile_ent, q->val, q->meta, q->col,
-                                q->heavy};
-      c->psr_smem[k] = psr::smem_bytes(q->R, q->W);
+      c->psr_l[k] = psr::Layout{q->rows, q->cols, q->R, q->W, q->nblk, q->ntiles, q->ngroups,
+                                q->blk_tile_ptr, q->tile_bin, q->gstart, q->goff, q->val, q->col16,
+                                q->col, q->heavy};
+      c->psr_smem[k] = psr::smem_bytes(q->W);
     }
   }
   {
@@ -775,7 +766,7 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
     c->l2_maxwin = maxw;
     if (c->l2_persist > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp);
     cudaGetLastError();
-    const size_t sm = psr::smem_bytes(psr::kMaxRows, psr::kPanel);
+    const size_t sm = psr::smem_bytes(psr::kPanel);
     cudaFuncSetAttribute(k_step_psr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaFuncSetAttribute(k_step_psr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaGetLastError();

@@ -32,7 +32,6 @@ using pdhg_internal::set_error;
       return set_error(PDHG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));     \
   } while (0)
 
-constexpr int NW = psr::kWarps;
 
 struct Geo {
   int R, W, nblk, nbins;
@@ -201,8 +200,8 @@ __global__ void k_keys(int rows, const int* __restrict__ ptr, const int* __restr
 __global__ void k_scatter(long long nnz, const int* __restrict__ skey, const int* __restrict__ sidx,
                           const int* __restrict__ rid, const int* __restrict__ col,
                           const double* __restrict__ val, const int* __restrict__ tile_bin, int ntiles,
-                          int R, int W, double* __restrict__ val_out, unsigned* __restrict__ meta_out,
-                          int* __restrict__ col_out) {
+                          int R, int W, double* __restrict__ val_out, unsigned short* __restrict__ col16_out,
+                          int* __restrict__ col_out, int* __restrict__ rowl) {
   const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nnz) return;
   const int t = skey[s];
@@ -213,8 +212,8 @@ __global__ void k_scatter(long long nnz, const int* __restrict__ skey, const int
   const int bin = tile_bin[t];
   val_out[s] = val[e];
   col_out[s] = c;
-  const unsigned rl = (unsigned)(r - (r / R) * R);
-  meta_out[s] = (rl << 16) | (unsigned)(bin >= 0 ? c - bin * W : 0);
+  col16_out[s] = (unsigned short)(bin >= 0 ? c - bin * W : 0);
+  rowl[s] = r - (r / R) * R;
 }
 
 __global__ void k_tile_start(const int* __restrict__ skey, long long nnz, int ntiles,
@@ -229,51 +228,30 @@ __global__ void k_tile_start(const int* __restrict__ skey, long long nnz, int nt
   tstart[t] = (int)lo;
 }
 
-__global__ void k_warp_rows(int rows, int R, int nblk, const int* __restrict__ ptr,
-                            int* __restrict__ blk_warp_row) {
-  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= (long long)nblk * (NW + 1)) return;
-  const int b = (int)(g / (NW + 1)), w = (int)(g % (NW + 1));
-  const int r0 = b * R, r1 = min(rows, r0 + R);
-  int out;
-  if (w == 0) {
-    out = 0;
-  } else if (w == NW) {
-    out = r1 - r0;
-  } else {
-    const long long p0 = ptr[r0], p1 = ptr[r1];
-    const long long target = p0 + (p1 - p0) * w / NW;
-    int lo = r0, hi = r1;  // first row r with ptr[r] >= target
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (ptr[mid] < target) lo = mid + 1; else hi = mid;
-    }
-    out = lo - r0;
-  }
-  blk_warp_row[g] = out;
-}
-
-__global__ void k_tile_ent(int ntiles, int nblk, const int* __restrict__ bptr,
-                           const int* __restrict__ tstart, const int* __restrict__ blk_warp_row,
-                           const unsigned* __restrict__ meta, int* __restrict__ tile_ent) {
-  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= (long long)ntiles * (NW + 1)) return;
-  const int t = (int)(g / (NW + 1)), w = (int)(g % (NW + 1));
+// For tile t and block-local row r in [0, ngroups*32]: p(r) = first entry of
+// the tile whose row is >= r.  gstart[t][g] = p(32g); goff[t][r] = p(r) - p(32*(r/32)).
+__global__ void k_groups(int ntiles, int ngroups, const int* __restrict__ tstart,
+                         const int* __restrict__ rowl, int* __restrict__ gstart,
+                         unsigned short* __restrict__ goff) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per = (long long)ngroups * 32 + 1;
+  if (gid >= (long long)ntiles * per) return;
+  const int t = (int)(gid / per), r = (int)(gid % per);
   const int s = tstart[t], e = tstart[t + 1];
-  if (w == NW) { tile_ent[g] = e; return; }
-  if (w == 0) { tile_ent[g] = s; return; }
-  int lo = 0, hi = nblk;  // block of tile t: last b with bptr[b] <= t
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (bptr[mid] <= t) lo = mid; else hi = mid;
+  auto lb = [&](int target) {
+    int a = s, z = e;
+    while (a < z) {
+      const int mid = (a + z) >> 1;
+      if (rowl[mid] < target) a = mid + 1; else z = mid;
+    }
+    return a;
+  };
+  const int p = lb(r);
+  if ((r & 31) == 0) gstart[(size_t)t * (ngroups + 1) + (r >> 5)] = p;
+  if (r < ngroups * 32) {
+    const int p0 = (r & 31) ? lb(r & ~31) : p;
+    goff[(size_t)t * ngroups * 32 + r] = (unsigned short)(p - p0);
   }
-  const unsigned target = (unsigned)blk_warp_row[(size_t)lo * (NW + 1) + w];
-  int a = s, z = e;
-  while (a < z) {
-    const int mid = (a + z) >> 1;
-    if ((meta[mid] >> 16) < target) a = mid + 1; else z = mid;
-  }
-  tile_ent[g] = a;
 }
 
 __global__ void k_heavy_flags(int rows, const int* __restrict__ ptr, int H, unsigned char* out) {
@@ -295,7 +273,7 @@ size_t pdhg_psr_tmp_bytes(int32_t rows, int32_t cols, int64_t nnz) {
 int pdhg_psr_plan(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, const int32_t* col,
                   int32_t heavy_threshold, int32_t min_staged, void* tmp, size_t tmp_bytes,
                   void* stream, int32_t* R_out, int32_t* W_out, int32_t* nblk_out,
-                  int32_t* ntiles_out, int64_t* staged_out, int64_t* nent_out) {
+                  int32_t* ngroups_out, int32_t* ntiles_out, int64_t* staged_out, int64_t* nent_out) {
   if (rows <= 0 || cols <= 0 || nnz < 0 || nnz >= INT_MAX || !ptr || !tmp)
     return set_error(PDHG_ERR_ARG, "psr_plan: bad argument");
   if (tmp_bytes < tmp_size(rows, cols, nnz)) return set_error(PDHG_ERR_ARG, "psr_plan: tmp too small");
@@ -332,6 +310,7 @@ int pdhg_psr_plan(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, c
   if (R_out) *R_out = g.R;
   if (W_out) *W_out = g.W;
   if (nblk_out) *nblk_out = g.nblk;
+  if (ngroups_out) *ngroups_out = (g.R + 31) / 32;
   if (ntiles_out) *ntiles_out = ntiles;
   if (staged_out) *staged_out = staged;
   if (nent_out) *nent_out = nent;
@@ -340,21 +319,23 @@ int pdhg_psr_plan(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, c
 
 int pdhg_psr_build(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, const int32_t* col,
                    const double* val, int32_t heavy_threshold, void* tmp, size_t tmp_bytes,
-                   void* stream, int32_t* blk_tile_ptr, int32_t* blk_warp_row, int32_t* tile_bin,
-                   int32_t* tile_ent, double* val_out, uint32_t* meta_out, int32_t* col_out,
+                   void* stream, int32_t* blk_tile_ptr, int32_t* tile_bin, int32_t* gstart,
+                   uint16_t* goff, double* val_out, uint16_t* col16_out, int32_t* col_out,
                    uint8_t* heavy_out) {
   if (rows <= 0 || cols <= 0 || nnz < 0 || nnz >= INT_MAX || !tmp)
     return set_error(PDHG_ERR_ARG, "psr_build: bad argument");
   if (tmp_bytes < tmp_size(rows, cols, nnz)) return set_error(PDHG_ERR_ARG, "psr_build: tmp too small");
   cudaStream_t s = (cudaStream_t)stream;
   const Geo g = geometry(rows, cols);
-  if ((long long)g.R > 65535 || g.W > 65536) return set_error(PDHG_ERR_ARG, "psr: geometry overflow");
+  if ((long long)g.R > psr::kMaxRows || g.W > 65536) return set_error(PDHG_ERR_ARG, "psr: geometry overflow");
+  const int ngroups = (g.R + 31) / 32;
   Tmp t = carve(tmp, rows, cols, nnz);
   int ntiles = 0;
   PSR_TRY(cudaMemcpyAsync(&ntiles, t.bptr + g.nblk, 4, cudaMemcpyDeviceToHost, s));
   PSR_TRY(cudaStreamSynchronize(s));
   PSR_TRY(cudaMemcpyAsync(blk_tile_ptr, t.bptr, (size_t)(g.nblk + 1) * 4, cudaMemcpyDeviceToDevice, s));
   k_tile_bin<<<blocks(g.nblk, 128), 128, 0, s>>>(g.nblk, g.nbins, t.tile_of, t.bptr, tile_bin);
+  int* rowl = t.k1;
   if (nnz > 0) {
     k_keys<<<blocks((long long)rows * 32, 256), 256, 0, s>>>(rows, ptr, col, heavy_threshold, g.R, g.W,
                                                               g.nbins, t.tile_of, t.bptr, ntiles, t.k0,
@@ -364,17 +345,16 @@ int pdhg_psr_build(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, 
     cub::DoubleBuffer<int> kb(t.k0, t.k1), vb(t.v0, t.v1);
     size_t cb = t.cub_bytes;
     PSR_TRY(cub::DeviceRadixSort::SortPairs(t.cub, cb, kb, vb, (int)nnz, 0, bits, s));
-    k_scatter<<<blocks(nnz, 256), 256, 0, s>>>(nnz, kb.Current(), vb.Current(), t.rid, col, val,
-                                               tile_bin, ntiles, g.R, g.W, val_out, meta_out, col_out);
     k_tile_start<<<blocks(ntiles + 1, 256), 256, 0, s>>>(kb.Current(), nnz, ntiles, t.tstart);
+    rowl = kb.Alternate();  // free after the sort: reused for block-local row ids
+    k_scatter<<<blocks(nnz, 256), 256, 0, s>>>(nnz, kb.Current(), vb.Current(), t.rid, col, val,
+                                               tile_bin, ntiles, g.R, g.W, val_out, col16_out, col_out,
+                                               rowl);
   } else {
     PSR_TRY(cudaMemsetAsync(t.tstart, 0, (size_t)(ntiles + 1) * 4, s));
   }
-  k_warp_rows<<<blocks((long long)g.nblk * (NW + 1), 256), 256, 0, s>>>(rows, g.R, g.nblk, ptr,
-                                                                        blk_warp_row);
-  k_tile_ent<<<blocks((long long)ntiles * (NW + 1), 256), 256, 0, s>>>(ntiles, g.nblk, t.bptr,
-                                                                        t.tstart, blk_warp_row,
-                                                                        meta_out, tile_ent);
+  const long long ng = (long long)ntiles * ((long long)ngroups * 32 + 1);
+  k_groups<<<blocks(ng, 256), 256, 0, s>>>(ntiles, ngroups, t.tstart, rowl, gstart, goff);
   k_heavy_flags<<<blocks(rows, 256), 256, 0, s>>>(rows, ptr, heavy_threshold, heavy_out);
   PSR_TRY(cudaGetLastError());
   PSR_TRY(cudaStreamSynchronize(s));

@@ -162,36 +162,36 @@ class DeviceLp:
         sptr = self.stream.cuda_stream
         tb = lib.pdhg_psr_tmp_bytes(rows, cols, nnz)
         tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=dev)
-        R, W, nblk, ntiles = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        R, W, nblk, ngroups, ntiles = (C.c_int32() for _ in range(5))
         staged, nent = C.c_int64(), C.c_int64()
         N.check(lib.pdhg_psr_plan(rows, cols, nnz, ptr.data_ptr(), col.data_ptr(), H,
                                   int(opts.psr_min_staged), tmp.data_ptr(), tb, sptr,
-                                  C.byref(R), C.byref(W), C.byref(nblk), C.byref(ntiles),
-                                  C.byref(staged), C.byref(nent)))
+                                  C.byref(R), C.byref(W), C.byref(nblk), C.byref(ngroups),
+                                  C.byref(ntiles), C.byref(staged), C.byref(nent)))
         frac = staged.value / max(1, nnz)
         self.psr_info[key] = {"R": R.value, "W": W.value, "nblk": nblk.value, "ntiles": ntiles.value,
-                              "staged_fraction": frac, "nent": nent.value}
+                              "ngroups": ngroups.value, "staged_fraction": frac, "nent": nent.value}
         if opts.psr == "auto" and frac < opts.psr_min_fraction:
             return None
         i32 = torch.int32
+        nt = max(1, ntiles.value)
         bufs = {
             "blk_tile_ptr": torch.empty(nblk.value + 1, dtype=i32, device=dev),
-            "blk_warp_row": torch.empty(nblk.value * (N.PSR_WARPS + 1), dtype=i32, device=dev),
-            "tile_bin": torch.empty(max(1, ntiles.value), dtype=i32, device=dev),
-            "tile_ent": torch.empty(max(1, ntiles.value) * (N.PSR_WARPS + 1), dtype=i32, device=dev),
+            "tile_bin": torch.empty(nt, dtype=i32, device=dev),
+            "gstart": torch.empty(nt * (ngroups.value + 1), dtype=i32, device=dev),
+            "goff": torch.empty(nt * ngroups.value * 32, dtype=torch.int16, device=dev),
             "val": torch.empty(max(1, nnz), dtype=torch.float64, device=dev),
-            "meta": torch.empty(max(1, nnz), dtype=i32, device=dev),
+            "col16": torch.empty(max(1, nnz), dtype=torch.int16, device=dev),
             "col": torch.empty(max(1, nnz), dtype=i32, device=dev),
             "heavy": torch.empty(rows, dtype=torch.uint8, device=dev),
         }
-        N.check(lib.pdhg_psr_build(
-            rows, cols, nnz, ptr.data_ptr(), col.data_ptr(), val.data_ptr(), H, tmp.data_ptr(), tb,
-            sptr, *(bufs[k].data_ptr() for k in ("blk_tile_ptr", "blk_warp_row", "tile_bin",
-                                                 "tile_ent", "val", "meta", "col", "heavy"))))
+        names = ("blk_tile_ptr", "tile_bin", "gstart", "goff", "val", "col16", "col", "heavy")
+        N.check(lib.pdhg_psr_build(rows, cols, nnz, ptr.data_ptr(), col.data_ptr(), val.data_ptr(), H,
+                                   tmp.data_ptr(), tb, sptr, *(bufs[k].data_ptr() for k in names)))
         d = N.Psr()
         d.rows, d.cols, d.R, d.W = rows, cols, R.value, W.value
-        d.nblk, d.ntiles, d.nent = nblk.value, ntiles.value, nent.value
-        for k in ("blk_tile_ptr", "blk_warp_row", "tile_bin", "tile_ent", "val", "meta", "col", "heavy"):
+        d.nblk, d.ntiles, d.ngroups, d.nent = nblk.value, ntiles.value, ngroups.value, nent.value
+        for k in names:
             setattr(d, k, bufs[k].data_ptr())
         self.psr_info[key]["used"] = True
         return (d, bufs)

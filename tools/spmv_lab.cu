@@ -1,0 +1,256 @@
+// spmv_lab.cu -- kernel-variant lab for the PDHG SpMVs (development tool, not product).
+// Generates a config-4-shaped matrix on the device (5M x 10M, ~200M nnz,
+// lognormal rows mean 40, 70% banded +-50k, 30% uniform) and its transpose,
+// then times CSR SpMV variants on A (gather x, 80 MB) and A' (gather y, 40 MB).
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+#include <cub/cub.cuh>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
+
+__host__ __device__ inline uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__device__ inline double u01(uint64_t h) { return ((h >> 11) + 0.5) * (1.0 / 9007199254740992.0); }
+
+__global__ void k_rowlen(int m, int* len) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double u1 = u01(mix64(i * 2ULL + 1)), u2 = u01(mix64(i * 2ULL + 2));
+  double g = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+  double mu = log(40.0) - 0.5 * 0.8 * 0.8;
+  long l = lround(exp(mu + 0.8 * g));
+  len[i] = (int)min(max(l, 1L), 2000L);
+}
+__global__ void k_fill(int m, int n, const int* ptr, int* col, double* val) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+    uint64_t h = mix64(0x1234567ULL ^ (uint64_t)k * 0x100000001b3ULL);
+    long c;
+    if (u01(h) < 0.7) c = ((2L * i + (long)(mix64(h) % 100001ULL) - 50000) % n + n) % n;
+    else c = (long)(mix64(h + 7) % (uint64_t)n);
+    col[k] = (int)c;
+    val[k] = u01(mix64(h + 13)) - 0.5;
+  }
+}
+__global__ void k_sortrows(int m, const int* ptr, int* col) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  int s = ptr[i], e = ptr[i + 1];
+  for (int a = s + 1; a < e; ++a) {
+    int v = col[a]; int b = a - 1;
+    while (b >= s && col[b] > v) { col[b + 1] = col[b]; --b; }
+    col[b + 1] = v;
+  }
+}
+__global__ void k_rid(int m, const int* ptr, int* rid) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) rid[k] = i;
+}
+__global__ void k_iota(int* v, int n) { int i = blockIdx.x * blockDim.x + threadIdx.x; if (i < n) v[i] = i; }
+__global__ void k_gt(int nnz, const int* perm, const int* rid, const double* val, int* tc, double* tv) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nnz) return;
+  tc[k] = rid[perm[k]]; tv[k] = val[perm[k]];
+}
+__global__ void k_cptr(const int* keys, int nnz, int n, int* tp) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > n) return;
+  int lo = 0, hi = nnz;
+  while (lo < hi) { int mid = (lo + hi) >> 1; if (keys[mid] < j) lo = mid + 1; else hi = mid; }
+  tp[j] = lo;
+}
+
+struct Csr { int rows, cols, nnz; int* ptr; int* col; double* val; };
+
+template <int V>
+__device__ __forceinline__ double gsum(double v) {
+#pragma unroll
+  for (int o = V / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---- V1 baseline (library v1)
+template <int V>
+__global__ void __launch_bounds__(256) v1(Csr A, const double* __restrict__ x, double* __restrict__ y) {
+  const long long gid = (long long)blockIdx.x * 256 + threadIdx.x;
+  const int row = (int)(gid / V), lane = threadIdx.x % V;
+  int s = 0, e = 0;
+  if (row < A.rows) { s = A.ptr[row]; e = A.ptr[row + 1]; }
+  double acc = 0.0;
+  for (int k = s + lane; k < e; k += V) acc = fma(__ldcs(A.val + k), __ldg(x + __ldcs(A.col + k)), acc);
+  acc = gsum<V>(acc);
+  if (row < A.rows && lane == 0) y[row] = acc;
+}
+
+// ---- V2 unrolled x U: U independent (val, col, gather) triples in flight per lane
+template <int V, int U>
+__global__ void __launch_bounds__(256) v2(Csr A, const double* __restrict__ x, double* __restrict__ y) {
+  const long long gid = (long long)blockIdx.x * 256 + threadIdx.x;
+  const int row = (int)(gid / V), lane = threadIdx.x % V;
+  int s = 0, e = 0;
+  if (row < A.rows) { s = A.ptr[row]; e = A.ptr[row + 1]; }
+  double acc = 0.0;
+  for (int k = s + lane; k < e; k += U * V) {
+    double a[U], xv[U];
+    int j[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = k + u * V;
+      a[u] = kk < e ? __ldcs(A.val + kk) : 0.0;
+      j[u] = kk < e ? __ldcs(A.col + kk) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = j[u] >= 0 ? __ldg(x + j[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = fma(a[u], xv[u], acc);
+  }
+  acc = gsum<V>(acc);
+  if (row < A.rows && lane == 0) y[row] = acc;
+}
+
+// ---- V3 pairs: 16-byte val / 8-byte col loads, one peeled head element
+template <int V, int U>
+__global__ void __launch_bounds__(256) v3(Csr A, const double* __restrict__ x, double* __restrict__ y) {
+  const long long gid = (long long)blockIdx.x * 256 + threadIdx.x;
+  const int row = (int)(gid / V), lane = threadIdx.x % V;
+  int s = 0, e = 0;
+  if (row < A.rows) { s = A.ptr[row]; e = A.ptr[row + 1]; }
+  double acc = 0.0;
+  if ((s & 1) && s < e) {  // peel to even
+    if (lane == 0) acc = __ldcs(A.val + s) * __ldg(x + __ldcs(A.col + s));
+    ++s;
+  }
+  const int np = (e - s) >> 1;  // pairs
+  const double2* vp = reinterpret_cast<const double2*>(A.val + s);
+  const int2* cp = reinterpret_cast<const int2*>(A.col + s);
+  for (int p = lane; p < np; p += U * V) {
+    double2 a[U];
+    int2 j[U];
+    double x0[U], x1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int pp = p + u * V;
+      if (pp < np) { a[u] = __ldcs(vp + pp); j[u] = __ldcs(cp + pp); }
+      else { a[u] = make_double2(0, 0); j[u] = make_int2(-1, -1); }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      x0[u] = j[u].x >= 0 ? __ldg(x + j[u].x) : 0.0;
+      x1[u] = j[u].y >= 0 ? __ldg(x + j[u].y) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) { acc = fma(a[u].x, x0[u], acc); acc = fma(a[u].y, x1[u], acc); }
+  }
+  if ((e - s) & 1) {
+    if (lane == (np % V)) acc = fma(__ldcs(A.val + e - 1), __ldg(x + __ldcs(A.col + e - 1)), acc);
+  }
+  acc = gsum<V>(acc);
+  if (row < A.rows && lane == 0) y[row] = acc;
+}
+
+// ---- V4: one warp, several rows: 2 rows per 32-lane warp at V=16 etc. is V1/V2; skip.
+
+struct Timer {
+  cudaEvent_t a, b;
+  Timer() { cudaEventCreate(&a); cudaEventCreate(&b); }
+  void start() { cudaEventRecord(a); }
+  float stop() { cudaEventRecord(b); cudaEventSynchronize(b); float ms; cudaEventElapsedTime(&ms, a, b); return ms; }
+};
+
+int main(int argc, char** argv) {
+  int m = 5000000, n = 10000000;
+  int *len, *ptr;
+  CK(cudaMalloc(&len, (m + 1) * 4)); CK(cudaMalloc(&ptr, (m + 1) * 4));
+  k_rowlen<<<(m + 255) / 256, 256>>>(m, len);
+  CK(cudaMemset(len + m, 0, 4));
+  void* tmp = nullptr; size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(tmp, tb, len, ptr, m + 1);
+  CK(cudaMalloc(&tmp, tb));
+  cub::DeviceScan::ExclusiveSum(tmp, tb, len, ptr, m + 1);
+  int nnz; CK(cudaMemcpy(&nnz, ptr + m, 4, cudaMemcpyDeviceToHost));
+  Csr A{m, n, nnz, ptr, nullptr, nullptr};
+  CK(cudaMalloc(&A.col, (size_t)nnz * 4)); CK(cudaMalloc(&A.val, (size_t)nnz * 8));
+  k_fill<<<(m + 255) / 256, 256>>>(m, n, ptr, A.col, A.val);
+  k_sortrows<<<(m + 255) / 256, 256>>>(m, ptr, A.col);
+  // transpose
+  Csr T{n, m, nnz, nullptr, nullptr, nullptr};
+  {
+    int *k0, *k1, *v0, *v1, *rid;
+    CK(cudaMalloc(&k0, (size_t)nnz * 4)); CK(cudaMalloc(&k1, (size_t)nnz * 4));
+    CK(cudaMalloc(&v0, (size_t)nnz * 4)); CK(cudaMalloc(&v1, (size_t)nnz * 4)); CK(cudaMalloc(&rid, (size_t)nnz * 4));
+    CK(cudaMemcpy(k0, A.col, (size_t)nnz * 4, cudaMemcpyDeviceToDevice));
+    k_iota<<<(nnz + 255) / 256, 256>>>(v0, nnz);
+    k_rid<<<(m + 255) / 256, 256>>>(m, ptr, rid);
+    cub::DoubleBuffer<int> kb(k0, k1), vb(v0, v1);
+    void* t2 = nullptr; size_t b2 = 0;
+    cub::DeviceRadixSort::SortPairs(t2, b2, kb, vb, nnz);
+    CK(cudaMalloc(&t2, b2));
+    cub::DeviceRadixSort::SortPairs(t2, b2, kb, vb, nnz);
+    CK(cudaMalloc(&T.ptr, (size_t)(n + 1) * 4)); CK(cudaMalloc(&T.col, (size_t)nnz * 4)); CK(cudaMalloc(&T.val, (size_t)nnz * 8));
+    k_gt<<<(nnz + 255) / 256, 256>>>(nnz, vb.Current(), rid, A.val, T.col, T.val);
+    k_cptr<<<(n + 256) / 256, 256>>>(kb.Current(), nnz, n, T.ptr);
+    CK(cudaDeviceSynchronize());
+    cudaFree(k0); cudaFree(k1); cudaFree(v0); cudaFree(v1); cudaFree(rid); cudaFree(t2);
+  }
+  double *x, *yv, *yref, *ya;
+  CK(cudaMalloc(&x, (size_t)n * 8)); CK(cudaMalloc(&yv, (size_t)m * 8));
+  CK(cudaMalloc(&yref, (size_t)n * 8)); CK(cudaMalloc(&ya, (size_t)n * 8));
+  {
+    std::vector<double> hx(n);
+    for (int i = 0; i < n; ++i) hx[i] = ((mix64(i) >> 11) * (1.0 / 9007199254740992.0)) - 0.5;
+    CK(cudaMemcpy(x, hx.data(), (size_t)n * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(yv, hx.data(), (size_t)m * 8, cudaMemcpyHostToDevice));
+  }
+  printf("m=%d n=%d nnz=%d\n", m, n, nnz);
+  Timer t;
+  auto bench = [&](const char* name, const Csr& M, auto fn, const double* xin) {
+    for (int w = 0; w < 3; ++w) fn();
+    CK(cudaDeviceSynchronize());
+    t.start();
+    const int R = 20;
+    for (int r = 0; r < R; ++r) fn();
+    const float ms = t.stop() / R;
+    CK(cudaGetLastError());
+    // check vs reference result (v1 into yref)
+    std::vector<double> a(M.rows), b(M.rows);
+    CK(cudaMemcpy(a.data(), ya, (size_t)M.rows * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(b.data(), yref, (size_t)M.rows * 8, cudaMemcpyDeviceToHost));
+    double err = 0;
+    for (int i = 0; i < M.rows; ++i) err = fmax(err, fabs(a[i] - b[i]));
+    const double bytes = 12.0 * M.nnz + 4.0 * M.rows + 8.0 * M.cols + 8.0 * M.rows;
+    printf("%-34s %8.3f ms  %8.1f GB/s  maxdiff %.2e\n", name, ms, bytes / ms / 1e6, err);
+  };
+  auto grid = [](int rows, int V) { return (unsigned)(((long long)rows * V + 255) / 256); };
+  for (int op = 0; op < 2; ++op) {
+    const Csr& M = op == 0 ? A : T;
+    const double* xin = op == 0 ? x : yv;
+    printf("== %s (rows=%d, mean %.1f)\n", op == 0 ? "A x" : "A' y", M.rows, (double)M.nnz / M.rows);
+    if (op == 0) v1<8><<<grid(M.rows, 8), 256>>>(M, xin, yref); else v1<4><<<grid(M.rows, 4), 256>>>(M, xin, yref);
+#define RUN(NAME, K, VV) bench(NAME, M, [&] { K<<<grid(M.rows, VV), 256>>>(M, xin, ya); }, xin)
+    RUN("v1<4>", v1<4>, 4);
+    RUN("v1<8>", v1<8>, 8);
+    RUN("v1<16>", v1<16>, 16);
+    RUN("v2<4,2>", (v2<4, 2>), 4);
+    RUN("v2<4,4>", (v2<4, 4>), 4);
+    RUN("v2<8,2>", (v2<8, 2>), 8);
+    RUN("v2<8,4>", (v2<8, 4>), 8);
+    RUN("v2<16,2>", (v2<16, 2>), 16);
+    RUN("v3<2,2>", (v3<2, 2>), 2);
+    RUN("v3<4,1>", (v3<4, 1>), 4);
+    RUN("v3<4,2>", (v3<4, 2>), 4);
+    RUN("v3<8,1>", (v3<8, 1>), 8);
+    RUN("v3<8,2>", (v3<8, 2>), 8);
+    RUN("v3<16,1>", (v3<16, 1>), 16);
+  }
+  return 0;
+}
