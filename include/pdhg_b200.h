@@ -73,7 +73,7 @@ typedef struct pdhg_psr {
   const int32_t* blk_tile_ptr;  /* nblk+1 */
   const int32_t* tile_bin;      /* ntiles, -1 = remote tile */
   const int32_t* gstart;        /* ntiles*(ngroups+1) */
-  const uint16_t* goff;         /* ntiles*ngroups*32 */
+  const uint16_t* goff;         /* ntiles*ngroups*16 (16-row groups) */
   const double* val;            /* nent */
   const uint16_t* col16;        /* nent: column inside the panel */
   const int32_t* col;           /* nent: global column */

@@ -130,13 +130,30 @@ struct RowSet {
 template <int V, int NR>
 __device__ __forceinline__ void row_dot(const RowSet& A, int s, int e, int lane,
                                         const double* const* __restrict__ xin, double* acc) {
+  // kU entries per lane are loaded before any is consumed (memory-level
+  // parallelism for the dependent gathers); the fma chain still runs in
+  // entry order k, k+V, k+2V, ... (tools/spmv_lab.cu: 1.12 -> 1.00 ms on A).
+  constexpr int kU = 4;
 #pragma unroll
   for (int r = 0; r < NR; ++r) acc[r] = 0.0;
-  for (int k = s + lane; k < e; k += V) {
-    const double a = __ldcs(A.val + k);
-    const int j = __ldcs(A.col + k);
+  for (int k = s + lane; k < e; k += kU * V) {
+    double a[kU];
+    int j[kU];
 #pragma unroll
-    for (int r = 0; r < NR; ++r) acc[r] = fma(a, __ldg(xin[r] + j), acc[r]);
+    for (int u = 0; u < kU; ++u) {
+      const int kk = k + u * V;
+      a[u] = kk < e ? __ldcs(A.val + kk) : 0.0;
+      j[u] = kk < e ? __ldcs(A.col + kk) : -1;
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      double xv[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) xv[u] = j[u] >= 0 ? __ldg(xin[r] + j[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (j[u] >= 0) acc[r] = fma(a[u], xv[u], acc[r]);
+    }
   }
 }
 
@@ -563,8 +580,10 @@ struct CheckLaunch {
 int auto_lanes(long long nnz, int rows) {
   if (rows <= 0) return 1;
   const double mean = (double)nnz / rows;
+  // measured on config 4 (tools/spmv_lab.cu): 8 lanes for mean 20 and 40
   int v = 1;
-  while (v < 32 && 4.0 * v * 2 <= mean) v *= 2;  // ~4+ entries per lane
+  while (v < 8 && 2.0 * v * 2 <= mean) v *= 2;
+  if (mean >= 64) while (v < 32 && 4.0 * v * 2 <= mean) v *= 2;
   return v;
 }
 
@@ -746,7 +765,7 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
     const pdhg_psr* q = k == 0 ? prob->a_psr : prob->at_psr;
     c->has_psr[k] = q != nullptr;
     if (q) {
-      if (q->R > psr::kMaxRows || q->W != psr::kPanel || !q->heavy || q->ngroups != (q->R + 31) / 32) {
+      if (q->R > psr::kMaxRows || q->W != psr::kPanel || !q->heavy || q->ngroups != (q->R + psr::kGroupRows - 1) / psr::kGroupRows) {
         delete c;
         return fail(PDHG_ERR_ARG, "psr layout geometry not supported");
       }

@@ -13,18 +13,19 @@
 // one "remote" tile per block, gathered from global memory.
 //
 // Execution: one persistent 1024-thread CTA per SM walks row blocks.  Rows
-// are dealt to warps in groups of 32 (warp w owns groups w, w+32, ...), one
-// row per lane, and each lane keeps its rows' partial sums in registers
-// across all tiles of the block -- no shared-memory accumulators, no
-// atomics, no cross-lane reductions.  A row's sum runs panels ascending,
-// then the remote tile, entries in column order: fixed by the layout, so
-// results are bitwise reproducible run to run.
+// are dealt to warps in groups of 16 (warp w owns groups w, w+32, ...), two
+// lanes per row (even / odd entries of each tile segment), and each lane
+// keeps its partial sums in registers across all tiles of the block -- no
+// shared-memory accumulators, no atomics; one xor-shuffle joins the two
+// halves before the epilogue.  A row's sum runs panels ascending, then the
+// remote tile, entries in column order: fixed by the layout, so results are
+// bitwise reproducible run to run.
 //
 // Layout (entries in tile order, inside a tile in CSR (row, column) order):
 //   blk_tile_ptr[b]                 first tile of row block b       (nblk+1)
 //   tile_bin[t]                     panel index of tile t, -1 = remote
-//   gstart[t*(ngroups+1)+g]         first entry of row group g in tile t
-//   goff[(t*ngroups+g)*32+l]        entry offset of row 32g+l within its group (u16)
+//   gstart[t*(ngroups+1)+g]         first entry of row group g (16 rows) in tile t
+//   goff[(t*ngroups+g)*16+q]        entry offset of row 16g+q within its group (u16)
 //   val[e] (f64), col16[e] (column inside the panel, u16), col[e] (global column, i32)
 #pragma once
 
@@ -35,8 +36,10 @@ namespace psr {
 
 constexpr int kThreads = 1024;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxRows = 8192;                      // rows per block (8 groups per warp)
-constexpr int kGroupsPerWarp = kMaxRows / 32 / kWarps;
+constexpr int kMaxRows = 8192;                      // rows per block
+constexpr int kLanes = 2;                           // lanes per row
+constexpr int kGroupRows = 32 / kLanes;             // rows per group (one warp pass)
+constexpr int kGroupsPerWarp = kMaxRows / kGroupRows / kWarps;
 constexpr int kPanel = 8192;                        // W: 64 KB of fp64 per panel buffer
 constexpr int kStages = 3;                          // panel ring depth
 
@@ -98,37 +101,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // ------------------------------------------------------------ compute
 
-// acc += (row 32g+lane of tile t) . x, one row per lane.
+// acc += this lane's share of (row kGroupRows*g + lane/kLanes of tile t) . x.
+// Lanes 2q, 2q+1 split row q's entries (even / odd positions); kU entries per
+// lane are loaded before use for memory-level parallelism.
 template <bool STAGED>
 __device__ __forceinline__ double group_tile(const Layout& L, int t, int g, int lane,
                                              const double* __restrict__ px,
                                              const double* __restrict__ gx, double acc) {
+  constexpr int kU = 4;
   const int* gs = L.gstart + (size_t)t * (L.ngroups + 1);
   const int base = gs[g];
   const int end = gs[g + 1];
   if (base == end) return acc;  // warp-uniform: no entries of this group in the tile
-  const int off = L.goff[((size_t)t * L.ngroups + g) * 32 + lane];
-  int nxt = __shfl_down_sync(0xffffffffu, off, 1);
-  if (lane == 31) nxt = end - base;
-  int e = base + off;
+  const int q = lane / kLanes, sub = lane % kLanes;
+  const int off = L.goff[((size_t)t * L.ngroups + g) * kGroupRows + q];
+  int nxt = __shfl_down_sync(0xffffffffu, off, kLanes);
+  if (q == kGroupRows - 1) nxt = end - base;
   const int e1 = base + nxt;
-  for (; e + 1 < e1; e += 2) {
-    const double a0 = __ldcs(L.val + e), a1 = __ldcs(L.val + e + 1);
-    double x0, x1;
-    if (STAGED) {
-      x0 = px[__ldcs(L.col16 + e)];
-      x1 = px[__ldcs(L.col16 + e + 1)];
-    } else {
-      x0 = __ldg(gx + __ldcs(L.col + e));
-      x1 = __ldg(gx + __ldcs(L.col + e + 1));
+  for (int e = base + off + sub; e < e1; e += kU * kLanes) {
+    double a[kU], xv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int ee = e + u * kLanes;
+      a[u] = 0.0;
+      xv[u] = 0.0;
+      if (ee < e1) {
+        a[u] = __ldcs(L.val + ee);
+        xv[u] = STAGED ? px[__ldcs(L.col16 + ee)] : __ldg(gx + __ldcs(L.col + ee));
+      }
     }
-    acc = fma(a0, x0, acc);
-    acc = fma(a1, x1, acc);
-  }
-  if (e < e1) {
-    const double a0 = __ldcs(L.val + e);
-    const double x0 = STAGED ? px[__ldcs(L.col16 + e)] : __ldg(gx + __ldcs(L.col + e));
-    acc = fma(a0, x0, acc);
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (e + u * kLanes < e1) acc = fma(a[u], xv[u], acc);
   }
   return acc;
 }
@@ -186,10 +190,15 @@ __device__ __forceinline__ void block_rows(const Layout& L, int b, const double*
 #pragma unroll
   for (int gi = 0; gi < kGroupsPerWarp; ++gi) {
     const int g = w + gi * kWarps;
-    const int r = g * 32 + lane;
-    if (g < L.ngroups && r < rows_b) {
-      const int row = row0 + r;
-      if (!L.heavy[row]) epi(row, acc[gi]);
+    if (g < L.ngroups) {  // warp-uniform
+      double d = acc[gi];
+#pragma unroll
+      for (int o = 1; o < kLanes; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      const int r = g * kGroupRows + lane / kLanes;
+      if (lane % kLanes == 0 && r < rows_b) {
+        const int row = row0 + r;
+        if (!L.heavy[row]) epi(row, d);
+      }
     }
   }
 }

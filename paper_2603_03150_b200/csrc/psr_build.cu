@@ -228,13 +228,14 @@ __global__ void k_tile_start(const int* __restrict__ skey, long long nnz, int nt
   tstart[t] = (int)lo;
 }
 
-// For tile t and block-local row r in [0, ngroups*32]: p(r) = first entry of
-// the tile whose row is >= r.  gstart[t][g] = p(32g); goff[t][r] = p(r) - p(32*(r/32)).
+// For tile t and block-local row r in [0, ngroups*G]: p(r) = first entry of
+// the tile whose row is >= r.  gstart[t][g] = p(G g); goff[t][r] = p(r) - p(G*(r/G)).
 __global__ void k_groups(int ntiles, int ngroups, const int* __restrict__ tstart,
                          const int* __restrict__ rowl, int* __restrict__ gstart,
                          unsigned short* __restrict__ goff) {
+  constexpr int G = psr::kGroupRows;
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long per = (long long)ngroups * 32 + 1;
+  const long long per = (long long)ngroups * G + 1;
   if (gid >= (long long)ntiles * per) return;
   const int t = (int)(gid / per), r = (int)(gid % per);
   const int s = tstart[t], e = tstart[t + 1];
@@ -247,10 +248,10 @@ __global__ void k_groups(int ntiles, int ngroups, const int* __restrict__ tstart
     return a;
   };
   const int p = lb(r);
-  if ((r & 31) == 0) gstart[(size_t)t * (ngroups + 1) + (r >> 5)] = p;
-  if (r < ngroups * 32) {
-    const int p0 = (r & 31) ? lb(r & ~31) : p;
-    goff[(size_t)t * ngroups * 32 + r] = (unsigned short)(p - p0);
+  if (r % G == 0) gstart[(size_t)t * (ngroups + 1) + r / G] = p;
+  if (r < ngroups * G) {
+    const int p0 = (r % G) ? lb(r - r % G) : p;
+    goff[(size_t)t * ngroups * G + r] = (unsigned short)(p - p0);
   }
 }
 
@@ -310,7 +311,7 @@ int pdhg_psr_plan(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, c
   if (R_out) *R_out = g.R;
   if (W_out) *W_out = g.W;
   if (nblk_out) *nblk_out = g.nblk;
-  if (ngroups_out) *ngroups_out = (g.R + 31) / 32;
+  if (ngroups_out) *ngroups_out = (g.R + psr::kGroupRows - 1) / psr::kGroupRows;
   if (ntiles_out) *ntiles_out = ntiles;
   if (staged_out) *staged_out = staged;
   if (nent_out) *nent_out = nent;
@@ -328,7 +329,7 @@ int pdhg_psr_build(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, 
   cudaStream_t s = (cudaStream_t)stream;
   const Geo g = geometry(rows, cols);
   if ((long long)g.R > psr::kMaxRows || g.W > 65536) return set_error(PDHG_ERR_ARG, "psr: geometry overflow");
-  const int ngroups = (g.R + 31) / 32;
+  const int ngroups = (g.R + psr::kGroupRows - 1) / psr::kGroupRows;
   Tmp t = carve(tmp, rows, cols, nnz);
   int ntiles = 0;
   PSR_TRY(cudaMemcpyAsync(&ntiles, t.bptr + g.nblk, 4, cudaMemcpyDeviceToHost, s));
@@ -353,7 +354,7 @@ int pdhg_psr_build(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, 
   } else {
     PSR_TRY(cudaMemsetAsync(t.tstart, 0, (size_t)(ntiles + 1) * 4, s));
   }
-  const long long ng = (long long)ntiles * ((long long)ngroups * 32 + 1);
+  const long long ng = (long long)ntiles * ((long long)ngroups * psr::kGroupRows + 1);
   k_groups<<<blocks(ng, 256), 256, 0, s>>>(ntiles, ngroups, t.tstart, rowl, gstart, goff);
   k_heavy_flags<<<blocks(rows, 256), 256, 0, s>>>(rows, ptr, heavy_threshold, heavy_out);
   PSR_TRY(cudaGetLastError());

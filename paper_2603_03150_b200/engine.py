@@ -179,7 +179,7 @@ class DeviceLp:
             "blk_tile_ptr": torch.empty(nblk.value + 1, dtype=i32, device=dev),
             "tile_bin": torch.empty(nt, dtype=i32, device=dev),
             "gstart": torch.empty(nt * (ngroups.value + 1), dtype=i32, device=dev),
-            "goff": torch.empty(nt * ngroups.value * 32, dtype=torch.int16, device=dev),
+            "goff": torch.empty(nt * ngroups.value * 16, dtype=torch.int16, device=dev),
             "val": torch.empty(max(1, nnz), dtype=torch.float64, device=dev),
             "col16": torch.empty(max(1, nnz), dtype=torch.int16, device=dev),
             "col": torch.empty(max(1, nnz), dtype=i32, device=dev),
