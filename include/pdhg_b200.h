@@ -100,6 +100,12 @@ typedef struct pdhg_problem {
   const pdhg_psr* a_psr;   /* optional PSR layout of A  (dual step)   */
   const pdhg_psr* at_psr;  /* optional PSR layout of A' (primal step) */
   int32_t l2_persist;      /* 1: pin the gathered vector in L2 (persisting access-policy window) */
+  /* Sharding (multi-GPU).  This context owns rows [of A] that
+   * map to y-space slots [y_off, y_off+m) and rows [of A'] that map to
+   * x-space slots [x_off, x_off+n) of full (padded) vectors of length m_full
+   * and n_full; the column indices of A / A' are in x-space / y-space slots.
+   * 0 / 0 / 0 / 0 = unsharded (m_full = m, n_full = n). */
+  int32_t m_full, n_full, y_off, x_off;
 } pdhg_problem;
 
 typedef struct pdhg_ctx pdhg_ctx;
@@ -107,7 +113,8 @@ typedef struct pdhg_ctx pdhg_ctx;
 int pdhg_abi_version(void);
 const char* pdhg_last_error(void);
 
-/* Device workspace the caller must provide for a problem of size m x n. */
+/* Device workspace the caller must provide (m, n: full vector lengths --
+ * m_full, n_full when sharded). */
 size_t pdhg_workspace_bytes(int32_t m, int32_t n);
 
 /* Create / destroy an engine context bound to `stream` (a cudaStream_t). */
@@ -142,6 +149,11 @@ int pdhg_run_period(pdhg_ctx* ctx, int32_t iters, int64_t iter0, double tau_over
 #define PDHG_SPEC_BEST_Z 16
 int pdhg_check(pdhg_ctx* ctx, int32_t npts, const int32_t* specs, double* out_host);
 
+/* Same as pdhg_check but leaves the PDHG_NQ*npts scalars in device memory
+ * (pdhg_vector(ctx, PDHG_VEC_SCALARS)) without synchronising -- sharded
+ * hosts all-gather them and combine per-shard partials in rank order. */
+int pdhg_check_device(pdhg_ctx* ctx, int32_t npts, const int32_t* specs);
+
 /* Restart at point `which` (CUR or AVG): x, y, avg_x, avg_y <- that point
  * (pdhg.py:235-238). */
 int pdhg_restart(pdhg_ctx* ctx, int32_t which);
@@ -158,6 +170,39 @@ int pdhg_save_best(pdhg_ctx* ctx, int32_t which, int32_t flags);
 /* Copy point spec (as in pdhg_check) to host arrays (any may be NULL).
  * z is max(0, c - A'y) unless PDHG_SPEC_BEST_Z selects the stored best z. */
 int pdhg_fetch(pdhg_ctx* ctx, int32_t spec, double* x_host, double* y_host, double* z_host);
+
+/* Device vectors of the context (full, padded length), for host-driven
+ * exchanges between shards (NCCL all-gather or device copies). */
+#define PDHG_VEC_X 0
+#define PDHG_VEC_XE 1
+#define PDHG_VEC_XBAR 2
+#define PDHG_VEC_XBEST 3
+#define PDHG_VEC_ZBEST 4
+#define PDHG_VEC_TN1 5
+#define PDHG_VEC_TN2 6
+#define PDHG_VEC_Y 7
+#define PDHG_VEC_YBAR 8
+#define PDHG_VEC_YBEST 9
+#define PDHG_VEC_TM1 10
+#define PDHG_VEC_SCALARS 11
+void* pdhg_vector(pdhg_ctx* ctx, int32_t which);
+
+/* z = max(0, c - A'y) for this shard's rows of A' into z_slice (device). */
+int pdhg_reduced_costs(pdhg_ctx* ctx, int32_t spec, double* z_slice);
+
+/* Host-driven stepping (sharded execution exchanges vectors between the
+ * half steps): set the step parameters of the next steps (as
+ * pdhg_run_period does), launch one primal (primal=1) or dual half step
+ * number j, and read the first failing iteration (-1 = none, syncs). */
+int pdhg_set_step(pdhg_ctx* ctx, int64_t iter0, double tau_over_omega, double sigma_omega,
+                  double w0);
+int pdhg_half_step(pdhg_ctx* ctx, int32_t primal, int32_t j);
+int pdhg_fail_iter(pdhg_ctx* ctx, int64_t* fail_iter_out);
+
+/* Power-iteration building blocks for sharded hosts: *out_dev = sum v^2
+ * (fixed order) and v = w / s (IEEE division, pdhg.py:99). */
+int pdhg_sumsq(pdhg_ctx* ctx, const double* v, int64_t len, double* out_dev);
+int pdhg_div(pdhg_ctx* ctx, const double* w, double* v, int64_t len, double s);
 
 /* Average device time (ms) of one launch of kernel `which` (0 = primal
  * step over A' rows, 1 = dual step over A rows) over `reps` launches,

@@ -26,7 +26,12 @@ EXPORTS = (
     "pdhg_check", "pdhg_restart", "pdhg_save_best", "pdhg_fetch", "pdhg_time_kernel",
     "pdhg_transpose_tmp_bytes", "pdhg_transpose_csr",
     "pdhg_psr_tmp_bytes", "pdhg_psr_plan", "pdhg_psr_build",
+    "pdhg_check_device", "pdhg_vector", "pdhg_reduced_costs", "pdhg_set_step", "pdhg_half_step",
+    "pdhg_fail_iter", "pdhg_sumsq", "pdhg_div",
 )
+
+VEC = {name: i for i, name in enumerate(
+    ("x", "xe", "xbar", "xbest", "zbest", "tn1", "tn2", "y", "ybar", "ybest", "tm1", "scalars"))}
 
 
 class Psr(C.Structure):
@@ -54,6 +59,7 @@ class Problem(C.Structure):
         ("a_heavy", C.c_void_p), ("at_heavy", C.c_void_p),
         ("a_psr", C.POINTER(Psr)), ("at_psr", C.POINTER(Psr)),
         ("l2_persist", C.c_int32),
+        ("m_full", C.c_int32), ("n_full", C.c_int32), ("y_off", C.c_int32), ("x_off", C.c_int32),
     ]
 
 
@@ -107,6 +113,14 @@ def load():
              P(i32), P(i32), P(i32), P(i32), P(i32), P(i64), P(i64))
         _sig(lib, "pdhg_psr_build", C.c_int, i32, i32, i64, vp, vp, vp, i32, vp, szt, vp,
              vp, vp, vp, vp, vp, vp, vp, vp)
+        _sig(lib, "pdhg_check_device", C.c_int, vp, i32, P(i32))
+        _sig(lib, "pdhg_vector", vp, vp, i32)
+        _sig(lib, "pdhg_reduced_costs", C.c_int, vp, i32, vp)
+        _sig(lib, "pdhg_set_step", C.c_int, vp, i64, dbl, dbl, dbl)
+        _sig(lib, "pdhg_half_step", C.c_int, vp, i32, i32)
+        _sig(lib, "pdhg_fail_iter", C.c_int, vp, P(i64))
+        _sig(lib, "pdhg_sumsq", C.c_int, vp, vp, i64, vp)
+        _sig(lib, "pdhg_div", C.c_int, vp, vp, vp, i64, dbl)
         if lib.pdhg_abi_version() != 1:
             raise NativeError("libpdhg_b200.so ABI version mismatch")
         _lib = lib

@@ -227,22 +227,41 @@ __global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
     }
     return;
   }
-  const long long gid = (long long)(blockIdx.x - a.rs.n_heavy) * kBlock + threadIdx.x;
-  const int row = (int)(gid / V);
-  const int lane = threadIdx.x % V;
-  bool valid = row < a.rs.rows;
-  int s = 0, e = 0;
-  if (valid) {
-    s = a.rs.ptr[row];
-    e = a.rs.ptr[row + 1];
-    if (e - s > a.rs.heavy_threshold) { valid = false; e = s; }
+  // Light rows: a warp owns 32 consecutive rows.  It computes them in V
+  // passes of 32/V rows (V lanes per row, fixed lane order), parks row k's
+  // dot in lane k with one shuffle per pass, then all 32 lanes run the
+  // epilogue together -- full lane utilisation and coalesced x/c/avg
+  // traffic (v1 ran the epilogue on one lane in V: ncu showed ~110
+  // instructions per 32 entries, profiles/r01_csr_epilogue.md).
+  constexpr int G = 32 / V;
+  const int lane = threadIdx.x & 31;
+  const long long warp_id = ((long long)(blockIdx.x - a.rs.n_heavy) * kBlock + threadIdx.x) >> 5;
+  const long long row0 = warp_id * 32;
+  if (row0 >= a.rs.rows) return;  // warp-uniform
+  double mine = 0.0;
+  bool mine_valid = false;
+#pragma unroll 1
+  for (int pass = 0; pass < V; ++pass) {
+    const long long r = row0 + pass * G + lane / V;
+    bool valid = r < a.rs.rows;
+    int s = 0, e = 0;
+    if (valid) {
+      s = a.rs.ptr[r];
+      e = a.rs.ptr[r + 1];
+      if (e - s > a.rs.heavy_threshold) { valid = false; e = s; }
+    }
+    double acc[1];
+    row_dot<V, 1>(a.rs, s, e, lane % V, xin, acc);
+    const double d = group_sum<V>(acc[0]);
+    const int src = ((lane - pass * G) & (G - 1)) * V;
+    const double got = __shfl_sync(0xffffffffu, d, src);
+    const int vsrc = __shfl_sync(0xffffffffu, (int)valid, src);
+    if (lane / G == pass) { mine = got; mine_valid = vsrc != 0; }
   }
-  double acc[1];
-  row_dot<V, 1>(a.rs, s, e, lane, xin, acc);
-  const double d = group_sum<V>(acc[0]);
-  if (valid && lane == 0) {
-    if (PRIMAL) primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
-    else dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
+  if (mine_valid) {
+    const int row = (int)(row0 + lane);
+    if (PRIMAL) primal_epi(row, mine, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
+    else dual_epi(row, mine, a.cb, a.x, a.xbar, step, w, iter, P);
   }
 }
 
@@ -539,7 +558,8 @@ int dispatch_lanes(int lanes, Args&&... args) {
 }
 
 int grid_rows(const RowSet& rs, int lanes) {
-  return rs.n_heavy + (int)(((long long)rs.rows * lanes + kBlock - 1) / kBlock);
+  (void)lanes;  // a warp owns 32 rows whatever the lane count
+  return rs.n_heavy + (int)((rs.rows + (long long)kBlock - 1) / kBlock);
 }
 
 template <int V>
@@ -556,7 +576,7 @@ struct StepLaunch {
 template <int V>
 struct SpmvLaunch {
   static int run(const RowSet& rs, const double* in, double* out, cudaStream_t s) {
-    const int g = grid_rows(rs, V);
+    const int g = rs.n_heavy + (int)(((long long)rs.rows * V + kBlock - 1) / kBlock);
     if (g > 0) k_spmv<V><<<g, kBlock, 0, s>>>(rs, in, out);
     return 0;
   }
@@ -608,6 +628,8 @@ struct pdhg_ctx {
   StepParams* P_host;
   double* scal_host;
   std::map<int, cudaGraphExec_t> graphs;
+  int mf, nf;          // full (padded) lengths of the y- and x-space vectors
+  int yo, xo;          // this shard's slice offsets in them
   bool has_psr[2];     // [0] = A (dual), [1] = A' (primal)
   psr::Layout psr_l[2];
   size_t psr_smem[2];
@@ -679,13 +701,17 @@ struct StepLaunchEx {
 
 int launch_step(pdhg_ctx* c, bool primal, int j) {
   StepArgs a;
+  // gathers read the full (padded) vectors; the rows a shard owns are
+  // written through pointers offset to its slice
   if (primal) {
-    a.rs = c->At; a.gather = c->y; a.cb = c->prob.c; a.x = c->x; a.xe = c->xe; a.xbar = c->xbar;
+    a.rs = c->At; a.gather = c->y; a.cb = c->prob.c;
+    a.x = c->x + c->xo; a.xe = c->xe + c->xo; a.xbar = c->xbar + c->xo;
   } else {
-    a.rs = c->A; a.gather = c->xe; a.cb = c->prob.b; a.x = c->y; a.xe = nullptr; a.xbar = c->ybar;
+    a.rs = c->A; a.gather = c->xe; a.cb = c->prob.b;
+    a.x = c->y + c->yo; a.xe = nullptr; a.xbar = c->ybar + c->yo;
   }
   a.P = c->P;
-  const size_t win = (size_t)(primal ? c->prob.m : c->prob.n) * 8;
+  const size_t win = (size_t)(primal ? c->mf : c->nf) * 8;
   const int lanes = primal ? c->at_lanes : c->a_lanes;
   const int k = primal ? 1 : 0;
   if (c->has_psr[k]) {
@@ -740,7 +766,11 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
                     pdhg_ctx** out) {
   if (!prob || !out) return fail(PDHG_ERR_ARG, "null argument");
   if (prob->m <= 0 || prob->n <= 0) return fail(PDHG_ERR_ARG, "empty model");
-  if (workspace_bytes < carve_bytes(prob->m, prob->n))
+  const int mf = prob->m_full > 0 ? prob->m_full : prob->m;
+  const int nf = prob->n_full > 0 ? prob->n_full : prob->n;
+  if (prob->y_off < 0 || prob->x_off < 0 || prob->y_off + prob->m > mf || prob->x_off + prob->n > nf)
+    return fail(PDHG_ERR_ARG, "shard slice outside the full vectors");
+  if (workspace_bytes < carve_bytes(mf, nf))
     return fail(PDHG_ERR_ARG, "workspace too small");
   pdhg_ctx* c = new pdhg_ctx();
   c->prob = *prob;
@@ -752,7 +782,8 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->a_lanes = prob->a_lanes > 0 ? prob->a_lanes : auto_lanes(prob->nnz, prob->m);
   c->at_lanes = prob->at_lanes > 0 ? prob->at_lanes : auto_lanes(prob->nnz, prob->n);
   Carve cv{(char*)workspace};
-  const int n = prob->n, m = prob->m;
+  c->mf = mf; c->nf = nf; c->yo = prob->y_off; c->xo = prob->x_off;
+  const int n = nf, m = mf;
   c->x = cv.take<double>(n); c->xe = cv.take<double>(n); c->xbar = cv.take<double>(n);
   c->xbest = cv.take<double>(n); c->zbest = cv.take<double>(n);
   c->tn1 = cv.take<double>(n); c->tn2 = cv.take<double>(n);
@@ -821,6 +852,8 @@ int pdhg_opnorm(pdhg_ctx* c, const double* v0_host, double tol, int32_t max_iter
                 int32_t* iters_out) {
   // pdhg.py:80-109.  v (tn1) <- v0; loop: w (tn2) = A'(A v); ||w||; v = w/||w||.
   if (!c || !v0_host || !lam_out) return fail(PDHG_ERR_ARG, "null argument");
+  if (c->mf != c->prob.m || c->nf != c->prob.n)
+    return fail(PDHG_ERR_STATE, "pdhg_opnorm is single-shard; sharded hosts drive the power iteration");
   const int n = c->prob.n;
   CUDA_TRY(cudaMemcpyAsync(c->tn1, v0_host, (size_t)n * 8, cudaMemcpyHostToDevice, c->stream));
   double lam = 0.0;
@@ -856,7 +889,7 @@ int pdhg_opnorm(pdhg_ctx* c, const double* v0_host, double tol, int32_t max_iter
 
 int pdhg_reset(pdhg_ctx* c) {
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
-  const size_t nb = (size_t)c->prob.n * 8, mb = (size_t)c->prob.m * 8;
+  const size_t nb = (size_t)c->nf * 8, mb = (size_t)c->mf * 8;
   CUDA_TRY(cudaMemsetAsync(c->x, 0, nb, c->stream));
   CUDA_TRY(cudaMemsetAsync(c->xe, 0, nb, c->stream));
   CUDA_TRY(cudaMemsetAsync(c->xbar, 0, nb, c->stream));
@@ -902,24 +935,37 @@ int pdhg_run_period(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_over_o
   return 0;
 }
 
-int pdhg_check(pdhg_ctx* c, int32_t npts, const int32_t* specs, double* out_host) {
-  if (!c || !specs || !out_host || npts < 1 || npts > 2) return fail(PDHG_ERR_ARG, "bad argument");
-  CheckPts pts{};
+int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
+  if (!c || !specs || npts < 1 || npts > 2) return fail(PDHG_ERR_ARG, "bad argument");
+  // primal side (rows of A): gathers full x, row-indexed y slice;
+  // dual side (rows of A'): gathers full y, row-indexed x / z slices.
+  CheckPts pp{}, pd{};
   for (int p = 0; p < npts; ++p) {
-    point_xy(c, specs[p], &pts.x[p], &pts.y[p]);
-    pts.zin[p] = (specs[p] & PDHG_SPEC_BEST_Z) ? c->zbest : nullptr;
-    pts.zout[p] = nullptr;
+    const double *x, *y;
+    point_xy(c, specs[p], &x, &y);
+    pp.x[p] = x; pp.y[p] = y + c->yo; pp.zin[p] = nullptr; pp.zout[p] = nullptr;
+    pd.x[p] = x + c->xo; pd.y[p] = y;
+    pd.zin[p] = (specs[p] & PDHG_SPEC_BEST_Z) ? c->zbest + c->xo : nullptr;
+    pd.zout[p] = nullptr;
   }
   CUDA_TRY(cudaMemsetAsync(c->partials, 0, (size_t)kCheckBlocks * kMaxQ * 8, c->stream));
-  int rc = dispatch_lanes<CheckLaunch>(c->a_lanes, true, (int)npts, c->A, c->prob.b, pts, c->partials,
+  int rc = dispatch_lanes<CheckLaunch>(c->a_lanes, true, (int)npts, c->A, c->prob.b, pp, c->partials,
                                        c->stream);
   if (rc) return rc;
-  rc = dispatch_lanes<CheckLaunch>(c->at_lanes, false, (int)npts, c->At, c->prob.c, pts, c->partials,
+  rc = dispatch_lanes<CheckLaunch>(c->at_lanes, false, (int)npts, c->At, c->prob.c, pd, c->partials,
                                    c->stream);
   if (rc) return rc;
   const int nq = npts * PDHG_NQ;
   k_reduce<<<nq, kBlock, 0, c->stream>>>(c->partials, kCheckBlocks, kMaxQ, nq, c->scalars);
   CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int pdhg_check(pdhg_ctx* c, int32_t npts, const int32_t* specs, double* out_host) {
+  if (!out_host) return fail(PDHG_ERR_ARG, "null out_host");
+  int rc = pdhg_check_device(c, npts, specs);
+  if (rc) return rc;
+  const int nq = npts * PDHG_NQ;
   CUDA_TRY(cudaMemcpyAsync(c->scal_host, c->scalars, nq * sizeof(double), cudaMemcpyDeviceToHost,
                            c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -929,7 +975,7 @@ int pdhg_check(pdhg_ctx* c, int32_t npts, const int32_t* specs, double* out_host
 
 int pdhg_restart(pdhg_ctx* c, int32_t which) {
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
-  const size_t nb = (size_t)c->prob.n * 8, mb = (size_t)c->prob.m * 8;
+  const size_t nb = (size_t)c->nf * 8, mb = (size_t)c->mf * 8;
   if (which == PDHG_PT_CUR) {
     CUDA_TRY(cudaMemcpyAsync(c->xbar, c->x, nb, cudaMemcpyDeviceToDevice, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->ybar, c->y, mb, cudaMemcpyDeviceToDevice, c->stream));
@@ -942,21 +988,29 @@ int pdhg_restart(pdhg_ctx* c, int32_t which) {
   return 0;
 }
 
+int reduced_costs(pdhg_ctx* c, int32_t spec, double* z_slice) {
+  const double *x, *y;
+  point_xy(c, spec, &x, &y);
+  CheckPts pd{};
+  pd.x[0] = x + c->xo; pd.y[0] = y; pd.zin[0] = nullptr; pd.zout[0] = z_slice;
+  int rc = dispatch_lanes<CheckLaunch>(c->at_lanes, false, 1, c->At, c->prob.c, pd, c->partials,
+                                       c->stream);
+  if (rc) return rc;
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 int pdhg_save_best(pdhg_ctx* c, int32_t which, int32_t flags) {
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
   const double *x, *y;
   point_xy(c, which, &x, &y);
   if (flags & PDHG_BEST_Z) {
-    CheckPts pts{};
-    pts.x[0] = x; pts.y[0] = y; pts.zin[0] = nullptr; pts.zout[0] = c->zbest;
-    int rc = dispatch_lanes<CheckLaunch>(c->at_lanes, false, 1, c->At, c->prob.c, pts, c->partials,
-                                         c->stream);
+    int rc = reduced_costs(c, which, c->zbest + c->xo);
     if (rc) return rc;
-    CUDA_TRY(cudaGetLastError());
   }
   if ((flags & PDHG_BEST_XY) && (which & 3) != PDHG_PT_BEST) {
-    CUDA_TRY(cudaMemcpyAsync(c->xbest, x, (size_t)c->prob.n * 8, cudaMemcpyDeviceToDevice, c->stream));
-    CUDA_TRY(cudaMemcpyAsync(c->ybest, y, (size_t)c->prob.m * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->xbest, x, (size_t)c->nf * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->ybest, y, (size_t)c->mf * 8, cudaMemcpyDeviceToDevice, c->stream));
   }
   return 0;
 }
@@ -965,22 +1019,85 @@ int pdhg_fetch(pdhg_ctx* c, int32_t spec, double* x_host, double* y_host, double
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
   const double *x, *y;
   point_xy(c, spec, &x, &y);
-  const size_t nb = (size_t)c->prob.n * 8, mb = (size_t)c->prob.m * 8;
+  const size_t nb = (size_t)c->nf * 8, mb = (size_t)c->mf * 8;
   if (x_host) CUDA_TRY(cudaMemcpyAsync(x_host, x, nb, cudaMemcpyDeviceToHost, c->stream));
   if (y_host) CUDA_TRY(cudaMemcpyAsync(y_host, y, mb, cudaMemcpyDeviceToHost, c->stream));
   if (z_host) {
     if (spec & PDHG_SPEC_BEST_Z) {
       CUDA_TRY(cudaMemcpyAsync(z_host, c->zbest, nb, cudaMemcpyDeviceToHost, c->stream));
     } else {
-      CheckPts pts{};
-      pts.x[0] = x; pts.y[0] = y; pts.zin[0] = nullptr; pts.zout[0] = c->tn1;
-      int rc = dispatch_lanes<CheckLaunch>(c->at_lanes, false, 1, c->At, c->prob.c, pts, c->partials,
-                                           c->stream);
+      int rc = reduced_costs(c, spec, c->tn1 + c->xo);
       if (rc) return rc;
       CUDA_TRY(cudaMemcpyAsync(z_host, c->tn1, nb, cudaMemcpyDeviceToHost, c->stream));
     }
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+void* pdhg_vector(pdhg_ctx* c, int32_t which) {
+  if (!c) return nullptr;
+  switch (which) {
+    case PDHG_VEC_X: return c->x;
+    case PDHG_VEC_XE: return c->xe;
+    case PDHG_VEC_XBAR: return c->xbar;
+    case PDHG_VEC_XBEST: return c->xbest;
+    case PDHG_VEC_ZBEST: return c->zbest;
+    case PDHG_VEC_TN1: return c->tn1;
+    case PDHG_VEC_TN2: return c->tn2;
+    case PDHG_VEC_Y: return c->y;
+    case PDHG_VEC_YBAR: return c->ybar;
+    case PDHG_VEC_YBEST: return c->ybest;
+    case PDHG_VEC_TM1: return c->tm1;
+    case PDHG_VEC_SCALARS: return c->scalars;
+    default: fail(PDHG_ERR_ARG, "unknown vector id"); return nullptr;
+  }
+}
+
+int pdhg_reduced_costs(pdhg_ctx* c, int32_t spec, double* z_slice) {
+  if (!c || !z_slice) return fail(PDHG_ERR_ARG, "null argument");
+  return reduced_costs(c, spec, z_slice);
+}
+
+int pdhg_set_step(pdhg_ctx* c, int64_t iter0, double tau_over_omega, double sigma_omega, double w0) {
+  if (!c) return fail(PDHG_ERR_ARG, "null ctx");
+  CUDA_TRY(cudaStreamSynchronize(c->stream));  // the pinned staging struct is reused
+  StepParams& h = *c->P_host;
+  h.tau_w = tau_over_omega; h.sigma_w = sigma_omega; h.w0 = w0; h.iter0 = iter0;
+  h.fail_iter = LLONG_MAX;
+  CUDA_TRY(cudaMemcpyAsync(c->P, c->P_host, sizeof(StepParams), cudaMemcpyHostToDevice, c->stream));
+  return 0;
+}
+
+int pdhg_half_step(pdhg_ctx* c, int32_t primal, int32_t j) {
+  if (!c) return fail(PDHG_ERR_ARG, "null ctx");
+  int rc = launch_step(c, primal != 0, j);
+  if (rc) return rc;
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int pdhg_fail_iter(pdhg_ctx* c, int64_t* fail_iter_out) {
+  if (!c || !fail_iter_out) return fail(PDHG_ERR_ARG, "null argument");
+  CUDA_TRY(cudaMemcpyAsync(&c->P_host->fail_iter, &c->P->fail_iter, sizeof(long long),
+                           cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  *fail_iter_out = (c->P_host->fail_iter == LLONG_MAX) ? -1 : c->P_host->fail_iter;
+  return 0;
+}
+
+int pdhg_sumsq(pdhg_ctx* c, const double* v, int64_t len, double* out_dev) {
+  if (!c || !v || !out_dev || len < 0 || len >= INT_MAX) return fail(PDHG_ERR_ARG, "bad argument");
+  k_sumsq<<<kCheckBlocks, kBlock, 0, c->stream>>>(v, (int)len, c->partials);
+  k_reduce<<<1, kBlock, 0, c->stream>>>(c->partials, kCheckBlocks, 1, 1, out_dev);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int pdhg_div(pdhg_ctx* c, const double* w, double* v, int64_t len, double s) {
+  if (!c || !w || !v || len < 0 || len >= INT_MAX) return fail(PDHG_ERR_ARG, "bad argument");
+  if (len > 0) k_div<<<(unsigned)((len + kBlock - 1) / kBlock), kBlock, 0, c->stream>>>(w, v, s, (int)len);
+  CUDA_TRY(cudaGetLastError());
   return 0;
 }
 
