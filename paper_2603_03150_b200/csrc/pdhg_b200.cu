@@ -195,6 +195,28 @@ __device__ __forceinline__ void dual_epi(int i, double ax, const double* __restr
   if (!finite(yn)) atomicMin(&P->fail_iter, iter);
 }
 
+// Same epilogues with the row's operands already in registers.
+__device__ __forceinline__ void primal_epi_pre(int j, double aty, double cj, double xj, double xb,
+                                               double* __restrict__ x, double* __restrict__ xe,
+                                               double* __restrict__ xbar, double tau_w, double w,
+                                               long long iter, StepParams* P) {
+  const double g = __dsub_rn(cj, aty);
+  const double xn = np_max0(__dsub_rn(xj, __dmul_rn(tau_w, g)));
+  x[j] = xn;
+  xe[j] = __dsub_rn(__dmul_rn(2.0, xn), xj);
+  xbar[j] = __dadd_rn(xb, __ddiv_rn(__dsub_rn(xn, xb), w));
+  if (!finite(xn)) atomicMin(&P->fail_iter, iter);
+}
+
+__device__ __forceinline__ void dual_epi_pre(int i, double ax, double bi, double yi, double yb,
+                                             double* __restrict__ y, double* __restrict__ ybar,
+                                             double sigma_w, double w, long long iter, StepParams* P) {
+  const double yn = __dadd_rn(yi, __dmul_rn(sigma_w, __dsub_rn(bi, ax)));
+  y[i] = yn;
+  ybar[i] = __dadd_rn(yb, __ddiv_rn(__dsub_rn(yn, yb), w));
+  if (!finite(yn)) atomicMin(&P->fail_iter, iter);
+}
+
 struct StepArgs {
   RowSet rs;
   const double* __restrict__ gather;  // y (primal) or xe (dual)
@@ -238,30 +260,36 @@ __global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
   const long long warp_id = ((long long)(blockIdx.x - a.rs.n_heavy) * kBlock + threadIdx.x) >> 5;
   const long long row0 = warp_id * 32;
   if (row0 >= a.rs.rows) return;  // warp-uniform
+  // lane l fetches row (row0+l)'s extent and epilogue operands up front
+  // (coalesced, independent of the SpMV) and hands the extents out per pass
+  const long long rl = row0 + lane;
+  int my_s = 0, my_e = 0;
+  bool my_ok = rl < a.rs.rows;
+  double o1 = 0.0, o2 = 0.0, o3 = 0.0;
+  if (my_ok) {
+    my_s = a.rs.ptr[rl];
+    my_e = a.rs.ptr[rl + 1];
+    if (my_e - my_s > a.rs.heavy_threshold) { my_ok = false; my_e = my_s; }
+    o1 = a.cb[rl];
+    o2 = a.x[rl];
+    o3 = a.xbar[rl];
+  }
   double mine = 0.0;
-  bool mine_valid = false;
 #pragma unroll 1
   for (int pass = 0; pass < V; ++pass) {
-    const long long r = row0 + pass * G + lane / V;
-    bool valid = r < a.rs.rows;
-    int s = 0, e = 0;
-    if (valid) {
-      s = a.rs.ptr[r];
-      e = a.rs.ptr[r + 1];
-      if (e - s > a.rs.heavy_threshold) { valid = false; e = s; }
-    }
+    const int src = pass * G + lane / V;  // lane holding this group's row
+    const int s = __shfl_sync(0xffffffffu, my_s, src);
+    const int e = __shfl_sync(0xffffffffu, my_e, src);
     double acc[1];
     row_dot<V, 1>(a.rs, s, e, lane % V, xin, acc);
     const double d = group_sum<V>(acc[0]);
-    const int src = ((lane - pass * G) & (G - 1)) * V;
-    const double got = __shfl_sync(0xffffffffu, d, src);
-    const int vsrc = __shfl_sync(0xffffffffu, (int)valid, src);
-    if (lane / G == pass) { mine = got; mine_valid = vsrc != 0; }
+    const double got = __shfl_sync(0xffffffffu, d, ((lane - pass * G) & (G - 1)) * V);
+    if (lane / G == pass) mine = got;
   }
-  if (mine_valid) {
-    const int row = (int)(row0 + lane);
-    if (PRIMAL) primal_epi(row, mine, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
-    else dual_epi(row, mine, a.cb, a.x, a.xbar, step, w, iter, P);
+  if (my_ok) {
+    const int row = (int)rl;
+    if (PRIMAL) primal_epi_pre(row, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P);
+    else dual_epi_pre(row, mine, o1, o2, o3, a.x, a.xbar, step, w, iter, P);
   }
 }
 

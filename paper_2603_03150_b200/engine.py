@@ -90,7 +90,12 @@ class DeviceLp:
     library carves its iterate buffers from.
     """
 
-    def __init__(self, A, b, c, opts: GpuOptions):
+    def __init__(self, A, b, c, opts: GpuOptions, *, shard=None, stream=None):
+        """``shard`` (sharded.ShardBlock) makes this the context of one shard:
+        A is then the shard's row block with column indices in padded
+        x-space slots, ``shard.At`` its block of A' rows (CSR, y-space
+        slots), and the iterate vectors have the padded full lengths.
+        ``stream``: a torch.cuda.Stream to share (loopback shards)."""
         torch = _torch()
         self.lib = N.load()
         dev = torch.device("cuda", torch.cuda.current_device() if opts.device is None else opts.device)
@@ -101,9 +106,20 @@ class DeviceLp:
         nnz = int(A.nnz)
         if nnz >= 2**31 - 1:
             raise ValueError("nnz >= 2^31 is not supported by the int32 layout")
+        if shard is not None:
+            At = _as_csr(shard.At)
+            n = At.shape[0]                       # rows of A' this shard owns
+            m_full, n_full = shard.m_full, shard.n_full
+            y_off, x_off = shard.y_off, shard.x_off
+            if A.shape[1] != n_full or At.shape[1] != m_full or At.nnz != nnz:
+                raise ValueError("inconsistent shard block shapes")
+        else:
+            At = None
+            m_full, n_full, y_off, x_off = m, n, 0, 0
         self.m, self.n, self.nnz = m, n, nnz
+        self.m_full, self.n_full, self.y_off, self.x_off = m_full, n_full, y_off, x_off
         with torch.cuda.device(dev):
-            self.stream = torch.cuda.Stream(dev)
+            self.stream = stream if stream is not None else torch.cuda.Stream(dev)
             with torch.cuda.stream(self.stream):
                 t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
                 self.a_ptr = t(A.indptr, np.int32)
@@ -111,25 +127,32 @@ class DeviceLp:
                 self.a_val = t(A.data, np.float64)
                 self.b = t(b, np.float64)
                 self.c = t(c, np.float64)
-                self.at_ptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
-                self.at_col = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
-                self.at_val = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
                 sptr = self.stream.cuda_stream
-                tmp_bytes = self.lib.pdhg_transpose_tmp_bytes(nnz, m, n)
-                tmp = torch.empty(max(tmp_bytes, 1), dtype=torch.uint8, device=dev)
-                N.check(self.lib.pdhg_transpose_csr(
-                    m, n, nnz, self.a_ptr.data_ptr(), self.a_col.data_ptr(), self.a_val.data_ptr(),
-                    self.at_ptr.data_ptr(), self.at_col.data_ptr(), self.at_val.data_ptr(),
-                    tmp.data_ptr(), tmp_bytes, sptr))
+                tmp = None
+                if At is None:
+                    self.at_ptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
+                    self.at_col = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+                    self.at_val = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+                    tmp_bytes = self.lib.pdhg_transpose_tmp_bytes(nnz, m, n)
+                    tmp = torch.empty(max(tmp_bytes, 1), dtype=torch.uint8, device=dev)
+                    N.check(self.lib.pdhg_transpose_csr(
+                        m, n, nnz, self.a_ptr.data_ptr(), self.a_col.data_ptr(), self.a_val.data_ptr(),
+                        self.at_ptr.data_ptr(), self.at_col.data_ptr(), self.at_val.data_ptr(),
+                        tmp.data_ptr(), tmp_bytes, sptr))
+                else:
+                    self.at_ptr = t(At.indptr, np.int32)
+                    self.at_col = t(At.indices, np.int32)
+                    self.at_val = t(At.data, np.float64)
                 H = int(opts.heavy_threshold)
                 self.a_heavy = torch.nonzero((self.a_ptr[1:] - self.a_ptr[:-1]) > H).flatten().to(torch.int32)
                 self.at_heavy = torch.nonzero((self.at_ptr[1:] - self.at_ptr[:-1]) > H).flatten().to(torch.int32)
                 self.psr_info = {}
                 self._psr = {}
-                for key, rows, cols, ptr, col, val in (("A", m, n, self.a_ptr, self.a_col, self.a_val),
-                                                      ("At", n, m, self.at_ptr, self.at_col, self.at_val)):
+                for key, rows, cols, ptr, col, val in (
+                        ("A", m, n_full, self.a_ptr, self.a_col, self.a_val),
+                        ("At", n, m_full, self.at_ptr, self.at_col, self.at_val)):
                     self._psr[key] = self._build_psr(torch, dev, key, rows, cols, ptr, col, val, H, opts)
-                ws_bytes = self.lib.pdhg_workspace_bytes(m, n)
+                ws_bytes = self.lib.pdhg_workspace_bytes(m_full, n_full)
                 self.ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
                 self.stream.synchronize()
                 del tmp
@@ -145,6 +168,7 @@ class DeviceLp:
         p.a_psr = C.pointer(self._psr["A"][0]) if self._psr["A"] else None
         p.at_psr = C.pointer(self._psr["At"][0]) if self._psr["At"] else None
         p.l2_persist = 1 if opts.l2_persist else 0
+        p.m_full, p.n_full, p.y_off, p.x_off = m_full, n_full, y_off, x_off
         self._prob = p
         ctx = C.c_void_p()
         N.check(self.lib.pdhg_ctx_create(C.byref(p), self.ws.data_ptr(), ws_bytes,
@@ -226,9 +250,9 @@ class DeviceLp:
         N.check(self.lib.pdhg_save_best(self.ctx, which, flags))
 
     def fetch(self, spec: int, want_z: bool = True):
-        x = np.empty(self.n)
-        y = np.empty(self.m)
-        z = np.empty(self.n) if want_z else None
+        x = np.empty(self.n_full)
+        y = np.empty(self.m_full)
+        z = np.empty(self.n_full) if want_z else None
         N.check(self.lib.pdhg_fetch(self.ctx, spec, x.ctypes.data, y.ctypes.data,
                                     z.ctypes.data if want_z else None))
         return x, y, z
@@ -242,6 +266,62 @@ class DeviceLp:
             N.check(self.lib.pdhg_spmv(self.ctx, 1 if transpose else 0, vin.data_ptr(), out.data_ptr()))
             self.stream.synchronize()
             return out.cpu().numpy()
+
+    # --- sharded-execution building blocks (sharded.py) ---------------------
+    def vec(self, name: str):
+        """torch float64 view (full padded length) of one of the context's vectors."""
+        ptr = self.lib.pdhg_vector(self.ctx, N.VEC[name])
+        if not ptr:
+            N.check(-1)
+        off = ptr - self.ws.data_ptr()
+        count = 64 if name == "scalars" else (self.n_full if name in
+                                              ("x", "xe", "xbar", "xbest", "zbest", "tn1", "tn2")
+                                              else self.m_full)
+        return self.ws[off:off + 8 * count].view(self._torch.float64)
+
+    @property
+    def _torch(self):
+        import torch
+
+        return torch
+
+    def vec_ptr(self, name: str) -> int:
+        return self.lib.pdhg_vector(self.ctx, N.VEC[name])
+
+    def set_step(self, iter0: int, tau_w: float, sigma_w: float, w0: float):
+        N.check(self.lib.pdhg_set_step(self.ctx, int(iter0), float(tau_w), float(sigma_w), float(w0)))
+
+    def half_step(self, primal: bool, j: int):
+        N.check(self.lib.pdhg_half_step(self.ctx, 1 if primal else 0, int(j)))
+
+    def fail_iter(self) -> int:
+        f = C.c_int64()
+        N.check(self.lib.pdhg_fail_iter(self.ctx, C.byref(f)))
+        return int(f.value)
+
+    def check_device(self, *specs: int):
+        arr = (C.c_int32 * len(specs))(*specs)
+        N.check(self.lib.pdhg_check_device(self.ctx, len(specs), arr))
+        return self.vec("scalars")[:len(specs) * N.NQ]
+
+    def reduced_costs(self, spec: int, out_name: str):
+        N.check(self.lib.pdhg_reduced_costs(self.ctx, spec, self.vec_ptr(out_name) + 8 * self.x_off))
+
+    def spmv_named(self, transpose: bool, in_name: str, out_name: str):
+        """out[local slice] = (A or A') @ in (full vector)."""
+        off = self.x_off if transpose else self.y_off
+        N.check(self.lib.pdhg_spmv(self.ctx, 1 if transpose else 0, self.vec_ptr(in_name),
+                                   self.vec_ptr(out_name) + 8 * off))
+
+    def sumsq_named(self, name: str):
+        """sum of squares of this shard's x-space slice of `name` -> scalars[0] (device)."""
+        N.check(self.lib.pdhg_sumsq(self.ctx, self.vec_ptr(name) + 8 * self.x_off, self.n,
+                                    self.vec_ptr("scalars")))
+        return self.vec("scalars")[:1]
+
+    def div_named(self, src: str, dst: str, s: float):
+        N.check(self.lib.pdhg_div(self.ctx, self.vec_ptr(src) + 8 * self.x_off,
+                                  self.vec_ptr(dst) + 8 * self.x_off, self.n, float(s)))
 
     def time_kernel(self, which: int, reps: int, tau_w: float = 0.0, sigma_w: float = 0.0) -> float:
         ms = C.c_double()
