@@ -458,6 +458,16 @@ def run_pdhg(p, params=None, seed: int = 0, *, gpu: GpuOptions | None = None):
         return _run(T, dev, p, params, seed, opts, t0)
 
 
+def run_on_device(dev, p, params=None, seed: int = 0, *, gpu: GpuOptions | None = None):
+    """run_pdhg's control flow over an already-built device (DeviceLp or
+    sharded.ShardedDevice).  The clock starts here, after the layout build."""
+    T = resolve()
+    if params is None:
+        params = T.PdhgParams()
+    t0 = time.monotonic()
+    return _run(T, dev, p, params, seed, gpu or GpuOptions(), t0)
+
+
 def _run(T, dev: DeviceLp, p, params, seed, opts, t0):
     S = T.SolveStatus
     b = np.asarray(p.b, dtype=float)

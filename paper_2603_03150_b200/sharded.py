@@ -1,0 +1,398 @@
+"""Multi-GPU execution of the PDHG path: row/column sharding with all-gathers.
+
+Design.  For G shards:
+
+* rows of A are cut into G contiguous blocks of ~equal nnz (shard g owns
+  y-space rows [r_g, r_{g+1})), and columns of A -- rows of A' -- likewise
+  (shard g owns x-space rows [c_g, c_{g+1}));
+* every vector is stored at full, *padded* length: slice g of the y-space
+  vector is [g*maxR, g*maxR + (r_{g+1}-r_g)) with maxR = max block height,
+  so every slice has the same size and an in-place all-gather of equal
+  chunks completes the vector; matrix indices are remapped to these slots
+  once, on the host (monotone, so CSR column order is kept);
+* per iteration: primal half step on A' rows (gathers full y, writes the
+  x / xe / avg_x slice) -> all-gather xe -> dual half step on A rows
+  (gathers full xe, writes the y / avg_y slice) -> all-gather y;
+* at a check every shard scores its own rows; the per-shard partial sums and
+  maxima are all-gathered and combined in rank order, so every rank takes
+  the identical restart / termination decision (pdhg.py:206-247).
+
+``ShardedDevice`` exposes the same interface engine._run drives for one GPU
+(opnorm, reset, run_period, check, restart, save_best, fetch), so the host
+control flow is shared verbatim.  A shard backend is a DeviceLp (CUDA
+kernels behind the C ABI); a communicator moves slices between shards:
+
+* ``TorchComm``    -- one shard per process, torch.distributed all_gather
+                      (NCCL over NVLink on a B200 box; gloo in CPU tests);
+* ``LoopbackComm`` -- all G shards in one process on one device (tests the
+                      sharded kernels and the rank-order combine on 1 GPU);
+                      the all-gather is a set of device-to-device copies.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _native as N
+
+X_SPACE = ("x", "xe", "xbar", "xbest", "zbest", "tn1", "tn2")
+Y_SPACE = ("y", "ybar", "ybest", "tm1")
+
+
+# ----------------------------------------------------------------- partition
+
+
+def _cuts(counts_ptr: np.ndarray, G: int) -> np.ndarray:
+    """G+1 monotone cut points over rows with ~equal entries (ptr = cumulative counts)."""
+    total = int(counts_ptr[-1])
+    rows = counts_ptr.size - 1
+    cuts = [0]
+    for g in range(1, G):
+        c = int(np.searchsorted(counts_ptr, g * total / G, side="left"))
+        cuts.append(min(max(c, cuts[-1]), rows))
+    cuts.append(rows)
+    return np.asarray(cuts, dtype=np.int64)
+
+
+@dataclass
+class ShardBlock:
+    """What shard g needs: its A rows, its A' rows, b/c slices and slice offsets."""
+
+    g: int
+    A: sp.csr_matrix       # rows [r_g, r_g+1) of A, columns in x-space slots (width n_full)
+    At: sp.csr_matrix      # rows [c_g, c_g+1) of A', columns in y-space slots (width m_full)
+    b: np.ndarray
+    c: np.ndarray
+    m_full: int
+    n_full: int
+    y_off: int
+    x_off: int
+
+
+class ShardPlan:
+    """Equal-nnz row and column partition of A over G shards, with padded slots."""
+
+    def __init__(self, A, G: int):
+        A = sp.csr_matrix(A)
+        self.G = int(G)
+        self.m, self.n = A.shape
+        self.nnz = int(A.nnz)
+        self.rcut = _cuts(np.asarray(A.indptr, dtype=np.int64), self.G)
+        col_counts = np.bincount(A.indices, minlength=self.n)
+        cptr = np.zeros(self.n + 1, dtype=np.int64)
+        np.cumsum(col_counts, out=cptr[1:])
+        self.ccut = _cuts(cptr, self.G)
+        self.maxR = max(1, int(np.max(np.diff(self.rcut))))
+        self.maxC = max(1, int(np.max(np.diff(self.ccut))))
+        self.m_full = self.G * self.maxR
+        self.n_full = self.G * self.maxC
+        rg = np.repeat(np.arange(self.G), np.diff(self.rcut))
+        cg = np.repeat(np.arange(self.G), np.diff(self.ccut))
+        self.yslot = (rg * self.maxR + np.arange(self.m) - self.rcut[rg]).astype(np.int64)
+        self.xslot = (cg * self.maxC + np.arange(self.n) - self.ccut[cg]).astype(np.int64)
+
+    def block(self, g: int, A, b, c) -> ShardBlock:
+        A = sp.csr_matrix(A)
+        r0, r1 = int(self.rcut[g]), int(self.rcut[g + 1])
+        c0, c1 = int(self.ccut[g]), int(self.ccut[g + 1])
+        Ar = A[r0:r1]
+        Ag = sp.csr_matrix((Ar.data, self.xslot[Ar.indices].astype(np.int32), Ar.indptr),
+                           shape=(r1 - r0, self.n_full))
+        Ac = A[:, c0:c1].tocsc()   # CSC of the column block = CSR of its transpose
+        Atg = sp.csr_matrix((Ac.data, self.yslot[Ac.indices].astype(np.int32), Ac.indptr),
+                            shape=(c1 - c0, self.m_full))
+        return ShardBlock(g, Ag, Atg, np.asarray(b, float)[r0:r1], np.asarray(c, float)[c0:c1],
+                          self.m_full, self.n_full, g * self.maxR, g * self.maxC)
+
+    def slice_len(self, space: str) -> int:
+        return self.maxC if space == "x" else self.maxR
+
+
+# ------------------------------------------------------------- communicators
+
+
+class LoopbackComm:
+    """All shards in this process (one device): all-gather = device copies."""
+
+    def __init__(self, plan: ShardPlan):
+        self.plan = plan
+        self.rank, self.world = 0, plan.G
+        self.local = list(range(plan.G))
+
+    def allgather(self, shards, name: str):
+        L = self.plan.slice_len("x" if name in X_SPACE else "y")
+        views = [s.vec(name) for s in shards]
+        for g, src in enumerate(views):
+            part = src[g * L:(g + 1) * L]
+            for h, dst in enumerate(views):
+                if h != g:
+                    dst[g * L:(g + 1) * L].copy_(part)
+
+    def gather_rows(self, shards, per_shard):
+        """per_shard: one device tensor per local shard -> (G, k) numpy, rank order."""
+        return np.stack([t.double().cpu().numpy() for t in per_shard])
+
+    def allgather_int(self, value_per_shard):
+        return list(value_per_shard)
+
+
+class TorchComm:
+    """One shard per process over torch.distributed (NCCL on GPUs, gloo in tests)."""
+
+    def __init__(self, plan: ShardPlan, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.plan = plan
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.world != plan.G:
+            raise ValueError("world size must equal the number of shards")
+        self.local = [self.rank]
+
+    def allgather(self, shards, name: str):
+        (s,) = shards
+        L = self.plan.slice_len("x" if name in X_SPACE else "y")
+        full = s.vec(name)[:L * self.world]
+        mine = full[self.rank * L:(self.rank + 1) * L].clone()
+        self.dist.all_gather_into_tensor(full, mine, group=self.group)
+
+    def gather_rows(self, shards, per_shard):
+        import torch
+
+        (t,) = per_shard
+        out = torch.empty((self.world, t.numel()), dtype=t.dtype, device=t.device)
+        self.dist.all_gather_into_tensor(out.view(-1), t.contiguous(), group=self.group)
+        return out.double().cpu().numpy()
+
+    def allgather_int(self, value_per_shard):
+        import torch
+
+        (v,) = value_per_shard
+        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.tensor([int(v)], dtype=torch.int64, device=dev)
+        out = torch.empty(self.world, dtype=torch.int64, device=dev)
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+        return [int(u) for u in out.cpu()]
+
+
+# --------------------------------------------------------------- the device
+
+
+def _combine(rows: np.ndarray, npts: int) -> list[np.ndarray]:
+    """Rank-order combine of per-shard check partials: sums left to right,
+    maxima with NaN propagation (np.max semantics)."""
+    out = []
+    for p in range(npts):
+        blk = rows[:, p * N.NQ:(p + 1) * N.NQ]
+        q = np.zeros(N.NQ)
+        for k in range(N.NQ):
+            if k in (N.Q_RPMAX, N.Q_RDMAX):
+                v = blk[0, k]
+                for r in range(1, blk.shape[0]):
+                    w = blk[r, k]
+                    v = w if (w != w or w > v) and v == v else v
+                q[k] = v
+            else:
+                acc = 0.0
+                for r in range(blk.shape[0]):
+                    acc = acc + float(blk[r, k])
+                q[k] = acc
+        out.append(q)
+    return out
+
+
+class ShardedDevice:
+    """G shards behind engine._run's device interface (see module doc)."""
+
+    def __init__(self, plan: ShardPlan, shards, comm):
+        self.plan = plan
+        self.shards = list(shards)   # local shard backends, in comm.local order
+        self.comm = comm
+        self.m, self.n = plan.m, plan.n
+
+    def _on_stream(self):
+        """torch work (copies, collectives) must queue behind the kernels on
+        the shards' stream (loopback shards share one stream)."""
+        import contextlib
+
+        st = getattr(self.shards[0], "stream", None)
+        if st is None:
+            return contextlib.nullcontext()
+        import torch
+
+        return torch.cuda.stream(st)
+
+    def _ag(self, *names):
+        with self._on_stream():
+            for nm in names:
+                self.comm.allgather(self.shards, nm)
+
+    # -- power iteration (pdhg.py:80-109), host-driven across shards
+    def opnorm(self, v0: np.ndarray, tol: float = 1e-4, max_iters: int = 100) -> float:
+        full = np.zeros(self.plan.n_full)
+        full[self.plan.xslot] = v0
+        with self._on_stream():
+            for s in self.shards:
+                s.vec("tn1").copy_(_to_like(full, s.vec("tn1")))
+        lam = 0.0
+        for _ in range(max_iters):
+            norm_w = self._aat_norm()
+            if norm_w == 0.0:
+                break
+            new_lam = math.sqrt(norm_w)
+            for s in self.shards:
+                s.div_named("tn2", "tn1", norm_w)
+            self._ag("tn1")
+            if lam > 0 and abs(new_lam - lam) <= tol * new_lam:
+                lam = new_lam
+                break
+            lam = new_lam
+        norm_w = self._aat_norm()
+        if norm_w > 0:
+            lam = max(lam, float(math.sqrt(norm_w)))
+        return float(lam)
+
+    def _aat_norm(self) -> float:
+        for s in self.shards:
+            s.spmv_named(False, "tn1", "tm1")
+        self._ag("tm1")
+        for s in self.shards:
+            s.spmv_named(True, "tm1", "tn2")
+        with self._on_stream():
+            parts = self.comm.gather_rows(self.shards, [s.sumsq_named("tn2") for s in self.shards])
+        ss = 0.0
+        for r in range(parts.shape[0]):
+            ss = ss + float(parts[r, 0])
+        return math.sqrt(ss)
+
+    def reset(self):
+        for s in self.shards:
+            s.reset()
+
+    def run_period(self, iters: int, iter0: int, tau_w: float, sigma_w: float, w0: float) -> int:
+        for s in self.shards:
+            s.set_step(iter0, tau_w, sigma_w, w0)
+        for j in range(iters):
+            for s in self.shards:
+                s.half_step(True, j)
+            self._ag("xe")
+            for s in self.shards:
+                s.half_step(False, j)
+            self._ag("y")
+        with self._on_stream():
+            fails = self.comm.allgather_int([s.fail_iter() for s in self.shards])
+        bad = [f for f in fails if f >= 0]
+        return min(bad) if bad else -1
+
+    def _complete(self, spec: int):
+        which = spec & 3
+        xs = {N.PT_CUR: "x", N.PT_AVG: "xbar", N.PT_BEST: "xbest"}[which]
+        ys = {N.PT_CUR: "y", N.PT_AVG: "ybar", N.PT_BEST: "ybest"}[which]
+        self._ag(xs, ys)
+
+    def check(self, *specs: int):
+        for sp_ in specs:
+            self._complete(sp_)
+        with self._on_stream():
+            rows = self.comm.gather_rows(self.shards, [s.check_device(*specs) for s in self.shards])
+        return _combine(rows, len(specs))
+
+    def restart(self, which: int):
+        self._complete(which)
+        for s in self.shards:
+            s.restart(which)
+
+    def save_best(self, which: int, flags: int):
+        self._complete(which)
+        for s in self.shards:
+            s.save_best(which, flags)
+
+    def fetch(self, spec: int, want_z: bool = True):
+        self._complete(spec)
+        if want_z:
+            if spec & N.SPEC_BEST_Z:
+                self._ag("zbest")
+                zname = "zbest"
+            else:
+                for s in self.shards:
+                    s.reduced_costs(spec, "tn1")
+                self._ag("tn1")
+                zname = "tn1"
+        which = spec & 3
+        xs = {N.PT_CUR: "x", N.PT_AVG: "xbar", N.PT_BEST: "xbest"}[which]
+        ys = {N.PT_CUR: "y", N.PT_AVG: "ybar", N.PT_BEST: "ybest"}[which]
+        s0 = self.shards[0]
+        with self._on_stream():
+            x = _np(s0.vec(xs))[self.plan.xslot]
+            y = _np(s0.vec(ys))[self.plan.yslot]
+            z = _np(s0.vec(zname))[self.plan.xslot] if want_z else None
+        return x, y, z
+
+
+def _np(t) -> np.ndarray:
+    return t.detach().cpu().numpy().copy()
+
+
+def _to_like(a: np.ndarray, like):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(like.device)
+
+
+# ----------------------------------------------------------- entry points
+
+
+def build_sharded(p, G: int, comm_kind: str = "loopback", opts=None, group=None):
+    """ShardedDevice for StandardLp ``p`` over G shards of CUDA contexts.
+
+    comm_kind="loopback": all G shards on the current device (one process);
+    comm_kind="torch": this process's shard (rank) of a torch.distributed job.
+    """
+    import torch
+
+    from .engine import DeviceLp, GpuOptions
+
+    opts = opts or GpuOptions()
+    plan = ShardPlan(p.A, G)
+    if comm_kind == "loopback":
+        comm = LoopbackComm(plan)
+        stream = torch.cuda.Stream()
+        shards = [DeviceLp(blk.A, blk.b, blk.c, opts, shard=blk, stream=stream)
+                  for blk in (plan.block(g, p.A, p.b, p.c) for g in range(G))]
+    elif comm_kind == "torch":
+        comm = TorchComm(plan, group)
+        blk = plan.block(comm.rank, p.A, p.b, p.c)
+        shards = [DeviceLp(blk.A, blk.b, blk.c, opts, shard=blk)]
+    else:
+        raise ValueError(comm_kind)
+    return ShardedDevice(plan, shards, comm)
+
+
+def run_pdhg_sharded(p, params=None, seed: int = 0, *, G: int, comm_kind: str = "loopback",
+                     gpu=None, group=None):
+    """run_pdhg (pdhg.py:162-258) over G shards; same results contract."""
+    import threading
+    import time
+
+    from . import engine
+    from .lp_types import resolve
+
+    T = resolve()
+    opts = gpu or engine.GpuOptions()
+    if params is None:
+        params = T.PdhgParams()
+    m, n = p.A.shape
+    if m == 0 or n == 0:
+        raise T.InvalidModelError("pdhg requires a nonempty model")
+    t0 = time.monotonic()
+    if p.A.nnz == 0:
+        raise T.InvalidModelError("cannot estimate the norm of an empty matrix")
+    dev = build_sharded(p, G, comm_kind, opts, group)
+    dev.lock = threading.Lock()
+    return engine._run(T, dev, p, params, seed, opts, t0)

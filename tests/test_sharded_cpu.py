@@ -1,0 +1,155 @@
+"""Multi-GPU host logic on CPU: shard plan, rank-order combine, and a
+world_size-2 gloo run of the sharded engine (numpy shard doubles) against
+the oracle.  The CUDA shards are exercised on the GPU in test_gpu_sharded.py."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch.multiprocessing as mp
+
+import oracle
+from conftest import load_golden
+from oracle.pdhg_port import Model
+from paper_2603_03150_b200 import _native as N
+from paper_2603_03150_b200.sharded import ShardPlan, ShardedDevice, LoopbackComm, _combine
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 5])
+def test_shard_plan_reassembles_the_matrix(G):
+    gm = load_golden("config0_s0")
+    plan = ShardPlan(gm.A, G)
+    assert plan.rcut[0] == 0 and plan.rcut[-1] == gm.m
+    assert plan.ccut[0] == 0 and plan.ccut[-1] == gm.n
+    assert np.all(np.diff(plan.rcut) >= 0) and np.all(np.diff(plan.ccut) >= 0)
+    # slots are injective and monotone
+    assert np.all(np.diff(plan.yslot) > 0) and np.all(np.diff(plan.xslot) > 0)
+    assert plan.yslot.max() < plan.m_full and plan.xslot.max() < plan.n_full
+    # the blocks, mapped back to original coordinates, are A and A'
+    inv_x = np.full(plan.n_full, -1)
+    inv_x[plan.xslot] = np.arange(gm.n)
+    inv_y = np.full(plan.m_full, -1)
+    inv_y[plan.yslot] = np.arange(gm.m)
+    rows, cols = [], []
+    trows, tcols = [], []
+    nnz_per = []
+    for g in range(G):
+        blk = plan.block(g, gm.A, gm.b, gm.c)
+        Ab = blk.A.tocoo()
+        rows.append(Ab.row + plan.rcut[g])
+        cols.append(inv_x[Ab.col])
+        At = blk.At.tocoo()
+        trows.append(At.row + plan.ccut[g])
+        tcols.append(inv_y[At.col])
+        nnz_per.append(blk.A.nnz)
+        np.testing.assert_array_equal(blk.b, gm.b[plan.rcut[g]:plan.rcut[g + 1]])
+        np.testing.assert_array_equal(blk.c, gm.c[plan.ccut[g]:plan.ccut[g + 1]])
+    R = sp.coo_matrix((np.ones(sum(map(len, rows))), (np.concatenate(rows), np.concatenate(cols))),
+                      shape=gm.A.shape).tocsr()
+    assert (R != (gm.A != 0)).nnz == 0
+    T = sp.coo_matrix((np.ones(sum(map(len, trows))), (np.concatenate(trows), np.concatenate(tcols))),
+                      shape=(gm.n, gm.m)).tocsr()
+    assert (T != (gm.A.T != 0)).nnz == 0
+    # balanced: no shard holds much more than its share of entries
+    assert max(nnz_per) <= gm.A.nnz / G + gm.A.getnnz(axis=1).max() + 1
+
+
+def test_combine_is_rank_ordered_and_nan_propagating():
+    rows = np.zeros((3, N.NQ))
+    rows[:, N.Q_RP2] = [1e16, 1.0, -1e16]
+    rows[:, N.Q_RPMAX] = [1.0, np.nan, 2.0]
+    rows[:, N.Q_RDMAX] = [1.0, 3.0, 2.0]
+    (q,) = _combine(rows, 1)
+    assert q[N.Q_RP2] == ((1e16 + 1.0) + -1e16)
+    assert np.isnan(q[N.Q_RPMAX])
+    assert q[N.Q_RDMAX] == 3.0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, name, eps, limit, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch.distributed as dist
+
+    from conftest import load_golden
+    from paper_2603_03150_b200 import engine
+    from paper_2603_03150_b200.lp_types import resolve
+    from paper_2603_03150_b200.sharded import ShardPlan, ShardedDevice, TorchComm
+    from shard_double import NumpyShard
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        gm = load_golden(name)
+        plan = ShardPlan(gm.A, world)
+        comm = TorchComm(plan)
+        dev = ShardedDevice(plan, [NumpyShard(plan.block(rank, gm.A, gm.b, gm.c))], comm)
+        T = resolve()
+        pt, st = engine.run_on_device(dev, gm, T.PdhgParams(eps_rel=eps, max_kkt_passes=limit))
+        q.put((rank, st.status.value, st.iterations, st.restarts, pt.x, pt.y, pt.z,
+               st.termination.primal_lhs))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,eps,limit", [("config0_s0", 1e-4, 200_000),
+                                            ("eq_20x35_s17_ruiz", 1e-6, 200_000),
+                                            ("eq_10x18_s7_ruiz", 1e-12, 200)])
+def test_gloo_two_ranks_match_oracle(name, eps, limit):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, eps, limit, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    gm = load_golden(name)
+    opt, ost = oracle.run_pdhg(Model(gm.A, gm.b, gm.c),
+                               oracle.PdhgParams(eps_rel=eps, max_kkt_passes=limit))
+    (_, s0, it0, rs0, x0, y0, z0, pl0), (_, s1, it1, rs1, x1, y1, z1, pl1) = res
+    # every rank took the same decisions and returns the same point
+    assert (s0, it0, rs0) == (s1, it1, rs1)
+    np.testing.assert_array_equal(x0, x1)
+    np.testing.assert_array_equal(y0, y1)
+    assert pl0 == pl1
+    # and it is the reference's run (sums combined per shard: rounding only)
+    assert s0 == ost.status.value
+    assert it0 == ost.iterations and rs0 == ost.restarts
+    np.testing.assert_allclose(x0, opt.x, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(y0, opt.y, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(z0, opt.z, rtol=1e-9, atol=1e-12)
+
+
+def test_loopback_numpy_three_shards_match_oracle():
+    """Loopback communicator over three numpy shards in one process."""
+    from shard_double import NumpyShard
+
+    from paper_2603_03150_b200 import engine
+    from paper_2603_03150_b200.lp_types import resolve
+
+    gm = load_golden("config0_s0")
+    plan = ShardPlan(gm.A, 3)
+    shards = [NumpyShard(plan.block(g, gm.A, gm.b, gm.c)) for g in range(3)]
+    dev = ShardedDevice(plan, shards, LoopbackComm(plan))
+    T = resolve()
+    pt, st = engine.run_on_device(dev, gm, T.PdhgParams(eps_rel=1e-4))
+    opt, ost = oracle.run_pdhg(Model(gm.A, gm.b, gm.c), oracle.PdhgParams(eps_rel=1e-4))
+    assert st.iterations == ost.iterations and st.restarts == ost.restarts
+    np.testing.assert_allclose(pt.x, opt.x, rtol=1e-9, atol=1e-12)
