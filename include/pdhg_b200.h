@@ -106,6 +106,7 @@ typedef struct pdhg_problem {
    * and n_full; the column indices of A / A' are in x-space / y-space slots.
    * 0 / 0 / 0 / 0 = unsharded (m_full = m, n_full = n). */
   int32_t m_full, n_full, y_off, x_off;
+  int64_t at_nnz;          /* entries of the A' block (0 = nnz; differs from nnz when sharded) */
 } pdhg_problem;
 
 typedef struct pdhg_ctx pdhg_ctx;

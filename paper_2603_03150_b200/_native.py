@@ -60,6 +60,7 @@ class Problem(C.Structure):
         ("a_psr", C.POINTER(Psr)), ("at_psr", C.POINTER(Psr)),
         ("l2_persist", C.c_int32),
         ("m_full", C.c_int32), ("n_full", C.c_int32), ("y_off", C.c_int32), ("x_off", C.c_int32),
+        ("at_nnz", C.c_int64),
     ]
 
 

@@ -808,7 +808,8 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->At = RowSet{prob->at_ptr, prob->at_col, prob->at_val, prob->n, prob->heavy_threshold,
                  prob->at_n_heavy, prob->at_heavy};
   c->a_lanes = prob->a_lanes > 0 ? prob->a_lanes : auto_lanes(prob->nnz, prob->m);
-  c->at_lanes = prob->at_lanes > 0 ? prob->at_lanes : auto_lanes(prob->nnz, prob->n);
+  c->at_lanes = prob->at_lanes > 0 ? prob->at_lanes
+                                    : auto_lanes(prob->at_nnz > 0 ? prob->at_nnz : prob->nnz, prob->n);
   Carve cv{(char*)workspace};
   c->mf = mf; c->nf = nf; c->yo = prob->y_off; c->xo = prob->x_off;
   const int n = nf, m = mf;

@@ -111,12 +111,13 @@ class DeviceLp:
             n = At.shape[0]                       # rows of A' this shard owns
             m_full, n_full = shard.m_full, shard.n_full
             y_off, x_off = shard.y_off, shard.x_off
-            if A.shape[1] != n_full or At.shape[1] != m_full or At.nnz != nnz:
+            if A.shape[1] != n_full or At.shape[1] != m_full:
                 raise ValueError("inconsistent shard block shapes")
         else:
             At = None
             m_full, n_full, y_off, x_off = m, n, 0, 0
         self.m, self.n, self.nnz = m, n, nnz
+        self.at_nnz = int(At.nnz) if At is not None else nnz
         self.m_full, self.n_full, self.y_off, self.x_off = m_full, n_full, y_off, x_off
         with torch.cuda.device(dev):
             self.stream = stream if stream is not None else torch.cuda.Stream(dev)
@@ -148,10 +149,11 @@ class DeviceLp:
                 self.at_heavy = torch.nonzero((self.at_ptr[1:] - self.at_ptr[:-1]) > H).flatten().to(torch.int32)
                 self.psr_info = {}
                 self._psr = {}
-                for key, rows, cols, ptr, col, val in (
-                        ("A", m, n_full, self.a_ptr, self.a_col, self.a_val),
-                        ("At", n, m_full, self.at_ptr, self.at_col, self.at_val)):
-                    self._psr[key] = self._build_psr(torch, dev, key, rows, cols, ptr, col, val, H, opts)
+                for key, rows, cols, nz, ptr, col, val in (
+                        ("A", m, n_full, nnz, self.a_ptr, self.a_col, self.a_val),
+                        ("At", n, m_full, self.at_nnz, self.at_ptr, self.at_col, self.at_val)):
+                    self._psr[key] = self._build_psr(torch, dev, key, rows, cols, nz, ptr, col, val,
+                                                     H, opts)
                 ws_bytes = self.lib.pdhg_workspace_bytes(m_full, n_full)
                 self.ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
                 self.stream.synchronize()
@@ -169,6 +171,7 @@ class DeviceLp:
         p.at_psr = C.pointer(self._psr["At"][0]) if self._psr["At"] else None
         p.l2_persist = 1 if opts.l2_persist else 0
         p.m_full, p.n_full, p.y_off, p.x_off = m_full, n_full, y_off, x_off
+        p.at_nnz = self.at_nnz
         self._prob = p
         ctx = C.c_void_p()
         N.check(self.lib.pdhg_ctx_create(C.byref(p), self.ws.data_ptr(), ws_bytes,
@@ -177,12 +180,11 @@ class DeviceLp:
         self._fin = weakref.finalize(self, self.lib.pdhg_ctx_destroy, ctx)
         self._scal = (C.c_double * (2 * N.NQ))()
 
-    def _build_psr(self, torch, dev, key, rows, cols, ptr, col, val, H, opts):
+    def _build_psr(self, torch, dev, key, rows, cols, nnz, ptr, col, val, H, opts):
         """Plan + build the PSR layout of one operator on the device (or None)."""
         if opts.psr == "off" or (opts.psr == "auto" and rows < opts.psr_min_rows):
             return None
         lib = self.lib
-        nnz = self.nnz
         sptr = self.stream.cuda_stream
         tb = lib.pdhg_psr_tmp_bytes(rows, cols, nnz)
         tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=dev)
