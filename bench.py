@@ -195,7 +195,7 @@ def run_reference(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_iter * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
         "config": {"workload": f"config4 (m={inst.m}, n={inst.n}, nnz={inst.nnz}) PDHG iteration",
                    "scale": args.scale, "seed": args.seed},
@@ -219,14 +219,21 @@ def run_ours(args):
     import paper_2603_03150_b200 as eng
     from paper_2603_03150_b200 import _native as N
 
-    inst = _instance(args.scale, args.seed + rank)  # replicas: one LP per rank (no sharding yet)
+    inst = _instance(args.scale, args.seed)  # every rank builds the same LP; N>1 shards it
     T = eng.types()
     m, n, nnz = inst.m, inst.n, inst.nnz
     ab = algorithmic_bytes(m, n, nnz)
+    opts = eng.GpuOptions(cache_layout=False, psr=args.psr)
 
     # ---- device-resident timing: K periods of 64 iterations + check
     t_setup = time.perf_counter()
-    dev = eng.DeviceLp(inst.A, inst.b, inst.c, eng.GpuOptions(cache_layout=False))
+    if world > 1:
+        from paper_2603_03150_b200.sharded import build_sharded
+
+        dev = build_sharded(inst, world, "torch", opts)
+        kdev = dev.shards[0]   # this rank's shard context (kernel timing)
+    else:
+        dev = kdev = eng.DeviceLp(inst.A, inst.b, inst.c, opts)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
     rng = np.random.default_rng(0)
@@ -240,7 +247,7 @@ def run_ours(args):
         dev.run_period(CHECK_EVERY, it, step, step, float(it))
         dev.check(N.PT_CUR, N.PT_AVG)
         it += CHECK_EVERY
-    s = dev.stream
+    s = kdev.stream
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -260,12 +267,16 @@ def run_ours(args):
         ms = float(t.item())
         dist.barrier()
     iters = args.steps * CHECK_EVERY
-    value = world * iters / (ms / 1e3)
+    value = iters / (ms / 1e3)   # iterations of the one LP per second, all ranks together
     ms_per_step = ms / args.steps
+    if world > 1:   # kernel roofline below is for this rank's shard
+        ab = algorithmic_bytes(kdev.m, kdev.n, kdev.nnz)
+        ab["primal"] = 12 * kdev.at_nnz + 4 * (kdev.n + 1) + 8 * kdev.m_full + 48 * kdev.n
+        ab["dual"] = 12 * kdev.nnz + 4 * (kdev.m + 1) + 8 * kdev.n_full + 40 * kdev.m
 
     # ---- per-kernel timing for the roofline (CUDA events on the engine stream)
     reps = 20
-    tk = {"primal": dev.time_kernel(0, reps, step, step), "dual": dev.time_kernel(1, reps, step, step)}
+    tk = {"primal": kdev.time_kernel(0, reps, step, step), "dual": kdev.time_kernel(1, reps, step, step)}
     top = max(tk, key=tk.get)
     peaks = _peaks()
     peak = peaks["hbm_gbs"] if peaks else 6650.0
@@ -284,7 +295,7 @@ def run_ours(args):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
                 "kernels_ms": tk, "algorithmic_bytes": ab,
                 "iteration_gbs": (ab["iter"] + ab["check"] / CHECK_EVERY) / (iter_ms * 1e-3) / 1e9}
-    del dev
+    del dev, kdev
     torch.cuda.empty_cache()
 
     # ---- e2e through the public drop-in call, host arrays in, host arrays out
@@ -294,18 +305,27 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     t0 = time.perf_counter()
-    pt, st = eng.run_pdhg(inst, params, gpu=eng.GpuOptions(cache_layout=False))
+    if world > 1:
+        from paper_2603_03150_b200.sharded import run_pdhg_sharded
+
+        pt, st = run_pdhg_sharded(inst, params, G=world, comm_kind="torch", gpu=opts)
+    else:
+        pt, st = eng.run_pdhg(inst, params, gpu=opts)
     e1.record()
     torch.cuda.synchronize()
     wall_e2e = time.perf_counter() - t0
     e2e_ms = e0.elapsed_time(e1)
-    e2e_value = world * st.iterations / (e2e_ms / 1e3)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = st.iterations / (e2e_ms / 1e3)
     h2d = 12 * nnz + 4 * (m + 1) + 8 * (m + n) + 8 * n
     d2h = 8 * (2 * n + m)
 
     out = None
-    if args.ttk:
-        pt2, st2 = eng.run_pdhg(inst, T.PdhgParams(eps_rel=1e-4, time_limit_s=args.ttk_limit))
+    if args.ttk and world == 1:
+        pt2, st2 = eng.run_pdhg(inst, T.PdhgParams(eps_rel=1e-4, time_limit_s=args.ttk_limit), gpu=opts)
         out = {"status": st2.status.value, "iterations": st2.iterations, "restarts": st2.restarts,
                "wall_s": st2.wall_seconds}
 
@@ -323,11 +343,13 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"config4 (m={m}, n={n}, nnz={nnz}) PDHG period = 64 iterations + KKT check",
                    "scale": args.scale, "seed": args.seed,
                    "l2": "no flush: 4.8 GB matrix > 126 MB L2 (inputs larger than L2)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+                   "parallelism": (f"A rows / A' rows sharded x{world}, equal nnz; NCCL all-gather of "
+                                   "xe and y per iteration" if world > 1 else "1 GPU"),
+                   "kernel_layout": "psr" if args.psr == "on" else "csr-vector"},
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / K,
                 "d2h_bytes_per_step": d2h / K, "iterations": st.iterations,
@@ -356,6 +378,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ttk", action="store_true", help="also run to eps_rel=1e-4 (time-to-1e-4)")
     ap.add_argument("--ttk-limit", type=float, default=300.0)
+    ap.add_argument("--psr", default="off", choices=["off", "on", "auto"],
+                    help="step-kernel layout (off = CSR-vector, the measured fastest)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

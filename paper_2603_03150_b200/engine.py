@@ -56,7 +56,7 @@ class GpuOptions:
     heavy_threshold: int = 1024
     opnorm: float | None = None
     cache_layout: bool = True
-    psr: str = "auto"
+    psr: str = "off"
     psr_min_staged: int = 1024
     psr_min_fraction: float = 0.3
     psr_min_rows: int = 148 * 256
