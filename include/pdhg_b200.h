@@ -99,7 +99,7 @@ typedef struct pdhg_problem {
   const int32_t* at_heavy; /* device list of heavy rows of A' */
   const pdhg_psr* a_psr;   /* optional PSR layout of A  (dual step)   */
   const pdhg_psr* at_psr;  /* optional PSR layout of A' (primal step) */
-  int32_t l2_persist;      /* 1: pin the gathered vector in L2 (persisting access-policy window) */
+  int32_t l2_persist;      /* bit0/bit1: pin y (primal step) / xe (dual step) in L2 with a persisting access-policy window */
   /* Sharding (multi-GPU).  This context owns rows [of A] that
    * map to y-space slots [y_off, y_off+m) and rows [of A'] that map to
    * x-space slots [x_off, x_off+n) of full (padded) vectors of length m_full

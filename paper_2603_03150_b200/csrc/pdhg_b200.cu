@@ -662,6 +662,7 @@ struct pdhg_ctx {
   psr::Layout psr_l[2];
   size_t psr_smem[2];
   int l2_persist, l2_maxwin;
+  int l2_mask;         // bit0: window on y for the primal step, bit1: on xe for the dual step
 };
 
 namespace {
@@ -720,10 +721,11 @@ int launch_ex(const pdhg_ctx* c, K kernel, dim3 grid, dim3 block, size_t smem, c
 
 template <int V>
 struct StepLaunchEx {
-  static int run(const pdhg_ctx* c, bool primal, const StepArgs& a, int j, int grid, size_t win) {
+  static int run(const pdhg_ctx* c, bool primal, const StepArgs& a, int j, int grid,
+                 const void* win_base, size_t win) {
     if (grid == 0) return 0;
-    if (primal) return launch_ex(c, k_step<V, true>, dim3(grid), dim3(kBlock), 0, a.gather, win, a, j);
-    return launch_ex(c, k_step<V, false>, dim3(grid), dim3(kBlock), 0, a.gather, win, a, j);
+    if (primal) return launch_ex(c, k_step<V, true>, dim3(grid), dim3(kBlock), 0, win_base, win, a, j);
+    return launch_ex(c, k_step<V, false>, dim3(grid), dim3(kBlock), 0, win_base, win, a, j);
   }
 };
 
@@ -740,20 +742,21 @@ int launch_step(pdhg_ctx* c, bool primal, int j) {
   }
   a.P = c->P;
   const size_t win = (size_t)(primal ? c->mf : c->nf) * 8;
+  const void* win_base = (c->l2_mask & (primal ? 1 : 2)) ? a.gather : nullptr;
   const int lanes = primal ? c->at_lanes : c->a_lanes;
   const int k = primal ? 1 : 0;
   if (c->has_psr[k]) {
     PsrStepArgs pa{c->psr_l[k], a.gather, a.cb, a.x, a.xe, a.xbar, a.P};
     const int grid = std::min(c->psr_l[k].nblk, 148);
     int rc = primal ? launch_ex(c, k_step_psr<true>, dim3(grid), dim3(psr::kThreads), c->psr_smem[k],
-                                a.gather, win, pa, j)
+                                win_base, win, pa, j)
                     : launch_ex(c, k_step_psr<false>, dim3(grid), dim3(psr::kThreads), c->psr_smem[k],
-                                a.gather, win, pa, j);
+                                win_base, win, pa, j);
     if (rc) return rc;
     // heavy rows: block per row through the CSR kernel (grid = n_heavy => no light rows)
-    return dispatch_lanes<StepLaunchEx>(lanes, c, primal, a, j, a.rs.n_heavy, win);
+    return dispatch_lanes<StepLaunchEx>(lanes, c, primal, a, j, a.rs.n_heavy, win_base, win);
   }
-  return dispatch_lanes<StepLaunchEx>(lanes, c, primal, a, j, grid_rows(a.rs, lanes), win);
+  return dispatch_lanes<StepLaunchEx>(lanes, c, primal, a, j, grid_rows(a.rs, lanes), win_base, win);
 }
 
 int spmv(pdhg_ctx* c, bool transpose, const double* in, double* out) {
@@ -841,7 +844,8 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
     int maxp = 0, maxw = 0;
     cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
     cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-    c->l2_persist = prob->l2_persist ? maxp : 0;
+    c->l2_mask = prob->l2_persist & 3;
+    c->l2_persist = c->l2_mask ? maxp : 0;
     c->l2_maxwin = maxw;
     if (c->l2_persist > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp);
     cudaGetLastError();

@@ -47,7 +47,8 @@ class GpuOptions:
                      kernels (csrc/psr.cuh); auto uses it when >= psr_min_fraction of
                      the entries fall in staged panels and the operator has enough rows.
     psr_min_staged:  entries a (row block, panel) needs to be staged in shared memory.
-    l2_persist:      pin the gathered vector in L2 with a persisting access window.
+    l2_persist:      bit mask: 1 = pin y in L2 for the primal step, 2 = pin xe for the
+                     dual step (persisting access-policy window; L2 holds 79 MB persisting).
     """
 
     device: int | None = None
@@ -60,7 +61,7 @@ class GpuOptions:
     psr_min_staged: int = 1024
     psr_min_fraction: float = 0.3
     psr_min_rows: int = 148 * 256
-    l2_persist: bool = False
+    l2_persist: int = 0
 
 
 def _torch():
@@ -169,7 +170,7 @@ class DeviceLp:
         p.at_heavy = self.at_heavy.data_ptr() if p.at_n_heavy else None
         p.a_psr = C.pointer(self._psr["A"][0]) if self._psr["A"] else None
         p.at_psr = C.pointer(self._psr["At"][0]) if self._psr["At"] else None
-        p.l2_persist = 1 if opts.l2_persist else 0
+        p.l2_persist = int(opts.l2_persist) & 3
         p.m_full, p.n_full, p.y_off, p.x_off = m_full, n_full, y_off, x_off
         p.at_nnz = self.at_nnz
         self._prob = p

@@ -18,7 +18,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--reps", type=int, default=20)
-    ap.add_argument("--variants", default="csr,csr_l2,psr,psr_l2")
+    ap.add_argument("--variants", default="csr,csr_l2d,csr_l2p,csr_l2")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -32,10 +32,12 @@ def main():
     print(f"gen {time.time() - t:.1f}s m={inst.m} n={inst.n} nnz={inst.nnz}", flush=True)
     ab = algorithmic_bytes(inst.m, inst.n, inst.nnz)
     variants = {
-        "csr": dict(psr="off", l2_persist=False),
-        "csr_l2": dict(psr="off", l2_persist=True),
-        "psr": dict(psr="on", l2_persist=False),
-        "psr_l2": dict(psr="on", l2_persist=True),
+        "csr": dict(psr="off", l2_persist=0),
+        "csr_l2d": dict(psr="off", l2_persist=2),
+        "csr_l2p": dict(psr="off", l2_persist=1),
+        "csr_l2": dict(psr="off", l2_persist=3),
+        "psr": dict(psr="on", l2_persist=0),
+        "psr_l2d": dict(psr="on", l2_persist=2),
     }
     out = {}
     for name in args.variants.split(","):
@@ -46,7 +48,16 @@ def main():
         dev.reset()
         tp = dev.time_kernel(0, args.reps, 1e-3, 1e-3)
         td = dev.time_kernel(1, args.reps, 1e-3, 1e-3)
-        out[name] = {"build_s": build, "primal_ms": tp, "dual_ms": td,
+        # alternating primal/dual as in a real period (graph of 64 iterations)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dev.run_period(64, 0, 1e-3, 1e-3, 0.0)
+        ev0.record(dev.stream)
+        for k in range(3):
+            dev.run_period(64, 64 * (k + 1), 1e-3, 1e-3, float(64 * (k + 1)))
+        ev1.record(dev.stream)
+        torch.cuda.synchronize()
+        per_iter = ev0.elapsed_time(ev1) / (3 * 64)
+        out[name] = {"build_s": build, "primal_ms": tp, "dual_ms": td, "iter_ms": per_iter,
                      "primal_gbs": ab["primal"] / tp / 1e6, "dual_gbs": ab["dual"] / td / 1e6,
                      "psr": dev.psr_info}
         print(name, json.dumps(out[name]), flush=True)
