@@ -132,8 +132,9 @@ __device__ __forceinline__ void row_dot(const RowSet& A, int s, int e, int lane,
                                         const double* const* __restrict__ xin, double* acc) {
   // kU entries per lane are loaded before any is consumed (memory-level
   // parallelism for the dependent gathers); the fma chain still runs in
-  // entry order k, k+V, k+2V, ... (tools/spmv_lab.cu: 1.12 -> 1.00 ms on A).
-  constexpr int kU = 4;
+  // entry order k, k+V, k+2V, ...  (V, kU) from tools/spmv_lab.cu on config 4
+  // (profiles/r01_spmv_lab2.log): (16, 4) for mean-40 rows, (8, 2) for mean 20.
+  constexpr int kU = V >= 16 ? 4 : 2;
 #pragma unroll
   for (int r = 0; r < NR; ++r) acc[r] = 0.0;
   for (int k = s + lane; k < e; k += kU * V) {
@@ -155,6 +156,39 @@ __device__ __forceinline__ void row_dot(const RowSet& A, int s, int e, int lane,
         if (j[u] >= 0) acc[r] = fma(a[u], xv[u], acc[r]);
     }
   }
+}
+
+// Light rows, one warp per 32 consecutive rows: lane l fetches row
+// (row0+l)'s extent (coalesced), the rows are computed in V passes of 32/V
+// rows with V lanes each (row_dot's fixed lane order + butterfly), and row
+// row0+l's dot is parked in lane l, so the caller's epilogue runs on all 32
+// lanes with coalesced traffic (v1 ran it on one lane in V: ~110
+// instructions per 32 entries in ncu).  ok = row exists and is not heavy.
+template <int V>
+__device__ __forceinline__ double warp_rows_dot(const RowSet& rs, long long row0, int lane,
+                                                const double* const* __restrict__ xin, bool& ok) {
+  constexpr int G = 32 / V;
+  const long long rl = row0 + lane;
+  int my_s = 0, my_e = 0;
+  ok = rl < rs.rows;
+  if (ok) {
+    my_s = rs.ptr[rl];
+    my_e = rs.ptr[rl + 1];
+    if (my_e - my_s > rs.heavy_threshold) { ok = false; my_e = my_s; }
+  }
+  double mine = 0.0;
+#pragma unroll 1
+  for (int pass = 0; pass < V; ++pass) {
+    const int src = pass * G + lane / V;  // lane holding this group's row
+    const int s = __shfl_sync(0xffffffffu, my_s, src);
+    const int e = __shfl_sync(0xffffffffu, my_e, src);
+    double acc[1];
+    row_dot<V, 1>(rs, s, e, lane % V, xin, acc);
+    const double d = group_sum<V>(acc[0]);
+    const double got = __shfl_sync(0xffffffffu, d, ((lane - pass * G) & (G - 1)) * V);
+    if (lane / G == pass) mine = got;
+  }
+  return mine;
 }
 
 // Device-resident per-period parameters (updated by one H2D copy per period
@@ -255,37 +289,21 @@ __global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
   // epilogue together -- full lane utilisation and coalesced x/c/avg
   // traffic (v1 ran the epilogue on one lane in V: ncu showed ~110
   // instructions per 32 entries, profiles/r01_csr_epilogue.md).
-  constexpr int G = 32 / V;
   const int lane = threadIdx.x & 31;
   const long long warp_id = ((long long)(blockIdx.x - a.rs.n_heavy) * kBlock + threadIdx.x) >> 5;
   const long long row0 = warp_id * 32;
   if (row0 >= a.rs.rows) return;  // warp-uniform
-  // lane l fetches row (row0+l)'s extent and epilogue operands up front
-  // (coalesced, independent of the SpMV) and hands the extents out per pass
   const long long rl = row0 + lane;
-  int my_s = 0, my_e = 0;
-  bool my_ok = rl < a.rs.rows;
+  const bool in_range = rl < a.rs.rows;
+  // epilogue operands first: coalesced and independent of the SpMV
   double o1 = 0.0, o2 = 0.0, o3 = 0.0;
-  if (my_ok) {
-    my_s = a.rs.ptr[rl];
-    my_e = a.rs.ptr[rl + 1];
-    if (my_e - my_s > a.rs.heavy_threshold) { my_ok = false; my_e = my_s; }
+  if (in_range) {
     o1 = a.cb[rl];
     o2 = a.x[rl];
     o3 = a.xbar[rl];
   }
-  double mine = 0.0;
-#pragma unroll 1
-  for (int pass = 0; pass < V; ++pass) {
-    const int src = pass * G + lane / V;  // lane holding this group's row
-    const int s = __shfl_sync(0xffffffffu, my_s, src);
-    const int e = __shfl_sync(0xffffffffu, my_e, src);
-    double acc[1];
-    row_dot<V, 1>(a.rs, s, e, lane % V, xin, acc);
-    const double d = group_sum<V>(acc[0]);
-    const double got = __shfl_sync(0xffffffffu, d, ((lane - pass * G) & (G - 1)) * V);
-    if (lane / G == pass) mine = got;
-  }
+  bool my_ok;
+  const double mine = warp_rows_dot<V>(a.rs, row0, lane, xin, my_ok);
   if (my_ok) {
     const int row = (int)rl;
     if (PRIMAL) primal_epi_pre(row, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P);
@@ -346,20 +364,12 @@ __global__ void __launch_bounds__(kBlock) k_spmv(RowSet rs, const double* __rest
     if (threadIdx.x == 0) out[row] = d;
     return;
   }
-  const long long gid = (long long)(blockIdx.x - rs.n_heavy) * kBlock + threadIdx.x;
-  const int row = (int)(gid / V);
-  const int lane = threadIdx.x % V;
-  bool valid = row < rs.rows;
-  int s = 0, e = 0;
-  if (valid) {
-    s = rs.ptr[row];
-    e = rs.ptr[row + 1];
-    if (e - s > rs.heavy_threshold) { valid = false; e = s; }
-  }
-  double acc[1];
-  row_dot<V, 1>(rs, s, e, lane, xin, acc);
-  const double d = group_sum<V>(acc[0]);
-  if (valid && lane == 0) out[row] = d;
+  const int lane = threadIdx.x & 31;
+  const long long row0 = (((long long)(blockIdx.x - rs.n_heavy) * kBlock + threadIdx.x) >> 5) * 32;
+  if (row0 >= rs.rows) return;
+  bool ok;
+  const double d = warp_rows_dot<V>(rs, row0, lane, xin, ok);
+  if (ok) out[row0 + lane] = d;
 }
 
 __global__ void k_div(const double* __restrict__ w, double* __restrict__ v, double s, int n) {
@@ -604,7 +614,7 @@ struct StepLaunch {
 template <int V>
 struct SpmvLaunch {
   static int run(const RowSet& rs, const double* in, double* out, cudaStream_t s) {
-    const int g = rs.n_heavy + (int)(((long long)rs.rows * V + kBlock - 1) / kBlock);
+    const int g = grid_rows(rs, V);
     if (g > 0) k_spmv<V><<<g, kBlock, 0, s>>>(rs, in, out);
     return 0;
   }
@@ -628,11 +638,14 @@ struct CheckLaunch {
 int auto_lanes(long long nnz, int rows) {
   if (rows <= 0) return 1;
   const double mean = (double)nnz / rows;
-  // measured on config 4 (tools/spmv_lab.cu): 8 lanes for mean 20 and 40
-  int v = 1;
-  while (v < 8 && 2.0 * v * 2 <= mean) v *= 2;
-  if (mean >= 64) while (v < 32 && 4.0 * v * 2 <= mean) v *= 2;
-  return v;
+  // measured on config 4 (tools/spmv_lab.cu, profiles/r01_spmv_lab2.log):
+  // 16 lanes for mean-40 rows (A), 8 for mean 20 (A')
+  if (mean >= 80) return 32;
+  if (mean >= 32) return 16;
+  if (mean >= 12) return 8;
+  if (mean >= 6) return 4;
+  if (mean >= 3) return 2;
+  return 1;
 }
 
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }

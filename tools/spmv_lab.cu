@@ -158,6 +158,96 @@ __global__ void __launch_bounds__(256) v3(Csr A, const double* __restrict__ x, d
   if (row < A.rows && lane == 0) y[row] = acc;
 }
 
+
+// ---- V5: library v3 scheme: warp owns 32 rows, V passes, extents prefetched, U-deep loads
+template <int V, int U>
+__global__ void __launch_bounds__(256) v5(Csr A, const double* __restrict__ x, double* __restrict__ y) {
+  constexpr int G = 32 / V;
+  const int lane = threadIdx.x & 31;
+  const long long row0 = (((long long)blockIdx.x * 256 + threadIdx.x) >> 5) * 32;
+  if (row0 >= A.rows) return;
+  const long long rl = row0 + lane;
+  int my_s = 0, my_e = 0;
+  if (rl < A.rows) { my_s = A.ptr[rl]; my_e = A.ptr[rl + 1]; }
+  double mine = 0.0;
+#pragma unroll 1
+  for (int pass = 0; pass < V; ++pass) {
+    const int src = pass * G + lane / V;
+    const int s = __shfl_sync(0xffffffffu, my_s, src);
+    const int e = __shfl_sync(0xffffffffu, my_e, src);
+    double acc = 0.0;
+    for (int k = s + lane % V; k < e; k += U * V) {
+      double a[U], xv[U];
+      int j[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kk = k + u * V;
+        a[u] = kk < e ? __ldcs(A.val + kk) : 0.0;
+        j[u] = kk < e ? __ldcs(A.col + kk) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = j[u] >= 0 ? __ldg(x + j[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) if (j[u] >= 0) acc = fma(a[u], xv[u], acc);
+    }
+    acc = gsum<V>(acc);
+    const double got = __shfl_sync(0xffffffffu, acc, ((lane - pass * G) & (G - 1)) * V);
+    if (lane / G == pass) mine = got;
+  }
+  if (rl < A.rows) y[rl] = mine;
+}
+
+// ---- V6: like V5 but two passes in flight (rows of pass p and p+1 interleaved)
+template <int V, int U>
+__global__ void __launch_bounds__(256) v6(Csr A, const double* __restrict__ x, double* __restrict__ y) {
+  constexpr int G = 32 / V;
+  const int lane = threadIdx.x & 31;
+  const long long row0 = (((long long)blockIdx.x * 256 + threadIdx.x) >> 5) * 32;
+  if (row0 >= A.rows) return;
+  const long long rl = row0 + lane;
+  int my_s = 0, my_e = 0;
+  if (rl < A.rows) { my_s = A.ptr[rl]; my_e = A.ptr[rl + 1]; }
+  double mine = 0.0;
+#pragma unroll 1
+  for (int pass = 0; pass < V; pass += 2) {
+    const int src0 = pass * G + lane / V, src1 = src0 + G;
+    const int s0 = __shfl_sync(0xffffffffu, my_s, src0), e0 = __shfl_sync(0xffffffffu, my_e, src0);
+    const int s1 = __shfl_sync(0xffffffffu, my_s, src1), e1 = __shfl_sync(0xffffffffu, my_e, src1);
+    double acc0 = 0.0, acc1 = 0.0;
+    const int n0 = e0 - s0, n1 = e1 - s1;
+    const int nmax = n0 > n1 ? n0 : n1;
+    for (int o = lane % V; o < nmax; o += U * V) {
+      double a0[U], a1[U], x0[U], x1[U];
+      int j0[U], j1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int oo = o + u * V;
+        a0[u] = oo < n0 ? __ldcs(A.val + s0 + oo) : 0.0;
+        j0[u] = oo < n0 ? __ldcs(A.col + s0 + oo) : -1;
+        a1[u] = oo < n1 ? __ldcs(A.val + s1 + oo) : 0.0;
+        j1[u] = oo < n1 ? __ldcs(A.col + s1 + oo) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        x0[u] = j0[u] >= 0 ? __ldg(x + j0[u]) : 0.0;
+        x1[u] = j1[u] >= 0 ? __ldg(x + j1[u]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (j0[u] >= 0) acc0 = fma(a0[u], x0[u], acc0);
+        if (j1[u] >= 0) acc1 = fma(a1[u], x1[u], acc1);
+      }
+    }
+    acc0 = gsum<V>(acc0);
+    acc1 = gsum<V>(acc1);
+    const double g0 = __shfl_sync(0xffffffffu, acc0, ((lane - pass * G) & (G - 1)) * V);
+    const double g1 = __shfl_sync(0xffffffffu, acc1, ((lane - (pass + 1) * G) & (G - 1)) * V);
+    if (lane / G == pass) mine = g0;
+    if (lane / G == pass + 1) mine = g1;
+  }
+  if (rl < A.rows) y[rl] = mine;
+}
+
 // ---- V4: one warp, several rows: 2 rows per 32-lane warp at V=16 etc. is V1/V2; skip.
 
 struct Timer {
@@ -237,6 +327,18 @@ int main(int argc, char** argv) {
     printf("== %s (rows=%d, mean %.1f)\n", op == 0 ? "A x" : "A' y", M.rows, (double)M.nnz / M.rows);
     if (op == 0) v1<8><<<grid(M.rows, 8), 256>>>(M, xin, yref); else v1<4><<<grid(M.rows, 4), 256>>>(M, xin, yref);
 #define RUN(NAME, K, VV) bench(NAME, M, [&] { K<<<grid(M.rows, VV), 256>>>(M, xin, ya); }, xin)
+#define RUNW(NAME, K) bench(NAME, M, [&] { K<<<(unsigned)((M.rows + 255) / 256), 256>>>(M, xin, ya); }, xin)
+    RUNW("v5<4,4>", (v5<4, 4>));
+    RUNW("v5<4,8>", (v5<4, 8>));
+    RUNW("v5<8,2>", (v5<8, 2>));
+    RUNW("v5<8,4>", (v5<8, 4>));
+    RUNW("v5<8,8>", (v5<8, 8>));
+    RUNW("v5<16,2>", (v5<16, 2>));
+    RUNW("v5<16,4>", (v5<16, 4>));
+    RUNW("v6<4,4>", (v6<4, 4>));
+    RUNW("v6<8,2>", (v6<8, 2>));
+    RUNW("v6<8,4>", (v6<8, 4>));
+    RUNW("v6<16,2>", (v6<16, 2>));
     RUN("v1<4>", v1<4>, 4);
     RUN("v1<8>", v1<8>, 8);
     RUN("v1<16>", v1<16>, 16);
@@ -245,12 +347,6 @@ int main(int argc, char** argv) {
     RUN("v2<8,2>", (v2<8, 2>), 8);
     RUN("v2<8,4>", (v2<8, 4>), 8);
     RUN("v2<16,2>", (v2<16, 2>), 16);
-    RUN("v3<2,2>", (v3<2, 2>), 2);
-    RUN("v3<4,1>", (v3<4, 1>), 4);
-    RUN("v3<4,2>", (v3<4, 2>), 4);
-    RUN("v3<8,1>", (v3<8, 1>), 8);
-    RUN("v3<8,2>", (v3<8, 2>), 8);
-    RUN("v3<16,1>", (v3<16, 1>), 16);
   }
   return 0;
 }
