@@ -240,6 +240,16 @@ int pdhg_psr_build(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, 
                    uint16_t* goff, double* val_out, uint16_t* col16_out, int32_t* col_out,
                    uint8_t* heavy_out);
 
+/* Ruiz equilibration on the device (hybridlp.transform.ruiz_equilibrate,
+ * transform.py:35-77), bit-identical scales and scaled values: val (CSR of
+ * A, nnz entries) is scaled in place; row_scale (m) and col_scale (n) are
+ * written; lo/hi = 1/(1+tol), 1+tol; *applied_out = passes applied.  The
+ * structural empty-row/column check (ScalingError) is the caller's. */
+size_t pdhg_ruiz_tmp_bytes(int32_t m, int32_t n);
+int pdhg_ruiz(int32_t m, int32_t n, int64_t nnz, const int32_t* ptr, const int32_t* col, double* val,
+              double* row_scale, double* col_scale, int32_t max_iters, double lo, double hi,
+              void* tmp, size_t tmp_bytes, void* stream, int32_t* applied_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -137,5 +137,42 @@ def main():
               f"restarts={int(d['run_e4_restarts'])} status={d['run_e4_status']}")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--ruiz" not in sys.argv:
     main()
+
+
+def ruiz_models():
+    """Unscaled standard-form models the reference's prepare_model would
+    equilibrate (transform.py:35-77), for the GPU Ruiz parity gate."""
+    out = {}
+    p, _ = hybridlp.to_standard_form(lp2().model)
+    out["ruiz_lp2"] = p
+    p, _ = hybridlp.to_standard_form(planted_equality_lp(40, 70, 20).model)
+    out["ruiz_eq_40x70"] = p
+    p, _ = hybridlp.to_standard_form(planted_inequality_lp(35, 60, 34).model)
+    out["ruiz_ineq_35x60"] = p
+    A, b, c, _, _ = config0_general(seed=0)
+    g = hybridlp.GeneralLp(c=c, A=A, senses=[hybridlp.EQ] * A.shape[0], rhs=b,
+                           lower=np.zeros(A.shape[1]), upper=np.full(A.shape[1], np.inf))
+    prep = hybridlp.warmstart.prepare_model(g, use_scaling=False)
+    out["ruiz_config0"] = prep.solve_model
+    return out
+
+
+def main_ruiz():
+    for name, p in ruiz_models().items():
+        A = p.A.tocsr()
+        scaled, info = hybridlp.ruiz_equilibrate(p)
+        S = scaled.A.tocsr()
+        np.savez_compressed(
+            OUT / f"{name}.npz",
+            numpy_version=np.__version__, scipy_version=scipy.__version__,
+            A_data=A.data, A_indices=A.indices, A_indptr=A.indptr, A_shape=np.array(A.shape),
+            b=p.b, c=p.c, row_scale=info.row_scale, col_scale=info.col_scale,
+            applied=np.array(info.applied_iterations), S_data=S.data, S_indices=S.indices,
+            S_indptr=S.indptr, Sb=scaled.b, Sc=scaled.c)
+        print(f"{name}: m={p.m} n={p.n} nnz={A.nnz} applied={info.applied_iterations}")
+
+
+if __name__ == "__main__" and "--ruiz" in sys.argv:
+    main_ruiz()

@@ -14,9 +14,10 @@ from __future__ import annotations
 
 from .engine import DeviceLp, GpuOptions, clear_cache, device_lp, estimate_opnorm, run_pdhg
 from .lp_types import resolve as types
+from .ruiz import ruiz_equilibrate
 
-__all__ = ["run_pdhg", "estimate_opnorm", "GpuOptions", "DeviceLp", "device_lp", "clear_cache",
-           "install", "uninstall", "types"]
+__all__ = ["run_pdhg", "estimate_opnorm", "ruiz_equilibrate", "GpuOptions", "DeviceLp", "device_lp",
+           "clear_cache", "install", "uninstall", "types"]
 
 # the four modules that bind `run_pdhg` at import time:
 # hybridlp/__init__.py:35, pdhg.py:162, warmstart.py:33, bench.py:24
@@ -24,20 +25,29 @@ _REBIND = ("hybridlp", "hybridlp.pdhg", "hybridlp.warmstart", "hybridlp.bench")
 _saved: dict = {}
 
 
-def install() -> None:
-    """Route every ``run_pdhg`` name of the reference package to this engine."""
+# ruiz_equilibrate is bound in transform.py:35 and imported into warmstart.py:42
+_REBIND_RUIZ = ("hybridlp", "hybridlp.transform", "hybridlp.warmstart")
+
+
+def install(ruiz: bool = False) -> None:
+    """Route every ``run_pdhg`` name of the reference package to this engine;
+    with ``ruiz=True`` also its ``ruiz_equilibrate`` (device Ruiz, whose
+    scaled matrix then stays on the device for the PDHG solve)."""
     import importlib
 
-    for name in _REBIND:
+    targets = [(n, "run_pdhg", run_pdhg) for n in _REBIND]
+    if ruiz:
+        targets += [(n, "ruiz_equilibrate", ruiz_equilibrate) for n in _REBIND_RUIZ]
+    for name, attr, fn in targets:
         mod = importlib.import_module(name)
-        if name not in _saved:
-            _saved[name] = getattr(mod, "run_pdhg")
-        setattr(mod, "run_pdhg", run_pdhg)
+        if (name, attr) not in _saved:
+            _saved[(name, attr)] = getattr(mod, attr)
+        setattr(mod, attr, fn)
 
 
 def uninstall() -> None:
     import importlib
 
-    for name, fn in list(_saved.items()):
-        setattr(importlib.import_module(name), "run_pdhg", fn)
-        del _saved[name]
+    for (name, attr), fn in list(_saved.items()):
+        setattr(importlib.import_module(name), attr, fn)
+        del _saved[(name, attr)]

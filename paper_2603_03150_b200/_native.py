@@ -27,7 +27,7 @@ EXPORTS = (
     "pdhg_transpose_tmp_bytes", "pdhg_transpose_csr",
     "pdhg_psr_tmp_bytes", "pdhg_psr_plan", "pdhg_psr_build",
     "pdhg_check_device", "pdhg_vector", "pdhg_reduced_costs", "pdhg_set_step", "pdhg_half_step",
-    "pdhg_fail_iter", "pdhg_sumsq", "pdhg_div",
+    "pdhg_fail_iter", "pdhg_sumsq", "pdhg_div", "pdhg_ruiz_tmp_bytes", "pdhg_ruiz",
 )
 
 VEC = {name: i for i, name in enumerate(
@@ -122,6 +122,9 @@ def load():
         _sig(lib, "pdhg_fail_iter", C.c_int, vp, P(i64))
         _sig(lib, "pdhg_sumsq", C.c_int, vp, vp, i64, vp)
         _sig(lib, "pdhg_div", C.c_int, vp, vp, vp, i64, dbl)
+        _sig(lib, "pdhg_ruiz_tmp_bytes", szt, i32, i32)
+        _sig(lib, "pdhg_ruiz", C.c_int, i32, i32, i64, vp, vp, vp, vp, vp, i32, dbl, dbl, vp, szt, vp,
+             P(i32))
         if lib.pdhg_abi_version() != 1:
             raise NativeError("libpdhg_b200.so ABI version mismatch")
         _lib = lib

@@ -91,12 +91,14 @@ class DeviceLp:
     library carves its iterate buffers from.
     """
 
-    def __init__(self, A, b, c, opts: GpuOptions, *, shard=None, stream=None):
+    def __init__(self, A, b, c, opts: GpuOptions, *, shard=None, stream=None, device_arrays=None):
         """``shard`` (sharded.ShardBlock) makes this the context of one shard:
         A is then the shard's row block with column indices in padded
         x-space slots, ``shard.At`` its block of A' rows (CSR, y-space
         slots), and the iterate vectors have the padded full lengths.
-        ``stream``: a torch.cuda.Stream to share (loopback shards)."""
+        ``stream``: a torch.cuda.Stream to share (loopback shards).
+        ``device_arrays``: (indptr, indices, data) of A already on the device
+        (e.g. the output of the device Ruiz pass) -- not uploaded again."""
         torch = _torch()
         self.lib = N.load()
         dev = torch.device("cuda", torch.cuda.current_device() if opts.device is None else opts.device)
@@ -124,9 +126,12 @@ class DeviceLp:
             self.stream = stream if stream is not None else torch.cuda.Stream(dev)
             with torch.cuda.stream(self.stream):
                 t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
-                self.a_ptr = t(A.indptr, np.int32)
-                self.a_col = t(A.indices, np.int32)
-                self.a_val = t(A.data, np.float64)
+                if device_arrays is not None:
+                    self.a_ptr, self.a_col, self.a_val = device_arrays
+                else:
+                    self.a_ptr = t(A.indptr, np.int32)
+                    self.a_col = t(A.indices, np.int32)
+                    self.a_val = t(A.data, np.float64)
                 self.b = t(b, np.float64)
                 self.c = t(c, np.float64)
                 sptr = self.stream.cuda_stream
@@ -377,6 +382,21 @@ def device_lp(p, opts: GpuOptions) -> DeviceLp:
             return lay
         _cache[key] = (ref, lay, fp, b.copy(), c.copy(), GpuOptions(**vars(opts)))
     return lay
+
+
+def _cache_register(p, lay: DeviceLp, opts: GpuOptions) -> None:
+    """Make `lay` the cached device layout of model `p` (used by the device
+    Ruiz pass, whose output matrix already lives on the device)."""
+    key = id(p)
+    try:
+        ref = weakref.ref(p, lambda _r, k=key: _cache.pop(k, None))
+    except TypeError:
+        return
+    with _cache_lock:
+        while len(_cache) >= _CACHE_MAX:
+            _cache.pop(next(iter(_cache)))
+        _cache[key] = (ref, lay, _fingerprint(p), np.asarray(p.b, dtype=float).copy(),
+                       np.asarray(p.c, dtype=float).copy(), GpuOptions(**vars(opts)))
 
 
 def clear_cache() -> None:

@@ -1,0 +1,101 @@
+"""Device Ruiz equilibration: drop-in for hybridlp.transform.ruiz_equilibrate.
+
+transform.py:35-77 runs right before the PDHG path (prepare_model,
+warmstart.py:178-197) and, on config 4, costs minutes on the CPU.  Here the
+passes run on the GPU (csrc/ruiz.cu) with the reference's exact arithmetic,
+so the scales and the scaled matrix are bit-identical to scipy's, and the
+scaled matrix can stay on the device: the returned model's device layout is
+registered in the engine's cache, so the following run_pdhg does not upload
+it again.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _native as N
+
+
+class _ScalingError(ValueError):
+    """Equilibration met a structurally empty row or column."""
+
+
+@dataclass
+class _ScalingInfo:
+    row_scale: np.ndarray
+    col_scale: np.ndarray
+    applied_iterations: int
+
+
+def _types():
+    try:
+        from hybridlp import lp_core, transform  # type: ignore
+
+        return transform.ScalingError, transform.ScalingInfo, lp_core.StandardLp
+    except ImportError:
+        from .instances import Instance
+
+        def make(A, b, c):
+            return Instance("scaled", A, b, c)
+
+        return _ScalingError, _ScalingInfo, make
+
+
+def ruiz_equilibrate(p, max_iters: int = 20, tol: float = 1e-2, *, gpu=None, register_layout=True):
+    """Iterative infinity-norm equilibration on the GPU (transform.py:35-77).
+
+    Returns (scaled StandardLp, ScalingInfo), the reference's classes when
+    hybridlp is importable.  Raises ScalingError on an empty row or column
+    exactly like the reference (transform.py:47-54).
+    """
+    import torch
+
+    from .engine import DeviceLp, GpuOptions, _as_csr, _cache_register
+
+    ScalingError, ScalingInfo, StandardLp = _types()
+    A = _as_csr(p.A)
+    A = sp.csr_matrix((A.data.copy(), A.indices.copy(), A.indptr.copy()), shape=A.shape)
+    m, n = A.shape
+    row_nnz = np.diff(A.indptr)
+    if (row_nnz == 0).any():
+        i = int(np.nonzero(row_nnz == 0)[0][0])
+        raise ScalingError(f"row {i} has no nonzero entries")
+    col_nnz = np.bincount(A.indices, minlength=n)
+    if (col_nnz == 0).any():
+        j = int(np.nonzero(col_nnz == 0)[0][0])
+        raise ScalingError(f"column {j} has no nonzero entries")
+    if not torch.cuda.is_available():
+        raise N.NativeError("ruiz_equilibrate needs a CUDA device; there is no CPU fallback")
+    lib = N.load()
+    opts = gpu or GpuOptions()
+    dev = torch.device("cuda", torch.cuda.current_device() if opts.device is None else opts.device)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.device(dev), torch.cuda.stream(stream):
+        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
+        ptr, col, val = t(A.indptr, np.int32), t(A.indices, np.int32), t(A.data, np.float64)
+        rs = torch.empty(m, dtype=torch.float64, device=dev)
+        cs = torch.empty(n, dtype=torch.float64, device=dev)
+        tb = lib.pdhg_ruiz_tmp_bytes(m, n)
+        tmp = torch.empty(tb, dtype=torch.uint8, device=dev)
+        applied = C.c_int32()
+        lo, hi = 1.0 / (1.0 + tol), 1.0 + tol                      # transform.py:59
+        N.check(lib.pdhg_ruiz(m, n, int(A.nnz), ptr.data_ptr(), col.data_ptr(), val.data_ptr(),
+                              rs.data_ptr(), cs.data_ptr(), int(max_iters), lo, hi,
+                              tmp.data_ptr(), tb, stream.cuda_stream, C.byref(applied)))
+        row_scale = rs.cpu().numpy()
+        col_scale = cs.cpu().numpy()
+        data = val.cpu().numpy()
+    S = sp.csr_matrix((data, A.indices, A.indptr), shape=A.shape)
+    b = row_scale * np.asarray(p.b, dtype=float)                    # transform.py:75
+    c = col_scale * np.asarray(p.c, dtype=float)
+    scaled = StandardLp(S, b, c)
+    info = ScalingInfo(row_scale, col_scale, int(applied.value))
+    if register_layout:
+        lay = DeviceLp(scaled.A, scaled.b, scaled.c, opts,
+                       device_arrays=(ptr, col, val), stream=stream)
+        _cache_register(scaled, lay, opts)
+    return scaled, info
