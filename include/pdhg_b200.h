@@ -107,6 +107,11 @@ typedef struct pdhg_problem {
    * 0 / 0 / 0 / 0 = unsharded (m_full = m, n_full = n). */
   int32_t m_full, n_full, y_off, x_off;
   int64_t at_nnz;          /* entries of the A' block (0 = nnz; differs from nnz when sharded) */
+  /* Optional split-K of the dual step over column chunks of A (see
+   * pdhg_split_build): a_nsplit passes, a_split = (a_nsplit-1) arrays of m
+   * split points.  1 / NULL = unsplit. */
+  int32_t a_nsplit;
+  const int32_t* a_split;
 } pdhg_problem;
 
 typedef struct pdhg_ctx pdhg_ctx;
@@ -210,6 +215,13 @@ int pdhg_div(pdhg_ctx* ctx, const double* w, double* v, int64_t len, double s);
  * CUDA events on the context stream.  The iterate is advanced. */
 int pdhg_time_kernel(pdhg_ctx* ctx, int32_t which, int32_t reps, double tau_over_omega,
                      double sigma_omega, double* avg_ms_out);
+
+/* Layout helper for the split dual step: split_out[(k-1)*m + i] = first
+ * entry of row i whose column is >= k*chunk, k = 1..K-1.  Rows must have
+ * sorted columns; *unsorted_out = 1 reports a row that has not (then do not
+ * split).  flag_dev: 4 bytes of device scratch. */
+int pdhg_split_build(int32_t m, const int32_t* ptr, const int32_t* col, int32_t K, int32_t chunk,
+                     int32_t* split_out, int32_t* flag_dev, void* stream, int32_t* unsorted_out);
 
 /* Layout helper: A' (CSR of the transpose, = CSC of A with rows ascending
  * in each column, as scipy's tocsc) from CSR A, all on the device.

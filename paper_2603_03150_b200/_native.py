@@ -28,6 +28,7 @@ EXPORTS = (
     "pdhg_psr_tmp_bytes", "pdhg_psr_plan", "pdhg_psr_build",
     "pdhg_check_device", "pdhg_vector", "pdhg_reduced_costs", "pdhg_set_step", "pdhg_half_step",
     "pdhg_fail_iter", "pdhg_sumsq", "pdhg_div", "pdhg_ruiz_tmp_bytes", "pdhg_ruiz",
+    "pdhg_split_build",
 )
 
 VEC = {name: i for i, name in enumerate(
@@ -61,6 +62,7 @@ class Problem(C.Structure):
         ("l2_persist", C.c_int32),
         ("m_full", C.c_int32), ("n_full", C.c_int32), ("y_off", C.c_int32), ("x_off", C.c_int32),
         ("at_nnz", C.c_int64),
+        ("a_nsplit", C.c_int32), ("a_split", C.c_void_p),
     ]
 
 
@@ -125,6 +127,7 @@ def load():
         _sig(lib, "pdhg_ruiz_tmp_bytes", szt, i32, i32)
         _sig(lib, "pdhg_ruiz", C.c_int, i32, i32, i64, vp, vp, vp, vp, vp, i32, dbl, dbl, vp, szt, vp,
              P(i32))
+        _sig(lib, "pdhg_split_build", C.c_int, i32, vp, vp, i32, i32, vp, vp, vp, P(i32))
         if lib.pdhg_abi_version() != 1:
             raise NativeError("libpdhg_b200.so ABI version mismatch")
         _lib = lib

@@ -164,17 +164,24 @@ __device__ __forceinline__ void row_dot(const RowSet& A, int s, int e, int lane,
 // row0+l's dot is parked in lane l, so the caller's epilogue runs on all 32
 // lanes with coalesced traffic (v1 ran it on one lane in V: ~110
 // instructions per 32 entries in ncu).  ok = row exists and is not heavy.
+// Segment form: row r's entries [sp[r], ep[r]) (a column chunk of the row
+// when the SpMV is split by columns); "heavy" is judged on the full row.
 template <int V>
-__device__ __forceinline__ double warp_rows_dot(const RowSet& rs, long long row0, int lane,
-                                                const double* const* __restrict__ xin, bool& ok) {
+__device__ __forceinline__ double warp_rows_dot_seg(const RowSet& rs, const int* __restrict__ sp,
+                                                    const int* __restrict__ ep, long long row0,
+                                                    int lane, const double* const* __restrict__ xin,
+                                                    bool& ok) {
   constexpr int G = 32 / V;
   const long long rl = row0 + lane;
   int my_s = 0, my_e = 0;
   ok = rl < rs.rows;
   if (ok) {
-    my_s = rs.ptr[rl];
-    my_e = rs.ptr[rl + 1];
-    if (my_e - my_s > rs.heavy_threshold) { ok = false; my_e = my_s; }
+    if (rs.ptr[rl + 1] - rs.ptr[rl] > rs.heavy_threshold) {
+      ok = false;
+    } else {
+      my_s = sp[rl];
+      my_e = ep[rl];
+    }
   }
   double mine = 0.0;
 #pragma unroll 1
@@ -189,6 +196,12 @@ __device__ __forceinline__ double warp_rows_dot(const RowSet& rs, long long row0
     if (lane / G == pass) mine = got;
   }
   return mine;
+}
+
+template <int V>
+__device__ __forceinline__ double warp_rows_dot(const RowSet& rs, long long row0, int lane,
+                                                const double* const* __restrict__ xin, bool& ok) {
+  return warp_rows_dot_seg<V>(rs, rs.ptr, rs.ptr + 1, row0, lane, xin, ok);
 }
 
 // Device-resident per-period parameters (updated by one H2D copy per period
@@ -253,6 +266,9 @@ __device__ __forceinline__ void dual_epi_pre(int i, double ax, double bi, double
 
 struct StepArgs {
   RowSet rs;
+  const int* __restrict__ split;      // column-chunk split points, (nsplit-1) arrays of rows
+  int nsplit;                         // 1 = unsplit
+  double* partial;                    // per-row partial sums between split passes
   const double* __restrict__ gather;  // y (primal) or xe (dual)
   const double* __restrict__ cb;      // c (primal) or b (dual)
   double* x;      // x (primal) or y (dual)
@@ -309,6 +325,57 @@ __global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
     if (PRIMAL) primal_epi_pre(row, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P);
     else dual_epi_pre(row, mine, o1, o2, o3, a.x, a.xbar, step, w, iter, P);
   }
+}
+
+// Dual step split by column chunks (split-K over the columns of A): pass k
+// sums each row's entries whose column lies in chunk k, so the xe gathers
+// of a pass come from an L2-sized window of the 80 MB vector instead of all
+// of it (v4 profile: the unsplit dual step moved 1.67x its algorithmic
+// bytes, the scattered gathers missing L2).  Passes run in order; a row's
+// sum is ((chunk 0) + chunk 1) + ...: fixed, bitwise reproducible.  Heavy
+// rows (whole rows, block per row) go with the last pass.
+template <int V>
+__global__ void __launch_bounds__(kBlock) k_dual_split(StepArgs a, int j_in_period, int pass,
+                                                       int n_heavy_now) {
+  __shared__ double red[kWarps];
+  StepParams* P = a.P;
+  const long long iter = P->iter0 + j_in_period + 1;
+  if (P->fail_iter < iter) return;
+  const double w = P->w0 + (double)(j_in_period + 1);
+  const double step = P->sigma_w;
+  const double* xin[1] = {a.gather};
+  const bool last = pass == a.nsplit - 1;
+  if ((int)blockIdx.x < n_heavy_now) {
+    const int row = a.rs.heavy[blockIdx.x];
+    double acc[1];
+    row_dot<kBlock, 1>(a.rs, a.rs.ptr[row], a.rs.ptr[row + 1], threadIdx.x, xin, acc);
+    const double d = block_sum(acc[0], red);
+    if (threadIdx.x == 0) dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const long long row0 = (((long long)(blockIdx.x - n_heavy_now) * kBlock + threadIdx.x) >> 5) * 32;
+  if (row0 >= a.rs.rows) return;
+  const long long rl = row0 + lane;
+  const bool in_range = rl < a.rs.rows;
+  double o1 = 0.0, o2 = 0.0, o3 = 0.0, part = 0.0;
+  if (in_range) {
+    if (last) {
+      o1 = a.cb[rl];
+      o2 = a.x[rl];
+      o3 = a.xbar[rl];
+    }
+    if (pass > 0) part = a.partial[rl];
+  }
+  const long long m = a.rs.rows;
+  const int* sp = pass == 0 ? a.rs.ptr : a.split + (pass - 1) * m;
+  const int* ep = last ? a.rs.ptr + 1 : a.split + pass * m;
+  bool ok;
+  const double dot = warp_rows_dot_seg<V>(a.rs, sp, ep, row0, lane, xin, ok);
+  if (!ok) return;
+  const double d = pass > 0 ? part + dot : dot;
+  if (last) dual_epi_pre((int)rl, d, o1, o2, o3, a.x, a.xbar, step, w, iter, P);
+  else a.partial[rl] = d;
 }
 
 // PSR step: persistent CTAs (one per SM) walk row blocks; the SpMV lands in
@@ -553,6 +620,26 @@ __global__ void k_row_ids(const int* __restrict__ ptr, int rows, int* __restrict
   for (int k = ptr[i]; k < ptr[i + 1]; ++k) rid[k] = i;
 }
 
+// split[k-1][i] = first entry of row i with column >= k*chunk (k = 1..K-1);
+// flags rows whose columns are not sorted (the split needs sorted rows).
+__global__ void k_split(int m, const int* __restrict__ ptr, const int* __restrict__ col, int K,
+                        int chunk, int* __restrict__ split, int* __restrict__ unsorted) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int s = ptr[i], e = ptr[i + 1];
+  for (int k = s + 1; k < e; ++k)
+    if (col[k] < col[k - 1]) { atomicOr(unsorted, 1); break; }
+  for (int k = 1; k < K; ++k) {
+    const int target = k * chunk;
+    int lo = s, hi = e;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (col[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    split[(size_t)(k - 1) * m + i] = lo;
+  }
+}
+
 __global__ void k_iota(int* __restrict__ v, long long n) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = (int)i;
@@ -661,7 +748,7 @@ struct pdhg_ctx {
   cudaStream_t stream;
   // workspace carve
   double *x, *xe, *xbar, *xbest, *zbest, *tn1, *tn2;
-  double *y, *ybar, *ybest, *tm1;
+  double *y, *ybar, *ybest, *tm1, *tm2;
   double* partials;
   double* scalars;
   StepParams* P;
@@ -694,7 +781,7 @@ struct Carve {
 size_t carve_bytes(int32_t m, int32_t n) {
   size_t b = 0;
   b += 7 * align_up((size_t)n * 8 + 256);
-  b += 4 * align_up((size_t)m * 8 + 256);
+  b += 5 * align_up((size_t)m * 8 + 256);
   b += align_up((size_t)kCheckBlocks * kMaxQ * 8 + 256);
   b += align_up(64 * 8 + 256);
   b += align_up(sizeof(StepParams) + 256);
@@ -733,6 +820,19 @@ int launch_ex(const pdhg_ctx* c, K kernel, dim3 grid, dim3 block, size_t smem, c
 }
 
 template <int V>
+struct SplitLaunch {
+  static int run(const pdhg_ctx* c, const StepArgs& a, int j) {
+    for (int pass = 0; pass < a.nsplit; ++pass) {
+      const int nh = pass == a.nsplit - 1 ? a.rs.n_heavy : 0;
+      const int g = nh + (int)((a.rs.rows + (long long)kBlock - 1) / kBlock);
+      int rc = launch_ex(c, k_dual_split<V>, dim3(g), dim3(kBlock), 0, nullptr, 0, a, j, pass, nh);
+      if (rc) return rc;
+    }
+    return 0;
+  }
+};
+
+template <int V>
 struct StepLaunchEx {
   static int run(const pdhg_ctx* c, bool primal, const StepArgs& a, int j, int grid,
                  const void* win_base, size_t win) {
@@ -754,6 +854,15 @@ int launch_step(pdhg_ctx* c, bool primal, int j) {
     a.x = c->y + c->yo; a.xe = nullptr; a.xbar = c->ybar + c->yo;
   }
   a.P = c->P;
+  a.split = nullptr;
+  a.nsplit = 1;
+  a.partial = nullptr;
+  if (!primal && c->prob.a_nsplit > 1 && !c->has_psr[0]) {
+    a.split = c->prob.a_split;
+    a.nsplit = c->prob.a_nsplit;
+    a.partial = c->tm2;
+    return dispatch_lanes<SplitLaunch>(c->a_lanes, c, a, j);
+  }
   const size_t win = (size_t)(primal ? c->mf : c->nf) * 8;
   const void* win_base = (c->l2_mask & (primal ? 1 : 2)) ? a.gather : nullptr;
   const int lanes = primal ? c->at_lanes : c->a_lanes;
@@ -834,6 +943,7 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->tn1 = cv.take<double>(n); c->tn2 = cv.take<double>(n);
   c->y = cv.take<double>(m); c->ybar = cv.take<double>(m); c->ybest = cv.take<double>(m);
   c->tm1 = cv.take<double>(m);
+  c->tm2 = cv.take<double>(m);
   c->partials = cv.take<double>((size_t)kCheckBlocks * kMaxQ);
   c->scalars = cv.take<double>(64);
   c->P = cv.take<StepParams>(1);
@@ -1168,6 +1278,20 @@ int pdhg_time_kernel(pdhg_ctx* c, int32_t which, int32_t reps, double tau_over_o
   cudaEventDestroy(e1);
   if (rc) return rc;
   *avg_ms_out = ms / reps;
+  return 0;
+}
+
+int pdhg_split_build(int32_t m, const int32_t* ptr, const int32_t* col, int32_t K, int32_t chunk,
+                     int32_t* split_out, int32_t* flag_dev, void* stream, int32_t* unsorted_out) {
+  if (m <= 0 || K < 2 || chunk <= 0 || !ptr || !col || !split_out || !flag_dev)
+    return fail(PDHG_ERR_ARG, "split_build: bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(flag_dev, 0, 4, s));
+  k_split<<<(m + 255) / 256, 256, 0, s>>>(m, ptr, col, K, chunk, split_out, flag_dev);
+  int h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h, flag_dev, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (unsorted_out) *unsorted_out = h;
   return 0;
 }
 

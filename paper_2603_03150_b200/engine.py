@@ -47,6 +47,8 @@ class GpuOptions:
                      kernels (csrc/psr.cuh); auto uses it when >= psr_min_fraction of
                      the entries fall in staged panels and the operator has enough rows.
     psr_min_staged:  entries a (row block, panel) needs to be staged in shared memory.
+    dual_split:      column chunks of the dual step's SpMV (split-K, csrc k_dual_split):
+                     each pass gathers from an L2-sized window of xe; 1 = unsplit.
     l2_persist:      bit mask: 1 = pin y in L2 for the primal step, 2 = pin xe for the
                      dual step (persisting access-policy window; L2 holds 79 MB persisting).
     """
@@ -62,6 +64,7 @@ class GpuOptions:
     psr_min_fraction: float = 0.3
     psr_min_rows: int = 148 * 256
     l2_persist: int = 0
+    dual_split: int = 2
 
 
 def _torch():
@@ -160,6 +163,19 @@ class DeviceLp:
                         ("At", n, m_full, self.at_nnz, self.at_ptr, self.at_col, self.at_val)):
                     self._psr[key] = self._build_psr(torch, dev, key, rows, cols, nz, ptr, col, val,
                                                      H, opts)
+                self.a_split = None
+                self.nsplit = 1
+                K = int(opts.dual_split)
+                if K > 1 and n_full >= 4 * K and m * (K - 1) < 2**31:
+                    chunk = (n_full + K - 1) // K
+                    split = torch.empty((K - 1) * m, dtype=torch.int32, device=dev)
+                    flag = torch.empty(1, dtype=torch.int32, device=dev)
+                    uns = C.c_int32()
+                    N.check(self.lib.pdhg_split_build(m, self.a_ptr.data_ptr(), self.a_col.data_ptr(), K,
+                                                      chunk, split.data_ptr(), flag.data_ptr(), sptr,
+                                                      C.byref(uns)))
+                    if not uns.value:
+                        self.a_split, self.nsplit = split, K
                 ws_bytes = self.lib.pdhg_workspace_bytes(m_full, n_full)
                 self.ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
                 self.stream.synchronize()
@@ -178,6 +194,8 @@ class DeviceLp:
         p.l2_persist = int(opts.l2_persist) & 3
         p.m_full, p.n_full, p.y_off, p.x_off = m_full, n_full, y_off, x_off
         p.at_nnz = self.at_nnz
+        p.a_nsplit = self.nsplit
+        p.a_split = self.a_split.data_ptr() if self.a_split is not None else None
         self._prob = p
         ctx = C.c_void_p()
         N.check(self.lib.pdhg_ctx_create(C.byref(p), self.ws.data_ptr(), ws_bytes,

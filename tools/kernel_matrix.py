@@ -33,6 +33,9 @@ def main():
     ab = algorithmic_bytes(inst.m, inst.n, inst.nnz)
     variants = {
         "csr": dict(psr="off", l2_persist=0),
+        "csr_k1": dict(psr="off", dual_split=1),
+        "csr_k3": dict(psr="off", dual_split=3),
+        "csr_k4": dict(psr="off", dual_split=4),
         "csr_l2d": dict(psr="off", l2_persist=2),
         "csr_l2p": dict(psr="off", l2_persist=1),
         "csr_l2": dict(psr="off", l2_persist=3),
