@@ -64,7 +64,7 @@ class GpuOptions:
     psr_min_fraction: float = 0.3
     psr_min_rows: int = 148 * 256
     l2_persist: int = 0
-    dual_split: int = 2
+    dual_split: int = 1
 
 
 def _torch():

@@ -33,6 +33,7 @@ def eng():
 # staged in shared-memory panels or every entry gathered from global memory
 LAYOUTS = {
     "csr": dict(psr="off"),
+    "csr_split2": dict(psr="off", dual_split=2),
     "psr_staged": dict(psr="on", psr_min_staged=1),
     "psr_remote": dict(psr="on", psr_min_staged=10**9),
 }
