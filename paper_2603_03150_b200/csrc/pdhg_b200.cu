@@ -278,7 +278,7 @@ struct StepArgs {
 };
 
 template <int V, bool PRIMAL>
-__global__ void __launch_bounds__(kBlock, 8) k_step(StepArgs a, int j_in_period) {
+__global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
   __shared__ double red[kWarps];
   StepParams* P = a.P;
   const long long iter = P->iter0 + j_in_period + 1;  // state.iterations after this step

@@ -248,6 +248,75 @@ __global__ void __launch_bounds__(256) v6(Csr A, const double* __restrict__ x, d
   if (rl < A.rows) y[rl] = mine;
 }
 
+
+// ---- V7: V5 + software pipelining across passes: the next pass's first
+// U*V entries (val, col) are loaded before the current pass's gathers.
+template <int V, int U>
+__global__ void __launch_bounds__(256) v7(Csr A, const double* __restrict__ x, double* __restrict__ y) {
+  constexpr int G = 32 / V;
+  const int lane = threadIdx.x & 31, sub = lane % V;
+  const long long row0 = (((long long)blockIdx.x * 256 + threadIdx.x) >> 5) * 32;
+  if (row0 >= A.rows) return;
+  const long long rl = row0 + lane;
+  int my_s = 0, my_e = 0;
+  if (rl < A.rows) { my_s = A.ptr[rl]; my_e = A.ptr[rl + 1]; }
+  double mine = 0.0;
+  int s = __shfl_sync(0xffffffffu, my_s, lane / V);
+  int e = __shfl_sync(0xffffffffu, my_e, lane / V);
+  double ac[U];
+  int jc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int kk = s + sub + u * V;
+    ac[u] = kk < e ? __ldcs(A.val + kk) : 0.0;
+    jc[u] = kk < e ? __ldcs(A.col + kk) : -1;
+  }
+#pragma unroll 1
+  for (int pass = 0; pass < V; ++pass) {
+    int sn = 0, en = 0;
+    double an[U];
+    int jn[U];
+    if (pass + 1 < V) {
+      const int src = (pass + 1) * G + lane / V;
+      sn = __shfl_sync(0xffffffffu, my_s, src);
+      en = __shfl_sync(0xffffffffu, my_e, src);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = sn + sub + u * V;
+      an[u] = kk < en ? __ldcs(A.val + kk) : 0.0;
+      jn[u] = kk < en ? __ldcs(A.col + kk) : -1;
+    }
+    double xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = jc[u] >= 0 ? __ldg(x + jc[u]) : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) if (jc[u] >= 0) acc = fma(ac[u], xv[u], acc);
+    for (int k = s + sub + U * V; k < e; k += U * V) {
+      double a2[U], x2[U];
+      int j2[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kk = k + u * V;
+        a2[u] = kk < e ? __ldcs(A.val + kk) : 0.0;
+        j2[u] = kk < e ? __ldcs(A.col + kk) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) x2[u] = j2[u] >= 0 ? __ldg(x + j2[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) if (j2[u] >= 0) acc = fma(a2[u], x2[u], acc);
+    }
+    acc = gsum<V>(acc);
+    const double got = __shfl_sync(0xffffffffu, acc, ((lane - pass * G) & (G - 1)) * V);
+    if (lane / G == pass) mine = got;
+#pragma unroll
+    for (int u = 0; u < U; ++u) { ac[u] = an[u]; jc[u] = jn[u]; }
+    s = sn; e = en;
+  }
+  if (rl < A.rows) y[rl] = mine;
+}
+
 // ---- V4: one warp, several rows: 2 rows per 32-lane warp at V=16 etc. is V1/V2; skip.
 
 struct Timer {
@@ -328,25 +397,18 @@ int main(int argc, char** argv) {
     if (op == 0) v1<8><<<grid(M.rows, 8), 256>>>(M, xin, yref); else v1<4><<<grid(M.rows, 4), 256>>>(M, xin, yref);
 #define RUN(NAME, K, VV) bench(NAME, M, [&] { K<<<grid(M.rows, VV), 256>>>(M, xin, ya); }, xin)
 #define RUNW(NAME, K) bench(NAME, M, [&] { K<<<(unsigned)((M.rows + 255) / 256), 256>>>(M, xin, ya); }, xin)
-    RUNW("v5<4,4>", (v5<4, 4>));
-    RUNW("v5<4,8>", (v5<4, 8>));
     RUNW("v5<8,2>", (v5<8, 2>));
     RUNW("v5<8,4>", (v5<8, 4>));
-    RUNW("v5<8,8>", (v5<8, 8>));
     RUNW("v5<16,2>", (v5<16, 2>));
     RUNW("v5<16,4>", (v5<16, 4>));
-    RUNW("v6<4,4>", (v6<4, 4>));
-    RUNW("v6<8,2>", (v6<8, 2>));
-    RUNW("v6<8,4>", (v6<8, 4>));
-    RUNW("v6<16,2>", (v6<16, 2>));
-    RUN("v1<4>", v1<4>, 4);
-    RUN("v1<8>", v1<8>, 8);
-    RUN("v1<16>", v1<16>, 16);
-    RUN("v2<4,2>", (v2<4, 2>), 4);
-    RUN("v2<4,4>", (v2<4, 4>), 4);
-    RUN("v2<8,2>", (v2<8, 2>), 8);
-    RUN("v2<8,4>", (v2<8, 4>), 8);
-    RUN("v2<16,2>", (v2<16, 2>), 16);
+    RUNW("v5<16,8>", (v5<16, 8>));
+    RUNW("v5<32,2>", (v5<32, 2>));
+    RUNW("v7<4,4>", (v7<4, 4>));
+    RUNW("v7<8,2>", (v7<8, 2>));
+    RUNW("v7<8,4>", (v7<8, 4>));
+    RUNW("v7<16,2>", (v7<16, 2>));
+    RUNW("v7<16,4>", (v7<16, 4>));
+    RUNW("v7<32,2>", (v7<32, 2>));
   }
   return 0;
 }
