@@ -73,7 +73,7 @@ typedef struct pdhg_psr {
   const int32_t* blk_tile_ptr;  /* nblk+1 */
   const int32_t* tile_bin;      /* ntiles, -1 = remote tile */
   const int32_t* gstart;        /* ntiles*(ngroups+1) */
-  const uint16_t* goff;         /* ntiles*ngroups*16 (16-row groups) */
+  const uint16_t* rcnt;         /* ntiles*ngroups*32: entries of each row in each tile */
   const double* val;            /* nent */
   const uint16_t* col16;        /* nent: column inside the panel */
   const int32_t* col;           /* nent: global column */
@@ -249,7 +249,7 @@ int pdhg_psr_plan(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, c
 int pdhg_psr_build(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, const int32_t* col,
                    const double* val, int32_t heavy_threshold, void* tmp, size_t tmp_bytes,
                    void* stream, int32_t* blk_tile_ptr, int32_t* tile_bin, int32_t* gstart,
-                   uint16_t* goff, double* val_out, uint16_t* col16_out, int32_t* col_out,
+                   uint16_t* rcnt, double* val_out, uint16_t* col16_out, int32_t* col_out,
                    uint8_t* heavy_out);
 
 /* Ruiz equilibration on the device (hybridlp.transform.ruiz_equilibrate,

@@ -42,7 +42,7 @@ class Psr(C.Structure):
         ("rows", C.c_int32), ("cols", C.c_int32), ("R", C.c_int32), ("W", C.c_int32),
         ("nblk", C.c_int32), ("ntiles", C.c_int32), ("ngroups", C.c_int32), ("nent", C.c_int64),
         ("blk_tile_ptr", C.c_void_p), ("tile_bin", C.c_void_p), ("gstart", C.c_void_p),
-        ("goff", C.c_void_p), ("val", C.c_void_p), ("col16", C.c_void_p), ("col", C.c_void_p),
+        ("rcnt", C.c_void_p), ("val", C.c_void_p), ("col16", C.c_void_p), ("col", C.c_void_p),
         ("heavy", C.c_void_p),
     ]
 

@@ -956,7 +956,7 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
         return fail(PDHG_ERR_ARG, "psr layout geometry not supported");
       }
       c->psr_l[k] = psr::Layout{q->rows, q->cols, q->R, q->W, q->nblk, q->ntiles, q->ngroups,
-                                q->blk_tile_ptr, q->tile_bin, q->gstart, q->goff, q->val, q->col16,
+                                q->blk_tile_ptr, q->tile_bin, q->gstart, q->rcnt, q->val, q->col16,
                                 q->col, q->heavy};
       c->psr_smem[k] = psr::smem_bytes(q->W);
     }

@@ -13,19 +13,19 @@
 // one "remote" tile per block, gathered from global memory.
 //
 // Execution: one persistent 1024-thread CTA per SM walks row blocks.  Rows
-// are dealt to warps in groups of 16 (warp w owns groups w, w+32, ...), two
-// lanes per row (even / odd entries of each tile segment), and each lane
-// keeps its partial sums in registers across all tiles of the block -- no
-// shared-memory accumulators, no atomics; one xor-shuffle joins the two
-// halves before the epilogue.  A row's sum runs panels ascending, then the
-// remote tile, entries in column order: fixed by the layout, so results are
-// bitwise reproducible run to run.
+// are dealt to warps in groups of 32 (warp w owns groups w, w+32, ...), one
+// row per lane, and each lane keeps its rows' partial sums in registers
+// across all tiles of the block -- no shared-memory accumulators, no
+// atomics, no cross-lane reductions.  A row's sum runs panels ascending,
+// then the remote tile, entries in column order: fixed by the layout, so
+// results are bitwise reproducible run to run.
 //
 // Layout (entries in tile order, inside a tile in CSR (row, column) order):
 //   blk_tile_ptr[b]                 first tile of row block b       (nblk+1)
 //   tile_bin[t]                     panel index of tile t, -1 = remote
-//   gstart[t*(ngroups+1)+g]         first entry of row group g (16 rows) in tile t
-//   goff[(t*ngroups+g)*16+q]        entry offset of row 16g+q within its group (u16)
+//   gstart[t*(ngroups+1)+g]         first entry of row group g (32 rows) in tile t
+//   rcnt[(t*ngroups+g)*32+l]        entries of row 32g+l in tile t (u16)
+//   entries of a (tile, group) are stored slot-major (see group_tile)
 //   val[e] (f64), col16[e] (column inside the panel, u16), col[e] (global column, i32)
 #pragma once
 
@@ -37,7 +37,7 @@ namespace psr {
 constexpr int kThreads = 1024;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxRows = 8192;                      // rows per block
-constexpr int kLanes = 2;                           // lanes per row
+constexpr int kLanes = 1;                           // lanes per row
 constexpr int kGroupRows = 32 / kLanes;             // rows per group (one warp pass)
 constexpr int kGroupsPerWarp = kMaxRows / kGroupRows / kWarps;
 constexpr int kPanel = 8192;                        // W: 64 KB of fp64 per panel buffer
@@ -48,7 +48,7 @@ struct Layout {
   const int* __restrict__ blk_tile_ptr;
   const int* __restrict__ tile_bin;
   const int* __restrict__ gstart;
-  const unsigned short* __restrict__ goff;
+  const unsigned short* __restrict__ rcnt;
   const double* __restrict__ val;
   const unsigned short* __restrict__ col16;
   const int* __restrict__ col;
@@ -101,38 +101,45 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // ------------------------------------------------------------ compute
 
-// acc += this lane's share of (row kGroupRows*g + lane/kLanes of tile t) . x.
-// Lanes 2q, 2q+1 split row q's entries (even / odd positions); kU entries per
-// lane are loaded before use for memory-level parallelism.
+// acc += (row 32g+lane of tile t) . x, one row per lane.  A (tile, group)
+// stores its entries slot-major: slot k holds the k-th entry of every row
+// with more than k entries, in lane order, so the loads of a slot are
+// contiguous across the active lanes (coalesced) and a lane finds its entry
+// with one ballot + popc; slot k of a row is its k-th entry in column order,
+// so the row sum runs in column order.  kU slots are loaded before use.
 template <bool STAGED>
 __device__ __forceinline__ double group_tile(const Layout& L, int t, int g, int lane,
                                              const double* __restrict__ px,
                                              const double* __restrict__ gx, double acc) {
   constexpr int kU = 4;
   const int* gs = L.gstart + (size_t)t * (L.ngroups + 1);
-  const int base = gs[g];
+  int base = gs[g];
   const int end = gs[g + 1];
   if (base == end) return acc;  // warp-uniform: no entries of this group in the tile
-  const int q = lane / kLanes, sub = lane % kLanes;
-  const int off = L.goff[((size_t)t * L.ngroups + g) * kGroupRows + q];
-  int nxt = __shfl_down_sync(0xffffffffu, off, kLanes);
-  if (q == kGroupRows - 1) nxt = end - base;
-  const int e1 = base + nxt;
-  for (int e = base + off + sub; e < e1; e += kU * kLanes) {
-    double a[kU], xv[kU];
+  const int cnt = L.rcnt[((size_t)t * L.ngroups + g) * kGroupRows + lane];
+  const int maxc = __reduce_max_sync(0xffffffffu, cnt);
+  const unsigned lt = (1u << lane) - 1u;
+  for (int k = 0; k < maxc; k += kU) {
+    int idx[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int ee = e + u * kLanes;
-      a[u] = 0.0;
-      xv[u] = 0.0;
-      if (ee < e1) {
-        a[u] = __ldcs(L.val + ee);
-        xv[u] = STAGED ? px[__ldcs(L.col16 + ee)] : __ldg(gx + __ldcs(L.col + ee));
-      }
+      const bool has = cnt > k + u;
+      const unsigned mask = __ballot_sync(0xffffffffu, has);
+      idx[u] = has ? base + __popc(mask & lt) : -1;
+      base += __popc(mask);
+    }
+    double a[kU], xv[kU];
+    int c[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      a[u] = idx[u] >= 0 ? __ldcs(L.val + idx[u]) : 0.0;
+      c[u] = idx[u] >= 0 ? (STAGED ? (int)__ldcs(L.col16 + idx[u]) : __ldcs(L.col + idx[u])) : 0;
     }
 #pragma unroll
+    for (int u = 0; u < kU; ++u) xv[u] = idx[u] >= 0 ? (STAGED ? px[c[u]] : __ldg(gx + c[u])) : 0.0;
+#pragma unroll
     for (int u = 0; u < kU; ++u)
-      if (e + u * kLanes < e1) acc = fma(a[u], xv[u], acc);
+      if (idx[u] >= 0) acc = fma(a[u], xv[u], acc);
   }
   return acc;
 }

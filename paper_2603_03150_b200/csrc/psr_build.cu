@@ -62,6 +62,7 @@ struct Tmp {
   long long* staged_b;  // nblk
   int* scal;      // 4
   int* k0; int* k1; int* v0; int* v1; int* rid;  // nnz each
+  double* rm_val; unsigned short* rm_c16; int* rm_col;  // row-major staging before slot-major
   int* tstart;    // nblk*(nbins+1)+1
   void* cub; size_t cub_bytes;
 };
@@ -83,6 +84,8 @@ size_t tmp_size(int rows, int cols, long long nnz) {
   s += a256((size_t)g.nblk * 8);
   s += a256(16);
   s += 5 * a256((size_t)std::max(1LL, nnz) * 4);
+  s += a256((size_t)std::max(1LL, nnz) * 8) + a256((size_t)std::max(1LL, nnz) * 2) +
+       a256((size_t)std::max(1LL, nnz) * 4);
   s += a256(((size_t)g.nblk * (g.nbins + 1) + 2) * 4);
   s += a256(cub_need(nnz, g.nblk));
   return s;
@@ -103,6 +106,9 @@ Tmp carve(void* base, int rows, int cols, long long nnz) {
   const size_t ne = (size_t)std::max(1LL, nnz) * 4;
   t.k0 = (int*)take(ne); t.k1 = (int*)take(ne); t.v0 = (int*)take(ne); t.v1 = (int*)take(ne);
   t.rid = (int*)take(ne);
+  t.rm_val = (double*)take((size_t)std::max(1LL, nnz) * 8);
+  t.rm_c16 = (unsigned short*)take((size_t)std::max(1LL, nnz) * 2);
+  t.rm_col = (int*)take((size_t)std::max(1LL, nnz) * 4);
   t.tstart = (int*)take(((size_t)g.nblk * (g.nbins + 1) + 2) * 4);
   t.cub_bytes = cub_need(nnz, g.nblk);
   t.cub = take(t.cub_bytes);
@@ -229,10 +235,10 @@ __global__ void k_tile_start(const int* __restrict__ skey, long long nnz, int nt
 }
 
 // For tile t and block-local row r in [0, ngroups*G]: p(r) = first entry of
-// the tile whose row is >= r.  gstart[t][g] = p(G g); goff[t][r] = p(r) - p(G*(r/G)).
+// the tile whose row is >= r.  gstart[t][g] = p(G g); rcnt[t][r] = p(r+1) - p(r).
 __global__ void k_groups(int ntiles, int ngroups, const int* __restrict__ tstart,
                          const int* __restrict__ rowl, int* __restrict__ gstart,
-                         unsigned short* __restrict__ goff) {
+                         unsigned short* __restrict__ rcnt) {
   constexpr int G = psr::kGroupRows;
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long per = (long long)ngroups * G + 1;
@@ -249,9 +255,46 @@ __global__ void k_groups(int ntiles, int ngroups, const int* __restrict__ tstart
   };
   const int p = lb(r);
   if (r % G == 0) gstart[(size_t)t * (ngroups + 1) + r / G] = p;
-  if (r < ngroups * G) {
-    const int p0 = (r % G) ? lb(r - r % G) : p;
-    goff[(size_t)t * ngroups * G + r] = (unsigned short)(p - p0);
+  if (r < ngroups * G) rcnt[(size_t)t * ngroups * G + r] = (unsigned short)(lb(r + 1) - p);
+}
+
+// One warp per (tile, group): move the group's entries from row-major to
+// slot-major order (slot k = k-th entry of each row with > k entries, lanes
+// in row order), the order group_tile consumes.
+__global__ void k_slot_major(int ntiles, int ngroups, const int* __restrict__ gstart,
+                             const unsigned short* __restrict__ rcnt,
+                             const double* __restrict__ val_in, const unsigned short* __restrict__ c16_in,
+                             const int* __restrict__ col_in, double* __restrict__ val_out,
+                             unsigned short* __restrict__ c16_out, int* __restrict__ col_out) {
+  constexpr int G = psr::kGroupRows;
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= (long long)ntiles * ngroups) return;
+  const int t = (int)(w / ngroups), g = (int)(w % ngroups);
+  const int base = gstart[(size_t)t * (ngroups + 1) + g];
+  const int cnt = rcnt[((size_t)t * ngroups + g) * G + lane];
+  // row-major start of this lane's row: exclusive prefix of counts
+  int pre = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, pre, o);
+    if (lane >= o) pre += v;
+  }
+  const int src0 = base + pre - cnt;
+  const int maxc = __reduce_max_sync(0xffffffffu, cnt);
+  const unsigned lt = (1u << lane) - 1u;
+  int slot_base = base;
+  for (int k = 0; k < maxc; ++k) {
+    const bool has = cnt > k;
+    const unsigned mask = __ballot_sync(0xffffffffu, has);
+    if (has) {
+      const int dst = slot_base + __popc(mask & lt);
+      const int src = src0 + k;
+      val_out[dst] = val_in[src];
+      c16_out[dst] = c16_in[src];
+      col_out[dst] = col_in[src];
+    }
+    slot_base += __popc(mask);
   }
 }
 
@@ -321,7 +364,7 @@ int pdhg_psr_plan(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, c
 int pdhg_psr_build(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, const int32_t* col,
                    const double* val, int32_t heavy_threshold, void* tmp, size_t tmp_bytes,
                    void* stream, int32_t* blk_tile_ptr, int32_t* tile_bin, int32_t* gstart,
-                   uint16_t* goff, double* val_out, uint16_t* col16_out, int32_t* col_out,
+                   uint16_t* rcnt, double* val_out, uint16_t* col16_out, int32_t* col_out,
                    uint8_t* heavy_out) {
   if (rows <= 0 || cols <= 0 || nnz < 0 || nnz >= INT_MAX || !tmp)
     return set_error(PDHG_ERR_ARG, "psr_build: bad argument");
@@ -349,13 +392,16 @@ int pdhg_psr_build(int32_t rows, int32_t cols, int64_t nnz, const int32_t* ptr, 
     k_tile_start<<<blocks(ntiles + 1, 256), 256, 0, s>>>(kb.Current(), nnz, ntiles, t.tstart);
     rowl = kb.Alternate();  // free after the sort: reused for block-local row ids
     k_scatter<<<blocks(nnz, 256), 256, 0, s>>>(nnz, kb.Current(), vb.Current(), t.rid, col, val,
-                                               tile_bin, ntiles, g.R, g.W, val_out, col16_out, col_out,
+                                               tile_bin, ntiles, g.R, g.W, t.rm_val, t.rm_c16, t.rm_col,
                                                rowl);
   } else {
     PSR_TRY(cudaMemsetAsync(t.tstart, 0, (size_t)(ntiles + 1) * 4, s));
   }
   const long long ng = (long long)ntiles * ((long long)ngroups * psr::kGroupRows + 1);
-  k_groups<<<blocks(ng, 256), 256, 0, s>>>(ntiles, ngroups, t.tstart, rowl, gstart, goff);
+  k_groups<<<blocks(ng, 256), 256, 0, s>>>(ntiles, ngroups, t.tstart, rowl, gstart, rcnt);
+  if (nnz > 0)
+    k_slot_major<<<blocks((long long)ntiles * ngroups * 32, 256), 256, 0, s>>>(
+        ntiles, ngroups, gstart, rcnt, t.rm_val, t.rm_c16, t.rm_col, val_out, col16_out, col_out);
   k_heavy_flags<<<blocks(rows, 256), 256, 0, s>>>(rows, ptr, heavy_threshold, heavy_out);
   PSR_TRY(cudaGetLastError());
   PSR_TRY(cudaStreamSynchronize(s));

@@ -229,13 +229,13 @@ class DeviceLp:
             "blk_tile_ptr": torch.empty(nblk.value + 1, dtype=i32, device=dev),
             "tile_bin": torch.empty(nt, dtype=i32, device=dev),
             "gstart": torch.empty(nt * (ngroups.value + 1), dtype=i32, device=dev),
-            "goff": torch.empty(nt * ngroups.value * 16, dtype=torch.int16, device=dev),
+            "rcnt": torch.empty(nt * ngroups.value * 32, dtype=torch.int16, device=dev),
             "val": torch.empty(max(1, nnz), dtype=torch.float64, device=dev),
             "col16": torch.empty(max(1, nnz), dtype=torch.int16, device=dev),
             "col": torch.empty(max(1, nnz), dtype=i32, device=dev),
             "heavy": torch.empty(rows, dtype=torch.uint8, device=dev),
         }
-        names = ("blk_tile_ptr", "tile_bin", "gstart", "goff", "val", "col16", "col", "heavy")
+        names = ("blk_tile_ptr", "tile_bin", "gstart", "rcnt", "val", "col16", "col", "heavy")
         N.check(lib.pdhg_psr_build(rows, cols, nnz, ptr.data_ptr(), col.data_ptr(), val.data_ptr(), H,
                                    tmp.data_ptr(), tb, sptr, *(bufs[k].data_ptr() for k in names)))
         d = N.Psr()
