@@ -88,8 +88,10 @@ def test_first_100_iterates_1e9(eng, name, layout):
         opts = _opts(eng, layout)
         eng.run_pdhg(gm, _params(eng, eps_rel=1e-12, max_kkt_passes=k, check_every=ce), gpu=opts)
         dev = eng.device_lp(gm, opts)
-        if layout != "csr":
+        if layout.startswith("psr"):
             assert dev.psr_info["A"].get("used") and dev.psr_info["At"].get("used")
+        if layout == "csr_split2":
+            assert dev.nsplit == 2
         x, y, _ = dev.fetch(N.PT_CUR, want_z=False)
         ax, ay, _ = dev.fetch(N.PT_AVG, want_z=False)
         assert _rel(x, g["it_x"][j]) <= ITER_RTOL, (name, k)
