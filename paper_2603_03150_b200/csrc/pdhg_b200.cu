@@ -198,9 +198,94 @@ __device__ __forceinline__ double warp_rows_dot_seg(const RowSet& rs, const int*
   return mine;
 }
 
+// Software-pipelined form for short rows (V <= 8): the next pass's first
+// kU*V entries (values, indices) are loaded before the current pass's
+// gathers, so index-load latency overlaps gather latency
+// (tools/spmv_lab.cu v7: A' 0.888 -> 0.839 ms on config 4).  Summation
+// order is row_dot's: entries k, k+V, ... of the lane, then the butterfly.
+template <int V>
+__device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long row0, int lane,
+                                                     const double* const* __restrict__ xin,
+                                                     bool& ok) {
+  constexpr int G = 32 / V;
+  constexpr int kU = 4;
+  const int sub = lane % V;
+  const long long rl = row0 + lane;
+  int my_s = 0, my_e = 0;
+  ok = rl < rs.rows;
+  if (ok) {
+    my_s = rs.ptr[rl];
+    my_e = rs.ptr[rl + 1];
+    if (my_e - my_s > rs.heavy_threshold) { ok = false; my_e = my_s; }
+  }
+  const double* __restrict__ x = xin[0];
+  int s = __shfl_sync(0xffffffffu, my_s, lane / V);
+  int e = __shfl_sync(0xffffffffu, my_e, lane / V);
+  double ac[kU];
+  int jc[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int kk = s + sub + u * V;
+    ac[u] = kk < e ? __ldcs(rs.val + kk) : 0.0;
+    jc[u] = kk < e ? __ldcs(rs.col + kk) : -1;
+  }
+  double mine = 0.0;
+#pragma unroll 1
+  for (int pass = 0; pass < V; ++pass) {
+    int sn = 0, en = 0;
+    if (pass + 1 < V) {
+      const int src = (pass + 1) * G + lane / V;
+      sn = __shfl_sync(0xffffffffu, my_s, src);
+      en = __shfl_sync(0xffffffffu, my_e, src);
+    }
+    double an[kU];
+    int jn[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int kk = sn + sub + u * V;
+      an[u] = kk < en ? __ldcs(rs.val + kk) : 0.0;
+      jn[u] = kk < en ? __ldcs(rs.col + kk) : -1;
+    }
+    double xv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) xv[u] = jc[u] >= 0 ? __ldg(x + jc[u]) : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (jc[u] >= 0) acc = fma(ac[u], xv[u], acc);
+    for (int k = s + sub + kU * V; k < e; k += kU * V) {  // rows longer than kU*V
+      double a2[kU], x2[kU];
+      int j2[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int kk = k + u * V;
+        a2[u] = kk < e ? __ldcs(rs.val + kk) : 0.0;
+        j2[u] = kk < e ? __ldcs(rs.col + kk) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) x2[u] = j2[u] >= 0 ? __ldg(x + j2[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (j2[u] >= 0) acc = fma(a2[u], x2[u], acc);
+    }
+    const double d = group_sum<V>(acc);
+    const double got = __shfl_sync(0xffffffffu, d, ((lane - pass * G) & (G - 1)) * V);
+    if (lane / G == pass) mine = got;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      ac[u] = an[u];
+      jc[u] = jn[u];
+    }
+    s = sn;
+    e = en;
+  }
+  return mine;
+}
+
 template <int V>
 __device__ __forceinline__ double warp_rows_dot(const RowSet& rs, long long row0, int lane,
                                                 const double* const* __restrict__ xin, bool& ok) {
+  if (V <= 8) return warp_rows_dot_pipe<V>(rs, row0, lane, xin, ok);
   return warp_rows_dot_seg<V>(rs, rs.ptr, rs.ptr + 1, row0, lane, xin, ok);
 }
 

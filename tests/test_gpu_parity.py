@@ -90,7 +90,7 @@ def test_first_100_iterates_1e9(eng, name, layout):
         dev = eng.device_lp(gm, opts)
         if layout.startswith("psr"):
             assert dev.psr_info["A"].get("used") and dev.psr_info["At"].get("used")
-        if layout == "csr_split2":
+        if layout == "csr_split2" and gm.n >= 8:
             assert dev.nsplit == 2
         x, y, _ = dev.fetch(N.PT_CUR, want_z=False)
         ax, ay, _ = dev.fetch(N.PT_AVG, want_z=False)
