@@ -73,3 +73,33 @@ def test_sharded_opnorm_matches(eng):
     v = rng.standard_normal(gm.n)
     v /= np.linalg.norm(v)
     assert dev.opnorm(v) == pytest.approx(float(gm.g["opnorm_seed0"]), rel=1e-12)
+
+
+def test_torch_comm_over_nccl_world1(eng):
+    """The one-process-per-GPU path (TorchComm over NCCL) on a world of one:
+    exercises the torch views of the library's vectors, the NCCL
+    all_gather_into_tensor calls on the engine's stream and the rank-order
+    combine, against the golden reference run."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2603_03150_b200.sharded import run_pdhg_sharded
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        gm = load_golden("config0_s0")
+        T = eng.types()
+        pt, st = run_pdhg_sharded(gm, T.PdhgParams(eps_rel=1e-4), G=1, comm_kind="torch")
+        r = gm.run("e4")
+        assert st.status.value == "Optimal"
+        assert st.iterations == int(r["iterations"]) and st.restarts == int(r["restarts"])
+        assert float(gm.c @ pt.x) == pytest.approx(float(r["obj"]), rel=1e-6)
+    finally:
+        dist.destroy_process_group()
