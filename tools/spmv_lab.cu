@@ -399,6 +399,66 @@ __global__ void __launch_bounds__(256) v8(Csr A, const double* __restrict__ x, d
   if (rl < A.rows) y[rl] = mine;
 }
 
+
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+  // cp.async.bulk.prefetch.L2: address 16-B aligned, size a multiple of 16
+  const unsigned long long a = (unsigned long long)p;
+  unsigned long long off = a & ~15ULL;
+  const unsigned long long end = (a + bytes + 15) & ~15ULL;
+  while (off < end) {
+    const unsigned chunk = (end - off) > (1ull << 20) ? (1u << 20) : (unsigned)(end - off);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(off), "r"(chunk) : "memory");
+    off += chunk;
+  }
+}
+
+// ---- V9: V5 + one bulk L2 prefetch per block of the entries of block (b + D)
+template <int V, int U, int D>
+__global__ void __launch_bounds__(256) v9(Csr A, const double* __restrict__ x, double* __restrict__ y) {
+  if (threadIdx.x == 0) {
+    const long long nb = (long long)blockIdx.x + D;
+    const long long r0 = nb * 256, r1 = min((long long)A.rows, r0 + 256);
+    if (r0 < A.rows) {
+      const int s = A.ptr[r0], e = A.ptr[r1];
+      l2_prefetch(A.val + s, (unsigned)(e - s) * 8u);
+      l2_prefetch(A.col + s, (unsigned)(e - s) * 4u);
+    }
+  }
+  constexpr int G = 32 / V;
+  const int lane = threadIdx.x & 31;
+  const long long row0 = (((long long)blockIdx.x * 256 + threadIdx.x) >> 5) * 32;
+  if (row0 >= A.rows) return;
+  const long long rl = row0 + lane;
+  int my_s = 0, my_e = 0;
+  if (rl < A.rows) { my_s = A.ptr[rl]; my_e = A.ptr[rl + 1]; }
+  double mine = 0.0;
+#pragma unroll 1
+  for (int pass = 0; pass < V; ++pass) {
+    const int src = pass * G + lane / V;
+    const int s = __shfl_sync(0xffffffffu, my_s, src);
+    const int e = __shfl_sync(0xffffffffu, my_e, src);
+    double acc = 0.0;
+    for (int k = s + lane % V; k < e; k += U * V) {
+      double a[U], xv[U];
+      int j[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kk = k + u * V;
+        a[u] = kk < e ? __ldcs(A.val + kk) : 0.0;
+        j[u] = kk < e ? __ldcs(A.col + kk) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = j[u] >= 0 ? __ldg(x + j[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) if (j[u] >= 0) acc = fma(a[u], xv[u], acc);
+    }
+    acc = gsum<V>(acc);
+    const double got = __shfl_sync(0xffffffffu, acc, ((lane - pass * G) & (G - 1)) * V);
+    if (lane / G == pass) mine = got;
+  }
+  if (rl < A.rows) y[rl] = mine;
+}
+
 // ---- V4: one warp, several rows: 2 rows per 32-lane warp at V=16 etc. is V1/V2; skip.
 
 struct Timer {
@@ -481,13 +541,12 @@ int main(int argc, char** argv) {
 #define RUNW(NAME, K) bench(NAME, M, [&] { K<<<(unsigned)((M.rows + 255) / 256), 256>>>(M, xin, ya); }, xin)
     RUNW("v5<8,2>", (v5<8, 2>));
     RUNW("v5<16,4>", (v5<16, 4>));
-    RUNW("v7<8,4>", (v7<8, 4>));
-    RUNW("v7<16,4>", (v7<16, 4>));
-    RUNW("v8<4,4>", (v8<4, 4>));
-    RUNW("v8<8,2>", (v8<8, 2>));
-    RUNW("v8<8,4>", (v8<8, 4>));
-    RUNW("v8<16,2>", (v8<16, 2>));
-    RUNW("v8<16,4>", (v8<16, 4>));
+    RUNW("v9<8,2,148>", (v9<8, 2, 148>));
+    RUNW("v9<8,2,592>", (v9<8, 2, 592>));
+    RUNW("v9<8,2,1184>", (v9<8, 2, 1184>));
+    RUNW("v9<16,4,148>", (v9<16, 4, 148>));
+    RUNW("v9<16,4,592>", (v9<16, 4, 592>));
+    RUNW("v9<16,4,1184>", (v9<16, 4, 1184>));
   }
   return 0;
 }
