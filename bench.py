@@ -367,7 +367,8 @@ def run_ours(args):
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / K,
                 "d2h_bytes_per_step": d2h / K, "iterations": st.iterations,
-                "wall_s": wall_e2e, "note": "run_pdhg(StandardLp on host) incl. upload, transpose, opnorm"},
+                "wall_s": wall_e2e, "timings": getattr(st, "timings", None),
+                "note": "run_pdhg(StandardLp on host) incl. upload, transpose, opnorm"},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": args.steps * (2 * CHECK_EVERY + 3),

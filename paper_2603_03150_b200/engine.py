@@ -103,6 +103,7 @@ class DeviceLp:
         ``device_arrays``: (indptr, indices, data) of A already on the device
         (e.g. the output of the device Ruiz pass) -- not uploaded again."""
         torch = _torch()
+        t_start = time.monotonic()
         self.lib = N.load()
         dev = torch.device("cuda", torch.cuda.current_device() if opts.device is None else opts.device)
         self.device = dev
@@ -137,6 +138,8 @@ class DeviceLp:
                     self.a_val = t(A.data, np.float64)
                 self.b = t(b, np.float64)
                 self.c = t(c, np.float64)
+                self.stream.synchronize()
+                t_up = time.monotonic()
                 sptr = self.stream.cuda_stream
                 tmp = None
                 if At is None:
@@ -201,6 +204,8 @@ class DeviceLp:
         N.check(self.lib.pdhg_ctx_create(C.byref(p), self.ws.data_ptr(), ws_bytes,
                                          self.stream.cuda_stream, C.byref(ctx)))
         self.ctx = ctx
+        t_end = time.monotonic()
+        self.timings = {"upload_s": t_up - t_start, "layout_s": t_end - t_up}
         self._fin = weakref.finalize(self, self.lib.pdhg_ctx_destroy, ctx)
         self._scal = (C.c_double * (2 * N.NQ))()
 
@@ -495,8 +500,14 @@ def run_pdhg(p, params=None, seed: int = 0, *, gpu: GpuOptions | None = None):
     if p.A.nnz == 0:                                           # pdhg.py:87-88
         raise T.InvalidModelError("cannot estimate the norm of an empty matrix")
     dev = device_lp(p, opts)
+    t_layout = time.monotonic() - t0
     with dev.lock:
-        return _run(T, dev, p, params, seed, opts, t0)
+        pt, st = _run(T, dev, p, params, seed, opts, t0)
+    if hasattr(st, "timings"):
+        st.timings["layout_s"] = t_layout
+        st.timings.update({k: v for k, v in getattr(dev, "timings", {}).items()
+                           if k == "upload_s"})
+    return pt, st
 
 
 def run_on_device(dev, p, params=None, seed: int = 0, *, gpu: GpuOptions | None = None):
@@ -517,6 +528,8 @@ def _run(T, dev: DeviceLp, p, params, seed, opts, t0):
     norm_c = float(np.linalg.norm(c)) if c.size else 0.0       # lp_core.py:461
     eps = params.eps_rel
 
+    tm = {}
+    t_op = time.monotonic()
     # initial_state (pdhg.py:117-137)
     if opts.opnorm is not None:
         opnorm = float(opts.opnorm)
@@ -526,6 +539,8 @@ def _run(T, dev: DeviceLp, p, params, seed, opts, t0):
         v /= np.linalg.norm(v)
         opnorm = dev.opnorm(v, tol=1e-4, max_iters=100)
     step = 1.0 / (1.05 * opnorm)                               # pdhg.py:119
+    tm["opnorm_s"] = time.monotonic() - t_op
+    t_it = time.monotonic()
     dev.reset()
     tau = sigma = step
     omega = params.primal_weight_init
@@ -579,11 +594,14 @@ def _run(T, dev: DeviceLp, p, params, seed, opts, t0):
                    ((N.PT_CUR, cur_term, cur_sum), (N.PT_AVG, avg_term, avg_sum)) if term.ok]
         if passing:                                            # pdhg.py:214-224
             which, term, summ = min(passing, key=lambda t: t[2].max_violation)
+            tm["iterate_s"] = time.monotonic() - t_it
+            t_f = time.monotonic()
             x, y, z = dev.fetch(which)
+            tm["fetch_s"] = time.monotonic() - t_f
             stats = T.SolveStats(
                 status=S.OPTIMAL, iterations=iterations, restarts=restarts,
                 wall_seconds=time.monotonic() - t0, termination=term,
-                max_violation=summ.max_violation, history=history,
+                max_violation=summ.max_violation, history=history, timings=tm,
             )
             return T.KktPoint(x, y, z), stats
 
@@ -615,14 +633,17 @@ def _run(T, dev: DeviceLp, p, params, seed, opts, t0):
             rec["restart"] = True
 
     # failure exit (pdhg.py:249-258): best point, re-checked with its own z
+    tm["iterate_s"] = time.monotonic() - t_it
+    t_f = time.monotonic()
     spec = (N.PT_AVG if best_live_avg else N.PT_BEST) | N.SPEC_BEST_Z
     (q_best,) = dev.check(spec)
     termination = _termination(T, _score(q_best), eps, norm_b, norm_c)
     x, y, z = dev.fetch(spec)
+    tm["fetch_s"] = time.monotonic() - t_f
     stats = T.SolveStats(
         status=status, iterations=iterations, restarts=restarts,
         wall_seconds=time.monotonic() - t0, termination=termination,
-        max_violation=best_summary.max_violation, history=history,
+        max_violation=best_summary.max_violation, history=history, timings=tm,
     )
     return T.KktPoint(x, y, z), stats
 

@@ -141,11 +141,14 @@ def resolve() -> SimpleNamespace:
             reference=False,
         )
     ns.SolveStats = make_dataclass(
-        "SolveStats", [("history", list, field(default_factory=list))],
+        "SolveStats", [("history", list, field(default_factory=list)),
+                       ("timings", dict, field(default_factory=dict))],
         bases=(ns.BaseSolveStats,),
     )
     ns.SolveStats.__doc__ = ("SolveStats (pdhg.py:70-77) plus `history`: one dict per "
-                             "KKT check (iteration, scores, termination sides, omega, restart).")
+                             "KKT check (iteration, scores, termination sides, omega, restart), "
+                             "and `timings`: wall seconds of the layout build, power "
+                             "iteration, iterations and result download.")
     _cache = ns
     return ns
 

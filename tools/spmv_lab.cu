@@ -251,8 +251,8 @@ __global__ void __launch_bounds__(256) v6(Csr A, const double* __restrict__ x, d
 
 // ---- V7: V5 + software pipelining across passes: the next pass's first
 // U*V entries (val, col) are loaded before the current pass's gathers.
-template <int V, int U>
-__global__ void __launch_bounds__(256) v7(Csr A, const double* __restrict__ x, double* __restrict__ y) {
+template <int V, int U, int MB = 1>
+__global__ void __launch_bounds__(256, MB) v7(Csr A, const double* __restrict__ x, double* __restrict__ y) {
   constexpr int G = 32 / V;
   const int lane = threadIdx.x & 31, sub = lane % V;
   const long long row0 = (((long long)blockIdx.x * 256 + threadIdx.x) >> 5) * 32;
@@ -539,12 +539,15 @@ int main(int argc, char** argv) {
     if (op == 0) v1<8><<<grid(M.rows, 8), 256>>>(M, xin, yref); else v1<4><<<grid(M.rows, 4), 256>>>(M, xin, yref);
 #define RUN(NAME, K, VV) bench(NAME, M, [&] { K<<<grid(M.rows, VV), 256>>>(M, xin, ya); }, xin)
 #define RUNW(NAME, K) bench(NAME, M, [&] { K<<<(unsigned)((M.rows + 255) / 256), 256>>>(M, xin, ya); }, xin)
-    RUNW("v5<8,2>", (v5<8, 2>));
     RUNW("v5<16,4>", (v5<16, 4>));
-    RUNW("v9<8,2,148>", (v9<8, 2, 148>));
+    RUNW("v7<8,4>", (v7<8, 4>));
+    RUNW("v7<8,4,5>", (v7<8, 4, 5>));
+    RUNW("v7<8,4,6>", (v7<8, 4, 6>));
+    RUNW("v7<8,4,8>", (v7<8, 4, 8>));
+    RUNW("v7<16,4,5>", (v7<16, 4, 5>));
+    RUNW("v9<8,2,296>", (v9<8, 2, 296>));
     RUNW("v9<8,2,592>", (v9<8, 2, 592>));
-    RUNW("v9<8,2,1184>", (v9<8, 2, 1184>));
-    RUNW("v9<16,4,148>", (v9<16, 4, 148>));
+    RUNW("v9<16,4,296>", (v9<16, 4, 296>));
     RUNW("v9<16,4,592>", (v9<16, 4, 592>));
     RUNW("v9<16,4,1184>", (v9<16, 4, 1184>));
   }
