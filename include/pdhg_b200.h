@@ -262,6 +262,74 @@ int pdhg_ruiz(int32_t m, int32_t n, int64_t nnz, const int32_t* ptr, const int32
               double* row_scale, double* col_scale, int32_t max_iters, double lo, double hi,
               void* tmp, size_t tmp_bytes, void* stream, int32_t* applied_out);
 
+
+/* Standard form of a general LP on the device (hybridlp.lp_core.to_standard_form,
+ * lp_core.py:250-368).  Input: CSR of the general A
+ * (m x n, sorted column indices, no duplicates), one sense code per row,
+ * lower/upper bounds (+-inf allowed), rhs, c.  pdhg_stdform_plan sizes the
+ * output (and flags non-finite matrix entries, GeneralLp.validate
+ * lp_core.py:80-81); pdhg_stdform_build fills it: the standard-form CSR
+ * (m_std+1 / nnz_std / nnz_std), b_std (m_std), c_std (n_std) and the
+ * StandardFormMap arrays (lp_core.py:226-247): shifts, pos_col, neg_col (n),
+ * slack_of_row, slack_coef, bound_var (m_std).  Bit-identical to the
+ * reference's arrays.  obj_shift (a sequential sum over columns) is the
+ * caller's.  tmp (pdhg_stdform_tmp_bytes) carries the plan into the build
+ * and must not be touched in between. */
+#define PDHG_SENSE_EQ 0
+#define PDHG_SENSE_LE 1
+#define PDHG_SENSE_GE 2
+typedef struct pdhg_stdform_dims {
+  int32_t m_std, n_std;
+  int64_t nnz_std;
+  int32_t n_struct;          /* structural columns (split variables count twice) */
+  int32_t n_ineq;            /* slack/surplus columns of <= / >= rows */
+  int32_t n_bound;           /* bound rows (finite upper bounds) */
+  int32_t nonfinite_entries; /* 1 if A holds a NaN/inf entry */
+} pdhg_stdform_dims;
+size_t pdhg_stdform_tmp_bytes(int32_t m, int32_t n);
+int pdhg_stdform_plan(int32_t m, int32_t n, int64_t nnz, const int32_t* ptr, const int32_t* col,
+                      const double* val, const int8_t* sense, const double* lower,
+                      const double* upper, void* tmp, size_t tmp_bytes, void* stream,
+                      pdhg_stdform_dims* out);
+int pdhg_stdform_build(int32_t m, int32_t n, int64_t nnz, const int32_t* ptr, const int32_t* col,
+                       const double* val, const int8_t* sense, const double* rhs,
+                       const double* lower, const double* upper, const double* c,
+                       const pdhg_stdform_dims* dims, void* tmp, size_t tmp_bytes, void* stream,
+                       int32_t* s_ptr, int32_t* s_col, double* s_val, double* b_std, double* c_std,
+                       double* shifts, int32_t* pos_col, int32_t* neg_col, int32_t* slack_of_row,
+                       double* slack_coef, int32_t* bound_var);
+
+
+/* Finishing the PDHG point on the device: unscale_point
+ * (transform.py:87-93), restrict_point (lp_core.py:371-385), lift_point
+ * (lp_core.py:388-427), violation_summary (lp_core.py:468-485).
+ * pdhg_spmv_seq: out[r] = sum over row r in stored order from 0.0 (scipy's
+ * csr_matvec order, products rounded, no FMA) -- or base[r] - sum when base is
+ * non-null; over the CSR of A' it reproduces scipy's A.T @ y.  All buffers are
+ * device pointers; restrict/lift/unscale results are bit-identical to the
+ * reference's.  pdhg_violation writes 5 host doubles: max|b - Ax|,
+ * max|c - A'y - z|, c'x, b'y, x'z (dots in a fixed block-tree order). */
+int pdhg_spmv_seq(int32_t rows, const int32_t* ptr, const int32_t* col, const double* val,
+                  const double* v, const double* base, double* out, void* stream);
+int pdhg_unscale_point(int32_t n, int32_t m, const double* row_scale, const double* col_scale,
+                       const double* xs, const double* ys, const double* zs, double* x, double* y,
+                       double* z, void* stream);
+int pdhg_restrict_x(int32_t n_general, const int32_t* pos_col, const int32_t* neg_col,
+                    const double* shifts, const double* x_std, double* x, void* stream);
+int pdhg_lift_x(int32_t n_general, const double* x, const double* shifts, const int32_t* pos_col,
+                const int32_t* neg_col, double* x_std, void* stream);
+int pdhg_lift_slacks(int32_t m_std, const int32_t* slack_of_row, const double* slack_coef,
+                     const double* r, double* x_std, void* stream);
+int pdhg_lift_bound_duals(int32_t m_std, const int32_t* bound_var, const double* z_gen,
+                          double* y_std, void* stream);
+int pdhg_max0(int64_t len, const double* v, double* out, void* stream);
+size_t pdhg_violation_tmp_bytes(int32_t m, int32_t n);
+int pdhg_violation(int32_t m, int32_t n, const int32_t* a_ptr, const int32_t* a_col,
+                   const double* a_val, const int32_t* at_ptr, const int32_t* at_col,
+                   const double* at_val, const double* b, const double* c, const double* x,
+                   const double* y, const double* z, void* tmp, size_t tmp_bytes, void* stream,
+                   double* out_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,9 +15,10 @@ from __future__ import annotations
 from .engine import DeviceLp, GpuOptions, clear_cache, device_lp, estimate_opnorm, run_pdhg
 from .lp_types import resolve as types
 from .ruiz import ruiz_equilibrate
+from .stdform import to_standard_form
 
-__all__ = ["run_pdhg", "estimate_opnorm", "ruiz_equilibrate", "GpuOptions", "DeviceLp", "device_lp",
-           "clear_cache", "install", "uninstall", "types"]
+__all__ = ["run_pdhg", "estimate_opnorm", "ruiz_equilibrate", "to_standard_form", "GpuOptions",
+           "DeviceLp", "device_lp", "clear_cache", "install", "uninstall", "types"]
 
 # the four modules that bind `run_pdhg` at import time:
 # hybridlp/__init__.py:35, pdhg.py:162, warmstart.py:33, bench.py:24
@@ -27,17 +28,24 @@ _saved: dict = {}
 
 # ruiz_equilibrate is bound in transform.py:35 and imported into warmstart.py:42
 _REBIND_RUIZ = ("hybridlp", "hybridlp.transform", "hybridlp.warmstart")
+# to_standard_form is bound in lp_core.py:250 (also called by
+# evaluate_general_point, lp_core.py:490) and imported into warmstart.py:29
+_REBIND_STD = ("hybridlp", "hybridlp.lp_core", "hybridlp.warmstart")
 
 
-def install(ruiz: bool = False) -> None:
+def install(ruiz: bool = False, std_form: bool = False) -> None:
     """Route every ``run_pdhg`` name of the reference package to this engine;
     with ``ruiz=True`` also its ``ruiz_equilibrate`` (device Ruiz, whose
-    scaled matrix then stays on the device for the PDHG solve)."""
+    scaled matrix then stays on the device for the PDHG solve); with
+    ``std_form=True`` also ``to_standard_form`` (device builder, whose
+    matrix the device Ruiz then reuses)."""
     import importlib
 
     targets = [(n, "run_pdhg", run_pdhg) for n in _REBIND]
     if ruiz:
         targets += [(n, "ruiz_equilibrate", ruiz_equilibrate) for n in _REBIND_RUIZ]
+    if std_form:
+        targets += [(n, "to_standard_form", to_standard_form) for n in _REBIND_STD]
     for name, attr, fn in targets:
         mod = importlib.import_module(name)
         if (name, attr) not in _saved:

@@ -28,7 +28,9 @@ EXPORTS = (
     "pdhg_psr_tmp_bytes", "pdhg_psr_plan", "pdhg_psr_build",
     "pdhg_check_device", "pdhg_vector", "pdhg_reduced_costs", "pdhg_set_step", "pdhg_half_step",
     "pdhg_fail_iter", "pdhg_sumsq", "pdhg_div", "pdhg_ruiz_tmp_bytes", "pdhg_ruiz",
-    "pdhg_split_build",
+    "pdhg_split_build", "pdhg_stdform_tmp_bytes", "pdhg_stdform_plan", "pdhg_stdform_build",
+    "pdhg_spmv_seq", "pdhg_unscale_point", "pdhg_restrict_x", "pdhg_lift_x", "pdhg_lift_slacks",
+    "pdhg_lift_bound_duals", "pdhg_max0", "pdhg_violation_tmp_bytes", "pdhg_violation",
 )
 
 VEC = {name: i for i, name in enumerate(
@@ -128,6 +130,20 @@ def load():
         _sig(lib, "pdhg_ruiz", C.c_int, i32, i32, i64, vp, vp, vp, vp, vp, i32, dbl, dbl, vp, szt, vp,
              P(i32))
         _sig(lib, "pdhg_split_build", C.c_int, i32, vp, vp, i32, i32, vp, vp, vp, P(i32))
+        _sig(lib, "pdhg_stdform_tmp_bytes", szt, i32, i32)
+        _sig(lib, "pdhg_stdform_plan", C.c_int, i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, szt, vp, vp)
+        _sig(lib, "pdhg_stdform_build", C.c_int, i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+             vp, szt, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp)
+        _sig(lib, "pdhg_spmv_seq", C.c_int, i32, vp, vp, vp, vp, vp, vp, vp)
+        _sig(lib, "pdhg_unscale_point", C.c_int, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp)
+        _sig(lib, "pdhg_restrict_x", C.c_int, i32, vp, vp, vp, vp, vp, vp)
+        _sig(lib, "pdhg_lift_x", C.c_int, i32, vp, vp, vp, vp, vp, vp)
+        _sig(lib, "pdhg_lift_slacks", C.c_int, i32, vp, vp, vp, vp, vp)
+        _sig(lib, "pdhg_lift_bound_duals", C.c_int, i32, vp, vp, vp, vp)
+        _sig(lib, "pdhg_max0", C.c_int, i64, vp, vp, vp)
+        _sig(lib, "pdhg_violation_tmp_bytes", szt, i32, i32)
+        _sig(lib, "pdhg_violation", C.c_int, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+             vp, szt, vp, P(dbl))
         if lib.pdhg_abi_version() != 1:
             raise NativeError("libpdhg_b200.so ABI version mismatch")
         _lib = lib

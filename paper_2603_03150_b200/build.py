@@ -18,7 +18,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpdhg_b200.so"
-SOURCES = [CSRC / "pdhg_b200.cu", CSRC / "psr_build.cu", CSRC / "ruiz.cu"]
+SOURCES = [CSRC / "pdhg_b200.cu", CSRC / "psr_build.cu", CSRC / "ruiz.cu", CSRC / "stdform.cu", CSRC / "finish.cu"]
 HEADERS = [ROOT / "include" / "pdhg_b200.h"] + sorted(CSRC.glob("*.cuh"))
 
 NVCC_FLAGS = [
@@ -43,16 +43,31 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), *map(str, SOURCES),
-           "-o", str(LIB) + ".tmp"]
+def _run(cmd, verbose):
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile every source to an object in parallel (one nvcc per file),
+    then link the shared library."""
+    if not force and not _stale():
+        return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = PKG / "_obj"
+    objdir.mkdir(exist_ok=True)
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    objs = [objdir / (src.stem + ".o") for src in SOURCES]
+    cmds = [[nvcc(), *flags, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
+            for src, obj in zip(SOURCES, objs)]
+    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+        list(ex.map(lambda c: _run(c, verbose), cmds))
+    _run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *map(str, objs),
+          "-o", str(LIB) + ".tmp"], verbose)
     os.replace(str(LIB) + ".tmp", LIB)
     return LIB
 

@@ -4,7 +4,8 @@ When the reference package ``hybridlp`` is importable, its own classes are
 used (``PdhgParams`` pdhg.py:31-48, ``SolveStats`` pdhg.py:70-77, ``KktPoint``
 lp_core.py:145-166, ``TerminationCheck`` lp_core.py:180-206,
 ``ViolationSummary`` lp_core.py:209-221, ``SolveStatus`` status.py:8-16,
-``InvalidModelError`` lp_core.py:27-28), so callers such as the reference's
+``InvalidModelError`` lp_core.py:27-28, ``StandardFormMap`` lp_core.py:224-247,
+``StandardLp`` lp_core.py:106-142), so callers such as the reference's
 ``hybrid_solve`` and its IPM warm start consume our results unchanged.
 Otherwise (e.g. on a GPU box without the reference) field-for-field mirrors
 are used.  ``SolveStats`` gains one defaulted field, ``history`` (one dict
@@ -116,6 +117,30 @@ class _SolveStats:
     max_violation: float
 
 
+@dataclass
+class _StandardFormMap:
+    n_general: int
+    m_general: int
+    n_std: int
+    m_std: int
+    obj_shift: float
+    shifts: np.ndarray
+    pos_col: np.ndarray
+    neg_col: np.ndarray
+    slack_of_row: np.ndarray
+    slack_coef: np.ndarray
+    bound_var: np.ndarray
+
+    def slack_columns(self) -> np.ndarray:
+        return self.slack_of_row[self.slack_of_row >= 0]
+
+
+def _standard_lp(A, b, c):
+    from .instances import Instance
+
+    return Instance("standard", A, np.asarray(b, dtype=float), np.asarray(c, dtype=float))
+
+
 _cache = None
 
 
@@ -131,6 +156,7 @@ def resolve() -> SimpleNamespace:
             PdhgParams=Pm.PdhgParams, BaseSolveStats=Pm.SolveStats, KktPoint=L.KktPoint,
             TerminationCheck=L.TerminationCheck, ViolationSummary=L.ViolationSummary,
             SolveStatus=S.SolveStatus, InvalidModelError=L.InvalidModelError,
+            StandardFormMap=L.StandardFormMap, StandardLp=L.StandardLp,
             reference=True,
         )
     except ImportError:
@@ -138,6 +164,7 @@ def resolve() -> SimpleNamespace:
             PdhgParams=_PdhgParams, BaseSolveStats=_SolveStats, KktPoint=_KktPoint,
             TerminationCheck=_TerminationCheck, ViolationSummary=_ViolationSummary,
             SolveStatus=_SolveStatus, InvalidModelError=_InvalidModelError,
+            StandardFormMap=_StandardFormMap, StandardLp=_standard_lp,
             reference=False,
         )
     ns.SolveStats = make_dataclass(

@@ -76,7 +76,14 @@ def ruiz_equilibrate(p, max_iters: int = 20, tol: float = 1e-2, *, gpu=None, reg
     stream = torch.cuda.Stream(dev)
     with torch.cuda.device(dev), torch.cuda.stream(stream):
         t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
-        ptr, col, val = t(A.indptr, np.int32), t(A.indices, np.int32), t(A.data, np.float64)
+        from .stdform import device_csr
+
+        resident = device_csr(p)   # built on this device by stdform.to_standard_form
+        if resident is not None and resident[2].device == dev:
+            ptr, col = resident[0], resident[1]
+            val = resident[2].clone()    # scaled in place; the standard-form copy stays intact
+        else:
+            ptr, col, val = t(A.indptr, np.int32), t(A.indices, np.int32), t(A.data, np.float64)
         rs = torch.empty(m, dtype=torch.float64, device=dev)
         cs = torch.empty(n, dtype=torch.float64, device=dev)
         tb = lib.pdhg_ruiz_tmp_bytes(m, n)

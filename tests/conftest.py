@@ -20,7 +20,8 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
-GOLDEN_NAMES = sorted(p.stem for p in GOLDEN.glob("*.npz") if not p.stem.startswith("ruiz_"))
+GOLDEN_NAMES = sorted(p.stem for p in GOLDEN.glob("*.npz")
+                      if not p.stem.startswith(("ruiz_", "stdform_")))
 RUIZ_NAMES = sorted(p.stem for p in GOLDEN.glob("ruiz_*.npz"))
 
 
