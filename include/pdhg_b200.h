@@ -112,6 +112,8 @@ typedef struct pdhg_problem {
    * split points.  1 / NULL = unsplit. */
   int32_t a_nsplit;
   const int32_t* a_split;
+  /* Heavy-row threshold of A' rows when it differs from A's (0 = heavy_threshold). */
+  int32_t at_heavy_threshold;
 } pdhg_problem;
 
 typedef struct pdhg_ctx pdhg_ctx;
@@ -211,8 +213,9 @@ int pdhg_sumsq(pdhg_ctx* ctx, const double* v, int64_t len, double* out_dev);
 int pdhg_div(pdhg_ctx* ctx, const double* w, double* v, int64_t len, double s);
 
 /* Average device time (ms) of one launch of kernel `which` (0 = primal
- * step over A' rows, 1 = dual step over A rows) over `reps` launches,
- * CUDA events on the context stream.  The iterate is advanced. */
+ * step over A' rows, 1 = dual step over A rows, 2 = one whole iteration:
+ * primal then dual) over `reps` launches, CUDA events on the context
+ * stream.  The iterate is advanced. */
 int pdhg_time_kernel(pdhg_ctx* ctx, int32_t which, int32_t reps, double tau_over_omega,
                      double sigma_omega, double* avg_ms_out);
 

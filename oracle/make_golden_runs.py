@@ -1,0 +1,57 @@
+"""Full-size reference runs for BASELINE configs (TEST INFRASTRUCTURE).
+
+Runs the REAL reference (in this container only) through its own pipeline
+pieces -- to_standard_form, ruiz_equilibrate, run_pdhg at eps_rel=1e-4 --
+on a full-size seeded instance and stores the run summary (status,
+iterations, restarts, objective, termination sides, wall time) as JSON
+under tests/golden/, so the GPU tests can compare iteration counts and
+objectives at full size without the reference:
+
+    PYTHONDONTWRITEBYTECODE=1 OPENBLAS_NUM_THREADS=1 python oracle/make_golden_runs.py config1
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, str(ROOT))
+
+import hybridlp  # noqa: E402
+
+from paper_2603_03150_b200.instances import config1_general, config3_general  # noqa: E402
+
+
+def main(which: str, scale: float = 1.0):
+    g = (config1_general if which == "config1" else config3_general)(scale).to_reference()
+    t0 = time.perf_counter()
+    p, fmap = hybridlp.to_standard_form(g)
+    t1 = time.perf_counter()
+    s, info = hybridlp.ruiz_equilibrate(p)
+    t2 = time.perf_counter()
+    pt, st = hybridlp.run_pdhg(s, hybridlp.PdhgParams(eps_rel=1e-4))
+    t3 = time.perf_counter()
+    term = st.termination
+    out = {
+        "instance": f"{which}_general(scale={scale})", "m_std": p.m, "n_std": p.n, "nnz_std": int(p.A.nnz),
+        "status": st.status.value, "iterations": st.iterations, "restarts": st.restarts,
+        "objective_scaled": float(s.c @ pt.x), "max_violation": st.max_violation,
+        "termination": [term.primal_lhs, term.primal_rhs, term.dual_lhs, term.dual_rhs,
+                        term.gap_lhs, term.gap_rhs],
+        "ruiz_passes": info.applied_iterations,
+        "seconds": {"to_standard_form": t1 - t0, "ruiz": t2 - t1, "run_pdhg": t3 - t2},
+        "numpy": np.__version__, "threads": "OPENBLAS_NUM_THREADS=1",
+    }
+    path = ROOT / "tests" / "golden" / f"run_{which}_s{scale:g}.json"
+    path.write_text(json.dumps(out, indent=1))
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 1.0)

@@ -65,6 +65,7 @@ class Problem(C.Structure):
         ("m_full", C.c_int32), ("n_full", C.c_int32), ("y_off", C.c_int32), ("x_off", C.c_int32),
         ("at_nnz", C.c_int64),
         ("a_nsplit", C.c_int32), ("a_split", C.c_void_p),
+        ("at_heavy_threshold", C.c_int32),
     ]
 
 

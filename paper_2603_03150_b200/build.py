@@ -51,26 +51,32 @@ def _run(cmd, verbose):
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: Path | None = None) -> Path:
     """Compile every source to an object in parallel (one nvcc per file),
-    then link the shared library."""
-    if not force and not _stale():
+    then link the shared library.  ``defines``/``out``: an experiment variant
+    (e.g. ("PDHG_L2_HINT=1",)) linked to another path; the product library
+    is always the default build."""
+    lib = Path(out) if out is not None else LIB
+    if not force and out is None and not _stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
 
-    objdir = PKG / "_obj"
+    objdir = PKG / ("_obj" if not defines else "_obj_" + "_".join(d.replace("=", "") for d in defines))
     objdir.mkdir(exist_ok=True)
-    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    flags = [f for f in NVCC_FLAGS if f != "-shared"] + [f"-D{d}" for d in defines]
     objs = [objdir / (src.stem + ".o") for src in SOURCES]
     cmds = [[nvcc(), *flags, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
             for src, obj in zip(SOURCES, objs)]
     with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
         list(ex.map(lambda c: _run(c, verbose), cmds))
     _run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *map(str, objs),
-          "-o", str(LIB) + ".tmp"], verbose)
-    os.replace(str(LIB) + ".tmp", LIB)
-    return LIB
+          "-o", str(lib) + ".tmp"], verbose)
+    os.replace(str(lib) + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    outs = [a[len("--out="):] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose=True, defines=defs,
+                out=Path(outs[0]) if outs else None))

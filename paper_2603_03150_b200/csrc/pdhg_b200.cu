@@ -83,6 +83,55 @@ __device__ __forceinline__ double nan_max(double a, double b) {
 
 __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 
+// Matrix-stream and gather loads of the step/SpMV kernels.  PDHG_L2_HINT
+// (compile time, default 0) selects L2 eviction-priority policies for an
+// experiment: 1 = stream evict_first + gathers evict_last, 2 = stream
+// evict_first only (tools/kernel_matrix.py --lib).
+#ifndef PDHG_L2_HINT
+#define PDHG_L2_HINT 0
+#endif
+
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ double ld_stream(const double* p) {
+#if PDHG_L2_HINT
+  double v;
+  asm("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(p), "l"(l2_policy_first()));
+  return v;
+#else
+  return __ldcs(p);
+#endif
+}
+__device__ __forceinline__ int ld_stream(const int* p) {
+#if PDHG_L2_HINT
+  int v;
+  asm("ld.global.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+               : "=r"(v) : "l"(p), "l"(l2_policy_first()));
+  return v;
+#else
+  return __ldcs(p);
+#endif
+}
+__device__ __forceinline__ double ld_gather(const double* p) {
+#if PDHG_L2_HINT == 1
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_policy_last()));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
 template <int V>
 __device__ __forceinline__ double group_sum(double v) {
 #pragma unroll
@@ -143,14 +192,14 @@ __device__ __forceinline__ void row_dot(const RowSet& A, int s, int e, int lane,
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int kk = k + u * V;
-      a[u] = kk < e ? __ldcs(A.val + kk) : 0.0;
-      j[u] = kk < e ? __ldcs(A.col + kk) : -1;
+      a[u] = kk < e ? ld_stream(A.val + kk) : 0.0;
+      j[u] = kk < e ? ld_stream(A.col + kk) : -1;
     }
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       double xv[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) xv[u] = j[u] >= 0 ? __ldg(xin[r] + j[u]) : 0.0;
+      for (int u = 0; u < kU; ++u) xv[u] = j[u] >= 0 ? ld_gather(xin[r] + j[u]) : 0.0;
 #pragma unroll
       for (int u = 0; u < kU; ++u)
         if (j[u] >= 0) acc[r] = fma(a[u], xv[u], acc[r]);
@@ -226,8 +275,8 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
 #pragma unroll
   for (int u = 0; u < kU; ++u) {
     const int kk = s + sub + u * V;
-    ac[u] = kk < e ? __ldcs(rs.val + kk) : 0.0;
-    jc[u] = kk < e ? __ldcs(rs.col + kk) : -1;
+    ac[u] = kk < e ? ld_stream(rs.val + kk) : 0.0;
+    jc[u] = kk < e ? ld_stream(rs.col + kk) : -1;
   }
   double mine = 0.0;
 #pragma unroll 1
@@ -243,12 +292,12 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int kk = sn + sub + u * V;
-      an[u] = kk < en ? __ldcs(rs.val + kk) : 0.0;
-      jn[u] = kk < en ? __ldcs(rs.col + kk) : -1;
+      an[u] = kk < en ? ld_stream(rs.val + kk) : 0.0;
+      jn[u] = kk < en ? ld_stream(rs.col + kk) : -1;
     }
     double xv[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) xv[u] = jc[u] >= 0 ? __ldg(x + jc[u]) : 0.0;
+    for (int u = 0; u < kU; ++u) xv[u] = jc[u] >= 0 ? ld_gather(x + jc[u]) : 0.0;
     double acc = 0.0;
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -259,11 +308,11 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int kk = k + u * V;
-        a2[u] = kk < e ? __ldcs(rs.val + kk) : 0.0;
-        j2[u] = kk < e ? __ldcs(rs.col + kk) : -1;
+        a2[u] = kk < e ? ld_stream(rs.val + kk) : 0.0;
+        j2[u] = kk < e ? ld_stream(rs.col + kk) : -1;
       }
 #pragma unroll
-      for (int u = 0; u < kU; ++u) x2[u] = j2[u] >= 0 ? __ldg(x + j2[u]) : 0.0;
+      for (int u = 0; u < kU; ++u) x2[u] = j2[u] >= 0 ? ld_gather(x + j2[u]) : 0.0;
 #pragma unroll
       for (int u = 0; u < kU; ++u)
         if (j2[u] >= 0) acc = fma(a2[u], x2[u], acc);
@@ -1015,7 +1064,8 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->stream = (cudaStream_t)stream;
   c->A = RowSet{prob->a_ptr, prob->a_col, prob->a_val, prob->m, prob->heavy_threshold,
                 prob->a_n_heavy, prob->a_heavy};
-  c->At = RowSet{prob->at_ptr, prob->at_col, prob->at_val, prob->n, prob->heavy_threshold,
+  c->At = RowSet{prob->at_ptr, prob->at_col, prob->at_val, prob->n,
+                 prob->at_heavy_threshold > 0 ? prob->at_heavy_threshold : prob->heavy_threshold,
                  prob->at_n_heavy, prob->at_heavy};
   c->a_lanes = prob->a_lanes > 0 ? prob->a_lanes : auto_lanes(prob->nnz, prob->m);
   c->at_lanes = prob->at_lanes > 0 ? prob->at_lanes
@@ -1351,10 +1401,15 @@ int pdhg_time_kernel(pdhg_ctx* c, int32_t which, int32_t reps, double tau_over_o
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
-  int rc = launch_step(c, which == 0, 0);  // warm
+  // which: 0 = primal step, 1 = dual step, 2 = one iteration (primal then dual)
+  int rc = launch_step(c, which != 1, 0);  // warm
+  if (!rc && which == 2) rc = launch_step(c, false, 0);
   if (rc) return rc;
   CUDA_TRY(cudaEventRecord(e0, c->stream));
-  for (int r = 0; r < reps && !rc; ++r) rc = launch_step(c, which == 0, 0);
+  for (int r = 0; r < reps && !rc; ++r) {
+    rc = launch_step(c, which != 1, 0);
+    if (!rc && which == 2) rc = launch_step(c, false, 0);
+  }
   CUDA_TRY(cudaEventRecord(e1, c->stream));
   CUDA_TRY(cudaEventSynchronize(e1));
   float ms = 0.f;

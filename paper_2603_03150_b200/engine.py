@@ -40,7 +40,10 @@ class GpuOptions:
 
     device:          CUDA device index (default: current device).
     a_lanes/at_lanes: lanes per row for A / A' rows (0 = auto from the mean row length).
-    heavy_threshold: rows longer than this get a whole thread block.
+    heavy_threshold: rows longer than this get a whole thread block (0 = auto per
+                     operator: 32 x lanes per row, so a light warp never runs more
+                     than ~8 dependent load rounds on one row; measured on config 1,
+                     profiles/r01_pipeline.md).
     opnorm:          override the power-iteration estimate (parity fallback).
     cache_layout:    keep the device layout of a model for repeated solves.
     psr:             "auto" | "on" | "off" -- panel-staged rows layout for the step
@@ -56,7 +59,7 @@ class GpuOptions:
     device: int | None = None
     a_lanes: int = 0
     at_lanes: int = 0
-    heavy_threshold: int = 1024
+    heavy_threshold: int = 0
     opnorm: float | None = None
     cache_layout: bool = True
     psr: str = "off"
@@ -65,6 +68,23 @@ class GpuOptions:
     psr_min_rows: int = 148 * 256
     l2_persist: int = 0
     dual_split: int = 1
+
+
+def auto_lanes(nnz: int, rows: int) -> int:
+    """Lanes per row from the mean row length (csrc auto_lanes; measured on
+    config 4, profiles/r01_spmv_lab2.log)."""
+    if rows <= 0:
+        return 1
+    mean = nnz / rows
+    for lanes, lo in ((32, 80), (16, 32), (8, 12), (4, 6), (2, 3)):
+        if mean >= lo:
+            return lanes
+    return 1
+
+
+def heavy_threshold(lanes: int) -> int:
+    """Auto heavy-row threshold for an operator processed with `lanes` lanes per row."""
+    return max(32, 32 * lanes)
 
 
 def _torch():
@@ -156,16 +176,20 @@ class DeviceLp:
                     self.at_ptr = t(At.indptr, np.int32)
                     self.at_col = t(At.indices, np.int32)
                     self.at_val = t(At.data, np.float64)
-                H = int(opts.heavy_threshold)
+                self.a_lanes = int(opts.a_lanes) or auto_lanes(nnz, m)
+                self.at_lanes = int(opts.at_lanes) or auto_lanes(self.at_nnz, n)
+                H = int(opts.heavy_threshold) or heavy_threshold(self.a_lanes)
+                Ht = int(opts.heavy_threshold) or heavy_threshold(self.at_lanes)
+                self.heavy = (H, Ht)
                 self.a_heavy = torch.nonzero((self.a_ptr[1:] - self.a_ptr[:-1]) > H).flatten().to(torch.int32)
-                self.at_heavy = torch.nonzero((self.at_ptr[1:] - self.at_ptr[:-1]) > H).flatten().to(torch.int32)
+                self.at_heavy = torch.nonzero((self.at_ptr[1:] - self.at_ptr[:-1]) > Ht).flatten().to(torch.int32)
                 self.psr_info = {}
                 self._psr = {}
                 for key, rows, cols, nz, ptr, col, val in (
                         ("A", m, n_full, nnz, self.a_ptr, self.a_col, self.a_val),
                         ("At", n, m_full, self.at_nnz, self.at_ptr, self.at_col, self.at_val)):
                     self._psr[key] = self._build_psr(torch, dev, key, rows, cols, nz, ptr, col, val,
-                                                     H, opts)
+                                                     H if key == "A" else Ht, opts)
                 self.a_split = None
                 self.nsplit = 1
                 K = int(opts.dual_split)
@@ -188,7 +212,8 @@ class DeviceLp:
         p.a_ptr, p.a_col, p.a_val = self.a_ptr.data_ptr(), self.a_col.data_ptr(), self.a_val.data_ptr()
         p.at_ptr, p.at_col, p.at_val = self.at_ptr.data_ptr(), self.at_col.data_ptr(), self.at_val.data_ptr()
         p.b, p.c = self.b.data_ptr(), self.c.data_ptr()
-        p.a_lanes, p.at_lanes, p.heavy_threshold = opts.a_lanes, opts.at_lanes, H
+        p.a_lanes, p.at_lanes, p.heavy_threshold = self.a_lanes, self.at_lanes, H
+        p.at_heavy_threshold = Ht
         p.a_n_heavy, p.at_n_heavy = self.a_heavy.numel(), self.at_heavy.numel()
         p.a_heavy = self.a_heavy.data_ptr() if p.a_n_heavy else None
         p.at_heavy = self.at_heavy.data_ptr() if p.at_n_heavy else None

@@ -19,7 +19,12 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--variants", default="csr,csr_l2d,csr_l2p,csr_l2")
+    ap.add_argument("--lib", default=None, help="load this build of libpdhg_b200.so (experiment variants)")
     args = ap.parse_args()
+    if args.lib:
+        from paper_2603_03150_b200 import _native
+
+        _native.LIB_PATH = Path(args.lib).resolve()
     import numpy as np
     import torch
 
@@ -51,6 +56,7 @@ def main():
         dev.reset()
         tp = dev.time_kernel(0, args.reps, 1e-3, 1e-3)
         td = dev.time_kernel(1, args.reps, 1e-3, 1e-3)
+        talt = dev.time_kernel(2, args.reps, 1e-3, 1e-3)
         # alternating primal/dual as in a real period (graph of 64 iterations)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         dev.run_period(64, 0, 1e-3, 1e-3, 0.0)
@@ -60,7 +66,7 @@ def main():
         ev1.record(dev.stream)
         torch.cuda.synchronize()
         per_iter = ev0.elapsed_time(ev1) / (3 * 64)
-        out[name] = {"build_s": build, "primal_ms": tp, "dual_ms": td, "iter_ms": per_iter,
+        out[name] = {"build_s": build, "primal_ms": tp, "dual_ms": td, "iter_ms": per_iter, "alt_ms": talt,
                      "primal_gbs": ab["primal"] / tp / 1e6, "dual_gbs": ab["dual"] / td / 1e6,
                      "psr": dev.psr_info}
         print(name, json.dumps(out[name]), flush=True)
