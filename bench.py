@@ -391,7 +391,8 @@ def main():
     ap.add_argument("--seed", type=int, default=4)
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--ttk", action="store_true", help="also run to eps_rel=1e-4 (time-to-1e-4)")
+    ap.add_argument("--ttk", action=argparse.BooleanOptionalAction, default=True,
+                    help="also run to eps_rel=1e-4 (time-to-1e-4, part of the metric; --no-ttk skips)")
     ap.add_argument("--ttk-limit", type=float, default=300.0)
     ap.add_argument("--ttk-unscaled", action="store_true", help="also run to 1e-4 without Ruiz")
     ap.add_argument("--psr", default="off", choices=["off", "on", "auto"],
