@@ -182,6 +182,11 @@ struct Stripes {
   const int* seg_ptr;           // rows+1 (per row: its segments' slots, stripe order)
   const int* seg_slot;
   Csr rem;                      // remote entries (CSR, rows x cols)
+  // v3: chunk records (TMA bulk-copied): [int4 header][cnt ng*32 u16][col16 ne u16, pad16][val ne f64, pad16]
+  const unsigned char* rec;
+  const long long* chunk_off;   // nchunks+1 byte offsets into rec
+  const int* chunk_stripe;      // nchunks
+  const int* cta_chunk;         // ncta+1
 };
 
 // One group of 32 segments: lane l's segment is slot g*32+l.  V lanes per
@@ -384,13 +389,124 @@ __global__ void __launch_bounds__(256) k_final(Stripes L, const double* __restri
   if (rl < L.rows) y[rl] = ps + d;
 }
 
+// ---------------------------------------------------------------- v3: TMA-fed chunks
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(saddr(dst)), "l"(src), "r"(bytes), "r"(saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done) : "r"(saddr(bar)), "r"(parity) : "memory");
+  }
+}
+
+constexpr int kStage3 = 5328;  // 16 + 8*64 + 480*2 + 480*8 (CE = 480 entries, CG = 8 groups)
+
+template <int NW, int NS>
+__global__ void __launch_bounds__(NW * 32, 1) k_stripe3(Stripes L, const double* __restrict__ x,
+                                                        double* __restrict__ part) {
+  extern __shared__ __align__(16) unsigned char smem3[];
+  double* win = reinterpret_cast<double*>(smem3);
+  unsigned char* ring = smem3 + (size_t)L.W * 8;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)NW * NS * kStage3);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = L.cta_chunk[blockIdx.x], c1 = L.cta_chunk[blockIdx.x + 1];
+  if (c0 >= c1) return;
+  uint64_t* mybar = bars + warp * NS;
+  unsigned char* mystage = ring + (size_t)warp * NS * kStage3;
+  if (lane == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&mybar[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int ord) {
+    const int c = c0 + warp + ord * NW;
+    if (c >= c1) return;
+    const long long o0 = L.chunk_off[c], o1 = L.chunk_off[c + 1];
+    const int s = ord % NS;
+    mbar_expect_tx(&mybar[s], (uint32_t)(o1 - o0));
+    bulk_g2s(mystage + (size_t)s * kStage3, L.rec + o0, (uint32_t)(o1 - o0), &mybar[s]);
+  };
+  if (lane == 0) {
+    fence_proxy_async();
+    for (int k = 0; k < NS; ++k) issue(k);
+  }
+  const unsigned lt = (1u << lane) - 1u;
+  int ord = 0;
+  int cs = c0;
+  while (cs < c1) {
+    const int stripe = L.chunk_stripe[cs];
+    int ce = cs + 1;
+    while (ce < c1 && L.chunk_stripe[ce] == stripe) ++ce;
+    __syncthreads();
+    {
+      const long long col0 = (long long)stripe * L.W;
+      const int len = (int)min((long long)L.W, L.cols - col0);
+      const double2* src = reinterpret_cast<const double2*>(x + col0);
+      double2* dst = reinterpret_cast<double2*>(win);
+#pragma unroll 8
+      for (int k = threadIdx.x; k < len / 2; k += NW * 32) dst[k] = __ldg(src + k);
+      if ((len & 1) && threadIdx.x == 0) win[len - 1] = __ldg(x + col0 + len - 1);
+    }
+    __syncthreads();
+    for (; c0 + warp + ord * NW < ce; ++ord) {
+      const int s = ord % NS;
+      mbar_wait(&mybar[s], (uint32_t)((ord / NS) & 1));
+      const unsigned char* st = mystage + (size_t)s * kStage3;
+      const int4 hdr = *reinterpret_cast<const int4*>(st);
+      const unsigned short* cntp = reinterpret_cast<const unsigned short*>(st + 16);
+      const unsigned short* colp = cntp + hdr.x * 32;
+      const double* valp = reinterpret_cast<const double*>(st + 16 + hdr.x * 64 + ((hdr.y * 2 + 15) & ~15));
+      int base = 0;
+      for (int gi = 0; gi < hdr.x; ++gi) {
+        const int c = cntp[gi * 32 + lane];
+        const int maxc = __reduce_max_sync(0xffffffffu, c);
+        double acc = 0.0;
+        for (int k = 0; k < maxc; k += 4) {
+          double a[4];
+          int j[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const unsigned mask = __ballot_sync(0xffffffffu, c > k + u);
+            const int idx = base + __popc(mask & lt);
+            a[u] = c > k + u ? valp[idx] : 0.0;
+            j[u] = c > k + u ? (int)colp[idx] : -1;
+            base += __popc(mask);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (j[u] >= 0) acc = (k + u == 0) ? a[u] * win[j[u]] : fma(a[u], win[j[u]], acc);
+        }
+        part[(size_t)(hdr.z + gi) * 32 + lane] = acc;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        fence_proxy_async();
+        issue(ord + NS);
+      }
+    }
+    cs = ce;
+  }
+}
+
 struct HostStripes {
   Stripes d;
-  long long stripe_ent, remote_ent, nseg;
+  long long stripe_ent, remote_ent, nseg, nchunks, rec_bytes;
   int ncta;
 };
 
-static HostStripes build_stripes(const Csr& M, int W, int T, int ncta) {
+static HostStripes build_stripes(const Csr& M, int W, int T, int ncta, int smax = 0, int CE = 512, int CG = 8) {
   std::vector<int> ptr(M.rows + 1), col(M.nnz);
   std::vector<double> val(M.nnz);
   CK(cudaMemcpy(ptr.data(), M.ptr, (M.rows + 1) * 4, cudaMemcpyDeviceToHost));
@@ -406,7 +522,7 @@ static HostStripes build_stripes(const Csr& M, int W, int T, int ncta) {
       const int s = col[k] / W;
       int r = k;
       while (r < e && col[r] / W == s) ++r;
-      if (r - k >= T) { segc[s]++; entc[s] += r - k; } else remc[i] += r - k;
+      if (r - k >= T) { segc[s] += smax > 0 ? (r - k + smax - 1) / smax : 1; entc[s] += r - k; } else remc[i] += r - k;
       k = r;
     }
   }
@@ -436,10 +552,14 @@ static HostStripes build_stripes(const Csr& M, int W, int T, int ncta) {
       int r = k;
       while (r < e && col[r] / W == s) ++r;
       if (r - k >= T) {
-        const long long slot = (long long)stripe_g[s] * 32 + segfill[s]++;
-        cnt[slot] = (unsigned short)(r - k);
-        seg_slot.push_back((int)slot);
-        for (int q = k; q < r; ++q) { sval[ecur[s]] = val[q]; scol[ecur[s]] = (unsigned short)(col[q] - s * W); ++ecur[s]; }
+        for (int k2 = k; k2 < r;) {
+          const int r2 = smax > 0 ? std::min(r, k2 + smax) : r;
+          const long long slot = (long long)stripe_g[s] * 32 + segfill[s]++;
+          cnt[slot] = (unsigned short)(r2 - k2);
+          seg_slot.push_back((int)slot);
+          for (int q = k2; q < r2; ++q) { sval[ecur[s]] = val[q]; scol[ecur[s]] = (unsigned short)(col[q] - s * W); ++ecur[s]; }
+          k2 = r2;
+        }
       } else {
         for (int q = k; q < r; ++q) { rcol[rc] = col[q]; rval[rc] = val[q]; ++rc; }
       }
@@ -482,6 +602,49 @@ static HostStripes build_stripes(const Csr& M, int W, int T, int ncta) {
     cta_g[c] = (int)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
   }
   cta_g[ncta] = G;
+  // chunk records for v3: per CTA, consecutive groups of one stripe, <= CE entries, <= CG groups
+  std::vector<unsigned char> rec;
+  std::vector<long long> chunk_off;
+  std::vector<int> chunk_stripe, cta_chunk(ncta + 1, 0);
+  {
+    std::vector<int> g_stripe(G);
+    for (int s2 = 0; s2 < ns; ++s2) for (int g = stripe_g[s2]; g < stripe_g[s2 + 1]; ++g) g_stripe[g] = s2;
+    auto gent = [&](int g) { int t = 0; for (int l = 0; l < 32; ++l) t += cnt[(size_t)g * 32 + l]; return t; };
+    auto pad16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
+    auto emit = [&](int ga, int gb) {
+      int ne = 0;
+      for (int g = ga; g < gb; ++g) ne += gent(g);
+      const size_t off = rec.size();
+      const int ng = gb - ga;
+      const size_t hb = 16, cb = (size_t)ng * 64, colb = pad16((size_t)ne * 2), vb = pad16((size_t)ne * 8);
+      rec.resize(off + hb + cb + colb + vb, 0);
+      int hdr[4] = {ng, ne, ga, g_stripe[ga]};
+      memcpy(&rec[off], hdr, 16);
+      memcpy(&rec[off + hb], &cnt[(size_t)ga * 32], cb);
+      if (ne) {
+        memcpy(&rec[off + hb + cb], &scol2[gbase[ga]], (size_t)ne * 2);
+        memcpy(&rec[off + hb + cb + colb], &sval2[gbase[ga]], (size_t)ne * 8);
+      }
+      chunk_off.push_back((long long)off);
+      chunk_stripe.push_back(g_stripe[ga]);
+    };
+    for (int c = 0; c < ncta; ++c) {
+      cta_chunk[c] = (int)chunk_off.size();
+      int ga = cta_g[c];
+      while (ga < cta_g[c + 1]) {
+        int gb = ga, ne = 0;
+        while (gb < cta_g[c + 1] && gb - ga < CG && g_stripe[gb] == g_stripe[ga] && ne + gent(gb) <= CE) {
+          ne += gent(gb);
+          ++gb;
+        }
+        if (gb == ga) { fprintf(stderr, "group %d has %d entries > CE %d\n", ga, gent(ga), CE); exit(1); }
+        emit(ga, gb);
+        ga = gb;
+      }
+    }
+    cta_chunk[ncta] = (int)chunk_off.size();
+    chunk_off.push_back((long long)rec.size());
+  }
   auto up = [](const void* h, size_t bytes) { void* d; CK(cudaMalloc(&d, bytes ? bytes : 8)); if (bytes) CK(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice)); return d; };
   HostStripes H{};
   Stripes& L = H.d;
@@ -500,6 +663,12 @@ static HostStripes build_stripes(const Csr& M, int W, int T, int ncta) {
   L.rem.ptr = (int*)up(rptr.data(), rptr.size() * 4);
   L.rem.col = (int*)up(rcol.data(), rcol.size() * 4);
   L.rem.val = (double*)up(rval.data(), rval.size() * 8);
+  L.rec = (unsigned char*)up(rec.data(), rec.size());
+  L.chunk_off = (long long*)up(chunk_off.data(), chunk_off.size() * 8);
+  L.chunk_stripe = (int*)up(chunk_stripe.data(), chunk_stripe.size() * 4);
+  L.cta_chunk = (int*)up(cta_chunk.data(), cta_chunk.size() * 4);
+  H.nchunks = (long long)chunk_stripe.size();
+  H.rec_bytes = (long long)rec.size();
   H.stripe_ent = NE; H.remote_ent = rptr[M.rows]; H.nseg = (long long)seg_slot.size(); H.ncta = ncta;
   return H;
 }
@@ -601,6 +770,29 @@ int main(int argc, char** argv) {
         const float t3 = timeit([&] { ks<<<H.ncta, 1024, smem>>>(H.d, xin, part); kf<<<g256(M.rows), 256>>>(H.d, part, xin, ya); });
         printf("  %-28s stripe %7.3f  final %7.3f  both %7.3f ms  (%.2fx)  maxrel %.2e\n", name, t1, t2, t3, tb0 / t3, maxrel(M.rows));
       };
+      {
+        HostStripes H3 = build_stripes(M, WW, T, nsm, 15, 480, 8);
+        double* part3;
+        CK(cudaMalloc(&part3, (size_t)H3.d.ngroups * 32 * 8));
+        constexpr int NW3 = 6, NS3 = 3;
+        const size_t smem3 = (size_t)WW * 8 + (size_t)NW3 * NS3 * kStage3 + NW3 * NS3 * 8;
+        auto ks = k_stripe3<NW3, NS3>;
+        CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+        printf("  v3: %lld stripe entries, %lld segments (mean %.2f), %lld chunks, %.1f MB records, smem %zu\n",
+               H3.stripe_ent, H3.nseg, (double)H3.stripe_ent / H3.nseg, H3.nchunks, H3.rec_bytes / 1e6, smem3);
+        const float t1 = timeit([&] { ks<<<H3.ncta, NW3 * 32, smem3>>>(H3.d, xin, part3); });
+        float t2, t3;
+        if (op == 0) {
+          t2 = timeit([&] { k_final<8, 4><<<g256(M.rows), 256>>>(H3.d, part3, xin, ya); });
+          t3 = timeit([&] { ks<<<H3.ncta, NW3 * 32, smem3>>>(H3.d, xin, part3); k_final<8, 4><<<g256(M.rows), 256>>>(H3.d, part3, xin, ya); });
+        } else {
+          t2 = timeit([&] { k_final<4, 4><<<g256(M.rows), 256>>>(H3.d, part3, xin, ya); });
+          t3 = timeit([&] { ks<<<H3.ncta, NW3 * 32, smem3>>>(H3.d, xin, part3); k_final<4, 4><<<g256(M.rows), 256>>>(H3.d, part3, xin, ya); });
+        }
+        printf("  %-28s stripe %7.3f  final %7.3f  both %7.3f ms  (%.2fx)  maxrel %.2e\n", "v3 TMA chunks", t1, t2, t3,
+               tb0 / t3, maxrel(M.rows));
+        cudaFree(part3);
+      }
       auto runs2 = [&](auto ks, int nt, auto kf, const char* name) {
         CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const float t1 = timeit([&] { ks<<<H.ncta, nt, smem>>>(H.d, xin, part); });
@@ -608,26 +800,6 @@ int main(int argc, char** argv) {
         const float t3 = timeit([&] { ks<<<H.ncta, nt, smem>>>(H.d, xin, part); kf<<<g256(M.rows), 256>>>(H.d, part, xin, ya); });
         printf("  %-28s stripe %7.3f  final %7.3f  both %7.3f ms  (%.2fx)  maxrel %.2e\n", name, t1, t2, t3, tb0 / t3, maxrel(M.rows));
       };
-      if (op == 0) {
-        runs2(k_stripe2<12, 512>, 512, k_final2<8, 4>, "v2 K12x512 final2<8,4>");
-        runs2(k_stripe2<16, 512>, 512, k_final2<8, 4>, "v2 K16x512 final2<8,4>");
-        runs2(k_stripe2<12, 768>, 768, k_final2<8, 2>, "v2 K12x768 final2<8,2>");
-        runs2(k_stripe2<12, 512>, 512, k_final2<4, 4>, "v2 K12x512 final2<4,4>");
-      } else {
-        runs2(k_stripe2<12, 512>, 512, k_final2<4, 4>, "v2 K12x512 final2<4,4>");
-        runs2(k_stripe2<16, 512>, 512, k_final2<4, 4>, "v2 K16x512 final2<4,4>");
-        runs2(k_stripe2<12, 768>, 768, k_final2<4, 2>, "v2 K12x768 final2<4,2>");
-        runs2(k_stripe2<12, 512>, 512, k_final2<8, 2>, "v2 K12x512 final2<8,2>");
-      }
-      if (op == 0) {
-        runs(k_stripe<4>, k_final<8, 4>, "V=4 final<8,4>");
-        runs(k_stripe<8>, k_final<8, 4>, "V=8 final<8,4>");
-        runs(k_stripe<8>, k_final<4, 4>, "V=8 final<4,4>");
-      } else {
-        runs(k_stripe<4>, k_final<4, 4>, "V=4 final<4,4>");
-        runs(k_stripe<8>, k_final<4, 4>, "V=8 final<4,4>");
-        runs(k_stripe<8>, k_final<8, 2>, "V=8 final<8,2>");
-      }
       cudaFree(part);
     }
   }
