@@ -80,6 +80,18 @@ typedef struct pdhg_psr {
   const uint8_t* heavy;         /* rows */
 } pdhg_psr;
 
+/* Sliced-ELL layout of one operator (csrc/sell_build.cu): slices of 32
+ * consecutive rows, the k-th entry of a slice's rows stored contiguously at
+ * sptr[slice] + 32*k + lane.  Light rows only (heavy rows stay on the
+ * block-per-row CSR path); row lengths come from the operator's CSR ptr. */
+typedef struct pdhg_sell {
+  int32_t rows, nslices;
+  const int64_t* sptr;   /* nslices+1 slot offsets */
+  const int32_t* width;  /* nslices: longest light row of the slice */
+  const int32_t* col;    /* slots */
+  const double* val;     /* slots */
+} pdhg_sell;
+
 typedef struct pdhg_problem {
   int32_t m, n;
   int64_t nnz;
@@ -114,6 +126,9 @@ typedef struct pdhg_problem {
   const int32_t* a_split;
   /* Heavy-row threshold of A' rows when it differs from A's (0 = heavy_threshold). */
   int32_t at_heavy_threshold;
+  /* Optional sliced-ELL layouts for the step kernels (NULL = CSR-vector). */
+  const pdhg_sell* a_sell;   /* dual step (rows of A)    */
+  const pdhg_sell* at_sell;  /* primal step (rows of A') */
 } pdhg_problem;
 
 typedef struct pdhg_ctx pdhg_ctx;
@@ -332,6 +347,18 @@ int pdhg_violation(int32_t m, int32_t n, const int32_t* a_ptr, const int32_t* a_
                    const double* at_val, const double* b, const double* c, const double* x,
                    const double* y, const double* z, void* tmp, size_t tmp_bytes, void* stream,
                    double* out_host);
+
+
+/* Sliced-ELL build (device): plan writes width (nslices = ceil(rows/32)) and
+ * sptr (nslices+1) and returns the slot count; the caller allocates
+ * slots-sized col/val and calls fill.  Rows longer than heavy_threshold are
+ * left out. */
+size_t pdhg_sell_tmp_bytes(int32_t rows);
+int pdhg_sell_plan(int32_t rows, const int32_t* ptr, int32_t heavy_threshold, int32_t* width,
+                   int64_t* sptr, void* tmp, size_t tmp_bytes, void* stream, int64_t* slots_out);
+int pdhg_sell_fill(int32_t rows, const int32_t* ptr, const int32_t* col, const double* val,
+                   int32_t heavy_threshold, const int64_t* sptr, int32_t* scol, double* sval,
+                   void* stream);
 
 #ifdef __cplusplus
 }

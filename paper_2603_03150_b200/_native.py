@@ -31,6 +31,7 @@ EXPORTS = (
     "pdhg_split_build", "pdhg_stdform_tmp_bytes", "pdhg_stdform_plan", "pdhg_stdform_build",
     "pdhg_spmv_seq", "pdhg_unscale_point", "pdhg_restrict_x", "pdhg_lift_x", "pdhg_lift_slacks",
     "pdhg_lift_bound_duals", "pdhg_max0", "pdhg_violation_tmp_bytes", "pdhg_violation",
+    "pdhg_sell_tmp_bytes", "pdhg_sell_plan", "pdhg_sell_fill",
 )
 
 VEC = {name: i for i, name in enumerate(
@@ -47,6 +48,13 @@ class Psr(C.Structure):
         ("rcnt", C.c_void_p), ("val", C.c_void_p), ("col16", C.c_void_p), ("col", C.c_void_p),
         ("heavy", C.c_void_p),
     ]
+
+
+class Sell(C.Structure):
+    """struct pdhg_sell (sliced-ELL layout of one operator)."""
+
+    _fields_ = [("rows", C.c_int32), ("nslices", C.c_int32), ("sptr", C.c_void_p),
+                ("width", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p)]
 
 
 class Problem(C.Structure):
@@ -66,6 +74,7 @@ class Problem(C.Structure):
         ("at_nnz", C.c_int64),
         ("a_nsplit", C.c_int32), ("a_split", C.c_void_p),
         ("at_heavy_threshold", C.c_int32),
+        ("a_sell", C.POINTER(Sell)), ("at_sell", C.POINTER(Sell)),
     ]
 
 
@@ -143,6 +152,9 @@ def load():
         _sig(lib, "pdhg_lift_bound_duals", C.c_int, i32, vp, vp, vp, vp)
         _sig(lib, "pdhg_max0", C.c_int, i64, vp, vp, vp)
         _sig(lib, "pdhg_violation_tmp_bytes", szt, i32, i32)
+        _sig(lib, "pdhg_sell_tmp_bytes", szt, i32)
+        _sig(lib, "pdhg_sell_plan", C.c_int, i32, vp, i32, vp, vp, vp, szt, vp, P(i64))
+        _sig(lib, "pdhg_sell_fill", C.c_int, i32, vp, vp, vp, i32, vp, vp, vp, vp)
         _sig(lib, "pdhg_violation", C.c_int, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
              vp, szt, vp, P(dbl))
         if lib.pdhg_abi_version() != 1:

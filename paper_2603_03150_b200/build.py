@@ -18,7 +18,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpdhg_b200.so"
-SOURCES = [CSRC / "pdhg_b200.cu", CSRC / "psr_build.cu", CSRC / "ruiz.cu", CSRC / "stdform.cu", CSRC / "finish.cu"]
+SOURCES = [CSRC / "pdhg_b200.cu", CSRC / "psr_build.cu", CSRC / "ruiz.cu", CSRC / "stdform.cu", CSRC / "finish.cu",
+           CSRC / "sell_build.cu"]
 HEADERS = [ROOT / "include" / "pdhg_b200.h"] + sorted(CSRC.glob("*.cuh"))
 
 NVCC_FLAGS = [

@@ -461,6 +461,82 @@ __global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
   }
 }
 
+// Step over a sliced-ELL layout (csrc/sell_build.cu): a warp owns one slice
+// of 32 consecutive rows, lane l row 32*slice + l; each lane sums its row
+// sequentially in entry order (kU entries' loads in flight), so there are no
+// lane reductions and every matrix load instruction is 256 B (values) /
+// 128 B (indices) contiguous.  Heavy rows: one block each, as in k_step.
+struct SellSet {
+  int rows, nslices;
+  const long long* __restrict__ sptr;
+  const int* __restrict__ width;
+  const int* __restrict__ col;
+  const double* __restrict__ val;
+};
+
+template <bool PRIMAL>
+__global__ void __launch_bounds__(kBlock) k_step_sell(StepArgs a, SellSet S, int j_in_period) {
+  constexpr int kU = 4;
+  __shared__ double red[kWarps];
+  StepParams* P = a.P;
+  const long long iter = P->iter0 + j_in_period + 1;
+  if (P->fail_iter < iter) return;
+  const double w = P->w0 + (double)(j_in_period + 1);
+  const double step = PRIMAL ? P->tau_w : P->sigma_w;
+  if ((int)blockIdx.x < a.rs.n_heavy) {
+    const double* xin[1] = {a.gather};
+    const int row = a.rs.heavy[blockIdx.x];
+    const int s = a.rs.ptr[row], e = a.rs.ptr[row + 1];
+    double acc[1];
+    row_dot<kBlock, 1>(a.rs, s, e, threadIdx.x, xin, acc);
+    const double d = block_sum(acc[0], red);
+    if (threadIdx.x == 0) {
+      if (PRIMAL) primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
+      else dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const long long sl = ((long long)(blockIdx.x - a.rs.n_heavy) * kBlock + threadIdx.x) >> 5;
+  if (sl >= S.nslices) return;  // warp-uniform
+  const long long rl = sl * 32 + lane;
+  const bool in_range = rl < a.rs.rows;
+  double o1 = 0.0, o2 = 0.0, o3 = 0.0;
+  int len = 0;
+  if (in_range) {
+    o1 = a.cb[rl];
+    o2 = a.x[rl];
+    o3 = a.xbar[rl];
+    len = a.rs.ptr[rl + 1] - a.rs.ptr[rl];
+  }
+  const bool ok = in_range && len <= a.rs.heavy_threshold;
+  if (!ok) len = 0;
+  const int width = S.width[sl];
+  const long long base = S.sptr[sl] + lane;
+  const double* __restrict__ x = a.gather;
+  double acc = 0.0;
+  for (int k = 0; k < width; k += kU) {
+    double av[kU], xv[kU];
+    int jv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const bool on = k + u < len;
+      av[u] = on ? ld_stream(S.val + base + 32LL * (k + u)) : 0.0;
+      jv[u] = on ? ld_stream(S.col + base + 32LL * (k + u)) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) xv[u] = jv[u] >= 0 ? ld_gather(x + jv[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (jv[u] >= 0) acc = fma(av[u], xv[u], acc);
+  }
+  if (ok) {
+    const int row = (int)rl;
+    if (PRIMAL) primal_epi_pre(row, acc, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P);
+    else dual_epi_pre(row, acc, o1, o2, o3, a.x, a.xbar, step, w, iter, P);
+  }
+}
+
 // Dual step split by column chunks (split-K over the columns of A): pass k
 // sums each row's entries whose column lies in chunk k, so the xe gathers
 // of a pass come from an L2-sized window of the 80 MB vector instead of all
@@ -893,6 +969,8 @@ struct pdhg_ctx {
   int mf, nf;          // full (padded) lengths of the y- and x-space vectors
   int yo, xo;          // this shard's slice offsets in them
   bool has_psr[2];     // [0] = A (dual), [1] = A' (primal)
+  bool has_sell[2];    // same indexing
+  SellSet sell[2];
   psr::Layout psr_l[2];
   size_t psr_smem[2];
   int l2_persist, l2_maxwin;
@@ -1012,6 +1090,12 @@ int launch_step(pdhg_ctx* c, bool primal, int j) {
     // heavy rows: block per row through the CSR kernel (grid = n_heavy => no light rows)
     return dispatch_lanes<StepLaunchEx>(lanes, c, primal, a, j, a.rs.n_heavy, win_base, win);
   }
+  if (c->has_sell[k]) {
+    const SellSet& S = c->sell[k];
+    const int grid = a.rs.n_heavy + (int)(((long long)S.nslices * 32 + kBlock - 1) / kBlock);
+    return primal ? launch_ex(c, k_step_sell<true>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j)
+                  : launch_ex(c, k_step_sell<false>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
+  }
   return dispatch_lanes<StepLaunchEx>(lanes, c, primal, a, j, grid_rows(a.rs, lanes), win_base, win);
 }
 
@@ -1082,6 +1166,19 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->partials = cv.take<double>((size_t)kCheckBlocks * kMaxQ);
   c->scalars = cv.take<double>(64);
   c->P = cv.take<StepParams>(1);
+  for (int k = 0; k < 2; ++k) {
+    const pdhg_sell* q = k == 0 ? prob->a_sell : prob->at_sell;
+    c->has_sell[k] = q != nullptr;
+    if (q) {
+      const int rows = k == 0 ? prob->m : prob->n;
+      if (q->rows != rows || q->nslices != (rows + 31) / 32 || !q->sptr || !q->width) {
+        delete c;
+        return fail(PDHG_ERR_ARG, "sell layout does not match the operator");
+      }
+      c->sell[k] = SellSet{q->rows, q->nslices, reinterpret_cast<const long long*>(q->sptr), q->width,
+                           q->col, q->val};
+    }
+  }
   for (int k = 0; k < 2; ++k) {
     const pdhg_psr* q = k == 0 ? prob->a_psr : prob->at_psr;
     c->has_psr[k] = q != nullptr;

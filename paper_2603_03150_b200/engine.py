@@ -52,6 +52,12 @@ class GpuOptions:
     psr_min_staged:  entries a (row block, panel) needs to be staged in shared memory.
     dual_split:      column chunks of the dual step's SpMV (split-K, csrc k_dual_split):
                      each pass gathers from an L2-sized window of xe; 1 = unsplit.
+    sell:            "auto" | "on" | "off" -- sliced-ELL layout (csrc/sell_build.cu) for
+                     the step kernels; auto uses it for an operator with short rows
+                     (mean < sell_max_mean entries) whose padded slot count stays within
+                     sell_max_pad x its nonzeros and that has no PSR layout: config 3
+                     (primal 56 -> 51 us, dual 43 -> 34 us).  On config 4's A' (mean 20)
+                     it is neutral (0.94 vs 0.93 ms), so CSR-vector stays there.
     l2_persist:      bit mask: 1 = pin y in L2 for the primal step, 2 = pin xe for the
                      dual step (persisting access-policy window; L2 holds 79 MB persisting).
     """
@@ -68,6 +74,9 @@ class GpuOptions:
     psr_min_rows: int = 148 * 256
     l2_persist: int = 0
     dual_split: int = 1
+    sell: str = "auto"
+    sell_max_pad: float = 1.6
+    sell_max_mean: float = 12.0
 
 
 def auto_lanes(nnz: int, rows: int) -> int:
@@ -190,6 +199,13 @@ class DeviceLp:
                         ("At", n, m_full, self.at_nnz, self.at_ptr, self.at_col, self.at_val)):
                     self._psr[key] = self._build_psr(torch, dev, key, rows, cols, nz, ptr, col, val,
                                                      H if key == "A" else Ht, opts)
+                self._sell = {}
+                self.sell_info = {}
+                for key, rows, nz, ptr, col, val, Hk in (
+                        ("A", m, nnz, self.a_ptr, self.a_col, self.a_val, H),
+                        ("At", n, self.at_nnz, self.at_ptr, self.at_col, self.at_val, Ht)):
+                    self._sell[key] = None if self._psr[key] else self._build_sell(
+                        torch, dev, key, rows, nz, ptr, col, val, Hk, opts)
                 self.a_split = None
                 self.nsplit = 1
                 K = int(opts.dual_split)
@@ -214,6 +230,8 @@ class DeviceLp:
         p.b, p.c = self.b.data_ptr(), self.c.data_ptr()
         p.a_lanes, p.at_lanes, p.heavy_threshold = self.a_lanes, self.at_lanes, H
         p.at_heavy_threshold = Ht
+        p.a_sell = C.pointer(self._sell["A"][0]) if self._sell["A"] else None
+        p.at_sell = C.pointer(self._sell["At"][0]) if self._sell["At"] else None
         p.a_n_heavy, p.at_n_heavy = self.a_heavy.numel(), self.at_heavy.numel()
         p.a_heavy = self.a_heavy.data_ptr() if p.a_n_heavy else None
         p.at_heavy = self.at_heavy.data_ptr() if p.at_n_heavy else None
@@ -233,6 +251,36 @@ class DeviceLp:
         self.timings = {"upload_s": t_up - t_start, "layout_s": t_end - t_up}
         self._fin = weakref.finalize(self, self.lib.pdhg_ctx_destroy, ctx)
         self._scal = (C.c_double * (2 * N.NQ))()
+
+    def _build_sell(self, torch, dev, key, rows, nnz, ptr, col, val, H, opts):
+        """Plan + fill the sliced-ELL layout of one operator on the device (or None)."""
+        if opts.sell == "off" or rows <= 0 or nnz <= 0:
+            return None
+        if opts.sell == "auto" and nnz / rows >= opts.sell_max_mean:
+            return None
+        lib = self.lib
+        sptr_ = self.stream.cuda_stream
+        ns = (rows + 31) // 32
+        width = torch.empty(ns, dtype=torch.int32, device=dev)
+        sp = torch.empty(ns + 1, dtype=torch.int64, device=dev)
+        tb = lib.pdhg_sell_tmp_bytes(rows)
+        tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=dev)
+        slots = C.c_int64()
+        N.check(lib.pdhg_sell_plan(rows, ptr.data_ptr(), int(H), width.data_ptr(), sp.data_ptr(),
+                                   tmp.data_ptr(), tb, sptr_, C.byref(slots)))
+        pad = slots.value / max(1, nnz)
+        self.sell_info[key] = {"slots": slots.value, "pad": pad, "used": False}
+        if opts.sell == "auto" and pad > opts.sell_max_pad:
+            return None
+        scol = torch.empty(max(slots.value, 1), dtype=torch.int32, device=dev)
+        sval = torch.empty(max(slots.value, 1), dtype=torch.float64, device=dev)
+        N.check(lib.pdhg_sell_fill(rows, ptr.data_ptr(), col.data_ptr(), val.data_ptr(), int(H),
+                                   sp.data_ptr(), scol.data_ptr(), sval.data_ptr(), sptr_))
+        d = N.Sell()
+        d.rows, d.nslices = rows, ns
+        d.sptr, d.width, d.col, d.val = sp.data_ptr(), width.data_ptr(), scol.data_ptr(), sval.data_ptr()
+        self.sell_info[key]["used"] = True
+        return (d, (width, sp, scol, sval))
 
     def _build_psr(self, torch, dev, key, rows, cols, nnz, ptr, col, val, H, opts):
         """Plan + build the PSR layout of one operator on the device (or None)."""

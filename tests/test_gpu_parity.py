@@ -29,11 +29,12 @@ def eng():
     return eng
 
 
-# the step kernels have three layouts: CSR-vector, and PSR with every entry
-# staged in shared-memory panels or every entry gathered from global memory
+# the step kernels' layouts: CSR-vector (also split-K), sliced ELL, and PSR
+# with every entry staged in shared-memory panels or gathered from global memory
 LAYOUTS = {
-    "csr": dict(psr="off"),
-    "csr_split2": dict(psr="off", dual_split=2),
+    "csr": dict(psr="off", sell="off"),
+    "sell": dict(psr="off", sell="on"),
+    "csr_split2": dict(psr="off", sell="off", dual_split=2),
     "psr_staged": dict(psr="on", psr_min_staged=1),
     "psr_remote": dict(psr="on", psr_min_staged=10**9),
 }

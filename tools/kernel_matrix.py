@@ -37,7 +37,9 @@ def main():
     print(f"gen {time.time() - t:.1f}s m={inst.m} n={inst.n} nnz={inst.nnz}", flush=True)
     ab = algorithmic_bytes(inst.m, inst.n, inst.nnz)
     variants = {
-        "csr": dict(psr="off", l2_persist=0),
+        "csr": dict(psr="off", sell="off", l2_persist=0),
+        "sell": dict(psr="off", sell="on"),
+        "auto": dict(),
         "csr_k1": dict(psr="off", dual_split=1),
         "csr_k3": dict(psr="off", dual_split=3),
         "csr_k4": dict(psr="off", dual_split=4),
@@ -68,7 +70,7 @@ def main():
         per_iter = ev0.elapsed_time(ev1) / (3 * 64)
         out[name] = {"build_s": build, "primal_ms": tp, "dual_ms": td, "iter_ms": per_iter, "alt_ms": talt,
                      "primal_gbs": ab["primal"] / tp / 1e6, "dual_gbs": ab["dual"] / td / 1e6,
-                     "psr": dev.psr_info}
+                     "psr": dev.psr_info, "sell": dev.sell_info}
         print(name, json.dumps(out[name]), flush=True)
         del dev
         torch.cuda.empty_cache()
