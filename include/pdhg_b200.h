@@ -129,6 +129,10 @@ typedef struct pdhg_problem {
   /* Optional sliced-ELL layouts for the step kernels (NULL = CSR-vector). */
   const pdhg_sell* a_sell;   /* dual step (rows of A)    */
   const pdhg_sell* at_sell;  /* primal step (rows of A') */
+  /* 1: run each period as one cooperative (persistent) kernel with grid
+   * barriers between half steps instead of a graph of 2 kernels per
+   * iteration; CSR layouts, unsharded only (ignored otherwise). */
+  int32_t persistent;
 } pdhg_problem;
 
 typedef struct pdhg_ctx pdhg_ctx;

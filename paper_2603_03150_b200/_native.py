@@ -75,6 +75,7 @@ class Problem(C.Structure):
         ("a_nsplit", C.c_int32), ("a_split", C.c_void_p),
         ("at_heavy_threshold", C.c_int32),
         ("a_sell", C.POINTER(Sell)), ("at_sell", C.POINTER(Sell)),
+        ("persistent", C.c_int32),
     ]
 
 

@@ -26,6 +26,7 @@
 #include "psr.cuh"
 
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -36,6 +37,8 @@
 #include <map>
 #include <string>
 #include <vector>
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -176,7 +179,16 @@ struct RowSet {
 
 // Partial dot of one row over lanes [lane, lane+V, ...]; NR right-hand sides
 // share one pass over the row's values and indices.
-template <int V, int NR>
+// COH: gathered vector loads through L2 only (ld.global.cg) -- required in the
+// persistent period kernel, where the vector is rewritten between phases and
+// the non-coherent read-only path (ld.global.nc) could serve stale lines.
+template <bool COH>
+__device__ __forceinline__ double gather_ld(const double* p) {
+  if constexpr (COH) return __ldcg(p);
+  else return ld_gather(p);
+}
+
+template <int V, int NR, bool COH = false>
 __device__ __forceinline__ void row_dot(const RowSet& A, int s, int e, int lane,
                                         const double* const* __restrict__ xin, double* acc) {
   // kU entries per lane are loaded before any is consumed (memory-level
@@ -199,7 +211,7 @@ __device__ __forceinline__ void row_dot(const RowSet& A, int s, int e, int lane,
     for (int r = 0; r < NR; ++r) {
       double xv[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) xv[u] = j[u] >= 0 ? ld_gather(xin[r] + j[u]) : 0.0;
+      for (int u = 0; u < kU; ++u) xv[u] = j[u] >= 0 ? gather_ld<COH>(xin[r] + j[u]) : 0.0;
 #pragma unroll
       for (int u = 0; u < kU; ++u)
         if (j[u] >= 0) acc[r] = fma(a[u], xv[u], acc[r]);
@@ -215,7 +227,7 @@ __device__ __forceinline__ void row_dot(const RowSet& A, int s, int e, int lane,
 // instructions per 32 entries in ncu).  ok = row exists and is not heavy.
 // Segment form: row r's entries [sp[r], ep[r]) (a column chunk of the row
 // when the SpMV is split by columns); "heavy" is judged on the full row.
-template <int V>
+template <int V, bool COH = false>
 __device__ __forceinline__ double warp_rows_dot_seg(const RowSet& rs, const int* __restrict__ sp,
                                                     const int* __restrict__ ep, long long row0,
                                                     int lane, const double* const* __restrict__ xin,
@@ -239,7 +251,7 @@ __device__ __forceinline__ double warp_rows_dot_seg(const RowSet& rs, const int*
     const int s = __shfl_sync(0xffffffffu, my_s, src);
     const int e = __shfl_sync(0xffffffffu, my_e, src);
     double acc[1];
-    row_dot<V, 1>(rs, s, e, lane % V, xin, acc);
+    row_dot<V, 1, COH>(rs, s, e, lane % V, xin, acc);
     const double d = group_sum<V>(acc[0]);
     const double got = __shfl_sync(0xffffffffu, d, ((lane - pass * G) & (G - 1)) * V);
     if (lane / G == pass) mine = got;
@@ -252,7 +264,7 @@ __device__ __forceinline__ double warp_rows_dot_seg(const RowSet& rs, const int*
 // gathers, so index-load latency overlaps gather latency
 // (tools/spmv_lab.cu v7: A' 0.888 -> 0.839 ms on config 4).  Summation
 // order is row_dot's: entries k, k+V, ... of the lane, then the butterfly.
-template <int V>
+template <int V, bool COH = false>
 __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long row0, int lane,
                                                      const double* const* __restrict__ xin,
                                                      bool& ok) {
@@ -297,7 +309,7 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
     }
     double xv[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) xv[u] = jc[u] >= 0 ? ld_gather(x + jc[u]) : 0.0;
+    for (int u = 0; u < kU; ++u) xv[u] = jc[u] >= 0 ? gather_ld<COH>(x + jc[u]) : 0.0;
     double acc = 0.0;
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -312,7 +324,7 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
         j2[u] = kk < e ? ld_stream(rs.col + kk) : -1;
       }
 #pragma unroll
-      for (int u = 0; u < kU; ++u) x2[u] = j2[u] >= 0 ? ld_gather(x + j2[u]) : 0.0;
+      for (int u = 0; u < kU; ++u) x2[u] = j2[u] >= 0 ? gather_ld<COH>(x + j2[u]) : 0.0;
 #pragma unroll
       for (int u = 0; u < kU; ++u)
         if (j2[u] >= 0) acc = fma(a2[u], x2[u], acc);
@@ -331,11 +343,11 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
   return mine;
 }
 
-template <int V>
+template <int V, bool COH = false>
 __device__ __forceinline__ double warp_rows_dot(const RowSet& rs, long long row0, int lane,
                                                 const double* const* __restrict__ xin, bool& ok) {
-  if (V <= 8) return warp_rows_dot_pipe<V>(rs, row0, lane, xin, ok);
-  return warp_rows_dot_seg<V>(rs, rs.ptr, rs.ptr + 1, row0, lane, xin, ok);
+  if (V <= 8) return warp_rows_dot_pipe<V, COH>(rs, row0, lane, xin, ok);
+  return warp_rows_dot_seg<V, COH>(rs, rs.ptr, rs.ptr + 1, row0, lane, xin, ok);
 }
 
 // Device-resident per-period parameters (updated by one H2D copy per period
@@ -534,6 +546,84 @@ __global__ void __launch_bounds__(kBlock) k_step_sell(StepArgs a, SellSet S, int
     const int row = (int)rl;
     if (PRIMAL) primal_epi_pre(row, acc, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P);
     else dual_epi_pre(row, acc, o1, o2, o3, a.x, a.xbar, step, w, iter, P);
+  }
+}
+
+// ------------------------------------------------- persistent period kernel
+//
+// One cooperative launch runs a whole period (up to the next KKT check):
+// for each iteration the primal step over all rows of A', a grid barrier,
+// the dual step over all rows of A, a grid barrier.  Same per-row routines,
+// order of operations and epilogues as k_step (so the same results bit for
+// bit), minus 2 kernel launches + drains per iteration -- which dominate
+// small and mid-size models (GpuOptions.persistent).  Heavy rows: a block
+// each, grid-strided; light rows: 32 per warp, grid-strided.  The gathered
+// vector is re-read through L2 (COH) because it changes between phases.
+template <int V, bool PRIMAL>
+__device__ __forceinline__ void step_phase(const StepArgs& a, long long iter, double w, double step,
+                                           double* red) {
+  StepParams* P = a.P;
+  const double* xin[1] = {a.gather};
+  for (int h = blockIdx.x; h < a.rs.n_heavy; h += gridDim.x) {  // block-uniform
+    const int row = a.rs.heavy[h];
+    const int s = a.rs.ptr[row], e = a.rs.ptr[row + 1];
+    double acc[1];
+    row_dot<kBlock, 1, true>(a.rs, s, e, threadIdx.x, xin, acc);
+    const double d = block_sum(acc[0], red);
+    if (threadIdx.x == 0) {
+      if (PRIMAL) primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
+      else dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
+    }
+  }
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * kWarps;
+  for (long long wid = (long long)blockIdx.x * kWarps + (threadIdx.x >> 5); wid * 32 < a.rs.rows; wid += nw) {
+    const long long row0 = wid * 32, rl = row0 + lane;
+    double o1 = 0.0, o2 = 0.0, o3 = 0.0;
+    if (rl < a.rs.rows) {
+      o1 = a.cb[rl];
+      o2 = a.x[rl];
+      o3 = a.xbar[rl];
+    }
+    bool my_ok;
+    const double mine = warp_rows_dot<V, true>(a.rs, row0, lane, xin, my_ok);
+    if (my_ok) {
+      if (PRIMAL) primal_epi_pre((int)rl, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P);
+      else dual_epi_pre((int)rl, mine, o1, o2, o3, a.x, a.xbar, step, w, iter, P);
+    }
+  }
+}
+
+template <bool PRIMAL>
+__device__ __forceinline__ void step_phase_v(int V, const StepArgs& a, long long iter, double w,
+                                             double step, double* red) {
+  switch (V) {
+    case 1: step_phase<1, PRIMAL>(a, iter, w, step, red); break;
+    case 2: step_phase<2, PRIMAL>(a, iter, w, step, red); break;
+    case 4: step_phase<4, PRIMAL>(a, iter, w, step, red); break;
+    case 8: step_phase<8, PRIMAL>(a, iter, w, step, red); break;
+    case 16: step_phase<16, PRIMAL>(a, iter, w, step, red); break;
+    default: step_phase<32, PRIMAL>(a, iter, w, step, red); break;
+  }
+}
+
+__device__ __forceinline__ long long fail_iter_now(StepParams* P) {
+  return *reinterpret_cast<volatile long long*>(&P->fail_iter);
+}
+
+__global__ void __launch_bounds__(kBlock) k_period(StepArgs pa, StepArgs da, int va, int vd, int iters) {
+  __shared__ double red[kWarps];
+  cg::grid_group grid = cg::this_grid();
+  StepParams* P = pa.P;
+  for (int j = 0; j < iters; ++j) {
+    const long long iter = P->iter0 + j + 1;
+    if (fail_iter_now(P) < iter) break;  // grid-uniform: read after the barrier
+    const double w = P->w0 + (double)(j + 1);
+    step_phase_v<true>(va, pa, iter, w, P->tau_w, red);
+    grid.sync();
+    if (fail_iter_now(P) < iter) break;
+    step_phase_v<false>(vd, da, iter, w, P->sigma_w, red);
+    grid.sync();
   }
 }
 
@@ -975,6 +1065,7 @@ struct pdhg_ctx {
   size_t psr_smem[2];
   int l2_persist, l2_maxwin;
   int l2_mask;         // bit0: window on y for the primal step, bit1: on xe for the dual step
+  int coop_grid;       // > 0: periods run as one cooperative k_period launch of this many blocks
 };
 
 namespace {
@@ -1053,6 +1144,31 @@ struct StepLaunchEx {
     return launch_ex(c, k_step<V, false>, dim3(grid), dim3(kBlock), 0, win_base, win, a, j);
   }
 };
+
+StepArgs step_args(const pdhg_ctx* c, bool primal) {
+  StepArgs a;
+  if (primal) {
+    a.rs = c->At; a.gather = c->y; a.cb = c->prob.c;
+    a.x = c->x + c->xo; a.xe = c->xe + c->xo; a.xbar = c->xbar + c->xo;
+  } else {
+    a.rs = c->A; a.gather = c->xe; a.cb = c->prob.b;
+    a.x = c->y + c->yo; a.xe = nullptr; a.xbar = c->ybar + c->yo;
+  }
+  a.P = c->P;
+  a.split = nullptr;
+  a.nsplit = 1;
+  a.partial = nullptr;
+  return a;
+}
+
+int launch_period_persistent(pdhg_ctx* c, int iters) {
+  StepArgs pa = step_args(c, true), da = step_args(c, false);
+  int va = c->at_lanes, vd = c->a_lanes;
+  void* args[] = {&pa, &da, &va, &vd, &iters};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_period, dim3(c->coop_grid), dim3(kBlock), args, 0,
+                                       c->stream));
+  return 0;
+}
 
 int launch_step(pdhg_ctx* c, bool primal, int j) {
   StepArgs a;
@@ -1166,6 +1282,17 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->partials = cv.take<double>((size_t)kCheckBlocks * kMaxQ);
   c->scalars = cv.take<double>(64);
   c->P = cv.take<StepParams>(1);
+  c->coop_grid = 0;
+  if (prob->persistent && !prob->a_sell && !prob->at_sell && !prob->a_psr && !prob->at_psr &&
+      prob->a_nsplit <= 1 && mf == prob->m && nf == prob->n) {
+    int dev = 0, nsm = 0, per_sm = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_period, kBlock, 0);
+    cudaGetLastError();
+    if (coop && per_sm > 0) c->coop_grid = nsm * per_sm;
+  }
   for (int k = 0; k < 2; ++k) {
     const pdhg_sell* q = k == 0 ? prob->a_sell : prob->at_sell;
     c->has_sell[k] = q != nullptr;
@@ -1296,7 +1423,10 @@ int pdhg_run_period(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_over_o
   h.iter0 = iter0;
   h.fail_iter = LLONG_MAX;
   CUDA_TRY(cudaMemcpyAsync(c->P, c->P_host, sizeof(StepParams), cudaMemcpyHostToDevice, c->stream));
-  if (iters > 0) {
+  if (iters > 0 && c->coop_grid > 0) {
+    int rc = launch_period_persistent(c, iters);
+    if (rc) return rc;
+  } else if (iters > 0) {
     auto it = c->graphs.find(iters);
     if (it == c->graphs.end()) {
       cudaGraph_t g;

@@ -58,6 +58,9 @@ class GpuOptions:
                      sell_max_pad x its nonzeros and that has no PSR layout: config 3
                      (primal 56 -> 51 us, dual 43 -> 34 us).  On config 4's A' (mean 20)
                      it is neutral (0.94 vs 0.93 ms), so CSR-vector stays there.
+    persistent:      "auto" | "on" | "off" -- run each period as one cooperative kernel
+                     (grid barriers between half steps) instead of a CUDA graph of two
+                     kernels per iteration; CSR layouts, unsharded.
     l2_persist:      bit mask: 1 = pin y in L2 for the primal step, 2 = pin xe for the
                      dual step (persisting access-policy window; L2 holds 79 MB persisting).
     """
@@ -74,6 +77,7 @@ class GpuOptions:
     psr_min_rows: int = 148 * 256
     l2_persist: int = 0
     dual_split: int = 1
+    persistent: str = "off"
     sell: str = "auto"
     sell_max_pad: float = 1.6
     sell_max_mean: float = 12.0
@@ -230,6 +234,7 @@ class DeviceLp:
         p.b, p.c = self.b.data_ptr(), self.c.data_ptr()
         p.a_lanes, p.at_lanes, p.heavy_threshold = self.a_lanes, self.at_lanes, H
         p.at_heavy_threshold = Ht
+        p.persistent = 1 if opts.persistent == "on" else 0
         p.a_sell = C.pointer(self._sell["A"][0]) if self._sell["A"] else None
         p.at_sell = C.pointer(self._sell["At"][0]) if self._sell["At"] else None
         p.a_n_heavy, p.at_n_heavy = self.a_heavy.numel(), self.at_heavy.numel()

@@ -34,6 +34,7 @@ def eng():
 LAYOUTS = {
     "csr": dict(psr="off", sell="off"),
     "sell": dict(psr="off", sell="on"),
+    "persistent": dict(psr="off", sell="off", persistent="on"),
     "csr_split2": dict(psr="off", sell="off", dual_split=2),
     "psr_staged": dict(psr="on", psr_min_staged=1),
     "psr_remote": dict(psr="on", psr_min_staged=10**9),

@@ -40,6 +40,7 @@ def main():
         "csr": dict(psr="off", sell="off", l2_persist=0),
         "sell": dict(psr="off", sell="on"),
         "auto": dict(),
+        "persist": dict(psr="off", sell="off", persistent="on"),
         "csr_k1": dict(psr="off", dual_split=1),
         "csr_k3": dict(psr="off", dual_split=3),
         "csr_k4": dict(psr="off", dual_split=4),

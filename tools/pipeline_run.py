@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--eps", type=float, default=1e-4)
     ap.add_argument("--limit", type=float, default=600.0)
     ap.add_argument("--heavy", type=int, default=None, help="GpuOptions.heavy_threshold")
+    ap.add_argument("--opts", default="{}", help="GpuOptions fields as JSON")
     args = ap.parse_args()
     import torch
 
@@ -42,7 +43,10 @@ def main():
     t0 = time.perf_counter()
     scaled, info = eng.ruiz_equilibrate(p)
     t["ruiz_s"] = time.perf_counter() - t0
-    opts = eng.GpuOptions() if args.heavy is None else eng.GpuOptions(heavy_threshold=args.heavy)
+    kw = json.loads(args.opts)
+    if args.heavy is not None:
+        kw["heavy_threshold"] = args.heavy
+    opts = eng.GpuOptions(**kw)
     pt, st = eng.run_pdhg(scaled, T.PdhgParams(eps_rel=args.eps, time_limit_s=args.limit), gpu=opts)
     dev = eng.device_lp(scaled, opts)
     t["kernel_ms"] = {"primal": dev.time_kernel(0, 20, 1e-3, 1e-3), "dual": dev.time_kernel(1, 20, 1e-3, 1e-3)}
@@ -53,7 +57,7 @@ def main():
     x, y, z = finish.restrict_point(g, fmap, un)
     viol = finish.evaluate_general_point(g, x, y)
     t["finish_s"] = time.perf_counter() - t0
-    out = {"instance": f"{args.which}_general(scale={args.scale})", "m_std": p.m, "n_std": p.n,
+    out = {"instance": f"{args.which}_general(scale={args.scale})", "opts": kw, "m_std": p.m, "n_std": p.n,
            "nnz_std": int(p.A.nnz), "status": st.status.value, "iterations": st.iterations,
            "restarts": st.restarts, "objective_scaled": float(scaled.c @ pt.x),
            "objective_general": float(g.c @ x), "ruiz_passes": info.applied_iterations,
