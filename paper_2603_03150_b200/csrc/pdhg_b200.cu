@@ -87,9 +87,10 @@ __device__ __forceinline__ double nan_max(double a, double b) {
 __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 
 // Matrix-stream and gather loads of the step/SpMV kernels.  PDHG_L2_HINT
-// (compile time, default 0) selects L2 eviction-priority policies for an
-// experiment: 1 = stream evict_first + gathers evict_last, 2 = stream
-// evict_first only (tools/kernel_matrix.py --lib).
+// (compile time, default 0) selects cache policies for an experiment
+// (tools/kernel_matrix.py --lib; all measured slower, profiles/r01_pipeline.md):
+// 1 = stream L2 evict_first + gathers L2 evict_last, 2 = stream evict_first
+// only, 3 = gathers evict_last only, 4 = gathers L1::no_allocate, 5 = 3 + 4.
 #ifndef PDHG_L2_HINT
 #define PDHG_L2_HINT 0
 #endif
@@ -106,7 +107,7 @@ __device__ __forceinline__ uint64_t l2_policy_last() {
 }
 
 __device__ __forceinline__ double ld_stream(const double* p) {
-#if PDHG_L2_HINT
+#if PDHG_L2_HINT == 1 || PDHG_L2_HINT == 2
   double v;
   asm("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
                : "=d"(v) : "l"(p), "l"(l2_policy_first()));
@@ -116,7 +117,7 @@ __device__ __forceinline__ double ld_stream(const double* p) {
 #endif
 }
 __device__ __forceinline__ int ld_stream(const int* p) {
-#if PDHG_L2_HINT
+#if PDHG_L2_HINT == 1 || PDHG_L2_HINT == 2
   int v;
   asm("ld.global.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
                : "=r"(v) : "l"(p), "l"(l2_policy_first()));
@@ -126,9 +127,17 @@ __device__ __forceinline__ int ld_stream(const int* p) {
 #endif
 }
 __device__ __forceinline__ double ld_gather(const double* p) {
-#if PDHG_L2_HINT == 1
+#if PDHG_L2_HINT == 1 || PDHG_L2_HINT == 3
   double v;
   asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_policy_last()));
+  return v;
+#elif PDHG_L2_HINT == 4
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#elif PDHG_L2_HINT == 5
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_policy_last()));
   return v;
 #else
   return __ldg(p);
