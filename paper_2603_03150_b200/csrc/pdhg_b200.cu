@@ -94,6 +94,18 @@ __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 #ifndef PDHG_L2_HINT
 #define PDHG_L2_HINT 0
 #endif
+// Row reductions of the warp-owns-32-rows routines: 1 = per-pass partials
+// kept in registers and reduced once per warp by a reduce-scatter
+// (reduce_scatter_rows), 0 = butterfly + parking shuffle per pass.  Measured
+// on config 4 (profiles/r01_pipeline.md): the pipelined V <= 8 form gains 7 %
+// (primal 0.931 -> 0.862 ms); the V >= 16 form loses (dual 0.974 -> 1.199 ms:
+// 16 partials raise registers 40 -> 64 and cut occupancy).
+#ifndef PDHG_RS_PIPE
+#define PDHG_RS_PIPE 1
+#endif
+#ifndef PDHG_RS_SEG
+#define PDHG_RS_SEG 0
+#endif
 
 __device__ __forceinline__ uint64_t l2_policy_first() {
   uint64_t p;
@@ -149,6 +161,30 @@ __device__ __forceinline__ double group_sum(double v) {
 #pragma unroll
   for (int o = V / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Row totals of a warp that computed 32 rows in V passes of G = 32/V rows
+// (V lanes per row): lane (q*V + s) holds, in accs[p], its partial for row
+// p*G + q.  A reduce-scatter by recursive halving (V-1 64-bit shuffles
+// instead of V butterflies of log2 V) leaves lane (q*V + s) with the total
+// of row s*G + q; one more shuffle parks row r's total in lane r.  Each
+// step adds own + partner exactly as group_sum's butterfly does, in the
+// same tree, so the totals are bitwise identical to group_sum's.
+template <int V>
+__device__ __forceinline__ double reduce_scatter_rows(double (&accs)[V], int lane) {
+  constexpr int G = 32 / V;
+  const int sub = lane % V;
+#pragma unroll
+  for (int k = V / 2; k >= 1; k >>= 1) {
+    const bool upper = (sub & k) != 0;
+#pragma unroll
+    for (int i = 0; i < k; ++i) {
+      const double send = upper ? accs[i] : accs[i + k];
+      const double keep = upper ? accs[i + k] : accs[i];
+      accs[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+    }
+  }
+  return __shfl_sync(0xffffffffu, accs[0], (lane % G) * V + lane / G);
 }
 
 // Block-wide sum; result valid in every thread.  Fixed tree order.
@@ -253,6 +289,19 @@ __device__ __forceinline__ double warp_rows_dot_seg(const RowSet& rs, const int*
       my_e = ep[rl];
     }
   }
+#if PDHG_RS_SEG
+  double accs[V];
+#pragma unroll
+  for (int pass = 0; pass < V; ++pass) {
+    const int src = pass * G + lane / V;  // lane holding this group's row
+    const int s = __shfl_sync(0xffffffffu, my_s, src);
+    const int e = __shfl_sync(0xffffffffu, my_e, src);
+    double acc[1];
+    row_dot<V, 1, COH>(rs, s, e, lane % V, xin, acc);
+    accs[pass] = acc[0];
+  }
+  return reduce_scatter_rows<V>(accs, lane);
+#else
   double mine = 0.0;
 #pragma unroll 1
   for (int pass = 0; pass < V; ++pass) {
@@ -266,6 +315,7 @@ __device__ __forceinline__ double warp_rows_dot_seg(const RowSet& rs, const int*
     if (lane / G == pass) mine = got;
   }
   return mine;
+#endif
 }
 
 // Software-pipelined form for short rows (V <= 8): the next pass's first
@@ -299,8 +349,13 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
     ac[u] = kk < e ? ld_stream(rs.val + kk) : 0.0;
     jc[u] = kk < e ? ld_stream(rs.col + kk) : -1;
   }
+#if PDHG_RS_PIPE
+  double accs[V];
+#pragma unroll
+#else
   double mine = 0.0;
 #pragma unroll 1
+#endif
   for (int pass = 0; pass < V; ++pass) {
     int sn = 0, en = 0;
     if (pass + 1 < V) {
@@ -338,9 +393,13 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
       for (int u = 0; u < kU; ++u)
         if (j2[u] >= 0) acc = fma(a2[u], x2[u], acc);
     }
+#if PDHG_RS_PIPE
+    accs[pass] = acc;
+#else
     const double d = group_sum<V>(acc);
     const double got = __shfl_sync(0xffffffffu, d, ((lane - pass * G) & (G - 1)) * V);
     if (lane / G == pass) mine = got;
+#endif
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       ac[u] = an[u];
@@ -349,7 +408,11 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
     s = sn;
     e = en;
   }
+#if PDHG_RS_PIPE
+  return reduce_scatter_rows<V>(accs, lane);
+#else
   return mine;
+#endif
 }
 
 template <int V, bool COH = false>

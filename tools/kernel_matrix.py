@@ -41,6 +41,8 @@ def main():
         "sell": dict(psr="off", sell="on"),
         "auto": dict(),
         "persist": dict(psr="off", sell="off", persistent="on"),
+        "csr_a8": dict(psr="off", sell="off", a_lanes=8),
+        "csr_at16": dict(psr="off", sell="off", at_lanes=16),
         "csr_k1": dict(psr="off", dual_split=1),
         "csr_k3": dict(psr="off", dual_split=3),
         "csr_k4": dict(psr="off", dual_split=4),
