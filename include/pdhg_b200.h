@@ -131,7 +131,8 @@ typedef struct pdhg_problem {
   const pdhg_sell* at_sell;  /* primal step (rows of A') */
   /* 1: run each period as one cooperative (persistent) kernel with grid
    * barriers between half steps instead of a graph of 2 kernels per
-   * iteration; CSR layouts, unsharded only (ignored otherwise). */
+   * iteration; 2: as one single-block kernel (tiny models); CSR layouts,
+   * unsharded only (ignored otherwise). */
   int32_t persistent;
 } pdhg_problem;
 

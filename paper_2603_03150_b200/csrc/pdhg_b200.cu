@@ -227,13 +227,16 @@ struct RowSet {
 // COH: gathered vector loads through L2 only (ld.global.cg) -- required in the
 // persistent period kernel, where the vector is rewritten between phases and
 // the non-coherent read-only path (ld.global.nc) could serve stale lines.
-template <bool COH>
+// (COH 2: ld.global.ca -- L1-cached and coherent within one block, for the
+// single-block period kernel, where __syncthreads orders the phases.)
+template <int COH>
 __device__ __forceinline__ double gather_ld(const double* p) {
-  if constexpr (COH) return __ldcg(p);
+  if constexpr (COH == 1) return __ldcg(p);
+  else if constexpr (COH == 2) return __ldca(p);
   else return ld_gather(p);
 }
 
-template <int V, int NR, bool COH = false>
+template <int V, int NR, int COH = 0>
 __device__ __forceinline__ void row_dot(const RowSet& A, int s, int e, int lane,
                                         const double* const* __restrict__ xin, double* acc) {
   // kU entries per lane are loaded before any is consumed (memory-level
@@ -272,7 +275,7 @@ __device__ __forceinline__ void row_dot(const RowSet& A, int s, int e, int lane,
 // instructions per 32 entries in ncu).  ok = row exists and is not heavy.
 // Segment form: row r's entries [sp[r], ep[r]) (a column chunk of the row
 // when the SpMV is split by columns); "heavy" is judged on the full row.
-template <int V, bool COH = false>
+template <int V, int COH = 0>
 __device__ __forceinline__ double warp_rows_dot_seg(const RowSet& rs, const int* __restrict__ sp,
                                                     const int* __restrict__ ep, long long row0,
                                                     int lane, const double* const* __restrict__ xin,
@@ -323,7 +326,7 @@ __device__ __forceinline__ double warp_rows_dot_seg(const RowSet& rs, const int*
 // gathers, so index-load latency overlaps gather latency
 // (tools/spmv_lab.cu v7: A' 0.888 -> 0.839 ms on config 4).  Summation
 // order is row_dot's: entries k, k+V, ... of the lane, then the butterfly.
-template <int V, bool COH = false>
+template <int V, int COH = 0>
 __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long row0, int lane,
                                                      const double* const* __restrict__ xin,
                                                      bool& ok) {
@@ -415,7 +418,7 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
 #endif
 }
 
-template <int V, bool COH = false>
+template <int V, int COH = 0>
 __device__ __forceinline__ double warp_rows_dot(const RowSet& rs, long long row0, int lane,
                                                 const double* const* __restrict__ xin, bool& ok) {
   if (V <= 8) return warp_rows_dot_pipe<V, COH>(rs, row0, lane, xin, ok);
@@ -631,7 +634,19 @@ __global__ void __launch_bounds__(kBlock) k_step_sell(StepArgs a, SellSet S, int
 // small and mid-size models (GpuOptions.persistent).  Heavy rows: a block
 // each, grid-strided; light rows: 32 per warp, grid-strided.  The gathered
 // vector is re-read through L2 (COH) because it changes between phases.
-template <int V, bool PRIMAL>
+template <int NW>
+__device__ __forceinline__ double block_sum_nw(double v, double* red) {
+  v = group_sum<32>(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double t = (l < NW) ? red[l] : 0.0;
+  t = group_sum<32>(t);
+  return t;
+}
+
+template <int V, bool PRIMAL, int COH = 1, int NW = kWarps>
 __device__ __forceinline__ void step_phase(const StepArgs& a, long long iter, double w, double step,
                                            double* red) {
   StepParams* P = a.P;
@@ -640,16 +655,16 @@ __device__ __forceinline__ void step_phase(const StepArgs& a, long long iter, do
     const int row = a.rs.heavy[h];
     const int s = a.rs.ptr[row], e = a.rs.ptr[row + 1];
     double acc[1];
-    row_dot<kBlock, 1, true>(a.rs, s, e, threadIdx.x, xin, acc);
-    const double d = block_sum(acc[0], red);
+    row_dot<NW * 32, 1, COH>(a.rs, s, e, threadIdx.x, xin, acc);
+    const double d = NW == kWarps ? block_sum(acc[0], red) : block_sum_nw<NW>(acc[0], red);
     if (threadIdx.x == 0) {
       if (PRIMAL) primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
       else dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
     }
   }
   const int lane = threadIdx.x & 31;
-  const long long nw = (long long)gridDim.x * kWarps;
-  for (long long wid = (long long)blockIdx.x * kWarps + (threadIdx.x >> 5); wid * 32 < a.rs.rows; wid += nw) {
+  const long long nw = (long long)gridDim.x * NW;
+  for (long long wid = (long long)blockIdx.x * NW + (threadIdx.x >> 5); wid * 32 < a.rs.rows; wid += nw) {
     const long long row0 = wid * 32, rl = row0 + lane;
     double o1 = 0.0, o2 = 0.0, o3 = 0.0;
     if (rl < a.rs.rows) {
@@ -658,7 +673,7 @@ __device__ __forceinline__ void step_phase(const StepArgs& a, long long iter, do
       o3 = a.xbar[rl];
     }
     bool my_ok;
-    const double mine = warp_rows_dot<V, true>(a.rs, row0, lane, xin, my_ok);
+    const double mine = warp_rows_dot<V, COH>(a.rs, row0, lane, xin, my_ok);
     if (my_ok) {
       if (PRIMAL) primal_epi_pre((int)rl, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P);
       else dual_epi_pre((int)rl, mine, o1, o2, o3, a.x, a.xbar, step, w, iter, P);
@@ -666,16 +681,16 @@ __device__ __forceinline__ void step_phase(const StepArgs& a, long long iter, do
   }
 }
 
-template <bool PRIMAL>
+template <bool PRIMAL, int COH = 1, int NW = kWarps>
 __device__ __forceinline__ void step_phase_v(int V, const StepArgs& a, long long iter, double w,
                                              double step, double* red) {
   switch (V) {
-    case 1: step_phase<1, PRIMAL>(a, iter, w, step, red); break;
-    case 2: step_phase<2, PRIMAL>(a, iter, w, step, red); break;
-    case 4: step_phase<4, PRIMAL>(a, iter, w, step, red); break;
-    case 8: step_phase<8, PRIMAL>(a, iter, w, step, red); break;
-    case 16: step_phase<16, PRIMAL>(a, iter, w, step, red); break;
-    default: step_phase<32, PRIMAL>(a, iter, w, step, red); break;
+    case 1: step_phase<1, PRIMAL, COH, NW>(a, iter, w, step, red); break;
+    case 2: step_phase<2, PRIMAL, COH, NW>(a, iter, w, step, red); break;
+    case 4: step_phase<4, PRIMAL, COH, NW>(a, iter, w, step, red); break;
+    case 8: step_phase<8, PRIMAL, COH, NW>(a, iter, w, step, red); break;
+    case 16: step_phase<16, PRIMAL, COH, NW>(a, iter, w, step, red); break;
+    default: step_phase<32, PRIMAL, COH, NW>(a, iter, w, step, red); break;
   }
 }
 
@@ -696,6 +711,29 @@ __global__ void __launch_bounds__(kBlock) k_period(StepArgs pa, StepArgs da, int
     if (fail_iter_now(P) < iter) break;
     step_phase_v<false>(vd, da, iter, w, P->sigma_w, red);
     grid.sync();
+  }
+}
+
+// Single-block period kernel for tiny models (config 0 class, a few thousand
+// rows): one 1024-thread CTA runs the whole period with __syncthreads between
+// half steps; the model and the iterates stay in that SM's L1, gathers are
+// L1-cached (COH 2), so an iteration costs a few hundred cycles instead of
+// two kernel launches.
+constexpr int kTinyBlock = 1024;
+
+__global__ void __launch_bounds__(kTinyBlock, 1) k_period_tiny(StepArgs pa, StepArgs da, int va, int vd,
+                                                               int iters) {
+  __shared__ double red[32];
+  StepParams* P = pa.P;
+  for (int j = 0; j < iters; ++j) {
+    const long long iter = P->iter0 + j + 1;
+    if (fail_iter_now(P) < iter) break;  // block-uniform: read after the barrier
+    const double w = P->w0 + (double)(j + 1);
+    step_phase_v<true, 2, kTinyBlock / 32>(va, pa, iter, w, P->tau_w, red);
+    __syncthreads();
+    if (fail_iter_now(P) < iter) break;
+    step_phase_v<false, 2, kTinyBlock / 32>(vd, da, iter, w, P->sigma_w, red);
+    __syncthreads();
   }
 }
 
@@ -1138,6 +1176,7 @@ struct pdhg_ctx {
   int l2_persist, l2_maxwin;
   int l2_mask;         // bit0: window on y for the primal step, bit1: on xe for the dual step
   int coop_grid;       // > 0: periods run as one cooperative k_period launch of this many blocks
+  bool tiny;           // periods run as one single-block k_period_tiny launch
 };
 
 namespace {
@@ -1236,6 +1275,11 @@ StepArgs step_args(const pdhg_ctx* c, bool primal) {
 int launch_period_persistent(pdhg_ctx* c, int iters) {
   StepArgs pa = step_args(c, true), da = step_args(c, false);
   int va = c->at_lanes, vd = c->a_lanes;
+  if (c->tiny) {
+    k_period_tiny<<<1, kTinyBlock, 0, c->stream>>>(pa, da, va, vd, iters);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
   void* args[] = {&pa, &da, &va, &vd, &iters};
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_period, dim3(c->coop_grid), dim3(kBlock), args, 0,
                                        c->stream));
@@ -1355,7 +1399,12 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->scalars = cv.take<double>(64);
   c->P = cv.take<StepParams>(1);
   c->coop_grid = 0;
-  if (prob->persistent && !prob->a_sell && !prob->at_sell && !prob->a_psr && !prob->at_psr &&
+  c->tiny = false;
+  if (prob->persistent == 2 && !prob->a_sell && !prob->at_sell && !prob->a_psr && !prob->at_psr &&
+      prob->a_nsplit <= 1 && mf == prob->m && nf == prob->n) {
+    c->tiny = true;
+    c->coop_grid = 1;
+  } else if (prob->persistent == 1 && !prob->a_sell && !prob->at_sell && !prob->a_psr && !prob->at_psr &&
       prob->a_nsplit <= 1 && mf == prob->m && nf == prob->n) {
     int dev = 0, nsm = 0, per_sm = 0, coop = 0;
     cudaGetDevice(&dev);

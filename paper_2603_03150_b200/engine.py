@@ -58,9 +58,13 @@ class GpuOptions:
                      sell_max_pad x its nonzeros and that has no PSR layout: config 3
                      (primal 56 -> 51 us, dual 43 -> 34 us).  On config 4's A' (mean 20)
                      it is neutral (0.94 vs 0.93 ms), so CSR-vector stays there.
-    persistent:      "auto" | "on" | "off" -- run each period as one cooperative kernel
-                     (grid barriers between half steps) instead of a CUDA graph of two
-                     kernels per iteration; CSR layouts, unsharded.
+    persistent:      "off" | "on" | "tiny" | "auto" -- "off" (default): a CUDA graph of two
+                     kernels per iteration; "on": each period as one cooperative kernel
+                     (grid barriers between half steps); "tiny": each period as one
+                     single-block kernel (model in one SM's L1); "auto": tiny for
+                     nnz <= tiny_max_nnz and m + n <= tiny_max_rows.  Both persistent
+                     forms are parity-tested and measured no faster than the graph
+                     (profiles/r01_pipeline.md); CSR layouts, unsharded.
     l2_persist:      bit mask: 1 = pin y in L2 for the primal step, 2 = pin xe for the
                      dual step (persisting access-policy window; L2 holds 79 MB persisting).
     """
@@ -78,6 +82,8 @@ class GpuOptions:
     l2_persist: int = 0
     dual_split: int = 1
     persistent: str = "off"
+    tiny_max_nnz: int = 200_000
+    tiny_max_rows: int = 65_536
     sell: str = "auto"
     sell_max_pad: float = 1.6
     sell_max_mean: float = 12.0
@@ -203,13 +209,19 @@ class DeviceLp:
                         ("At", n, m_full, self.at_nnz, self.at_ptr, self.at_col, self.at_val)):
                     self._psr[key] = self._build_psr(torch, dev, key, rows, cols, nz, ptr, col, val,
                                                      H if key == "A" else Ht, opts)
+                pers = opts.persistent
+                if pers == "auto":
+                    pers = ("tiny" if nnz <= opts.tiny_max_nnz and m + n <= opts.tiny_max_rows
+                            and shard is None and opts.psr == "off" and int(opts.dual_split) <= 1
+                            else "off")
+                self.persistent_mode = pers
                 self._sell = {}
                 self.sell_info = {}
                 for key, rows, nz, ptr, col, val, Hk in (
                         ("A", m, nnz, self.a_ptr, self.a_col, self.a_val, H),
                         ("At", n, self.at_nnz, self.at_ptr, self.at_col, self.at_val, Ht)):
-                    self._sell[key] = None if self._psr[key] else self._build_sell(
-                        torch, dev, key, rows, nz, ptr, col, val, Hk, opts)
+                    self._sell[key] = None if (self._psr[key] or pers in ("tiny", "on")) else \
+                        self._build_sell(torch, dev, key, rows, nz, ptr, col, val, Hk, opts)
                 self.a_split = None
                 self.nsplit = 1
                 K = int(opts.dual_split)
@@ -234,7 +246,7 @@ class DeviceLp:
         p.b, p.c = self.b.data_ptr(), self.c.data_ptr()
         p.a_lanes, p.at_lanes, p.heavy_threshold = self.a_lanes, self.at_lanes, H
         p.at_heavy_threshold = Ht
-        p.persistent = 1 if opts.persistent == "on" else 0
+        p.persistent = {"on": 1, "tiny": 2}.get(self.persistent_mode, 0)
         p.a_sell = C.pointer(self._sell["A"][0]) if self._sell["A"] else None
         p.at_sell = C.pointer(self._sell["At"][0]) if self._sell["At"] else None
         p.a_n_heavy, p.at_n_heavy = self.a_heavy.numel(), self.at_heavy.numel()

@@ -32,10 +32,11 @@ def eng():
 # the step kernels' layouts: CSR-vector (also split-K), sliced ELL, and PSR
 # with every entry staged in shared-memory panels or gathered from global memory
 LAYOUTS = {
-    "csr": dict(psr="off", sell="off"),
-    "sell": dict(psr="off", sell="on"),
+    "csr": dict(psr="off", sell="off", persistent="off"),
+    "sell": dict(psr="off", sell="on", persistent="off"),
     "persistent": dict(psr="off", sell="off", persistent="on"),
-    "csr_split2": dict(psr="off", sell="off", dual_split=2),
+    "tiny": dict(psr="off", sell="off", persistent="tiny"),
+    "csr_split2": dict(psr="off", sell="off", persistent="off", dual_split=2),
     "psr_staged": dict(psr="on", psr_min_staged=1),
     "psr_remote": dict(psr="on", psr_min_staged=10**9),
 }

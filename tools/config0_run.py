@@ -22,7 +22,8 @@ def main():
         pass
 
     T = eng.types()
-    for kw in ({"sell": "off"}, {"sell": "off", "persistent": "on"}):
+    for kw in ({"sell": "off", "persistent": "off"}, {"sell": "off", "persistent": "on"},
+               {"persistent": "tiny"}, {}):
         p = P()
         p.A, p.b, p.c = A, g["b"].copy(), g["c"].copy()
         opts = eng.GpuOptions(**kw)
