@@ -230,7 +230,7 @@ def run_ours(args):
     if world > 1:
         from paper_2603_03150_b200.sharded import build_sharded
 
-        dev = build_sharded(inst, world, "torch", opts)
+        dev = build_sharded(inst, world, "torch_peer" if args.comm == "peer" else "torch", opts)
         kdev = dev.shards[0]   # this rank's shard context (kernel timing)
     else:
         dev = kdev = eng.DeviceLp(inst.A, inst.b, inst.c, opts)
@@ -308,7 +308,8 @@ def run_ours(args):
     if world > 1:
         from paper_2603_03150_b200.sharded import run_pdhg_sharded
 
-        pt, st = run_pdhg_sharded(inst, params, G=world, comm_kind="torch", gpu=opts)
+        pt, st = run_pdhg_sharded(inst, params, G=world, gpu=opts,
+                                  comm_kind="torch_peer" if args.comm == "peer" else "torch")
     else:
         pt, st = eng.run_pdhg(inst, params, gpu=opts)
     e1.record()
@@ -361,8 +362,11 @@ def run_ours(args):
         "config": {"workload": f"config4 (m={m}, n={n}, nnz={nnz}) PDHG period = 64 iterations + KKT check",
                    "scale": args.scale, "seed": args.seed,
                    "l2": "no flush: 4.8 GB matrix > 126 MB L2 (inputs larger than L2)",
-                   "parallelism": (f"A rows / A' rows sharded x{world}, equal nnz; NCCL all-gather of "
-                                   "xe and y per iteration" if world > 1 else "1 GPU"),
+                   "parallelism": ((f"A rows / A' rows sharded x{world}, equal nnz; " +
+                                    ("xe / y pushed to peers by the step epilogues (symmetric memory, "
+                                     "NVLink stores) + stream barrier" if args.comm == "peer" else
+                                     "NCCL all-gather of xe and y per iteration"))
+                                   if world > 1 else "1 GPU"),
                    "kernel_layout": "psr" if args.psr == "on" else "csr-vector"},
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / K,
@@ -395,6 +399,9 @@ def main():
                     help="also run to eps_rel=1e-4 (time-to-1e-4, part of the metric; --no-ttk skips)")
     ap.add_argument("--ttk-limit", type=float, default=300.0)
     ap.add_argument("--ttk-unscaled", action="store_true", help="also run to 1e-4 without Ruiz")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
+                    help="N>1: all-gather xe/y with NCCL after each half step, or push them "
+                         "from the step epilogues to the peers' symmetric memory")
     ap.add_argument("--psr", default="off", choices=["off", "on", "auto"],
                     help="step-kernel layout (off = CSR-vector, the measured fastest)")
     args = ap.parse_args()

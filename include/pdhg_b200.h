@@ -225,6 +225,14 @@ int pdhg_reduced_costs(pdhg_ctx* ctx, int32_t spec, double* z_slice);
 int pdhg_set_step(pdhg_ctx* ctx, int64_t iter0, double tau_over_omega, double sigma_omega,
                   double w0);
 int pdhg_half_step(pdhg_ctx* ctx, int32_t primal, int32_t j);
+/* Fused all-gather: from now on the primal (which = 0) / dual (which = 1)
+ * step's epilogue also stores every new xe / y value into the full vector
+ * of each of npeers peers, at this shard's slot (peers_dev: device array of
+ * npeers pointers to the peers' full xe / y vectors -- other shards in this
+ * process, or NVLink peer / symmetric-memory addresses).  npeers = 0 turns
+ * it off.  The caller orders the next half step after every peer's writes
+ * (stream order on one device; a cross-GPU barrier otherwise). */
+int pdhg_set_peers(pdhg_ctx* ctx, int32_t which, const double* const* peers_dev, int32_t npeers);
 int pdhg_fail_iter(pdhg_ctx* ctx, int64_t* fail_iter_out);
 
 /* Power-iteration building blocks for sharded hosts: *out_dev = sum v^2

@@ -31,7 +31,7 @@ EXPORTS = (
     "pdhg_split_build", "pdhg_stdform_tmp_bytes", "pdhg_stdform_plan", "pdhg_stdform_build",
     "pdhg_spmv_seq", "pdhg_unscale_point", "pdhg_restrict_x", "pdhg_lift_x", "pdhg_lift_slacks",
     "pdhg_lift_bound_duals", "pdhg_max0", "pdhg_violation_tmp_bytes", "pdhg_violation",
-    "pdhg_sell_tmp_bytes", "pdhg_sell_plan", "pdhg_sell_fill",
+    "pdhg_sell_tmp_bytes", "pdhg_sell_plan", "pdhg_sell_fill", "pdhg_set_peers",
 )
 
 VEC = {name: i for i, name in enumerate(
@@ -154,6 +154,7 @@ def load():
         _sig(lib, "pdhg_max0", C.c_int, i64, vp, vp, vp)
         _sig(lib, "pdhg_violation_tmp_bytes", szt, i32, i32)
         _sig(lib, "pdhg_sell_tmp_bytes", szt, i32)
+        _sig(lib, "pdhg_set_peers", C.c_int, vp, i32, vp, i32)
         _sig(lib, "pdhg_sell_plan", C.c_int, i32, vp, i32, vp, vp, vp, szt, vp, P(i64))
         _sig(lib, "pdhg_sell_fill", C.c_int, i32, vp, vp, vp, i32, vp, vp, vp, vp)
         _sig(lib, "pdhg_violation", C.c_int, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,

@@ -438,7 +438,7 @@ struct StepParams {
 // ------------------------------------------------------------------- steps
 
 // Epilogue of the primal step for row j of A' (= column j of A).
-__device__ __forceinline__ void primal_epi(int j, double aty, const double* __restrict__ c,
+__device__ __forceinline__ double primal_epi(int j, double aty, const double* __restrict__ c,
                                            double* __restrict__ x, double* __restrict__ xe,
                                            double* __restrict__ xbar, double tau_w, double w,
                                            long long iter, StepParams* P) {
@@ -447,12 +447,14 @@ __device__ __forceinline__ void primal_epi(int j, double aty, const double* __re
   const double xn = np_max0(__dsub_rn(xj, __dmul_rn(tau_w, g)));  // max(0, x - t g)
   const double xb = xbar[j];
   x[j] = xn;
-  xe[j] = __dsub_rn(__dmul_rn(2.0, xn), xj);                  // 2 x+ - x
+  const double xev = __dsub_rn(__dmul_rn(2.0, xn), xj);       // 2 x+ - x
+  xe[j] = xev;
   xbar[j] = __dadd_rn(xb, __ddiv_rn(__dsub_rn(xn, xb), w));    // avg += (x+ - avg)/w
   if (!finite(xn)) atomicMin(&P->fail_iter, iter);
+  return xev;
 }
 
-__device__ __forceinline__ void dual_epi(int i, double ax, const double* __restrict__ b,
+__device__ __forceinline__ double dual_epi(int i, double ax, const double* __restrict__ b,
                                          double* __restrict__ y, double* __restrict__ ybar,
                                          double sigma_w, double w, long long iter, StepParams* P) {
   const double yi = y[i];
@@ -461,31 +463,51 @@ __device__ __forceinline__ void dual_epi(int i, double ax, const double* __restr
   y[i] = yn;
   ybar[i] = __dadd_rn(yb, __ddiv_rn(__dsub_rn(yn, yb), w));
   if (!finite(yn)) atomicMin(&P->fail_iter, iter);
+  return yn;
 }
 
 // Same epilogues with the row's operands already in registers.
-__device__ __forceinline__ void primal_epi_pre(int j, double aty, double cj, double xj, double xb,
+__device__ __forceinline__ double primal_epi_pre(int j, double aty, double cj, double xj, double xb,
                                                double* __restrict__ x, double* __restrict__ xe,
                                                double* __restrict__ xbar, double tau_w, double w,
                                                long long iter, StepParams* P) {
   const double g = __dsub_rn(cj, aty);
   const double xn = np_max0(__dsub_rn(xj, __dmul_rn(tau_w, g)));
   x[j] = xn;
-  xe[j] = __dsub_rn(__dmul_rn(2.0, xn), xj);
+  const double xev = __dsub_rn(__dmul_rn(2.0, xn), xj);
+  xe[j] = xev;
   xbar[j] = __dadd_rn(xb, __ddiv_rn(__dsub_rn(xn, xb), w));
   if (!finite(xn)) atomicMin(&P->fail_iter, iter);
+  return xev;
 }
 
-__device__ __forceinline__ void dual_epi_pre(int i, double ax, double bi, double yi, double yb,
+__device__ __forceinline__ double dual_epi_pre(int i, double ax, double bi, double yi, double yb,
                                              double* __restrict__ y, double* __restrict__ ybar,
                                              double sigma_w, double w, long long iter, StepParams* P) {
   const double yn = __dadd_rn(yi, __dmul_rn(sigma_w, __dsub_rn(bi, ax)));
   y[i] = yn;
   ybar[i] = __dadd_rn(yb, __ddiv_rn(__dsub_rn(yn, yb), w));
   if (!finite(yn)) atomicMin(&P->fail_iter, iter);
+  return yn;
+}
+
+// Fused all-gather (multi-GPU): the step's epilogue also
+// stores each new xe (primal) / y (dual) value into every peer's full
+// vector at this shard's slot -- NVLink peer stores that overlap the
+// kernel, replacing the all-gather after it.  ptr: device array of n peer
+// vector bases (same padded layout everywhere); off: this shard's slice.
+struct Peers {
+  double* const* __restrict__ ptr;
+  int n;
+  int off;
+};
+
+__device__ __forceinline__ void bcast(const Peers& p, int row, double v) {
+  for (int q = 0; q < p.n; ++q) p.ptr[q][p.off + row] = v;
 }
 
 struct StepArgs {
+  Peers peers;
   RowSet rs;
   const int* __restrict__ split;      // column-chunk split points, (nsplit-1) arrays of rows
   int nsplit;                         // 1 = unsplit
@@ -515,8 +537,8 @@ __global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
     row_dot<kBlock, 1>(a.rs, s, e, threadIdx.x, xin, acc);
     const double d = block_sum(acc[0], red);
     if (threadIdx.x == 0) {
-      if (PRIMAL) primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
-      else dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
+      if (PRIMAL) bcast(a.peers, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast(a.peers, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
     }
     return;
   }
@@ -543,8 +565,8 @@ __global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
   const double mine = warp_rows_dot<V>(a.rs, row0, lane, xin, my_ok);
   if (my_ok) {
     const int row = (int)rl;
-    if (PRIMAL) primal_epi_pre(row, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P);
-    else dual_epi_pre(row, mine, o1, o2, o3, a.x, a.xbar, step, w, iter, P);
+    if (PRIMAL) bcast(a.peers, row, primal_epi_pre(row, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
+    else bcast(a.peers, row, dual_epi_pre(row, mine, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
   }
 }
 
@@ -578,8 +600,8 @@ __global__ void __launch_bounds__(kBlock) k_step_sell(StepArgs a, SellSet S, int
     row_dot<kBlock, 1>(a.rs, s, e, threadIdx.x, xin, acc);
     const double d = block_sum(acc[0], red);
     if (threadIdx.x == 0) {
-      if (PRIMAL) primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
-      else dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
+      if (PRIMAL) bcast(a.peers, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast(a.peers, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
     }
     return;
   }
@@ -619,8 +641,8 @@ __global__ void __launch_bounds__(kBlock) k_step_sell(StepArgs a, SellSet S, int
   }
   if (ok) {
     const int row = (int)rl;
-    if (PRIMAL) primal_epi_pre(row, acc, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P);
-    else dual_epi_pre(row, acc, o1, o2, o3, a.x, a.xbar, step, w, iter, P);
+    if (PRIMAL) bcast(a.peers, row, primal_epi_pre(row, acc, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
+    else bcast(a.peers, row, dual_epi_pre(row, acc, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
   }
 }
 
@@ -658,8 +680,8 @@ __device__ __forceinline__ void step_phase(const StepArgs& a, long long iter, do
     row_dot<NW * 32, 1, COH>(a.rs, s, e, threadIdx.x, xin, acc);
     const double d = NW == kWarps ? block_sum(acc[0], red) : block_sum_nw<NW>(acc[0], red);
     if (threadIdx.x == 0) {
-      if (PRIMAL) primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
-      else dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
+      if (PRIMAL) bcast(a.peers, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast(a.peers, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
     }
   }
   const int lane = threadIdx.x & 31;
@@ -675,8 +697,8 @@ __device__ __forceinline__ void step_phase(const StepArgs& a, long long iter, do
     bool my_ok;
     const double mine = warp_rows_dot<V, COH>(a.rs, row0, lane, xin, my_ok);
     if (my_ok) {
-      if (PRIMAL) primal_epi_pre((int)rl, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P);
-      else dual_epi_pre((int)rl, mine, o1, o2, o3, a.x, a.xbar, step, w, iter, P);
+      if (PRIMAL) bcast(a.peers, (int)rl, primal_epi_pre((int)rl, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast(a.peers, (int)rl, dual_epi_pre((int)rl, mine, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
     }
   }
 }
@@ -760,7 +782,7 @@ __global__ void __launch_bounds__(kBlock) k_dual_split(StepArgs a, int j_in_peri
     double acc[1];
     row_dot<kBlock, 1>(a.rs, a.rs.ptr[row], a.rs.ptr[row + 1], threadIdx.x, xin, acc);
     const double d = block_sum(acc[0], red);
-    if (threadIdx.x == 0) dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
+    if (threadIdx.x == 0) bcast(a.peers, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -784,13 +806,14 @@ __global__ void __launch_bounds__(kBlock) k_dual_split(StepArgs a, int j_in_peri
   const double dot = warp_rows_dot_seg<V>(a.rs, sp, ep, row0, lane, xin, ok);
   if (!ok) return;
   const double d = pass > 0 ? part + dot : dot;
-  if (last) dual_epi_pre((int)rl, d, o1, o2, o3, a.x, a.xbar, step, w, iter, P);
+  if (last) bcast(a.peers, (int)rl, dual_epi_pre((int)rl, d, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
   else a.partial[rl] = d;
 }
 
 // PSR step: persistent CTAs (one per SM) walk row blocks; the SpMV lands in
 // shared memory (psr::block_spmv), then the same epilogue as k_step.
 struct PsrStepArgs {
+  Peers peers;
   psr::Layout L;
   const double* __restrict__ gather;
   const double* __restrict__ cb;
@@ -820,8 +843,8 @@ __global__ void __launch_bounds__(psr::kThreads, 1) k_step_psr(PsrStepArgs a, in
   for (int k = 0; k < psr::kStages; ++k) ph[k] = 0u;
   for (int b = blockIdx.x; b < a.L.nblk; b += gridDim.x) {
     psr::block_rows(a.L, b, a.gather, panels, bars, ph, [&](int row, double d) {
-      if (PRIMAL) primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P);
-      else dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P);
+      if (PRIMAL) bcast(a.peers, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast(a.peers, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
     });
   }
 }
@@ -1177,6 +1200,8 @@ struct pdhg_ctx {
   int l2_mask;         // bit0: window on y for the primal step, bit1: on xe for the dual step
   int coop_grid;       // > 0: periods run as one cooperative k_period launch of this many blocks
   bool tiny;           // periods run as one single-block k_period_tiny launch
+  double* const* peers[2];  // fused all-gather targets: [0] xe (primal), [1] y (dual)
+  int npeers[2];
 };
 
 namespace {
@@ -1258,6 +1283,8 @@ struct StepLaunchEx {
 
 StepArgs step_args(const pdhg_ctx* c, bool primal) {
   StepArgs a;
+  const int k = primal ? 0 : 1;  // peers of xe (primal) / y (dual)
+  a.peers = Peers{c->peers[k], c->npeers[k], primal ? c->xo : c->yo};
   if (primal) {
     a.rs = c->At; a.gather = c->y; a.cb = c->prob.c;
     a.x = c->x + c->xo; a.xe = c->xe + c->xo; a.xbar = c->xbar + c->xo;
@@ -1287,20 +1314,9 @@ int launch_period_persistent(pdhg_ctx* c, int iters) {
 }
 
 int launch_step(pdhg_ctx* c, bool primal, int j) {
-  StepArgs a;
   // gathers read the full (padded) vectors; the rows a shard owns are
   // written through pointers offset to its slice
-  if (primal) {
-    a.rs = c->At; a.gather = c->y; a.cb = c->prob.c;
-    a.x = c->x + c->xo; a.xe = c->xe + c->xo; a.xbar = c->xbar + c->xo;
-  } else {
-    a.rs = c->A; a.gather = c->xe; a.cb = c->prob.b;
-    a.x = c->y + c->yo; a.xe = nullptr; a.xbar = c->ybar + c->yo;
-  }
-  a.P = c->P;
-  a.split = nullptr;
-  a.nsplit = 1;
-  a.partial = nullptr;
+  StepArgs a = step_args(c, primal);
   if (!primal && c->prob.a_nsplit > 1 && !c->has_psr[0]) {
     a.split = c->prob.a_split;
     a.nsplit = c->prob.a_nsplit;
@@ -1312,7 +1328,7 @@ int launch_step(pdhg_ctx* c, bool primal, int j) {
   const int lanes = primal ? c->at_lanes : c->a_lanes;
   const int k = primal ? 1 : 0;
   if (c->has_psr[k]) {
-    PsrStepArgs pa{c->psr_l[k], a.gather, a.cb, a.x, a.xe, a.xbar, a.P};
+    PsrStepArgs pa{a.peers, c->psr_l[k], a.gather, a.cb, a.x, a.xe, a.xbar, a.P};
     const int grid = std::min(c->psr_l[k].nblk, 148);
     int rc = primal ? launch_ex(c, k_step_psr<true>, dim3(grid), dim3(psr::kThreads), c->psr_smem[k],
                                 win_base, win, pa, j)
@@ -1713,6 +1729,16 @@ int pdhg_half_step(pdhg_ctx* c, int32_t primal, int32_t j) {
   int rc = launch_step(c, primal != 0, j);
   if (rc) return rc;
   CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int pdhg_set_peers(pdhg_ctx* c, int32_t which, const double* const* peers_dev, int32_t npeers) {
+  if (!c || which < 0 || which > 1 || npeers < 0 || (npeers > 0 && !peers_dev))
+    return fail(PDHG_ERR_ARG, "set_peers: bad argument");
+  c->peers[which] = const_cast<double* const*>(peers_dev);
+  c->npeers[which] = npeers;
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);  // captured StepArgs are stale
+  c->graphs.clear();
   return 0;
 }
 

@@ -133,14 +133,17 @@ class DeviceLp:
     library carves its iterate buffers from.
     """
 
-    def __init__(self, A, b, c, opts: GpuOptions, *, shard=None, stream=None, device_arrays=None):
+    def __init__(self, A, b, c, opts: GpuOptions, *, shard=None, stream=None, device_arrays=None,
+                 ws_alloc=None):
         """``shard`` (sharded.ShardBlock) makes this the context of one shard:
         A is then the shard's row block with column indices in padded
         x-space slots, ``shard.At`` its block of A' rows (CSR, y-space
         slots), and the iterate vectors have the padded full lengths.
         ``stream``: a torch.cuda.Stream to share (loopback shards).
         ``device_arrays``: (indptr, indices, data) of A already on the device
-        (e.g. the output of the device Ruiz pass) -- not uploaded again."""
+        (e.g. the output of the device Ruiz pass) -- not uploaded again.
+        ``ws_alloc``: allocator (nbytes, device) -> uint8 tensor for the iterate
+        workspace (symmetric memory for the fused multi-GPU all-gather)."""
         torch = _torch()
         t_start = time.monotonic()
         self.lib = N.load()
@@ -236,7 +239,8 @@ class DeviceLp:
                     if not uns.value:
                         self.a_split, self.nsplit = split, K
                 ws_bytes = self.lib.pdhg_workspace_bytes(m_full, n_full)
-                self.ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+                self.ws = (ws_alloc(ws_bytes, dev) if ws_alloc is not None
+                           else torch.empty(ws_bytes, dtype=torch.uint8, device=dev))
                 self.stream.synchronize()
                 del tmp
         p = N.Problem()
@@ -408,6 +412,14 @@ class DeviceLp:
 
     def vec_ptr(self, name: str) -> int:
         return self.lib.pdhg_vector(self.ctx, N.VEC[name])
+
+    def set_peers(self, which: int, ptrs):
+        """Fused all-gather targets (pdhg_set_peers): which 0 = xe (primal step),
+        1 = y (dual step); ptrs = int64 device tensor of peer vector bases (kept alive)."""
+        self._peers = getattr(self, "_peers", {})
+        self._peers[which] = ptrs
+        n = 0 if ptrs is None else int(ptrs.numel())
+        N.check(self.lib.pdhg_set_peers(self.ctx, int(which), ptrs.data_ptr() if n else None, n))
 
     def set_step(self, iter0: int, tau_w: float, sigma_w: float, w0: float):
         N.check(self.lib.pdhg_set_step(self.ctx, int(iter0), float(tau_w), float(sigma_w), float(w0)))

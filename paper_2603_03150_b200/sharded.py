@@ -26,7 +26,15 @@ kernels behind the C ABI); a communicator moves slices between shards:
                       (NCCL over NVLink on a B200 box; gloo in CPU tests);
 * ``LoopbackComm`` -- all G shards in one process on one device (tests the
                       sharded kernels and the rank-order combine on 1 GPU);
-                      the all-gather is a set of device-to-device copies.
+                      the all-gather is a set of device-to-device copies;
+* fused all-gather (``fused=True``): the step kernels' epilogues store each
+  new xe / y value straight into every peer's full vector at the shard's
+  slot (``pdhg_set_peers``), so no all-gather runs after a half step.  In
+  loopback the peers are the other shards' buffers on the same device
+  (stream order is the barrier); with ``comm_kind="torch_peer"`` the
+  workspace is torch symmetric memory, the peers are NVLink addresses
+  (``buffer_ptrs``) and a symmetric-memory barrier on the stream orders
+  each half step after every rank's stores.
 """
 
 from __future__ import annotations
@@ -118,10 +126,23 @@ class ShardPlan:
 class LoopbackComm:
     """All shards in this process (one device): all-gather = device copies."""
 
-    def __init__(self, plan: ShardPlan):
+    def __init__(self, plan: ShardPlan, fused: bool = False):
         self.plan = plan
         self.rank, self.world = 0, plan.G
         self.local = list(range(plan.G))
+        self.fused = fused
+
+    def connect_peers(self, shards):
+        """Fused all-gather: shard g's epilogues also write the other shards' xe / y."""
+        import torch
+
+        for g, s in enumerate(shards):
+            for which, name in ((0, "xe"), (1, "y")):
+                ptrs = [o.vec_ptr(name) for h, o in enumerate(shards) if h != g]
+                s.set_peers(which, torch.tensor(ptrs, dtype=torch.int64, device=s.device))
+
+    def barrier(self, shards):
+        pass   # one stream: stream order is the barrier
 
     def allgather(self, shards, name: str):
         L = self.plan.slice_len("x" if name in X_SPACE else "y")
@@ -143,7 +164,7 @@ class LoopbackComm:
 class TorchComm:
     """One shard per process over torch.distributed (NCCL on GPUs, gloo in tests)."""
 
-    def __init__(self, plan: ShardPlan, group=None):
+    def __init__(self, plan: ShardPlan, group=None, fused: bool = False):
         import torch.distributed as dist
 
         self.dist = dist
@@ -154,6 +175,35 @@ class TorchComm:
         if self.world != plan.G:
             raise ValueError("world size must equal the number of shards")
         self.local = [self.rank]
+        self.fused = fused
+        self.symm = None
+
+    def symmetric_workspace(self, nbytes: int, device):
+        """Workspace allocator for the fused mode: torch symmetric memory (identical
+        size on every rank -- the padded layout makes it so)."""
+        import torch.distributed._symmetric_memory as symm_mem
+        import torch
+
+        return symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+
+    def connect_peers(self, shards):
+        """Peer vector bases over NVLink: the symmetric workspace's buffer_ptrs plus
+        the (rank-independent) offsets of xe / y inside it."""
+        import torch
+        import torch.distributed._symmetric_memory as symm_mem
+
+        (s,) = shards
+        self.symm = symm_mem.rendezvous(s.ws, self.group or self.dist.group.WORLD)
+        base = s.ws.data_ptr()
+        for which, name in ((0, "xe"), (1, "y")):
+            off = s.vec_ptr(name) - base
+            ptrs = [int(self.symm.buffer_ptrs[r]) + off for r in range(self.world) if r != self.rank]
+            s.set_peers(which, torch.tensor(ptrs, dtype=torch.int64, device=s.device))
+
+    def barrier(self, shards):
+        """Stream-ordered cross-GPU barrier: the next half step starts after every
+        rank's epilogue stores (symmetric-memory signal pads, release/acquire)."""
+        self.symm.barrier(channel=0)
 
     def allgather(self, shards, name: str):
         (s,) = shards
@@ -278,13 +328,22 @@ class ShardedDevice:
     def run_period(self, iters: int, iter0: int, tau_w: float, sigma_w: float, w0: float) -> int:
         for s in self.shards:
             s.set_step(iter0, tau_w, sigma_w, w0)
+        fused = getattr(self.comm, "fused", False)
         for j in range(iters):
             for s in self.shards:
                 s.half_step(True, j)
-            self._ag("xe")
+            if fused:                   # xe slices already pushed by the epilogues
+                with self._on_stream():
+                    self.comm.barrier(self.shards)
+            else:
+                self._ag("xe")
             for s in self.shards:
                 s.half_step(False, j)
-            self._ag("y")
+            if fused:
+                with self._on_stream():
+                    self.comm.barrier(self.shards)
+            else:
+                self._ag("y")
         with self._on_stream():
             fails = self.comm.allgather_int([s.fail_iter() for s in self.shards])
         bad = [f for f in fails if f >= 0]
@@ -360,17 +419,20 @@ def build_sharded(p, G: int, comm_kind: str = "loopback", opts=None, group=None)
 
     opts = opts or GpuOptions()
     plan = ShardPlan(p.A, G)
-    if comm_kind == "loopback":
-        comm = LoopbackComm(plan)
+    if comm_kind in ("loopback", "loopback_fused"):
+        comm = LoopbackComm(plan, fused=comm_kind == "loopback_fused")
         stream = torch.cuda.Stream()
         shards = [DeviceLp(blk.A, blk.b, blk.c, opts, shard=blk, stream=stream)
                   for blk in (plan.block(g, p.A, p.b, p.c) for g in range(G))]
-    elif comm_kind == "torch":
-        comm = TorchComm(plan, group)
+    elif comm_kind in ("torch", "torch_peer"):
+        comm = TorchComm(plan, group, fused=comm_kind == "torch_peer")
         blk = plan.block(comm.rank, p.A, p.b, p.c)
-        shards = [DeviceLp(blk.A, blk.b, blk.c, opts, shard=blk)]
+        alloc = comm.symmetric_workspace if comm.fused else None
+        shards = [DeviceLp(blk.A, blk.b, blk.c, opts, shard=blk, ws_alloc=alloc)]
     else:
         raise ValueError(comm_kind)
+    if comm.fused:
+        comm.connect_peers(shards)
     return ShardedDevice(plan, shards, comm)
 
 

@@ -103,3 +103,67 @@ def test_torch_comm_over_nccl_world1(eng):
         assert float(gm.c @ pt.x) == pytest.approx(float(r["obj"]), rel=1e-6)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("G", [2, 3, 4])
+@pytest.mark.parametrize("psr", ["off", "on"])
+def test_fused_allgather_matches_copy_allgather(eng, G, psr):
+    """Fused all-gather (epilogue peer stores, pdhg_set_peers) vs the all-gather
+    after each half step: the same arithmetic, so bitwise-identical results."""
+    from paper_2603_03150_b200.sharded import run_pdhg_sharded
+
+    gm = load_golden("config0_s0")
+    T = eng.types()
+    opts = eng.GpuOptions(psr=psr, psr_min_staged=1)
+    params = T.PdhgParams(eps_rel=1e-4)
+    pa, sa = run_pdhg_sharded(gm, params, G=G, gpu=opts, comm_kind="loopback")
+    pb, sb = run_pdhg_sharded(gm, params, G=G, gpu=opts, comm_kind="loopback_fused")
+    assert (sa.status, sa.iterations, sa.restarts) == (sb.status, sb.iterations, sb.restarts)
+    assert pa.x.tobytes() == pb.x.tobytes() and pa.y.tobytes() == pb.y.tobytes()
+    assert pa.z.tobytes() == pb.z.tobytes()
+    r = gm.run("e4")
+    assert sb.iterations == int(r["iterations"]) and sb.restarts == int(r["restarts"])
+
+
+def test_fused_allgather_scaled_config4(eng):
+    """4 fused shards on a 2M-nnz config-4 instance reproduce the copy path bit for bit."""
+    from paper_2603_03150_b200.instances import config4
+    from paper_2603_03150_b200.sharded import run_pdhg_sharded
+
+    p = config4(scale=0.01, seed=21)
+    T = eng.types()
+    params = T.PdhgParams(eps_rel=1e-12, max_kkt_passes=256)
+    pa, sa = run_pdhg_sharded(p, params, G=4, comm_kind="loopback")
+    pb, sb = run_pdhg_sharded(p, params, G=4, comm_kind="loopback_fused")
+    assert sa.iterations == sb.iterations == 256
+    assert pa.x.tobytes() == pb.x.tobytes() and pa.y.tobytes() == pb.y.tobytes()
+
+
+def test_torch_peer_world1(eng):
+    """The symmetric-memory fused path on a world of one: symmetric workspace,
+    rendezvous, (empty) peer list and the stream barrier, against the golden run."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2603_03150_b200.sharded import run_pdhg_sharded
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        gm = load_golden("config0_s0")
+        T = eng.types()
+        try:
+            pt, st = run_pdhg_sharded(gm, T.PdhgParams(eps_rel=1e-4), G=1, comm_kind="torch_peer")
+        except (RuntimeError, NotImplementedError) as e:   # no symmetric memory on this stack
+            pytest.skip(f"symmetric memory unavailable: {e}")
+        r = gm.run("e4")
+        assert st.status.value == "Optimal"
+        assert st.iterations == int(r["iterations"]) and st.restarts == int(r["restarts"])
+    finally:
+        dist.destroy_process_group()
