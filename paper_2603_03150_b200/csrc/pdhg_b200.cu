@@ -427,13 +427,47 @@ __device__ __forceinline__ double warp_rows_dot(const RowSet& rs, long long row0
 
 // Device-resident per-period parameters (updated by one H2D copy per period
 // so the captured CUDA graph of a period can be replayed unchanged).
+// Fused all-gather (multi-GPU, DESIGN.md §6): the step's epilogue also
+// stores each new xe (primal) / y (dual) value into every peer's full
+// vector at this shard's slot -- NVLink peer stores that overlap the
+// kernel, replacing the all-gather after it.  ptr: device array of n peer
+// vector bases (same padded layout everywhere); off: this shard's slice.
+struct Peers {
+  double* const* __restrict__ ptr;
+  int n;
+  int off;
+};
+
+
+
 struct StepParams {
   double tau_w;    // tau / omega      (pdhg.py:142)
   double sigma_w;  // sigma * omega    (pdhg.py:143)
   double w0;       // avg_weight at period start (integer valued)
   long long iter0; // state.iterations at period start
   long long fail_iter;  // first iteration with a non-finite iterate (LLONG_MAX = none)
+  Peers peers[2];  // fused all-gather targets: [0] xe (primal step), [1] y (dual step)
 };
+
+// The peer list lives in device memory (StepParams) rather than in the kernel
+// parameters: read only in the epilogue, it keeps no registers live across
+// the row loop (as a StepArgs member it pushed the 40-register dual step into
+// a 16-byte spill, +9 %).
+__device__ __noinline__ void bcast_peers(const StepParams* P, int k, int row, double v) {
+  const int n = P->peers[k].n;
+  for (int q = 0; q < n; ++q) P->peers[k].ptr[q][P->peers[k].off + row] = v;
+}
+
+__device__ __forceinline__ void bcast(const StepParams* P, int k, int row, double v) {
+  if (P->peers[k].n) bcast_peers(P, k, row, v);  // out of line: no registers held in the hot loop
+}
+
+// k_step's form: the peer stores are compiled in only for the fused-all-gather
+// instantiation, so the single-GPU step kernels keep their exact code.
+template <bool PEERS>
+__device__ __forceinline__ void bcast_if(const StepParams* P, int k, int row, double v) {
+  if constexpr (PEERS) bcast(P, k, row, v);
+}
 
 // ------------------------------------------------------------------- steps
 
@@ -491,23 +525,7 @@ __device__ __forceinline__ double dual_epi_pre(int i, double ax, double bi, doub
   return yn;
 }
 
-// Fused all-gather (multi-GPU, DESIGN.md §6): the step's epilogue also
-// stores each new xe (primal) / y (dual) value into every peer's full
-// vector at this shard's slot -- NVLink peer stores that overlap the
-// kernel, replacing the all-gather after it.  ptr: device array of n peer
-// vector bases (same padded layout everywhere); off: this shard's slice.
-struct Peers {
-  double* const* __restrict__ ptr;
-  int n;
-  int off;
-};
-
-__device__ __forceinline__ void bcast(const Peers& p, int row, double v) {
-  for (int q = 0; q < p.n; ++q) p.ptr[q][p.off + row] = v;
-}
-
 struct StepArgs {
-  Peers peers;
   RowSet rs;
   const int* __restrict__ split;      // column-chunk split points, (nsplit-1) arrays of rows
   int nsplit;                         // 1 = unsplit
@@ -520,7 +538,7 @@ struct StepArgs {
   StepParams* P;
 };
 
-template <int V, bool PRIMAL>
+template <int V, bool PRIMAL, bool PEERS = false>
 __global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
   __shared__ double red[kWarps];
   StepParams* P = a.P;
@@ -537,8 +555,8 @@ __global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
     row_dot<kBlock, 1>(a.rs, s, e, threadIdx.x, xin, acc);
     const double d = block_sum(acc[0], red);
     if (threadIdx.x == 0) {
-      if (PRIMAL) bcast(a.peers, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
-      else bcast(a.peers, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
+      if (PRIMAL) bcast_if<PEERS>(P, 0, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast_if<PEERS>(P, 1, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
     }
     return;
   }
@@ -565,8 +583,8 @@ __global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
   const double mine = warp_rows_dot<V>(a.rs, row0, lane, xin, my_ok);
   if (my_ok) {
     const int row = (int)rl;
-    if (PRIMAL) bcast(a.peers, row, primal_epi_pre(row, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
-    else bcast(a.peers, row, dual_epi_pre(row, mine, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
+    if (PRIMAL) bcast_if<PEERS>(P, 0, row, primal_epi_pre(row, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
+    else bcast_if<PEERS>(P, 1, row, dual_epi_pre(row, mine, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
   }
 }
 
@@ -600,8 +618,8 @@ __global__ void __launch_bounds__(kBlock) k_step_sell(StepArgs a, SellSet S, int
     row_dot<kBlock, 1>(a.rs, s, e, threadIdx.x, xin, acc);
     const double d = block_sum(acc[0], red);
     if (threadIdx.x == 0) {
-      if (PRIMAL) bcast(a.peers, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
-      else bcast(a.peers, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
+      if (PRIMAL) bcast(P, 0, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast(P, 1, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
     }
     return;
   }
@@ -641,8 +659,8 @@ __global__ void __launch_bounds__(kBlock) k_step_sell(StepArgs a, SellSet S, int
   }
   if (ok) {
     const int row = (int)rl;
-    if (PRIMAL) bcast(a.peers, row, primal_epi_pre(row, acc, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
-    else bcast(a.peers, row, dual_epi_pre(row, acc, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
+    if (PRIMAL) bcast(P, 0, row, primal_epi_pre(row, acc, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
+    else bcast(P, 1, row, dual_epi_pre(row, acc, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
   }
 }
 
@@ -680,8 +698,8 @@ __device__ __forceinline__ void step_phase(const StepArgs& a, long long iter, do
     row_dot<NW * 32, 1, COH>(a.rs, s, e, threadIdx.x, xin, acc);
     const double d = NW == kWarps ? block_sum(acc[0], red) : block_sum_nw<NW>(acc[0], red);
     if (threadIdx.x == 0) {
-      if (PRIMAL) bcast(a.peers, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
-      else bcast(a.peers, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
+      if (PRIMAL) bcast(P, 0, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast(P, 1, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
     }
   }
   const int lane = threadIdx.x & 31;
@@ -697,8 +715,8 @@ __device__ __forceinline__ void step_phase(const StepArgs& a, long long iter, do
     bool my_ok;
     const double mine = warp_rows_dot<V, COH>(a.rs, row0, lane, xin, my_ok);
     if (my_ok) {
-      if (PRIMAL) bcast(a.peers, (int)rl, primal_epi_pre((int)rl, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
-      else bcast(a.peers, (int)rl, dual_epi_pre((int)rl, mine, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
+      if (PRIMAL) bcast(P, 0, (int)rl, primal_epi_pre((int)rl, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast(P, 1, (int)rl, dual_epi_pre((int)rl, mine, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
     }
   }
 }
@@ -782,7 +800,7 @@ __global__ void __launch_bounds__(kBlock) k_dual_split(StepArgs a, int j_in_peri
     double acc[1];
     row_dot<kBlock, 1>(a.rs, a.rs.ptr[row], a.rs.ptr[row + 1], threadIdx.x, xin, acc);
     const double d = block_sum(acc[0], red);
-    if (threadIdx.x == 0) bcast(a.peers, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
+    if (threadIdx.x == 0) bcast(P, 1, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -806,14 +824,13 @@ __global__ void __launch_bounds__(kBlock) k_dual_split(StepArgs a, int j_in_peri
   const double dot = warp_rows_dot_seg<V>(a.rs, sp, ep, row0, lane, xin, ok);
   if (!ok) return;
   const double d = pass > 0 ? part + dot : dot;
-  if (last) bcast(a.peers, (int)rl, dual_epi_pre((int)rl, d, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
+  if (last) bcast(P, 1, (int)rl, dual_epi_pre((int)rl, d, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
   else a.partial[rl] = d;
 }
 
 // PSR step: persistent CTAs (one per SM) walk row blocks; the SpMV lands in
 // shared memory (psr::block_spmv), then the same epilogue as k_step.
 struct PsrStepArgs {
-  Peers peers;
   psr::Layout L;
   const double* __restrict__ gather;
   const double* __restrict__ cb;
@@ -843,8 +860,8 @@ __global__ void __launch_bounds__(psr::kThreads, 1) k_step_psr(PsrStepArgs a, in
   for (int k = 0; k < psr::kStages; ++k) ph[k] = 0u;
   for (int b = blockIdx.x; b < a.L.nblk; b += gridDim.x) {
     psr::block_rows(a.L, b, a.gather, panels, bars, ph, [&](int row, double d) {
-      if (PRIMAL) bcast(a.peers, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
-      else bcast(a.peers, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
+      if (PRIMAL) bcast(P, 0, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast(P, 1, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
     });
   }
 }
@@ -1276,6 +1293,10 @@ struct StepLaunchEx {
   static int run(const pdhg_ctx* c, bool primal, const StepArgs& a, int j, int grid,
                  const void* win_base, size_t win) {
     if (grid == 0) return 0;
+    if (c->npeers[primal ? 0 : 1] > 0) {
+      if (primal) return launch_ex(c, k_step<V, true, true>, dim3(grid), dim3(kBlock), 0, win_base, win, a, j);
+      return launch_ex(c, k_step<V, false, true>, dim3(grid), dim3(kBlock), 0, win_base, win, a, j);
+    }
     if (primal) return launch_ex(c, k_step<V, true>, dim3(grid), dim3(kBlock), 0, win_base, win, a, j);
     return launch_ex(c, k_step<V, false>, dim3(grid), dim3(kBlock), 0, win_base, win, a, j);
   }
@@ -1283,8 +1304,6 @@ struct StepLaunchEx {
 
 StepArgs step_args(const pdhg_ctx* c, bool primal) {
   StepArgs a;
-  const int k = primal ? 0 : 1;  // peers of xe (primal) / y (dual)
-  a.peers = Peers{c->peers[k], c->npeers[k], primal ? c->xo : c->yo};
   if (primal) {
     a.rs = c->At; a.gather = c->y; a.cb = c->prob.c;
     a.x = c->x + c->xo; a.xe = c->xe + c->xo; a.xbar = c->xbar + c->xo;
@@ -1328,7 +1347,7 @@ int launch_step(pdhg_ctx* c, bool primal, int j) {
   const int lanes = primal ? c->at_lanes : c->a_lanes;
   const int k = primal ? 1 : 0;
   if (c->has_psr[k]) {
-    PsrStepArgs pa{a.peers, c->psr_l[k], a.gather, a.cb, a.x, a.xe, a.xbar, a.P};
+    PsrStepArgs pa{c->psr_l[k], a.gather, a.cb, a.x, a.xe, a.xbar, a.P};
     const int grid = std::min(c->psr_l[k].nblk, 148);
     int rc = primal ? launch_ex(c, k_step_psr<true>, dim3(grid), dim3(psr::kThreads), c->psr_smem[k],
                                 win_base, win, pa, j)
@@ -1479,6 +1498,8 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
     delete c;
     return fail(PDHG_ERR_CUDA, "cudaMallocHost failed");
   }
+  std::memset(c->P_host, 0, sizeof(StepParams));  // no peers until pdhg_set_peers
+  c->P_host->fail_iter = LLONG_MAX;
   *out = c;
   return 0;
 }
@@ -1737,6 +1758,10 @@ int pdhg_set_peers(pdhg_ctx* c, int32_t which, const double* const* peers_dev, i
     return fail(PDHG_ERR_ARG, "set_peers: bad argument");
   c->peers[which] = const_cast<double* const*>(peers_dev);
   c->npeers[which] = npeers;
+  c->P_host->peers[which] = Peers{c->peers[which], npeers, which == 0 ? c->xo : c->yo};
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaMemcpyAsync(&c->P->peers[which], &c->P_host->peers[which], sizeof(Peers),
+                           cudaMemcpyHostToDevice, c->stream));
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);  // captured StepArgs are stale
   c->graphs.clear();
   return 0;
