@@ -168,6 +168,12 @@ int pdhg_reset(pdhg_ctx* ctx);
  * (pdhg.py:194-196); *fail_iter_out receives that iteration or -1. */
 int pdhg_run_period(pdhg_ctx* ctx, int32_t iters, int64_t iter0, double tau_over_omega,
                     double sigma_omega, double w0, int64_t* fail_iter_out);
+/* pdhg_run_period followed by pdhg_check of npts points (0..2) with a single
+ * host synchronisation (one fewer round trip per period; the engine uses it
+ * whenever a period ends on a check).  out_host as in pdhg_check. */
+int pdhg_run_period_check(pdhg_ctx* ctx, int32_t iters, int64_t iter0, double tau_over_omega,
+                          double sigma_omega, double w0, int32_t npts, const int32_t* specs,
+                          int64_t* fail_iter_out, double* out_host);
 
 /* Score points.  specs[k] selects point k's (x, y) source (PDHG_PT_*) and,
  * with PDHG_SPEC_BEST_Z, takes z from the stored best z instead of

@@ -1611,6 +1611,59 @@ int pdhg_run_period(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_over_o
   return 0;
 }
 
+int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs);
+
+int pdhg_run_period_check(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_over_omega,
+                          double sigma_omega, double w0, int32_t npts, const int32_t* specs,
+                          int64_t* fail_iter_out, double* out_host) {
+  // run_period + check with one host synchronisation: the graph of the
+  // period, the check kernels and both device-to-host copies are queued
+  // back to back on the stream.
+  if (!c || iters < 0 || npts < 0 || npts > 2 || (npts > 0 && (!specs || !out_host)))
+    return fail(PDHG_ERR_ARG, "run_period_check: bad argument");
+  StepParams& h = *c->P_host;
+  h.tau_w = tau_over_omega;
+  h.sigma_w = sigma_omega;
+  h.w0 = w0;
+  h.iter0 = iter0;
+  h.fail_iter = LLONG_MAX;
+  CUDA_TRY(cudaMemcpyAsync(c->P, c->P_host, sizeof(StepParams), cudaMemcpyHostToDevice, c->stream));
+  int rc = 0;
+  if (iters > 0 && c->coop_grid > 0) {
+    rc = launch_period_persistent(c, iters);
+  } else if (iters > 0) {
+    auto it = c->graphs.find(iters);
+    if (it == c->graphs.end()) {
+      cudaGraph_t g;
+      CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      for (int j = 0; j < iters && !rc; ++j) {
+        rc = launch_step(c, true, j);
+        if (!rc) rc = launch_step(c, false, j);
+      }
+      cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+      if (rc) return rc;
+      if (ce != cudaSuccess) return fail(PDHG_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
+      cudaGraphExec_t ex;
+      CUDA_TRY(cudaGraphInstantiate(&ex, g, 0));
+      cudaGraphDestroy(g);
+      it = c->graphs.emplace(iters, ex).first;
+    }
+    CUDA_TRY(cudaGraphLaunch(it->second, c->stream));
+  }
+  if (rc) return rc;
+  if (npts > 0) {
+    if ((rc = pdhg_check_device(c, npts, specs))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->scal_host, c->scalars, (size_t)npts * PDHG_NQ * sizeof(double),
+                             cudaMemcpyDeviceToHost, c->stream));
+  }
+  CUDA_TRY(cudaMemcpyAsync(&c->P_host->fail_iter, &c->P->fail_iter, sizeof(long long),
+                           cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (fail_iter_out) *fail_iter_out = (c->P_host->fail_iter == LLONG_MAX) ? -1 : c->P_host->fail_iter;
+  if (npts > 0) std::memcpy(out_host, c->scal_host, (size_t)npts * PDHG_NQ * sizeof(double));
+  return 0;
+}
+
 int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
   if (!c || !specs || npts < 1 || npts > 2) return fail(PDHG_ERR_ARG, "bad argument");
   // primal side (rows of A): gathers full x, row-indexed y slice;

@@ -362,6 +362,17 @@ class DeviceLp:
                                          float(sigma_w), float(w0), C.byref(f)))
         return int(f.value)
 
+    def run_period_check(self, iters: int, iter0: int, tau_w: float, sigma_w: float, w0: float,
+                         *specs: int):
+        """run_period + check(*specs) with one synchronisation -> (fail_iter, [scalars...])."""
+        f = C.c_int64()
+        arr = (C.c_int32 * max(1, len(specs)))(*specs)
+        N.check(self.lib.pdhg_run_period_check(self.ctx, int(iters), int(iter0), float(tau_w),
+                                               float(sigma_w), float(w0), len(specs), arr,
+                                               C.byref(f), self._scal))
+        flat = np.frombuffer(self._scal, dtype=np.float64, count=len(specs) * N.NQ).copy()
+        return int(f.value), [flat[k * N.NQ:(k + 1) * N.NQ] for k in range(len(specs))]
+
     def check(self, *specs: int) -> list[np.ndarray]:
         arr = (C.c_int32 * len(specs))(*specs)
         N.check(self.lib.pdhg_check(self.ctx, len(specs), arr, self._scal))
@@ -669,7 +680,12 @@ def _run(T, dev: DeviceLp, p, params, seed, opts, t0):
             status = S.TIME_LIMIT
             break
         k = min(check_every - iterations % check_every, int(params.max_kkt_passes) - iterations)
-        fail = dev.run_period(k, iterations, tau / omega, sigma * omega, avg_weight)
+        at_check = (iterations + k) % check_every == 0
+        if at_check and hasattr(dev, "run_period_check"):      # one sync for steps + check
+            fail, qs = dev.run_period_check(k, iterations, tau / omega, sigma * omega, avg_weight,
+                                            N.PT_CUR, N.PT_AVG)
+        else:
+            fail, qs = dev.run_period(k, iterations, tau / omega, sigma * omega, avg_weight), None
         if fail >= 0:                                          # pdhg.py:194-196
             avg_weight += fail - iterations
             iterations = fail
@@ -680,7 +696,7 @@ def _run(T, dev: DeviceLp, p, params, seed, opts, t0):
         if iterations % check_every != 0:                      # pdhg.py:198-199
             continue
 
-        q_cur, q_avg = dev.check(N.PT_CUR, N.PT_AVG)           # pdhg.py:201-204
+        q_cur, q_avg = qs if qs is not None else dev.check(N.PT_CUR, N.PT_AVG)  # pdhg.py:201-204
         s_cur, s_avg = _score(q_cur), _score(q_avg)
         cur_sum, avg_sum = _summary(T, s_cur), _summary(T, s_avg)
         cur_term = _termination(T, s_cur, eps, norm_b, norm_c)
