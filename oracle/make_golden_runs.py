@@ -29,9 +29,16 @@ from paper_2603_03150_b200.instances import config1_general, config3_general  # 
 
 
 def main(which: str, scale: float = 1.0):
-    g = (config1_general if which == "config1" else config3_general)(scale).to_reference()
     t0 = time.perf_counter()
-    p, fmap = hybridlp.to_standard_form(g)
+    if which == "config2":   # built directly in standard form (instances.config2)
+        from paper_2603_03150_b200.instances import config2
+
+        inst = config2(scale)
+        p = hybridlp.StandardLp(inst.A, inst.b, inst.c)
+    else:
+        g = (config1_general if which == "config1" else config3_general)(scale).to_reference()
+        t0 = time.perf_counter()
+        p, fmap = hybridlp.to_standard_form(g)
     t1 = time.perf_counter()
     s, info = hybridlp.ruiz_equilibrate(p)
     t2 = time.perf_counter()
@@ -39,7 +46,7 @@ def main(which: str, scale: float = 1.0):
     t3 = time.perf_counter()
     term = st.termination
     out = {
-        "instance": f"{which}_general(scale={scale})", "m_std": p.m, "n_std": p.n, "nnz_std": int(p.A.nnz),
+        "instance": f"{which}{'' if which == 'config2' else '_general'}(scale={scale})", "m_std": p.m, "n_std": p.n, "nnz_std": int(p.A.nnz),
         "status": st.status.value, "iterations": st.iterations, "restarts": st.restarts,
         "objective_scaled": float(s.c @ pt.x), "max_violation": st.max_violation,
         "termination": [term.primal_lhs, term.primal_rhs, term.dual_lhs, term.dual_rhs,

@@ -40,6 +40,12 @@ def _rel(a, b):
     return float(np.max(np.abs(np.asarray(a) - np.asarray(b))) / max(1.0, float(np.max(np.abs(b)))))
 
 
+def _standard(which, scale):
+    from paper_2603_03150_b200.instances import config2
+
+    return config2(scale)
+
+
 def _general(which, scale, seed=None):
     from paper_2603_03150_b200.instances import config1_general, config3_general
 
@@ -81,7 +87,8 @@ def test_first_iterates_match_oracle(eng, which, scale):
         assert _rel(ax, oax) <= 1e-9 and _rel(ay, oay) <= 1e-9, k
 
 
-@pytest.mark.parametrize("which,scale", [("config1", 1.0), ("config3", 0.1), ("config3", 1.0)])
+@pytest.mark.parametrize("which,scale", [("config1", 1.0), ("config3", 0.1), ("config3", 1.0),
+                                         ("config2", 0.1)])
 def test_full_run_matches_reference(eng, which, scale):
     """Full-size run to eps_rel=1e-4 against the reference's own run."""
     path = GOLD / f"run_{which}_s{scale:g}.json"
@@ -89,8 +96,11 @@ def test_full_run_matches_reference(eng, which, scale):
         pytest.skip(f"no reference run recorded for {which} scale {scale}")
     ref = json.loads(path.read_text())
     T = eng.types()
-    g = _general(which, scale)
-    p, fmap, scaled, info = _device_pipeline(eng, g)
+    if which == "config2":   # standard form already: device Ruiz -> PDHG
+        scaled, info = eng.ruiz_equilibrate(_standard(which, scale))
+    else:
+        g = _general(which, scale)
+        p, fmap, scaled, info = _device_pipeline(eng, g)
     assert (scaled.A.shape[0], scaled.A.shape[1], int(scaled.A.nnz)) == (ref["m_std"], ref["n_std"], ref["nnz_std"])
     pt, st = eng.run_pdhg(scaled, T.PdhgParams(eps_rel=1e-4))
     assert st.status.value == ref["status"] == "Optimal"
