@@ -260,11 +260,18 @@ def _combine(rows: np.ndarray, npts: int) -> list[np.ndarray]:
 class ShardedDevice:
     """G shards behind engine._run's device interface (see module doc)."""
 
-    def __init__(self, plan: ShardPlan, shards, comm):
+    def __init__(self, plan: ShardPlan, shards, comm, graph: bool = True):
         self.plan = plan
         self.shards = list(shards)   # local shard backends, in comm.local order
         self.comm = comm
         self.m, self.n = plan.m, plan.n
+        # a period (kernels + all-gathers) is captured once per length and
+        # replayed, like the single-GPU engine's graphs; the symmetric-memory
+        # barrier of the torch_peer path stays eager
+        self.graph = (graph and all(getattr(sh, "stream", None) is not None for sh in self.shards)
+                      and not (isinstance(comm, TorchComm) and comm.fused))
+        self._graphs = {}
+        self._seen = set()
 
     def _on_stream(self):
         """torch work (copies, collectives) must queue behind the kernels on
@@ -328,6 +335,33 @@ class ShardedDevice:
     def run_period(self, iters: int, iter0: int, tau_w: float, sigma_w: float, w0: float) -> int:
         for s in self.shards:
             s.set_step(iter0, tau_w, sigma_w, w0)
+        if self.graph and iters > 0 and iters in self._seen:
+            g = self._graphs.get(iters)
+            if g is None:
+                g = self._capture(iters)
+            with self._on_stream():
+                g.replay()
+        else:
+            self._period_body(iters)
+            self._seen.add(iters)   # first run eager (lazy NCCL / allocator init), then capture
+        with self._on_stream():
+            fails = self.comm.allgather_int([s.fail_iter() for s in self.shards])
+        bad = [f for f in fails if f >= 0]
+        return min(bad) if bad else -1
+
+    def _capture(self, iters: int):
+        import torch
+
+        st = self.shards[0].stream
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            self._period_body(iters)
+        self._graphs[iters] = g
+        return g
+
+    def _period_body(self, iters: int):
+        """The kernels and all-gathers of one period, queued on the shards' stream."""
         fused = getattr(self.comm, "fused", False)
         for j in range(iters):
             for s in self.shards:
@@ -344,10 +378,6 @@ class ShardedDevice:
                     self.comm.barrier(self.shards)
             else:
                 self._ag("y")
-        with self._on_stream():
-            fails = self.comm.allgather_int([s.fail_iter() for s in self.shards])
-        bad = [f for f in fails if f >= 0]
-        return min(bad) if bad else -1
 
     def _complete(self, spec: int):
         which = spec & 3
