@@ -90,6 +90,8 @@ typedef struct pdhg_sell {
   const int32_t* width;  /* nslices: longest light row of the slice */
   const int32_t* col;    /* slots */
   const double* val;     /* slots */
+  const uint8_t* perm;   /* optional (rows rounded up to 32): lane -> row offset in its
+                            slice, rows sorted by length inside each slice (NULL = identity) */
 } pdhg_sell;
 
 typedef struct pdhg_problem {
@@ -369,15 +371,18 @@ int pdhg_violation(int32_t m, int32_t n, const int32_t* a_ptr, const int32_t* a_
 
 
 /* Sliced-ELL build (device): plan writes width (nslices = ceil(rows/32)) and
- * sptr (nslices+1) and returns the slot count; the caller allocates
- * slots-sized col/val and calls fill.  Rows longer than heavy_threshold are
- * left out. */
+ * sptr (nslices+1) and returns the slot count; optionally sort orders each
+ * slice's rows by length (perm: lane -> row offset, inv: row offset -> lane,
+ * both nslices*32 bytes); the caller allocates slots-sized col/val and calls
+ * fill (inv NULL = unsorted).  Rows longer than heavy_threshold are left out. */
 size_t pdhg_sell_tmp_bytes(int32_t rows);
 int pdhg_sell_plan(int32_t rows, const int32_t* ptr, int32_t heavy_threshold, int32_t* width,
                    int64_t* sptr, void* tmp, size_t tmp_bytes, void* stream, int64_t* slots_out);
-int pdhg_sell_fill(int32_t rows, const int32_t* ptr, const int32_t* col, const double* val,
-                   int32_t heavy_threshold, const int64_t* sptr, int32_t* scol, double* sval,
+int pdhg_sell_sort(int32_t rows, const int32_t* ptr, int32_t heavy_threshold, uint8_t* perm, uint8_t* inv,
                    void* stream);
+int pdhg_sell_fill(int32_t rows, const int32_t* ptr, const int32_t* col, const double* val,
+                   int32_t heavy_threshold, const int64_t* sptr, const uint8_t* inv, int32_t* scol,
+                   double* sval, void* stream);
 
 #ifdef __cplusplus
 }

@@ -31,7 +31,7 @@ EXPORTS = (
     "pdhg_split_build", "pdhg_stdform_tmp_bytes", "pdhg_stdform_plan", "pdhg_stdform_build",
     "pdhg_spmv_seq", "pdhg_unscale_point", "pdhg_restrict_x", "pdhg_lift_x", "pdhg_lift_slacks",
     "pdhg_lift_bound_duals", "pdhg_max0", "pdhg_violation_tmp_bytes", "pdhg_violation",
-    "pdhg_sell_tmp_bytes", "pdhg_sell_plan", "pdhg_sell_fill", "pdhg_set_peers",
+    "pdhg_sell_tmp_bytes", "pdhg_sell_plan", "pdhg_sell_fill", "pdhg_sell_sort", "pdhg_set_peers",
     "pdhg_run_period_check",
 )
 
@@ -55,7 +55,8 @@ class Sell(C.Structure):
     """struct pdhg_sell (sliced-ELL layout of one operator)."""
 
     _fields_ = [("rows", C.c_int32), ("nslices", C.c_int32), ("sptr", C.c_void_p),
-                ("width", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p)]
+                ("width", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p),
+                ("perm", C.c_void_p)]
 
 
 class Problem(C.Structure):
@@ -159,7 +160,8 @@ def load():
         _sig(lib, "pdhg_run_period_check", C.c_int, vp, i32, i64, dbl, dbl, dbl, i32, P(i32), P(i64),
              P(dbl))
         _sig(lib, "pdhg_sell_plan", C.c_int, i32, vp, i32, vp, vp, vp, szt, vp, P(i64))
-        _sig(lib, "pdhg_sell_fill", C.c_int, i32, vp, vp, vp, i32, vp, vp, vp, vp)
+        _sig(lib, "pdhg_sell_sort", C.c_int, i32, vp, i32, vp, vp, vp)
+        _sig(lib, "pdhg_sell_fill", C.c_int, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp)
         _sig(lib, "pdhg_violation", C.c_int, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
              vp, szt, vp, P(dbl))
         if lib.pdhg_abi_version() != 1:

@@ -599,6 +599,7 @@ struct SellSet {
   const int* __restrict__ width;
   const int* __restrict__ col;
   const double* __restrict__ val;
+  const unsigned char* __restrict__ perm;  // lane -> row offset in the slice (nullptr = identity)
 };
 
 template <bool PRIMAL>
@@ -626,7 +627,7 @@ __global__ void __launch_bounds__(kBlock) k_step_sell(StepArgs a, SellSet S, int
   const int lane = threadIdx.x & 31;
   const long long sl = ((long long)(blockIdx.x - a.rs.n_heavy) * kBlock + threadIdx.x) >> 5;
   if (sl >= S.nslices) return;  // warp-uniform
-  const long long rl = sl * 32 + lane;
+  const long long rl = sl * 32 + (S.perm ? S.perm[sl * 32 + lane] : lane);
   const bool in_range = rl < a.rs.rows;
   double o1 = 0.0, o2 = 0.0, o3 = 0.0;
   int len = 0;
@@ -1459,7 +1460,7 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
         return fail(PDHG_ERR_ARG, "sell layout does not match the operator");
       }
       c->sell[k] = SellSet{q->rows, q->nslices, reinterpret_cast<const long long*>(q->sptr), q->width,
-                           q->col, q->val};
+                           q->col, q->val, q->perm};
     }
   }
   for (int k = 0; k < 2; ++k) {

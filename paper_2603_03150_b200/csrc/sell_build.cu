@@ -53,17 +53,56 @@ __global__ void k_sell_width(int rows, const int* __restrict__ ptr, int heavy, i
   w32[sl] = 32LL * w;
 }
 
-// warp per row: copies the row's entries to its slice column
+// thread per slice: order the slice's rows by light length, descending
+// (stable; heavy rows count as empty), so the lanes still active in round k
+// are a prefix and every fetched sector is full.  perm[lane] = row offset,
+// inv[row offset] = lane.
+__global__ void k_sell_sort(int rows, const int* __restrict__ ptr, int heavy, unsigned char* __restrict__ perm,
+                            unsigned char* __restrict__ inv) {
+  const int sl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sl >= (rows + 31) / 32) return;
+  int len[32];
+  unsigned char idx[32];
+  for (int q = 0; q < 32; ++q) {
+    const long long r = (long long)sl * 32 + q;
+    int l = -1;  // rows past the end sort last
+    if (r < rows) {
+      l = ptr[r + 1] - ptr[r];
+      if (l > heavy) l = 0;
+    }
+    len[q] = l;
+    idx[q] = (unsigned char)q;
+  }
+  for (int a = 1; a < 32; ++a) {  // insertion sort, stable, descending
+    const int lv = len[a];
+    const unsigned char iv = idx[a];
+    int b = a - 1;
+    while (b >= 0 && len[b] < lv) {
+      len[b + 1] = len[b];
+      idx[b + 1] = idx[b];
+      --b;
+    }
+    len[b + 1] = lv;
+    idx[b + 1] = iv;
+  }
+  for (int q = 0; q < 32; ++q) {
+    perm[(size_t)sl * 32 + q] = idx[q];
+    inv[(size_t)sl * 32 + idx[q]] = (unsigned char)q;
+  }
+}
+
+// warp per row: copies the row's entries to its slice column (lane inv[r] when sorted)
 __global__ void k_sell_fill(int rows, const int* __restrict__ ptr, const int* __restrict__ col,
                             const double* __restrict__ val, int heavy, const long long* __restrict__ sptr,
-                            int* __restrict__ scol, double* __restrict__ sval) {
+                            const unsigned char* __restrict__ inv, int* __restrict__ scol,
+                            double* __restrict__ sval) {
   const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= rows) return;
   const int r = (int)w;
   const int s = ptr[r], e = ptr[r + 1];
   if (e - s > heavy) return;
-  const long long base = sptr[r >> 5] + (r & 31);
+  const long long base = sptr[r >> 5] + (inv ? inv[r] : (r & 31));
   for (int k = lane; k < e - s; k += 32) {
     scol[base + 32LL * k] = col[s + k];
     sval[base + 32LL * k] = val[s + k];
@@ -101,13 +140,22 @@ int pdhg_sell_plan(int32_t rows, const int32_t* ptr, int32_t heavy_threshold, in
   return 0;
 }
 
-int pdhg_sell_fill(int32_t rows, const int32_t* ptr, const int32_t* col, const double* val,
-                   int32_t heavy_threshold, const int64_t* sptr, int32_t* scol, double* sval,
+int pdhg_sell_sort(int32_t rows, const int32_t* ptr, int32_t heavy_threshold, uint8_t* perm, uint8_t* inv,
                    void* stream) {
+  if (rows <= 0 || !ptr || !perm || !inv) return set_error(PDHG_ERR_ARG, "sell_sort: bad argument");
+  const int ns = (rows + 31) / 32;
+  k_sell_sort<<<(ns + 127) / 128, 128, 0, (cudaStream_t)stream>>>(rows, ptr, heavy_threshold, perm, inv);
+  SELL_TRY(cudaGetLastError());
+  return 0;
+}
+
+int pdhg_sell_fill(int32_t rows, const int32_t* ptr, const int32_t* col, const double* val,
+                   int32_t heavy_threshold, const int64_t* sptr, const uint8_t* inv, int32_t* scol,
+                   double* sval, void* stream) {
   if (rows <= 0 || !ptr || !sptr || !scol || !sval) return set_error(PDHG_ERR_ARG, "sell_fill: bad argument");
   cudaStream_t s = (cudaStream_t)stream;
   k_sell_fill<<<(unsigned)(((long long)rows * 32 + 255) / 256), 256, 0, s>>>(
-      rows, ptr, col, val, heavy_threshold, reinterpret_cast<const long long*>(sptr), scol, sval);
+      rows, ptr, col, val, heavy_threshold, reinterpret_cast<const long long*>(sptr), inv, scol, sval);
   SELL_TRY(cudaGetLastError());
   return 0;
 }

@@ -53,11 +53,16 @@ class GpuOptions:
     dual_split:      column chunks of the dual step's SpMV (split-K, csrc k_dual_split):
                      each pass gathers from an L2-sized window of xe; 1 = unsplit.
     sell:            "auto" | "on" | "off" -- sliced-ELL layout (csrc/sell_build.cu) for
-                     the step kernels; auto uses it for an operator with short rows
-                     (mean < sell_max_mean entries) whose padded slot count stays within
-                     sell_max_pad x its nonzeros and that has no PSR layout: config 3
-                     (primal 56 -> 51 us, dual 43 -> 34 us).  On config 4's A' (mean 20)
-                     it is neutral (0.94 vs 0.93 ms), so CSR-vector stays there.
+                     the step kernels; auto uses it for an operator whose padded slot
+                     count stays within sell_max_pad x its nonzeros (near-uniform row
+                     lengths), that has no PSR layout, and either short rows (mean <
+                     sell_max_mean: config 3, steps 10-22 % faster) or >= sell_min_nnz
+                     entries (config 4's A': primal step 0.862 -> 0.820 ms; at 1.5-20M
+                     entries it measured neutral to 50 % slower).  Skewed rows (config 4's
+                     A: 4x padding) stay on CSR-vector.
+    sell_sort:       order each slice's rows by length (lanes active in a round form a
+                     prefix); measured neutral on config 4, slower on config 3's 1-3
+                     entry rows (one more dependent load per warp), so off.
     persistent:      "off" | "on" | "tiny" | "auto" -- "off" (default): a CUDA graph of two
                      kernels per iteration; "on": each period as one cooperative kernel
                      (grid barriers between half steps); "tiny": each period as one
@@ -87,6 +92,8 @@ class GpuOptions:
     sell: str = "auto"
     sell_max_pad: float = 1.6
     sell_max_mean: float = 12.0
+    sell_min_nnz: int = 50_000_000
+    sell_sort: bool = False
 
 
 def auto_lanes(nnz: int, rows: int) -> int:
@@ -277,7 +284,7 @@ class DeviceLp:
         """Plan + fill the sliced-ELL layout of one operator on the device (or None)."""
         if opts.sell == "off" or rows <= 0 or nnz <= 0:
             return None
-        if opts.sell == "auto" and nnz / rows >= opts.sell_max_mean:
+        if opts.sell == "auto" and nnz / rows >= opts.sell_max_mean and nnz < opts.sell_min_nnz:
             return None
         lib = self.lib
         sptr_ = self.stream.cuda_stream
@@ -295,13 +302,23 @@ class DeviceLp:
             return None
         scol = torch.empty(max(slots.value, 1), dtype=torch.int32, device=dev)
         sval = torch.empty(max(slots.value, 1), dtype=torch.float64, device=dev)
+        perm = inv = None
+        if opts.sell_sort:
+            perm = torch.empty(ns * 32, dtype=torch.uint8, device=dev)
+            inv = torch.empty(ns * 32, dtype=torch.uint8, device=dev)
+            N.check(lib.pdhg_sell_sort(rows, ptr.data_ptr(), int(H), perm.data_ptr(), inv.data_ptr(), sptr_))
         N.check(lib.pdhg_sell_fill(rows, ptr.data_ptr(), col.data_ptr(), val.data_ptr(), int(H),
-                                   sp.data_ptr(), scol.data_ptr(), sval.data_ptr(), sptr_))
+                                   sp.data_ptr(), inv.data_ptr() if inv is not None else None,
+                                   scol.data_ptr(), sval.data_ptr(), sptr_))
         d = N.Sell()
         d.rows, d.nslices = rows, ns
         d.sptr, d.width, d.col, d.val = sp.data_ptr(), width.data_ptr(), scol.data_ptr(), sval.data_ptr()
+        d.perm = perm.data_ptr() if perm is not None else None
+        self.stream.synchronize()
+        del inv
         self.sell_info[key]["used"] = True
-        return (d, (width, sp, scol, sval))
+        self.sell_info[key]["sorted"] = perm is not None
+        return (d, (width, sp, scol, sval, perm))
 
     def _build_psr(self, torch, dev, key, rows, cols, nnz, ptr, col, val, H, opts):
         """Plan + build the PSR layout of one operator on the device (or None)."""

@@ -39,6 +39,7 @@ def main():
     variants = {
         "csr": dict(psr="off", sell="off", l2_persist=0),
         "sell": dict(psr="off", sell="on"),
+        "sell_unsorted": dict(psr="off", sell="on", sell_sort=False),
         "auto": dict(),
         "persist": dict(psr="off", sell="off", persistent="on"),
         "csr_a8": dict(psr="off", sell="off", a_lanes=8),
