@@ -603,8 +603,12 @@ struct SellSet {
 };
 
 template <bool PRIMAL>
+#ifndef PDHG_SELL_U
+#define PDHG_SELL_U 4
+#endif
+
 __global__ void __launch_bounds__(kBlock) k_step_sell(StepArgs a, SellSet S, int j_in_period) {
-  constexpr int kU = 4;
+  constexpr int kU = PDHG_SELL_U;
   __shared__ double red[kWarps];
   StepParams* P = a.P;
   const long long iter = P->iter0 + j_in_period + 1;
@@ -658,6 +662,7 @@ __global__ void __launch_bounds__(kBlock) k_step_sell(StepArgs a, SellSet S, int
     for (int u = 0; u < kU; ++u)
       if (jv[u] >= 0) acc = fma(av[u], xv[u], acc);
   }
+
   if (ok) {
     const int row = (int)rl;
     if (PRIMAL) bcast(P, 0, row, primal_epi_pre(row, acc, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
