@@ -384,6 +384,17 @@ int pdhg_sell_fill(int32_t rows, const int32_t* ptr, const int32_t* col, const d
                    int32_t heavy_threshold, const int64_t* sptr, const uint8_t* inv, int32_t* scol,
                    double* sval, void* stream);
 
+
+/* IPM hand-off (warmstart.py:62-107): center_toward_target
+ * elementwise on the device with numpy's maximum / clip semantics (bit-identical
+ * to the reference for the same mu), and a fixed-order dot product for
+ * mu_target's x'z (OpenBLAS ddot in the reference; equal to rounding). */
+int pdhg_center_toward_target(int64_t n, const double* x, const double* z, double mu, double alpha_min,
+                              double delta_max, double* x_out, double* z_out, void* stream);
+size_t pdhg_dot_tmp_bytes(void);
+int pdhg_dot(int64_t n, const double* a, const double* b, void* tmp, size_t tmp_bytes, void* stream,
+             double* out_host);
+
 #ifdef __cplusplus
 }
 #endif

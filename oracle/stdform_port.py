@@ -218,3 +218,35 @@ def evaluate_general_point(g, x, y):
     p, fmap = to_standard_form(g)
     pt = lift_point(g, p, fmap, x, y)
     return violation_summary(p, pt)
+
+
+# ----------------------------------------------------------------- IPM hand-off (§8(f) row 4)
+
+
+def mu_target(x, z, n: int, mu_min: float) -> float:
+    """warmstart.py:62-68."""
+    x = np.asarray(x, dtype=float)
+    z = np.asarray(z, dtype=float)
+    if x.size != n or z.size != n or n < 1:
+        raise InvalidModelError("x and z must both have length n >= 1")
+    return max(float(x @ z) / n, mu_min)
+
+
+def center_toward_target(x, z, mu: float, alpha_min: float, delta_max: float):
+    """warmstart.py:71-96 (same numpy ufuncs, same order)."""
+    a, d = alpha_min, delta_max
+    xp = np.maximum(np.asarray(x, dtype=float), a)
+    zp = np.maximum(np.asarray(z, dtype=float), a)
+    x_first = xp < zp
+    x1 = np.clip(mu / zp, xp - d, xp + d)
+    z1 = np.clip(mu / x1, zp - d, zp + d)
+    z2 = np.clip(mu / xp, zp - d, zp + d)
+    x2 = np.clip(mu / z2, xp - d, xp + d)
+    return np.maximum(np.where(x_first, x1, x2), a), np.maximum(np.where(x_first, z1, z2), a)
+
+
+def centered_start(pt: KktPoint, mu_min=1e-6, alpha_min=1e-6, delta_max=1e-4) -> KktPoint:
+    """warmstart.py:99-107 (WarmStartParams defaults, warmstart.py:47-52)."""
+    mu = mu_target(pt.x, pt.z, pt.x.size, mu_min)
+    xn, zn = center_toward_target(pt.x, pt.z, mu, alpha_min, delta_max)
+    return KktPoint(xn, pt.y.copy(), zn)

@@ -33,12 +33,17 @@ _REBIND_RUIZ = ("hybridlp", "hybridlp.transform", "hybridlp.warmstart")
 _REBIND_STD = ("hybridlp", "hybridlp.lp_core", "hybridlp.warmstart")
 
 
-def install(ruiz: bool = False, std_form: bool = False) -> None:
+# centered_start is bound in warmstart.py:99 (called at 323) and re-exported in __init__.py:49
+_REBIND_CENTER = ("hybridlp", "hybridlp.warmstart")
+
+
+def install(ruiz: bool = False, std_form: bool = False, centered: bool = False) -> None:
     """Route every ``run_pdhg`` name of the reference package to this engine;
     with ``ruiz=True`` also its ``ruiz_equilibrate`` (device Ruiz, whose
     scaled matrix then stays on the device for the PDHG solve); with
     ``std_form=True`` also ``to_standard_form`` (device builder, whose
-    matrix the device Ruiz then reuses)."""
+    matrix the device Ruiz then reuses); with ``centered=True`` also
+    ``centered_start`` (the hand-off of the PDHG point to the IPM)."""
     import importlib
 
     targets = [(n, "run_pdhg", run_pdhg) for n in _REBIND]
@@ -46,6 +51,10 @@ def install(ruiz: bool = False, std_form: bool = False) -> None:
         targets += [(n, "ruiz_equilibrate", ruiz_equilibrate) for n in _REBIND_RUIZ]
     if std_form:
         targets += [(n, "to_standard_form", to_standard_form) for n in _REBIND_STD]
+    if centered:
+        from .finish import centered_start
+
+        targets += [(n, "centered_start", centered_start) for n in _REBIND_CENTER]
     for name, attr, fn in targets:
         mod = importlib.import_module(name)
         if (name, attr) not in _saved:

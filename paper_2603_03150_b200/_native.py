@@ -32,7 +32,7 @@ EXPORTS = (
     "pdhg_spmv_seq", "pdhg_unscale_point", "pdhg_restrict_x", "pdhg_lift_x", "pdhg_lift_slacks",
     "pdhg_lift_bound_duals", "pdhg_max0", "pdhg_violation_tmp_bytes", "pdhg_violation",
     "pdhg_sell_tmp_bytes", "pdhg_sell_plan", "pdhg_sell_fill", "pdhg_sell_sort", "pdhg_set_peers",
-    "pdhg_run_period_check",
+    "pdhg_run_period_check", "pdhg_center_toward_target", "pdhg_dot_tmp_bytes", "pdhg_dot",
 )
 
 VEC = {name: i for i, name in enumerate(
@@ -157,6 +157,9 @@ def load():
         _sig(lib, "pdhg_violation_tmp_bytes", szt, i32, i32)
         _sig(lib, "pdhg_sell_tmp_bytes", szt, i32)
         _sig(lib, "pdhg_set_peers", C.c_int, vp, i32, vp, i32)
+        _sig(lib, "pdhg_center_toward_target", C.c_int, i64, vp, vp, dbl, dbl, dbl, vp, vp, vp)
+        _sig(lib, "pdhg_dot_tmp_bytes", szt)
+        _sig(lib, "pdhg_dot", C.c_int, i64, vp, vp, vp, szt, vp, P(dbl))
         _sig(lib, "pdhg_run_period_check", C.c_int, vp, i32, i64, dbl, dbl, dbl, i32, P(i32), P(i64),
              P(dbl))
         _sig(lib, "pdhg_sell_plan", C.c_int, i32, vp, i32, vp, vp, vp, szt, vp, P(i64))

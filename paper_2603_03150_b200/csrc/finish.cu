@@ -150,9 +150,67 @@ __global__ void k_final(const double* __restrict__ part, int nparts, int is_max,
   *out = t;
 }
 
+// numpy's clip for floats: MIN(MAX(v, lo), hi) with MAX(a,b) = isnan(a) ? a :
+// (a > b ? a : b) and MIN(a,b) = isnan(a) ? a : (a < b ? a : b)
+__device__ __forceinline__ double np_clip(double v, double lo, double hi) {
+  const double t = (v != v) ? v : (v > lo ? v : lo);
+  return (t != t) ? t : (t < hi ? t : hi);
+}
+
+// center_toward_target (warmstart.py:71-96), elementwise, the reference's ops in order
+__global__ void k_center(long long n, const double* __restrict__ x, const double* __restrict__ z, double mu,
+                         double a, double d, double* __restrict__ xo, double* __restrict__ zo) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double xp = np_maximum(x[i], a);
+  const double zp = np_maximum(z[i], a);
+  const bool x_first = xp < zp;
+  double xn, zn;
+  if (x_first) {
+    const double x1 = np_clip(__ddiv_rn(mu, zp), __dsub_rn(xp, d), __dadd_rn(xp, d));
+    xn = x1;
+    zn = np_clip(__ddiv_rn(mu, x1), __dsub_rn(zp, d), __dadd_rn(zp, d));
+  } else {
+    const double z2 = np_clip(__ddiv_rn(mu, xp), __dsub_rn(zp, d), __dadd_rn(zp, d));
+    zn = z2;
+    xn = np_clip(__ddiv_rn(mu, z2), __dsub_rn(xp, d), __dadd_rn(xp, d));
+  }
+  xo[i] = np_maximum(xn, a);
+  zo[i] = np_maximum(zn, a);
+}
+
 }  // namespace
 
 extern "C" {
+
+int pdhg_center_toward_target(int64_t n, const double* x, const double* z, double mu, double alpha_min,
+                              double delta_max, double* x_out, double* z_out, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !z || !x_out || !z_out))) return set_error(PDHG_ERR_ARG, "center: bad argument");
+  if (n == 0) return 0;
+  k_center<<<nb(n), kT, 0, (cudaStream_t)stream>>>(n, x, z, mu, alpha_min, delta_max, x_out, z_out);
+  FN_TRY(cudaGetLastError());
+  return 0;
+}
+
+size_t pdhg_dot_tmp_bytes(void) { return a256((size_t)kDotBlocks * 8) + a256(8); }
+
+int pdhg_dot(int64_t n, const double* a, const double* b, void* tmp, size_t tmp_bytes, void* stream,
+             double* out_host) {
+  if (n < 0 || !tmp || !out_host || (n > 0 && (!a || !b))) return set_error(PDHG_ERR_ARG, "dot: bad argument");
+  if (tmp_bytes < pdhg_dot_tmp_bytes()) return set_error(PDHG_ERR_ARG, "dot: tmp too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  double* part = (double*)tmp;
+  double* res = (double*)((char*)tmp + a256((size_t)kDotBlocks * 8));
+  FN_TRY(cudaMemsetAsync(res, 0, 8, s));
+  if (n > 0) {
+    k_partial<<<kDotBlocks, kT, 0, s>>>(n, a, b, part);
+    k_final<<<1, 32, 0, s>>>(part, kDotBlocks, 0, res);
+  }
+  FN_TRY(cudaMemcpyAsync(out_host, res, 8, cudaMemcpyDeviceToHost, s));
+  FN_TRY(cudaStreamSynchronize(s));
+  FN_TRY(cudaGetLastError());
+  return 0;
+}
 
 int pdhg_spmv_seq(int32_t rows, const int32_t* ptr, const int32_t* col, const double* val,
                   const double* v, const double* base, double* out, void* stream) {

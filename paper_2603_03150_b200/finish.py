@@ -10,6 +10,8 @@ reference pipeline (``finish_point``, warmstart.py:209-224):
 * ``evaluate_general_point`` lp_core.py:488-492 (device standard form + lift + violation)
 * ``finish_point``           warmstart.py:209-224 (presolve replay stays the reference's
                              ``postsolve``; everything around it runs here)
+* ``mu_target``, ``center_toward_target``, ``centered_start``  warmstart.py:62-107 --
+                             the hand-off of the PDHG point to the reference IPM
 
 Each is a composition of sm_100a kernels (csrc/finish.cu) behind the C ABI:
 sparse products in scipy's csr_matvec order, elementwise steps with the
@@ -288,3 +290,61 @@ def finish_point(prep, pt_solve, *, gpu=None):
     restored = postsolve(prep.presolve_result.stack, T.KktPoint(x_r, y_r, z_r), prep.original)
     viol = evaluate_general_point(prep.original, restored.x, restored.y, gpu=gpu)
     return W.FinishedPoint(restored.x, restored.y, restored.z, viol, scaled_viol)
+
+
+# ----------------------------------------------------------------- IPM hand-off
+
+
+def mu_target(x, z, n: int, mu_min: float, *, gpu=None) -> float:
+    """warmstart.py:62-68: max(x'z / n, mu_min), x'z on the device."""
+    T = resolve()
+    x = np.asarray(x, dtype=float)
+    z = np.asarray(z, dtype=float)
+    if x.size != n or z.size != n or n < 1:
+        raise T.InvalidModelError("x and z must both have length n >= 1")
+    torch, dev = _torch_dev(gpu)
+    lib = N.load()
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.device(dev), torch.cuda.stream(stream):
+        a, b = _up(torch, dev, x.ravel()), _up(torch, dev, z.ravel())
+        tb = lib.pdhg_dot_tmp_bytes()
+        tmp = torch.empty(tb, dtype=torch.uint8, device=dev)
+        out = C.c_double()
+        N.check(lib.pdhg_dot(n, a.data_ptr(), b.data_ptr(), tmp.data_ptr(), tb, stream.cuda_stream,
+                             C.byref(out)))
+    return max(float(out.value) / n, mu_min)
+
+
+def center_toward_target(x, z, mu: float, alpha_min: float, delta_max: float, *, gpu=None):
+    """warmstart.py:71-96 on the device -> (x_new, z_new), bit-identical to the reference."""
+    x = np.asarray(x, dtype=float).ravel()
+    z = np.asarray(z, dtype=float).ravel()
+    torch, dev = _torch_dev(gpu)
+    lib = N.load()
+    n = x.size
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.device(dev), torch.cuda.stream(stream):
+        xd, zd = _up(torch, dev, x if n else np.zeros(1)), _up(torch, dev, z if n else np.zeros(1))
+        xo, zo = torch.empty_like(xd), torch.empty_like(zd)
+        N.check(lib.pdhg_center_toward_target(n, xd.data_ptr(), zd.data_ptr(), float(mu), float(alpha_min),
+                                              float(delta_max), xo.data_ptr(), zo.data_ptr(),
+                                              stream.cuda_stream))
+        return xo[:n].cpu().numpy(), zo[:n].cpu().numpy()
+
+
+def centered_start(pt, params=None, *, gpu=None):
+    """warmstart.py:99-107: perturb (x, z) toward max(x'z/n, mu_min); y untouched."""
+    T = resolve()
+    if params is None:
+        try:
+            from hybridlp.warmstart import WarmStartParams  # type: ignore
+
+            params = WarmStartParams()
+        except ImportError:
+            from types import SimpleNamespace
+
+            params = SimpleNamespace(mu_min=1e-6, alpha_min=1e-6, delta_max=1e-4)  # warmstart.py:47-52
+    x = np.asarray(pt.x, dtype=float)
+    mu = mu_target(x, pt.z, x.size, params.mu_min, gpu=gpu)
+    xn, zn = center_toward_target(x, pt.z, mu, params.alpha_min, params.delta_max, gpu=gpu)
+    return T.KktPoint(xn, np.asarray(pt.y, dtype=float).copy(), zn)

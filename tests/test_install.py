@@ -56,3 +56,20 @@ def test_result_types_are_the_references(hybridlp):
     st = T.SolveStats(status=hybridlp.SolveStatus.OPTIMAL, iterations=1, restarts=0,
                       wall_seconds=0.0, termination=None, max_violation=0.0)
     assert st.history == []
+
+
+def test_install_rebinds_std_form_and_centering(hybridlp):
+    import importlib
+
+    import paper_2603_03150_b200 as eng
+    from paper_2603_03150_b200 import finish
+
+    eng.install(std_form=True, centered=True)
+    try:
+        for m in ("hybridlp", "hybridlp.lp_core", "hybridlp.warmstart"):
+            assert importlib.import_module(m).to_standard_form is eng.to_standard_form
+        for m in ("hybridlp", "hybridlp.warmstart"):
+            assert importlib.import_module(m).centered_start is finish.centered_start
+    finally:
+        eng.uninstall()
+    assert importlib.import_module("hybridlp.warmstart").centered_start is not finish.centered_start

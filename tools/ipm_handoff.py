@@ -10,7 +10,9 @@ has no GPU:
 
 The ref half compares, for each tolerance, the reference IPM warm-started
 from the GPU point with the same IPM warm-started from the reference's own
-PDHG point (warmstart.py:99-154) and with the cold IPM (ipm.py:234).
+PDHG point (warmstart.py:99-154) and with the cold IPM (ipm.py:234), and
+the IPM warm-started from the device's centered_start of the GPU point
+(csrc/finish.cu k_center).
 """
 
 from __future__ import annotations
@@ -32,6 +34,7 @@ EPS = (1e-4, 1e-6)
 def gpu_half():
     import paper_2603_03150_b200 as eng
     from conftest import load_golden
+    from paper_2603_03150_b200 import finish
 
     gm = load_golden("config0_s0")
     T = eng.types()
@@ -42,6 +45,8 @@ def gpu_half():
         d[f"{tag}_x"], d[f"{tag}_y"], d[f"{tag}_z"] = pt.x, pt.y, pt.z
         d[f"{tag}_iterations"] = st.iterations
         d[f"{tag}_status"] = st.status.value
+        cs = finish.centered_start(pt)   # the hand-off on the device (warmstart.py:99-107)
+        d[f"{tag}_cs_x"], d[f"{tag}_cs_y"], d[f"{tag}_cs_z"] = cs.x, cs.y, cs.z
     OUT_GPU.parent.mkdir(exist_ok=True)
     np.savez(OUT_GPU, **d)
     print("wrote", OUT_GPU)
@@ -81,6 +86,17 @@ def ref_half():
             row[f"{who}_warm_ipm_status"] = w.stats.status.value
             row[f"{who}_final_max_violation"] = fin.violation.max_violation
         row["point_max_abs_diff_x"] = float(np.max(np.abs(gpu[f"{tag}_x"] - ref_pt.x)))
+        if f"{tag}_cs_x" in gpu.files:   # device centered_start -> reference warm IPM
+            ref_cs = centered_start(KktPoint(gpu[f"{tag}_x"], gpu[f"{tag}_y"], gpu[f"{tag}_z"]),
+                                    WarmStartParams())
+            dev_cs = KktPoint(gpu[f"{tag}_cs_x"], gpu[f"{tag}_cs_y"], gpu[f"{tag}_cs_z"])
+            row["device_centered_start_max_rel_diff"] = float(max(
+                np.max(np.abs(dev_cs.x - ref_cs.x) / np.maximum(np.abs(ref_cs.x), 1e-300)),
+                np.max(np.abs(dev_cs.z - ref_cs.z) / np.maximum(np.abs(ref_cs.z), 1e-300))))
+            w = warm_started_ipm(p, dev_cs, IpmParams(), WarmStartParams())
+            fin = finish_point(prep, w.point)
+            row["gpu_device_centered_warm_ipm_iterations"] = w.stats.iterations
+            row["gpu_device_centered_final_max_violation"] = fin.violation.max_violation
         res[tag] = row
     OUT_REF.write_text(json.dumps(res, indent=1))
     print(json.dumps(res, indent=1))
