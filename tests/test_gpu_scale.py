@@ -108,3 +108,57 @@ def test_spmv_scaled_1e12(eng, c4small):
     w = rng.standard_normal(p.m)
     assert _rel(dev.spmv(v), p.A @ v) <= 1e-12
     assert _rel(dev.spmv(w, transpose=True), p.A.T @ w) <= 1e-12
+
+
+# ---------------------------------------------------------------- full config-4 size
+@pytest.fixture(scope="module")
+def c4full():
+    from paper_2603_03150_b200.instances import config4
+
+    return config4(scale=1.0, seed=4)     # the bench instance: 5M x 10M, 199.9M nnz
+
+
+def test_full_config4_spmv_1e12(eng, c4full):
+    """Single SpMV gate (1e-12 relative) at the full 200M-nnz size, both operators."""
+    p = c4full
+    dev = eng.device_lp(p, eng.GpuOptions(cache_layout=False))
+    rng = np.random.default_rng(9)
+    v = rng.standard_normal(p.n)
+    w = rng.standard_normal(p.m)
+    assert _rel(dev.spmv(v), p.A @ v) <= 1e-12
+    assert _rel(dev.spmv(w, transpose=True), p.A.T @ w) <= 1e-12
+
+
+def test_full_config4_first_iterates_1e9(eng, c4full):
+    """Iterates 1-2 at full size against the oracle's pdhg_step with the same step size."""
+    from paper_2603_03150_b200 import _native as N
+
+    T = eng.types()
+    p = c4full
+    lam = eng.estimate_opnorm(p.A)
+    opts = eng.GpuOptions(opnorm=lam)
+    step = 1.0 / (1.05 * lam)                                 # pdhg.py:119
+    st = PdhgState(x=np.zeros(p.n), y=np.zeros(p.m), avg_x=np.zeros(p.n), avg_y=np.zeros(p.m),
+                   avg_weight=0.0, tau=step, sigma=step, omega=1.0, iterations=0, restarts=0,
+                   restart_x=None, restart_y=None, restart_score=1.0)
+    model = Model(p.A, p.b, p.c)
+    for k in (1, 2):
+        oracle.pdhg_step(st, model)
+        eng.run_pdhg(p, T.PdhgParams(eps_rel=1e-12, max_kkt_passes=k, check_every=10**6), gpu=opts)
+        dev = eng.device_lp(p, opts)
+        x, y, _ = dev.fetch(N.PT_CUR, want_z=False)
+        assert _rel(x, st.x) <= 1e-9 and _rel(y, st.y) <= 1e-9, k
+
+
+def test_full_config4_reaches_1e4(eng, c4full):
+    """Full run to 1e-4 at full size; the returned point re-passes the oracle's
+    termination test (size-independent property; iteration count is a multiple
+    of check_every)."""
+    T = eng.types()
+    p = c4full
+    pt, st = eng.run_pdhg(p, T.PdhgParams(eps_rel=1e-4, time_limit_s=300))
+    assert st.status.value == "Optimal"
+    assert st.iterations % 64 == 0
+    t = oracle.check_relative_termination(Model(p.A, p.b, p.c), KktPoint(pt.x, pt.y, pt.z), 1e-4)
+    assert t.ok
+    assert st.history and st.history[-1]["iteration"] == st.iterations
