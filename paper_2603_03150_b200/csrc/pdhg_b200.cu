@@ -538,8 +538,18 @@ struct StepArgs {
   StepParams* P;
 };
 
+// Occupancy: the V >= 16 form (config 4's dual step) is latency-bound and
+// fits 32 registers -- 8 blocks (64 warps) per SM -- once the epilogue
+// operands are loaded after the row loop: 0.975 -> 0.936 ms.  The pipelined
+// V <= 8 form keeps its registers (reduce-scatter partials): 4 blocks.
+// (Left to ptxas, an explicit minBlocks of 1 gave 56 / 80 registers and a
+// 23 % slower dual step; profiles/r01_pipeline.md.)
+template <int V>
+constexpr int step_min_blocks() { return V >= 16 ? 8 : 4; }
+
 template <int V, bool PRIMAL, bool PEERS = false>
-__global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
+__global__ void __launch_bounds__(kBlock, step_min_blocks<V>()) k_step(StepArgs a, int j_in_period) {
+  constexpr bool kLateEpi = V >= 16;
   __shared__ double red[kWarps];
   StepParams* P = a.P;
   const long long iter = P->iter0 + j_in_period + 1;  // state.iterations after this step
@@ -572,15 +582,21 @@ __global__ void __launch_bounds__(kBlock) k_step(StepArgs a, int j_in_period) {
   if (row0 >= a.rs.rows) return;  // warp-uniform
   const long long rl = row0 + lane;
   const bool in_range = rl < a.rs.rows;
-  // epilogue operands first: coalesced and independent of the SpMV
+  // epilogue operands: coalesced, loaded before the SpMV (V <= 8) or after it
+  // (V >= 16, so that fewer registers are live in the row loop)
   double o1 = 0.0, o2 = 0.0, o3 = 0.0;
-  if (in_range) {
+  if (!kLateEpi && in_range) {
     o1 = a.cb[rl];
     o2 = a.x[rl];
     o3 = a.xbar[rl];
   }
   bool my_ok;
   const double mine = warp_rows_dot<V>(a.rs, row0, lane, xin, my_ok);
+  if (kLateEpi && in_range) {
+    o1 = a.cb[rl];
+    o2 = a.x[rl];
+    o3 = a.xbar[rl];
+  }
   if (my_ok) {
     const int row = (int)rl;
     if (PRIMAL) bcast_if<PEERS>(P, 0, row, primal_epi_pre(row, mine, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
