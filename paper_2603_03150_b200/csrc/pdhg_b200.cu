@@ -623,7 +623,16 @@ template <bool PRIMAL>
 #define PDHG_SELL_U 4
 #endif
 
-__global__ void __launch_bounds__(kBlock) k_step_sell(StepArgs a, SellSet S, int j_in_period) {
+// 8 blocks per SM (32 registers) with the epilogue operands loaded after the
+// row loop: primal step 0.820 -> 0.812 ms on config 4; 6 blocks with early
+// loads measured 1.03 ms (profiles/r01_pipeline.md).
+#ifndef PDHG_SELL_MINB
+#define PDHG_SELL_MINB 8
+#endif
+#ifndef PDHG_SELL_LATE
+#define PDHG_SELL_LATE 1
+#endif
+__global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_step_sell(StepArgs a, SellSet S, int j_in_period) {
   constexpr int kU = PDHG_SELL_U;
   __shared__ double red[kWarps];
   StepParams* P = a.P;
@@ -652,9 +661,11 @@ __global__ void __launch_bounds__(kBlock) k_step_sell(StepArgs a, SellSet S, int
   double o1 = 0.0, o2 = 0.0, o3 = 0.0;
   int len = 0;
   if (in_range) {
-    o1 = a.cb[rl];
-    o2 = a.x[rl];
-    o3 = a.xbar[rl];
+    if (!PDHG_SELL_LATE) {
+      o1 = a.cb[rl];
+      o2 = a.x[rl];
+      o3 = a.xbar[rl];
+    }
     len = a.rs.ptr[rl + 1] - a.rs.ptr[rl];
   }
   const bool ok = in_range && len <= a.rs.heavy_threshold;
@@ -679,6 +690,11 @@ __global__ void __launch_bounds__(kBlock) k_step_sell(StepArgs a, SellSet S, int
       if (jv[u] >= 0) acc = fma(av[u], xv[u], acc);
   }
 
+  if (PDHG_SELL_LATE && ok) {
+    o1 = a.cb[rl];
+    o2 = a.x[rl];
+    o3 = a.xbar[rl];
+  }
   if (ok) {
     const int row = (int)rl;
     if (PRIMAL) bcast(P, 0, row, primal_epi_pre(row, acc, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
