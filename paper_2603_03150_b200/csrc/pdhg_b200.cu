@@ -541,11 +541,13 @@ struct StepArgs {
 // Occupancy: the V >= 16 form (config 4's dual step) is latency-bound and
 // fits 32 registers -- 8 blocks (64 warps) per SM -- once the epilogue
 // operands are loaded after the row loop: 0.975 -> 0.936 ms.  The pipelined
-// V <= 8 form keeps its registers (reduce-scatter partials): 4 blocks.
+// V = 4, 8 forms keep their registers (reduce-scatter partials): 4 blocks.
 // (Left to ptxas, an explicit minBlocks of 1 gave 56 / 80 registers and a
 // 23 % slower dual step; profiles/r01_pipeline.md.)
+// V <= 2 (short rows: config 1) fits 40 registers at 6 blocks: one config-1
+// iteration 24.6 -> 20.6 us; V = 4, 8 spill below 64 registers.
 template <int V>
-constexpr int step_min_blocks() { return V >= 16 ? 8 : 4; }
+constexpr int step_min_blocks() { return V >= 16 ? 8 : (V <= 2 ? 6 : 4); }
 
 template <int V, bool PRIMAL, bool PEERS = false>
 __global__ void __launch_bounds__(kBlock, step_min_blocks<V>()) k_step(StepArgs a, int j_in_period) {
