@@ -69,7 +69,10 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
-constexpr int kCheckBlocks = 148 * 4;  // fixed grid => fixed reduction order
+#ifndef PDHG_CHECK_BPS
+#define PDHG_CHECK_BPS 4
+#endif
+constexpr int kCheckBlocks = 148 * PDHG_CHECK_BPS;  // fixed grid => fixed reduction order
 constexpr int kMaxQ = 2 * PDHG_NQ;
 
 // ---------------------------------------------------------------- device utils
@@ -957,7 +960,7 @@ struct CheckPts {
 
 // Per-point primal-side terms over rows of A: r_p = b - A x (lp_core.py:436).
 template <int V, int NP>
-__global__ void __launch_bounds__(kBlock) k_check_primal(RowSet rs, const double* __restrict__ b,
+__global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_primal(RowSet rs, const double* __restrict__ b,
                                                          CheckPts pts, double* __restrict__ partials) {
   __shared__ double red[kWarps];
   double rp2[NP], rpmax[NP], by[NP];
@@ -1020,7 +1023,7 @@ __global__ void __launch_bounds__(kBlock) k_check_primal(RowSet rs, const double
 
 // Per-point dual-side terms over rows of A' (lp_core.py:437,441,443; pdhg.py:114).
 template <int V, int NP>
-__global__ void __launch_bounds__(kBlock) k_check_dual(RowSet rs, const double* __restrict__ c,
+__global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual(RowSet rs, const double* __restrict__ c,
                                                        CheckPts pts, double* __restrict__ partials) {
   __shared__ double red[kWarps];
   double rd2[NP], rdmax[NP], cx[NP], xz[NP];

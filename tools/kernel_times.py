@@ -15,6 +15,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--lib", default=None)
     ap.add_argument("--opts", default="{}")
+    ap.add_argument("--full4", action="store_true")
     args = ap.parse_args()
     if args.lib:
         from paper_2603_03150_b200 import _native
@@ -31,6 +32,8 @@ def main():
     p, _ = eng.to_standard_form(config3_general(1.0))
     models["config3"] = p
     models["config4_s0.05"] = config4(0.05)
+    if "--full4" in sys.argv:
+        models["config4"] = config4(1.0)
     for name, m in models.items():
         dev = eng.DeviceLp(m.A, m.b, m.c, eng.GpuOptions(cache_layout=False, **kw))
         dev.reset()
@@ -39,6 +42,18 @@ def main():
                "primal_us": 1e3 * dev.time_kernel(0, 50, 1e-3, 1e-3),
                "dual_us": 1e3 * dev.time_kernel(1, 50, 1e-3, 1e-3),
                "iter_us": 1e3 * dev.time_kernel(2, 50, 1e-3, 1e-3)}
+        import time
+
+        import torch
+
+        from paper_2603_03150_b200 import _native as N
+
+        dev.check(N.PT_CUR, N.PT_AVG)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(10):
+            dev.check(N.PT_CUR, N.PT_AVG)
+        row["check_us"] = 1e6 * (time.perf_counter() - t) / 10
         print(json.dumps(row), flush=True)
         del dev
 
