@@ -131,10 +131,11 @@ typedef struct pdhg_problem {
   /* Optional sliced-ELL layouts for the step kernels (NULL = CSR-vector). */
   const pdhg_sell* a_sell;   /* dual step (rows of A)    */
   const pdhg_sell* at_sell;  /* primal step (rows of A') */
-  /* 1: run each period as one cooperative (persistent) kernel with grid
-   * barriers between half steps instead of a graph of 2 kernels per
-   * iteration; 2: as one single-block kernel (tiny models); CSR layouts,
-   * unsharded only (ignored otherwise). */
+  /* Period mode.  0: a CUDA graph of 2 kernels per iteration (captured once
+   * per period length); 1: one cooperative (persistent) kernel with grid
+   * barriers between half steps; 2: one single-block kernel (tiny models);
+   * 3: direct stream launches, no graph.  1 and 2 need CSR layouts and an
+   * unsharded context (ignored otherwise). */
   int32_t persistent;
 } pdhg_problem;
 

@@ -1260,6 +1260,7 @@ struct pdhg_ctx {
   int l2_mask;         // bit0: window on y for the primal step, bit1: on xe for the dual step
   int coop_grid;       // > 0: periods run as one cooperative k_period launch of this many blocks
   bool tiny;           // periods run as one single-block k_period_tiny launch
+  bool period_direct;  // periods launched kernel by kernel instead of as a graph
   double* const* peers[2];  // fused all-gather targets: [0] xe (primal), [1] y (dual)
   int npeers[2];
 };
@@ -1359,6 +1360,42 @@ StepArgs step_args(const pdhg_ctx* c, bool primal) {
   a.nsplit = 1;
   a.partial = nullptr;
   return a;
+}
+
+int launch_period_persistent(pdhg_ctx* c, int iters);
+int launch_step(pdhg_ctx* c, bool primal, int j);
+
+// The iterations of one period: a cooperative / single-block kernel, direct
+// stream launches (period_direct), or a CUDA graph captured once per length.
+int launch_period(pdhg_ctx* c, int iters) {
+  if (iters <= 0) return 0;
+  if (c->coop_grid > 0) return launch_period_persistent(c, iters);
+  int rc = 0;
+  if (c->period_direct) {
+    for (int j = 0; j < iters && !rc; ++j) {
+      rc = launch_step(c, true, j);
+      if (!rc) rc = launch_step(c, false, j);
+    }
+    return rc;
+  }
+  auto it = c->graphs.find(iters);
+  if (it == c->graphs.end()) {
+    cudaGraph_t g;
+    CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    for (int j = 0; j < iters && !rc; ++j) {
+      rc = launch_step(c, true, j);
+      if (!rc) rc = launch_step(c, false, j);
+    }
+    cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+    if (rc) return rc;
+    if (ce != cudaSuccess) return fail(PDHG_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
+    cudaGraphExec_t ex;
+    CUDA_TRY(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    it = c->graphs.emplace(iters, ex).first;
+  }
+  CUDA_TRY(cudaGraphLaunch(it->second, c->stream));
+  return 0;
 }
 
 int launch_period_persistent(pdhg_ctx* c, int iters) {
@@ -1478,6 +1515,7 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->P = cv.take<StepParams>(1);
   c->coop_grid = 0;
   c->tiny = false;
+  c->period_direct = prob->persistent == 3;
   if (prob->persistent == 2 && !prob->a_sell && !prob->at_sell && !prob->a_psr && !prob->at_psr &&
       prob->a_nsplit <= 1 && mf == prob->m && nf == prob->n) {
     c->tiny = true;
@@ -1624,28 +1662,9 @@ int pdhg_run_period(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_over_o
   h.iter0 = iter0;
   h.fail_iter = LLONG_MAX;
   CUDA_TRY(cudaMemcpyAsync(c->P, c->P_host, sizeof(StepParams), cudaMemcpyHostToDevice, c->stream));
-  if (iters > 0 && c->coop_grid > 0) {
-    int rc = launch_period_persistent(c, iters);
+  {
+    int rc = launch_period(c, iters);
     if (rc) return rc;
-  } else if (iters > 0) {
-    auto it = c->graphs.find(iters);
-    if (it == c->graphs.end()) {
-      cudaGraph_t g;
-      CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-      int rc = 0;
-      for (int j = 0; j < iters && !rc; ++j) {
-        rc = launch_step(c, true, j);
-        if (!rc) rc = launch_step(c, false, j);
-      }
-      cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
-      if (rc) return rc;
-      if (ce != cudaSuccess) return fail(PDHG_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
-      cudaGraphExec_t ex;
-      CUDA_TRY(cudaGraphInstantiate(&ex, g, 0));
-      cudaGraphDestroy(g);
-      it = c->graphs.emplace(iters, ex).first;
-    }
-    CUDA_TRY(cudaGraphLaunch(it->second, c->stream));
   }
   CUDA_TRY(cudaMemcpyAsync(&c->P_host->fail_iter, &c->P->fail_iter, sizeof(long long),
                            cudaMemcpyDeviceToHost, c->stream));
@@ -1671,28 +1690,7 @@ int pdhg_run_period_check(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_
   h.iter0 = iter0;
   h.fail_iter = LLONG_MAX;
   CUDA_TRY(cudaMemcpyAsync(c->P, c->P_host, sizeof(StepParams), cudaMemcpyHostToDevice, c->stream));
-  int rc = 0;
-  if (iters > 0 && c->coop_grid > 0) {
-    rc = launch_period_persistent(c, iters);
-  } else if (iters > 0) {
-    auto it = c->graphs.find(iters);
-    if (it == c->graphs.end()) {
-      cudaGraph_t g;
-      CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-      for (int j = 0; j < iters && !rc; ++j) {
-        rc = launch_step(c, true, j);
-        if (!rc) rc = launch_step(c, false, j);
-      }
-      cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
-      if (rc) return rc;
-      if (ce != cudaSuccess) return fail(PDHG_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ce));
-      cudaGraphExec_t ex;
-      CUDA_TRY(cudaGraphInstantiate(&ex, g, 0));
-      cudaGraphDestroy(g);
-      it = c->graphs.emplace(iters, ex).first;
-    }
-    CUDA_TRY(cudaGraphLaunch(it->second, c->stream));
-  }
+  int rc = launch_period(c, iters);
   if (rc) return rc;
   if (npts > 0) {
     if ((rc = pdhg_check_device(c, npts, specs))) return rc;

@@ -87,6 +87,7 @@ class GpuOptions:
     l2_persist: int = 0
     dual_split: int = 1
     persistent: str = "off"
+    graphs: bool = True
     tiny_max_nnz: int = 200_000
     tiny_max_rows: int = 65_536
     sell: str = "auto"
@@ -257,7 +258,7 @@ class DeviceLp:
         p.b, p.c = self.b.data_ptr(), self.c.data_ptr()
         p.a_lanes, p.at_lanes, p.heavy_threshold = self.a_lanes, self.at_lanes, H
         p.at_heavy_threshold = Ht
-        p.persistent = {"on": 1, "tiny": 2}.get(self.persistent_mode, 0)
+        p.persistent = {"on": 1, "tiny": 2}.get(self.persistent_mode, 0 if opts.graphs else 3)
         p.a_sell = C.pointer(self._sell["A"][0]) if self._sell["A"] else None
         p.at_sell = C.pointer(self._sell["At"][0]) if self._sell["At"] else None
         p.a_n_heavy, p.at_n_heavy = self.a_heavy.numel(), self.at_heavy.numel()

@@ -41,6 +41,8 @@ def main():
         "sell": dict(psr="off", sell="on"),
         "sell_unsorted": dict(psr="off", sell="on", sell_sort=False),
         "auto": dict(),
+        "direct": dict(graphs=False),
+        "auto_sorted": dict(sell_sort=True),
         "persist": dict(psr="off", sell="off", persistent="on"),
         "csr_a8": dict(psr="off", sell="off", a_lanes=8),
         "csr_at16": dict(psr="off", sell="off", at_lanes=16),
@@ -63,6 +65,7 @@ def main():
         tp = dev.time_kernel(0, args.reps, 1e-3, 1e-3)
         td = dev.time_kernel(1, args.reps, 1e-3, 1e-3)
         talt = dev.time_kernel(2, args.reps, 1e-3, 1e-3)
+        talt192 = dev.time_kernel(2, 192, 1e-3, 1e-3)   # as long as the 3 graph periods below
         # alternating primal/dual as in a real period (graph of 64 iterations)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         dev.run_period(64, 0, 1e-3, 1e-3, 0.0)
@@ -72,7 +75,7 @@ def main():
         ev1.record(dev.stream)
         torch.cuda.synchronize()
         per_iter = ev0.elapsed_time(ev1) / (3 * 64)
-        out[name] = {"build_s": build, "primal_ms": tp, "dual_ms": td, "iter_ms": per_iter, "alt_ms": talt,
+        out[name] = {"build_s": build, "primal_ms": tp, "dual_ms": td, "iter_ms": per_iter, "alt_ms": talt, "alt192_ms": talt192,
                      "primal_gbs": ab["primal"] / tp / 1e6, "dual_gbs": ab["dual"] / td / 1e6,
                      "psr": dev.psr_info, "sell": dev.sell_info}
         print(name, json.dumps(out[name]), flush=True)
