@@ -60,9 +60,11 @@ class GpuOptions:
                      entries (config 4's A': primal step 0.862 -> 0.820 ms; at 1.5-20M
                      entries it measured neutral to 50 % slower).  Skewed rows (config 4's
                      A: 4x padding) stay on CSR-vector.
-    sell_sort:       order each slice's rows by length (lanes active in a round form a
-                     prefix); measured neutral on config 4, slower on config 3's 1-3
-                     entry rows (one more dependent load per warp), so off.
+    sell_sort:       "auto" | "on" | "off" -- order each slice's rows by length (lanes
+                     active in a round form a prefix, so fetched sectors are full):
+                     config 4's A' reads 3.55 instead of 3.85 GB per primal step (period
+                     ~0.5 % faster); config 3's 1-3 entry rows lose to the extra dependent
+                     load per warp, so auto sorts operators with mean row length >= 12.
     persistent:      "off" | "on" | "tiny" | "auto" -- "off" (default): a CUDA graph of two
                      kernels per iteration; "on": each period as one cooperative kernel
                      (grid barriers between half steps); "tiny": each period as one
@@ -94,7 +96,7 @@ class GpuOptions:
     sell_max_pad: float = 1.6
     sell_max_mean: float = 12.0
     sell_min_nnz: int = 50_000_000
-    sell_sort: bool = False
+    sell_sort: str = "auto"
 
 
 def auto_lanes(nnz: int, rows: int) -> int:
@@ -304,7 +306,8 @@ class DeviceLp:
         scol = torch.empty(max(slots.value, 1), dtype=torch.int32, device=dev)
         sval = torch.empty(max(slots.value, 1), dtype=torch.float64, device=dev)
         perm = inv = None
-        if opts.sell_sort:
+        sort = opts.sell_sort if isinstance(opts.sell_sort, str) else ("on" if opts.sell_sort else "off")
+        if sort == "on" or (sort == "auto" and nnz / rows >= 12):
             perm = torch.empty(ns * 32, dtype=torch.uint8, device=dev)
             inv = torch.empty(ns * 32, dtype=torch.uint8, device=dev)
             N.check(lib.pdhg_sell_sort(rows, ptr.data_ptr(), int(H), perm.data_ptr(), inv.data_ptr(), sptr_))

@@ -33,7 +33,8 @@ def eng():
 # with every entry staged in shared-memory panels or gathered from global memory
 LAYOUTS = {
     "csr": dict(psr="off", sell="off", persistent="off"),
-    "sell": dict(psr="off", sell="on", persistent="off"),
+    "sell": dict(psr="off", sell="on", sell_sort="off", persistent="off"),
+    "sell_sorted": dict(psr="off", sell="on", sell_sort="on", persistent="off"),
     "persistent": dict(psr="off", sell="off", persistent="on"),
     "tiny": dict(psr="off", sell="off", persistent="tiny"),
     "csr_split2": dict(psr="off", sell="off", persistent="off", dual_split=2),

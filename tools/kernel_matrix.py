@@ -39,10 +39,11 @@ def main():
     variants = {
         "csr": dict(psr="off", sell="off", l2_persist=0),
         "sell": dict(psr="off", sell="on"),
-        "sell_unsorted": dict(psr="off", sell="on", sell_sort=False),
+        "sell_unsorted": dict(psr="off", sell="on", sell_sort="off"),
         "auto": dict(),
         "direct": dict(graphs=False),
-        "auto_sorted": dict(sell_sort=True),
+        "auto_sorted": dict(sell_sort="on"),
+        "auto_unsorted": dict(sell_sort="off"),
         "persist": dict(psr="off", sell="off", persistent="on"),
         "csr_a8": dict(psr="off", sell="off", a_lanes=8),
         "csr_at16": dict(psr="off", sell="off", at_lanes=16),
