@@ -281,19 +281,24 @@ def run_ours(args):
     peaks = _peaks()
     peak = peaks["hbm_gbs"] if peaks else 6650.0
     achieved = ab[top] / (tk[top] * 1e-3) / 1e9
-    traffic = None
+    traffic = units = None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(top)
+            tj = json.loads(tf.read_text())
+            traffic, units = tj.get(top), tj.get(f"{top}_units")
         except Exception:
-            traffic = None
+            traffic = units = None
     iter_ms = ms_per_step / CHECK_EVERY
     roofline = {"bound": "hbm", "kernel": f"k_step<{'primal' if top == 'primal' else 'dual'}>",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
                 "kernels_ms": tk, "algorithmic_bytes": ab,
+                # the units that bind (ncu capture, profiles/traffic.json): every gather of the
+                # 40/80 MB vector is a 32 B L2 sector, so L1TEX / L2-slice throughput, not DRAM,
+                # caps the step kernels
+                "binding_units_pct_ncu": units,
                 "iteration_gbs": (ab["iter"] + ab["check"] / CHECK_EVERY) / (iter_ms * 1e-3) / 1e9}
     del dev, kdev
     torch.cuda.empty_cache()
