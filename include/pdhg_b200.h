@@ -222,6 +222,7 @@ int pdhg_fetch(pdhg_ctx* ctx, int32_t spec, double* x_host, double* y_host, doub
 #define PDHG_VEC_YBEST 9
 #define PDHG_VEC_TM1 10
 #define PDHG_VEC_SCALARS 11
+#define PDHG_VEC_FAILWORD 12  /* the int64 first-failure iteration word of this context */
 void* pdhg_vector(pdhg_ctx* ctx, int32_t which);
 
 /* z = max(0, c - A'y) for this shard's rows of A' into z_slice (device). */
@@ -240,7 +241,10 @@ int pdhg_half_step(pdhg_ctx* ctx, int32_t primal, int32_t j);
  * npeers pointers to the peers' full xe / y vectors -- other shards in this
  * process, or NVLink peer / symmetric-memory addresses).  npeers = 0 turns
  * it off.  The caller orders the next half step after every peer's writes
- * (stream order on one device; a cross-GPU barrier otherwise). */
+ * (stream order on one device; a cross-GPU barrier otherwise).
+ * which = 2: peers_dev lists the other shards' fail words
+ * (pdhg_vector(peer, PDHG_VEC_FAILWORD)); a non-finite iterate is then
+ * recorded in all of them, so every shard stops at that iteration. */
 int pdhg_set_peers(pdhg_ctx* ctx, int32_t which, const double* const* peers_dev, int32_t npeers);
 int pdhg_fail_iter(pdhg_ctx* ctx, int64_t* fail_iter_out);
 

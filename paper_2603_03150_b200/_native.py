@@ -36,7 +36,8 @@ EXPORTS = (
 )
 
 VEC = {name: i for i, name in enumerate(
-    ("x", "xe", "xbar", "xbest", "zbest", "tn1", "tn2", "y", "ybar", "ybest", "tm1", "scalars"))}
+    ("x", "xe", "xbar", "xbest", "zbest", "tn1", "tn2", "y", "ybar", "ybest", "tm1", "scalars",
+     "failword"))}
 
 
 class Psr(C.Structure):

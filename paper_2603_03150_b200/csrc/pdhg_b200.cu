@@ -450,6 +450,10 @@ struct StepParams {
   long long iter0; // state.iterations at period start
   long long fail_iter;  // first iteration with a non-finite iterate (LLONG_MAX = none)
   Peers peers[2];  // fused all-gather targets: [0] xe (primal step), [1] y (dual step)
+  // other shards' fail words (their StepParams::fail_iter): a non-finite
+  // iterate stops every shard at the same iteration, as on one GPU
+  unsigned long long* const* fail_peers;
+  int nfail;
 };
 
 // The peer list lives in device memory (StepParams) rather than in the kernel
@@ -463,6 +467,12 @@ __device__ __noinline__ void bcast_peers(const StepParams* P, int k, int row, do
 
 __device__ __forceinline__ void bcast(const StepParams* P, int k, int row, double v) {
   if (P->peers[k].n) bcast_peers(P, k, row, v);  // out of line: no registers held in the hot loop
+}
+
+// first non-finite iterate: record it here and in every peer shard's fail word
+__device__ __forceinline__ void fail_at(StepParams* P, long long iter) {
+  atomicMin(&P->fail_iter, iter);
+  for (int q = 0; q < P->nfail; ++q) atomicMin(reinterpret_cast<long long*>(P->fail_peers[q]), iter);
 }
 
 // k_step's form: the peer stores are compiled in only for the fused-all-gather
@@ -487,7 +497,7 @@ __device__ __forceinline__ double primal_epi(int j, double aty, const double* __
   const double xev = __dsub_rn(__dmul_rn(2.0, xn), xj);       // 2 x+ - x
   xe[j] = xev;
   xbar[j] = __dadd_rn(xb, __ddiv_rn(__dsub_rn(xn, xb), w));    // avg += (x+ - avg)/w
-  if (!finite(xn)) atomicMin(&P->fail_iter, iter);
+  if (!finite(xn)) fail_at(P, iter);
   return xev;
 }
 
@@ -499,7 +509,7 @@ __device__ __forceinline__ double dual_epi(int i, double ax, const double* __res
   const double yb = ybar[i];
   y[i] = yn;
   ybar[i] = __dadd_rn(yb, __ddiv_rn(__dsub_rn(yn, yb), w));
-  if (!finite(yn)) atomicMin(&P->fail_iter, iter);
+  if (!finite(yn)) fail_at(P, iter);
   return yn;
 }
 
@@ -514,7 +524,7 @@ __device__ __forceinline__ double primal_epi_pre(int j, double aty, double cj, d
   const double xev = __dsub_rn(__dmul_rn(2.0, xn), xj);
   xe[j] = xev;
   xbar[j] = __dadd_rn(xb, __ddiv_rn(__dsub_rn(xn, xb), w));
-  if (!finite(xn)) atomicMin(&P->fail_iter, iter);
+  if (!finite(xn)) fail_at(P, iter);
   return xev;
 }
 
@@ -524,7 +534,7 @@ __device__ __forceinline__ double dual_epi_pre(int i, double ax, double bi, doub
   const double yn = __dadd_rn(yi, __dmul_rn(sigma_w, __dsub_rn(bi, ax)));
   y[i] = yn;
   ybar[i] = __dadd_rn(yb, __ddiv_rn(__dsub_rn(yn, yb), w));
-  if (!finite(yn)) atomicMin(&P->fail_iter, iter);
+  if (!finite(yn)) fail_at(P, iter);
   return yn;
 }
 
@@ -1820,6 +1830,7 @@ void* pdhg_vector(pdhg_ctx* c, int32_t which) {
     case PDHG_VEC_YBEST: return c->ybest;
     case PDHG_VEC_TM1: return c->tm1;
     case PDHG_VEC_SCALARS: return c->scalars;
+    case PDHG_VEC_FAILWORD: return &c->P->fail_iter;
     default: fail(PDHG_ERR_ARG, "unknown vector id"); return nullptr;
   }
 }
@@ -1848,8 +1859,16 @@ int pdhg_half_step(pdhg_ctx* c, int32_t primal, int32_t j) {
 }
 
 int pdhg_set_peers(pdhg_ctx* c, int32_t which, const double* const* peers_dev, int32_t npeers) {
-  if (!c || which < 0 || which > 1 || npeers < 0 || (npeers > 0 && !peers_dev))
+  if (!c || which < 0 || which > 2 || npeers < 0 || (npeers > 0 && !peers_dev))
     return fail(PDHG_ERR_ARG, "set_peers: bad argument");
+  if (which == 2) {  // peers' fail words (pdhg_vector(peer, PDHG_VEC_FAILWORD))
+    c->P_host->fail_peers = reinterpret_cast<unsigned long long* const*>(const_cast<double**>(peers_dev));
+    c->P_host->nfail = npeers;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->P, c->P_host, sizeof(StepParams), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return 0;
+  }
   c->peers[which] = const_cast<double* const*>(peers_dev);
   c->npeers[which] = npeers;
   c->P_host->peers[which] = Peers{c->peers[which], npeers, which == 0 ? c->xo : c->yo};

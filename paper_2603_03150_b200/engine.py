@@ -447,11 +447,17 @@ class DeviceLp:
 
     def set_peers(self, which: int, ptrs):
         """Fused all-gather targets (pdhg_set_peers): which 0 = xe (primal step),
-        1 = y (dual step); ptrs = int64 device tensor of peer vector bases (kept alive)."""
+        1 = y (dual step), 2 = the peers' fail words; ptrs = int64 device tensor of
+        peer bases (kept alive)."""
         self._peers = getattr(self, "_peers", {})
         self._peers[which] = ptrs
         n = 0 if ptrs is None else int(ptrs.numel())
         N.check(self.lib.pdhg_set_peers(self.ctx, int(which), ptrs.data_ptr() if n else None, n))
+
+    def connect_fail(self, others):
+        """Shards on this device: record a non-finite iterate in their fail words too."""
+        ptrs = [o.vec_ptr("failword") for o in others]
+        self.set_peers(2, self._torch.tensor(ptrs, dtype=self._torch.int64, device=self.device))
 
     def set_step(self, iter0: int, tau_w: float, sigma_w: float, w0: float):
         N.check(self.lib.pdhg_set_step(self.ctx, int(iter0), float(tau_w), float(sigma_w), float(w0)))

@@ -141,6 +141,15 @@ class LoopbackComm:
                 ptrs = [o.vec_ptr(name) for h, o in enumerate(shards) if h != g]
                 s.set_peers(which, torch.tensor(ptrs, dtype=torch.int64, device=s.device))
 
+    def connect_fail(self, shards):
+        """A non-finite iterate on any shard stops every shard at that iteration
+        (as on one GPU): each shard's epilogues also record it in the others'
+        fail words."""
+        for g, s in enumerate(shards):
+            others = [o for h, o in enumerate(shards) if h != g]
+            if others:
+                s.connect_fail(others)
+
     def barrier(self, shards):
         pass   # one stream: stream order is the barrier
 
@@ -195,10 +204,14 @@ class TorchComm:
         (s,) = shards
         self.symm = symm_mem.rendezvous(s.ws, self.group or self.dist.group.WORLD)
         base = s.ws.data_ptr()
-        for which, name in ((0, "xe"), (1, "y")):
+        for which, name in ((0, "xe"), (1, "y"), (2, "failword")):
             off = s.vec_ptr(name) - base
             ptrs = [int(self.symm.buffer_ptrs[r]) + off for r in range(self.world) if r != self.rank]
-            s.set_peers(which, torch.tensor(ptrs, dtype=torch.int64, device=s.device))
+            if which < 2 or ptrs:
+                s.set_peers(which, torch.tensor(ptrs, dtype=torch.int64, device=s.device))
+
+    def connect_fail(self, shards):
+        pass   # done in connect_peers (the fail words live in the symmetric workspace)
 
     def barrier(self, shards):
         """Stream-ordered cross-GPU barrier: the next half step starts after every
@@ -363,6 +376,9 @@ class ShardedDevice:
     def _period_body(self, iters: int):
         """The kernels and all-gathers of one period, queued on the shards' stream."""
         fused = getattr(self.comm, "fused", False)
+        if fused and iters > 0:         # every rank has reset its fail word (set_step)
+            with self._on_stream():
+                self.comm.barrier(self.shards)
         for j in range(iters):
             for s in self.shards:
                 s.half_step(True, j)
@@ -463,6 +479,8 @@ def build_sharded(p, G: int, comm_kind: str = "loopback", opts=None, group=None)
         raise ValueError(comm_kind)
     if comm.fused:
         comm.connect_peers(shards)
+    if hasattr(comm, "connect_fail"):
+        comm.connect_fail(shards)   # loopback: same device; torch_peer: NVLink atomics
     return ShardedDevice(plan, shards, comm)
 
 

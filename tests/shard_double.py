@@ -34,6 +34,7 @@ class NumpyShard:
         self.v["scalars"] = np.zeros(64)
         self.params = None
         self.fail = -1
+        self.fail_peers = []
 
     def vec(self, name):
         return torch.from_numpy(self.v[name])
@@ -72,8 +73,13 @@ class NumpyShard:
             self.v["y"][ys] = yn
             self.v["ybar"][ys] += (yn - self.v["ybar"][ys]) / w
             bad = not np.all(np.isfinite(yn))
-        if bad and (self.fail < 0 or it < self.fail):
-            self.fail = it
+        if bad:
+            for sh in [self] + self.fail_peers:   # pdhg_set_peers(which = 2)
+                if sh.fail < 0 or it < sh.fail:
+                    sh.fail = it
+
+    def connect_fail(self, others):
+        self.fail_peers = list(others)
 
     def fail_iter(self):
         return self.fail

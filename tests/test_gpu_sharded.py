@@ -167,3 +167,40 @@ def test_torch_peer_world1(eng):
         assert st.iterations == int(r["iterations"]) and st.restarts == int(r["restarts"])
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("G", [2, 3])
+@pytest.mark.parametrize("kind", ["loopback", "loopback_fused"])
+def test_failure_stops_every_shard(eng, G, kind):
+    """Non-finite iterate on the last shard only (iteration 335, mid-period):
+    every shard's fail word reads 335 (pdhg_set_peers which = 2) and the run
+    returns the reference's failure exit."""
+    from test_sharded_cpu import failing_block_model
+
+    from paper_2603_03150_b200.engine import run_on_device
+    from paper_2603_03150_b200.sharded import build_sharded
+
+    p = failing_block_model()
+    T = eng.types()
+    params = T.PdhgParams(eps_rel=1e-6, max_kkt_passes=500)
+    dev = build_sharded(p, G, comm_kind=kind)
+    pt, st = run_on_device(dev, p, params)
+    opt, ost = oracle.run_pdhg(p, oracle.PdhgParams(eps_rel=1e-6, max_kkt_passes=500))
+    assert ost.status.value == "NumericalFailure" and ost.iterations == 335
+    assert st.status.value == ost.status.value and st.iterations == ost.iterations
+    assert [s.fail_iter() for s in dev.shards] == [335] * G
+    np.testing.assert_allclose(pt.x, opt.x, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(pt.y, opt.y, rtol=1e-9, atol=1e-12)
+
+
+def test_failure_single_gpu(eng):
+    """The same failure exit on one GPU (the kernels' atomicMin fail word)."""
+    from test_sharded_cpu import failing_block_model
+
+    p = failing_block_model()
+    T = eng.types()
+    pt, st = eng.run_pdhg(p, T.PdhgParams(eps_rel=1e-6, max_kkt_passes=500))
+    opt, ost = oracle.run_pdhg(p, oracle.PdhgParams(eps_rel=1e-6, max_kkt_passes=500))
+    assert st.status.value == "NumericalFailure" and st.iterations == ost.iterations == 335
+    np.testing.assert_allclose(pt.x, opt.x, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(pt.y, opt.y, rtol=1e-9, atol=1e-12)

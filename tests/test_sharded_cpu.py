@@ -153,3 +153,41 @@ def test_loopback_numpy_three_shards_match_oracle():
     opt, ost = oracle.run_pdhg(Model(gm.A, gm.b, gm.c), oracle.PdhgParams(eps_rel=1e-4))
     assert st.iterations == ost.iterations and st.restarts == ost.restarts
     np.testing.assert_allclose(pt.x, opt.x, rtol=1e-9, atol=1e-12)
+
+
+def failing_block_model():
+    """config0_s0 beside an unbounded 2-column block (x1 = x2, c = -1e306):
+    the last shard's x grows until it overflows at iteration 335 -- inside a
+    64-iteration period -- while the other shards' iterates stay finite."""
+    import scipy.sparse as sp
+
+    gm = load_golden("config0_s0")
+    A = sp.block_diag([gm.A, sp.csr_matrix(np.array([[1.0, -1.0]]))], format="csr")
+    b = np.concatenate([gm.b, [0.0]])
+    c = np.concatenate([gm.c, [-1e306, -1e306]])
+    return Model(A, b, c)
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_loopback_failure_stops_every_shard(G):
+    """A non-finite iterate on one shard stops all shards at that iteration
+    (connect_fail), so the sharded run returns the single-process failure point."""
+    from shard_double import NumpyShard
+
+    from paper_2603_03150_b200 import engine
+    from paper_2603_03150_b200.lp_types import resolve
+
+    p = failing_block_model()
+    plan = ShardPlan(p.A, G)
+    shards = [NumpyShard(plan.block(g, p.A, p.b, p.c)) for g in range(G)]
+    comm = LoopbackComm(plan)
+    comm.connect_fail(shards)
+    dev = ShardedDevice(plan, shards, comm)
+    T = resolve()
+    pt, st = engine.run_on_device(dev, p, T.PdhgParams(eps_rel=1e-6, max_kkt_passes=500))
+    opt, ost = oracle.run_pdhg(p, oracle.PdhgParams(eps_rel=1e-6, max_kkt_passes=500))
+    assert ost.status.value == "NumericalFailure" and ost.iterations == 335
+    assert st.status.value == ost.status.value and st.iterations == ost.iterations
+    np.testing.assert_allclose(pt.x, opt.x, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(pt.y, opt.y, rtol=1e-9, atol=1e-12)
+    assert [sh.fail for sh in shards] == [335] * G   # every shard stopped there
