@@ -342,7 +342,7 @@ def run_ours(args):
         pt2, st2 = eng.run_pdhg(scaled, T.PdhgParams(eps_rel=1e-4, time_limit_s=args.ttk_limit), gpu=opts)
         out = {"status": st2.status.value, "iterations": st2.iterations, "restarts": st2.restarts,
                "pdhg_wall_s": st2.wall_seconds, "ruiz_s": t_ruiz, "ruiz_passes": info.applied_iterations,
-               "total_s": t_ruiz + st2.wall_seconds,
+               "total_s": t_ruiz + st2.wall_seconds, "ruiz_phases_s": dict(eng.ruiz.last_timings),
                "note": "device Ruiz (bit-identical to transform.py:35-77) + run_pdhg to eps_rel=1e-4"}
         if args.ttk_unscaled:
             pt3, st3 = eng.run_pdhg(inst, T.PdhgParams(eps_rel=1e-4, time_limit_s=args.ttk_limit), gpu=opts)

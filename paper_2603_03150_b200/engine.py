@@ -29,6 +29,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
+from . import hostio
 from .lp_types import resolve
 
 _WEIGHT_CLIP = (1e-4, 1e4)  # pdhg.py:28
@@ -181,7 +182,7 @@ class DeviceLp:
         with torch.cuda.device(dev):
             self.stream = stream if stream is not None else torch.cuda.Stream(dev)
             with torch.cuda.stream(self.stream):
-                t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
+                t = lambda a, dt: hostio.h2d(a, dt, dev)
                 if device_arrays is not None:
                     self.a_ptr, self.a_col, self.a_val = device_arrays
                 else:

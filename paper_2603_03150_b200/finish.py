@@ -29,6 +29,7 @@ import weakref
 import numpy as np
 
 from . import _native as N
+from . import hostio
 from .lp_types import resolve
 
 _lock = threading.Lock()
@@ -59,7 +60,7 @@ class _DevCsr:
         A = _as_csr(A)
         self.m, self.n = A.shape
         self.nnz = int(A.nnz)
-        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
+        t = lambda a, dt: hostio.h2d(a, dt, dev)
         with torch.cuda.stream(stream):
             if arrays is not None:
                 self.ptr, self.col, self.val = arrays
@@ -113,7 +114,7 @@ def _dev_csr(model, torch, dev, stream) -> _DevCsr:
 
 
 def _up(torch, dev, a, dt=np.float64):
-    return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
+    return hostio.h2d(a, dt, dev)
 
 
 def unscale_point(s, pt_scaled, *, gpu=None):
@@ -130,7 +131,7 @@ def unscale_point(s, pt_scaled, *, gpu=None):
         N.check(lib.pdhg_unscale_point(n, m, rs.data_ptr(), cs.data_ptr(), xs.data_ptr(), ys.data_ptr(),
                                        zs.data_ptr(), x.data_ptr(), y.data_ptr(), z.data_ptr(),
                                        stream.cuda_stream))
-        out = (x[:n].cpu().numpy(), y[:m].cpu().numpy(), z[:n].cpu().numpy())
+        out = (hostio.d2h(x[:n]), hostio.d2h(y[:m]), hostio.d2h(z[:n]))
     return T.KktPoint(*out)
 
 
@@ -156,7 +157,7 @@ def restrict_point(g, fmap, pt, *, gpu=None):
         c = _up(torch, dev, g.c)
         z = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
         G.spmv(lib, True, y, c, z, stream)                               # z = c - A'y
-        out = (x[:n].cpu().numpy(), y_h, z[:n].cpu().numpy())
+        out = (hostio.d2h(x[:n]), y_h, hostio.d2h(z[:n]))
     return out
 
 
@@ -208,7 +209,7 @@ def lift_point(g, p, fmap, x, y, *, gpu=None):
         G, P = _dev_csr(g, torch, dev, stream), _dev_csr(p, torch, dev, stream)
         xs, ys, zs, _, _ = _lift_device(lib, torch, dev, stream, g, G, P, p, fmap, x, y)
         ns, ms = fmap.n_std, fmap.m_std
-        out = (xs[:ns].cpu().numpy(), ys[:ms].cpu().numpy(), zs[:ns].cpu().numpy())
+        out = (hostio.d2h(xs[:ns]), hostio.d2h(ys[:ms]), hostio.d2h(zs[:ns]))
     return T.KktPoint(*out)
 
 
@@ -329,7 +330,7 @@ def center_toward_target(x, z, mu: float, alpha_min: float, delta_max: float, *,
         N.check(lib.pdhg_center_toward_target(n, xd.data_ptr(), zd.data_ptr(), float(mu), float(alpha_min),
                                               float(delta_max), xo.data_ptr(), zo.data_ptr(),
                                               stream.cuda_stream))
-        return xo[:n].cpu().numpy(), zo[:n].cpu().numpy()
+        return hostio.d2h(xo[:n]), hostio.d2h(zo[:n])
 
 
 def centered_start(pt, params=None, *, gpu=None):

@@ -12,12 +12,17 @@ it again.
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass
 
 import numpy as np
 import scipy.sparse as sp
 
 from . import _native as N
+from . import hostio
+
+
+last_timings: dict = {}   # phase -> seconds of the latest ruiz_equilibrate call
 
 
 class _ScalingError(ValueError):
@@ -57,52 +62,75 @@ def ruiz_equilibrate(p, max_iters: int = 20, tol: float = 1e-2, *, gpu=None, reg
     from .engine import DeviceLp, GpuOptions, _as_csr, _cache_register
 
     ScalingError, ScalingInfo, StandardLp = _types()
+    tm = {}
+    t = time.perf_counter()
     A = _as_csr(p.A)
-    A = sp.csr_matrix((A.data.copy(), A.indices.copy(), A.indptr.copy()), shape=A.shape)
     m, n = A.shape
     row_nnz = np.diff(A.indptr)
     if (row_nnz == 0).any():
         i = int(np.nonzero(row_nnz == 0)[0][0])
         raise ScalingError(f"row {i} has no nonzero entries")
-    col_nnz = np.bincount(A.indices, minlength=n)
-    if (col_nnz == 0).any():
-        j = int(np.nonzero(col_nnz == 0)[0][0])
-        raise ScalingError(f"column {j} has no nonzero entries")
     if not torch.cuda.is_available():
         raise N.NativeError("ruiz_equilibrate needs a CUDA device; there is no CPU fallback")
+    # the scaled matrix gets its own index arrays (as the reference's product
+    # does): copied on a host thread while the device works
+    idx_copy = hostio._executor().submit(lambda: (A.indices.copy(), A.indptr.copy()))
+    tm["host_checks_s"] = time.perf_counter() - t
     lib = N.load()
     opts = gpu or GpuOptions()
     dev = torch.device("cuda", torch.cuda.current_device() if opts.device is None else opts.device)
     stream = torch.cuda.Stream(dev)
     with torch.cuda.device(dev), torch.cuda.stream(stream):
-        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
         from .stdform import device_csr
 
+        t = time.perf_counter()
         resident = device_csr(p)   # built on this device by stdform.to_standard_form
         if resident is not None and resident[2].device == dev:
             ptr, col = resident[0], resident[1]
             val = resident[2].clone()    # scaled in place; the standard-form copy stays intact
         else:
-            ptr, col, val = t(A.indptr, np.int32), t(A.indices, np.int32), t(A.data, np.float64)
+            ptr, col, val = (hostio.h2d(A.indptr, np.int32, dev), hostio.h2d(A.indices, np.int32, dev),
+                             hostio.h2d(A.data, np.float64, dev))
+        # structurally empty columns (transform.py:47-54; rows were checked above)
+        empty = torch.bincount(col[:A.nnz], minlength=n) == 0
+        if bool(empty.any()):
+            j = int(empty.nonzero()[0, 0])
+            idx_copy.result()
+            raise ScalingError(f"column {j} has no nonzero entries")
         rs = torch.empty(m, dtype=torch.float64, device=dev)
         cs = torch.empty(n, dtype=torch.float64, device=dev)
         tb = lib.pdhg_ruiz_tmp_bytes(m, n)
         tmp = torch.empty(tb, dtype=torch.uint8, device=dev)
+        stream.synchronize()
+        tm["upload_s"] = time.perf_counter() - t
+        t = time.perf_counter()
         applied = C.c_int32()
         lo, hi = 1.0 / (1.0 + tol), 1.0 + tol                      # transform.py:59
         N.check(lib.pdhg_ruiz(m, n, int(A.nnz), ptr.data_ptr(), col.data_ptr(), val.data_ptr(),
                               rs.data_ptr(), cs.data_ptr(), int(max_iters), lo, hi,
                               tmp.data_ptr(), tb, stream.cuda_stream, C.byref(applied)))
-        row_scale = rs.cpu().numpy()
-        col_scale = cs.cpu().numpy()
-        data = val.cpu().numpy()
-    S = sp.csr_matrix((data, A.indices, A.indptr), shape=A.shape)
+        stream.synchronize()
+        tm["passes_s"] = time.perf_counter() - t
+        t = time.perf_counter()
+        row_scale = hostio.d2h(rs)
+        col_scale = hostio.d2h(cs)
+        data = hostio.d2h(val)
+    tm["download_s"] = time.perf_counter() - t
+    t = time.perf_counter()
+    indices, indptr = idx_copy.result()
+    S = sp.csr_matrix((data, indices, indptr), shape=A.shape)
     b = row_scale * np.asarray(p.b, dtype=float)                    # transform.py:75
     c = col_scale * np.asarray(p.c, dtype=float)
     scaled = StandardLp(S, b, c)
     info = ScalingInfo(row_scale, col_scale, int(applied.value))
+    tm["assemble_s"] = time.perf_counter() - t
+    t = time.perf_counter()
     if register_layout:
         lay = DeviceLp(scaled.A, scaled.b, scaled.c, opts,
                        device_arrays=(ptr, col, val), stream=stream)
         _cache_register(scaled, lay, opts)
+        torch.cuda.synchronize(dev)
+    tm["layout_s"] = time.perf_counter() - t
+    last_timings.clear()
+    last_timings.update(tm)
     return scaled, info

@@ -19,6 +19,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from . import _native as N
+from . import hostio
 from .lp_types import resolve
 
 _SENSE_CODE = {"=": 0, "<=": 1, ">=": 2}   # PDHG_SENSE_* (lp_core.py:22-25)
@@ -121,7 +122,7 @@ def to_standard_form(g, *, gpu=None, register_device=True):
     codes = np.fromiter((_SENSE_CODE.get(s, 3) for s in senses), dtype=np.int8, count=m)
     stream = torch.cuda.Stream(dev)
     with torch.cuda.device(dev), torch.cuda.stream(stream):
-        t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
+        t = lambda a, dt: hostio.h2d(a, dt, dev)
         ptr, col, val = t(A.indptr, np.int32), t(A.indices, np.int32), t(A.data, np.float64)
         d_sense, d_lo, d_up = t(codes, np.int8), t(lower, np.float64), t(upper, np.float64)
         d_rhs, d_c = t(rhs, np.float64), t(c, np.float64)
@@ -149,7 +150,7 @@ def to_standard_form(g, *, gpu=None, register_device=True):
             b_std.data_ptr(), c_std.data_ptr(), shifts.data_ptr(), pos_col.data_ptr(),
             neg_col.data_ptr(), slack_of_row.data_ptr(), slack_coef.data_ptr(),
             bound_var.data_ptr()))
-        h = lambda x, k: x[:k].cpu().numpy()
+        h = lambda x, k: hostio.d2h(x[:k])
         A_std = sp.csr_matrix((h(s_val, nz), h(s_col, nz), h(s_ptr, ms + 1)), shape=(ms, ns))
         A_std.has_sorted_indices = True
         b_h, c_h = h(b_std, ms), h(c_std, ns)

@@ -106,3 +106,18 @@ def test_device_ruiz_scaled_config4():
     np.testing.assert_array_equal(info.row_scale, io.row_scale)
     np.testing.assert_array_equal(info.col_scale, io.col_scale)
     np.testing.assert_array_equal(_canon(S.A).data, _canon(So.A).data)
+
+
+@pytest.mark.gpu
+def test_empty_column_rejected():
+    """transform.py:47-54: the first structurally empty column is named (checked on the device)."""
+    import paper_2603_03150_b200 as eng
+
+    p = _P(_load(RUIZ_NAMES[0]))
+    A = p.A.tocsc()
+    A[:, 3] = 0
+    A = sp.csr_matrix(A)
+    A.eliminate_zeros()
+    p.A = A
+    with pytest.raises(ValueError, match="column 3 has no nonzero entries"):
+        eng.ruiz_equilibrate(p)
