@@ -633,10 +633,37 @@ struct SellSet {
   const unsigned char* __restrict__ perm;  // lane -> row offset in the slice (nullptr = identity)
 };
 
-template <bool PRIMAL>
 #ifndef PDHG_SELL_U
 #define PDHG_SELL_U 4
 #endif
+
+// Lane's row of slice sl: sequential sum over its len entries (kU entries'
+// loads in flight per round).
+__device__ __forceinline__ double sell_row_dot(const SellSet& S, long long sl, int lane, int len,
+                                               const double* __restrict__ x) {
+  constexpr int kU = PDHG_SELL_U;
+  const int width = S.width[sl];
+  const long long base = S.sptr[sl] + lane;
+  double acc = 0.0;
+  for (int k = 0; k < width; k += kU) {
+    double av[kU], xv[kU];
+    int jv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const bool on = k + u < len;
+      av[u] = on ? ld_stream(S.val + base + 32LL * (k + u)) : 0.0;
+      jv[u] = on ? ld_stream(S.col + base + 32LL * (k + u)) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) xv[u] = jv[u] >= 0 ? ld_gather(x + jv[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (jv[u] >= 0) acc = fma(av[u], xv[u], acc);
+  }
+  return acc;
+}
+
+template <bool PRIMAL>
 
 // 8 blocks per SM (32 registers) with the epilogue operands loaded after the
 // row loop: primal step 0.820 -> 0.812 ms on config 4; 6 blocks with early
@@ -648,7 +675,6 @@ template <bool PRIMAL>
 #define PDHG_SELL_LATE 1
 #endif
 __global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_step_sell(StepArgs a, SellSet S, int j_in_period) {
-  constexpr int kU = PDHG_SELL_U;
   __shared__ double red[kWarps];
   StepParams* P = a.P;
   const long long iter = P->iter0 + j_in_period + 1;
@@ -685,25 +711,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_step_sell(StepArgs a
   }
   const bool ok = in_range && len <= a.rs.heavy_threshold;
   if (!ok) len = 0;
-  const int width = S.width[sl];
-  const long long base = S.sptr[sl] + lane;
-  const double* __restrict__ x = a.gather;
-  double acc = 0.0;
-  for (int k = 0; k < width; k += kU) {
-    double av[kU], xv[kU];
-    int jv[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const bool on = k + u < len;
-      av[u] = on ? ld_stream(S.val + base + 32LL * (k + u)) : 0.0;
-      jv[u] = on ? ld_stream(S.col + base + 32LL * (k + u)) : -1;
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) xv[u] = jv[u] >= 0 ? ld_gather(x + jv[u]) : 0.0;
-#pragma unroll
-    for (int u = 0; u < kU; ++u)
-      if (jv[u] >= 0) acc = fma(av[u], xv[u], acc);
-  }
+  const double acc = sell_row_dot(S, sl, lane, len, a.gather);
 
   if (PDHG_SELL_LATE && ok) {
     o1 = a.cb[rl];
@@ -940,6 +948,32 @@ __global__ void __launch_bounds__(kBlock) k_spmv(RowSet rs, const double* __rest
   bool ok;
   const double d = warp_rows_dot<V>(rs, row0, lane, xin, ok);
   if (ok) out[row0 + lane] = d;
+}
+
+// out = M in over the sliced-ELL layout (the power iteration's products when
+// the operator has one): the step kernel's row loop without the epilogue.
+__global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_spmv_sell(RowSet rs, SellSet S,
+                                                                    const double* __restrict__ in,
+                                                                    double* __restrict__ out) {
+  __shared__ double red[kWarps];
+  if ((int)blockIdx.x < rs.n_heavy) {
+    const double* xin[1] = {in};
+    const int row = rs.heavy[blockIdx.x];
+    double acc[1];
+    row_dot<kBlock, 1>(rs, rs.ptr[row], rs.ptr[row + 1], threadIdx.x, xin, acc);
+    const double d = block_sum(acc[0], red);
+    if (threadIdx.x == 0) out[row] = d;
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const long long sl = ((long long)(blockIdx.x - rs.n_heavy) * kBlock + threadIdx.x) >> 5;
+  if (sl >= S.nslices) return;  // warp-uniform
+  const long long rl = sl * 32 + (S.perm ? S.perm[sl * 32 + lane] : lane);
+  int len = rl < rs.rows ? rs.ptr[rl + 1] - rs.ptr[rl] : -1;
+  const bool ok = len >= 0 && len <= rs.heavy_threshold;
+  if (!ok) len = 0;
+  const double acc = sell_row_dot(S, sl, lane, len, in);
+  if (ok) out[rl] = acc;
 }
 
 __global__ void k_div(const double* __restrict__ w, double* __restrict__ v, double s, int n) {
@@ -1457,6 +1491,15 @@ int launch_step(pdhg_ctx* c, bool primal, int j) {
 }
 
 int spmv(pdhg_ctx* c, bool transpose, const double* in, double* out) {
+  const int k = transpose ? 1 : 0;
+  if (c->has_sell[k]) {
+    const RowSet& rs = transpose ? c->At : c->A;
+    const SellSet& S = c->sell[k];
+    const int grid = rs.n_heavy + (int)(((long long)S.nslices * 32 + kBlock - 1) / kBlock);
+    if (grid > 0) k_spmv_sell<<<grid, kBlock, 0, c->stream>>>(rs, S, in, out);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
   return dispatch_lanes<SpmvLaunch>(transpose ? c->at_lanes : c->a_lanes, transpose ? c->At : c->A,
                                     in, out, c->stream);
 }

@@ -209,6 +209,8 @@ class DeviceLp:
                     self.at_ptr = t(At.indptr, np.int32)
                     self.at_col = t(At.indices, np.int32)
                     self.at_val = t(At.data, np.float64)
+                self.stream.synchronize()
+                t_tr = time.monotonic()
                 self.a_lanes = int(opts.a_lanes) or auto_lanes(nnz, m)
                 self.at_lanes = int(opts.at_lanes) or auto_lanes(self.at_nnz, n)
                 H = int(opts.heavy_threshold) or heavy_threshold(self.a_lanes)
@@ -236,6 +238,8 @@ class DeviceLp:
                         ("At", n, self.at_nnz, self.at_ptr, self.at_col, self.at_val, Ht)):
                     self._sell[key] = None if (self._psr[key] or pers in ("tiny", "on")) else \
                         self._build_sell(torch, dev, key, rows, nz, ptr, col, val, Hk, opts)
+                self.stream.synchronize()
+                t_sell = time.monotonic()
                 self.a_split = None
                 self.nsplit = 1
                 K = int(opts.dual_split)
@@ -280,7 +284,9 @@ class DeviceLp:
                                          self.stream.cuda_stream, C.byref(ctx)))
         self.ctx = ctx
         t_end = time.monotonic()
-        self.timings = {"upload_s": t_up - t_start, "layout_s": t_end - t_up}
+        self.timings = {"upload_s": t_up - t_start, "layout_s": t_end - t_up,
+                        "layout_detail": {"transpose_s": t_tr - t_up, "psr_sell_s": t_sell - t_tr,
+                                          "ctx_s": t_end - t_sell}}
         self._fin = weakref.finalize(self, self.lib.pdhg_ctx_destroy, ctx)
         self._scal = (C.c_double * (2 * N.NQ))()
 
@@ -640,14 +646,15 @@ def run_pdhg(p, params=None, seed: int = 0, *, gpu: GpuOptions | None = None):
     t0 = time.monotonic()                                      # pdhg.py:177
     if p.A.nnz == 0:                                           # pdhg.py:87-88
         raise T.InvalidModelError("cannot estimate the norm of an empty matrix")
+    v0 = hostio._executor().submit(_start_vector, n, seed) if opts.opnorm is None else None
     dev = device_lp(p, opts)
     t_layout = time.monotonic() - t0
     with dev.lock:
-        pt, st = _run(T, dev, p, params, seed, opts, t0)
+        pt, st = _run(T, dev, p, params, seed, opts, t0, v0)
     if hasattr(st, "timings"):
-        st.timings["layout_s"] = t_layout
+        st.timings["layout_s"] = t_layout      # device_lp: upload + layout build
         st.timings.update({k: v for k, v in getattr(dev, "timings", {}).items()
-                           if k == "upload_s"})
+                           if k in ("upload_s", "layout_detail")})
     return pt, st
 
 
@@ -661,7 +668,15 @@ def run_on_device(dev, p, params=None, seed: int = 0, *, gpu: GpuOptions | None 
     return _run(T, dev, p, params, seed, gpu or GpuOptions(), t0)
 
 
-def _run(T, dev: DeviceLp, p, params, seed, opts, t0):
+def _start_vector(n: int, seed: int) -> np.ndarray:
+    """The power iteration's start vector, exactly the reference's
+    (pdhg.py:89-91: default_rng(seed).standard_normal(n), normalised)."""
+    v = np.random.default_rng(seed).standard_normal(n)
+    v /= np.linalg.norm(v)
+    return v
+
+
+def _run(T, dev: DeviceLp, p, params, seed, opts, t0, v0_future=None):
     S = T.SolveStatus
     b = np.asarray(p.b, dtype=float)
     c = np.asarray(p.c, dtype=float)
@@ -675,9 +690,8 @@ def _run(T, dev: DeviceLp, p, params, seed, opts, t0):
     if opts.opnorm is not None:
         opnorm = float(opts.opnorm)
     else:
-        rng = np.random.default_rng(seed)                      # pdhg.py:89-91
-        v = rng.standard_normal(dev.n)
-        v /= np.linalg.norm(v)
+        # generated on a host thread while the model was uploaded (run_pdhg)
+        v = v0_future.result() if v0_future is not None else _start_vector(dev.n, seed)
         opnorm = dev.opnorm(v, tol=1e-4, max_iters=100)
     step = 1.0 / (1.05 * opnorm)                               # pdhg.py:119
     tm["opnorm_s"] = time.monotonic() - t_op
@@ -808,7 +822,4 @@ def estimate_opnorm(A, seed: int = 0, tol: float = 1e-4, max_iters: int = 100,
     q = _P()
     q.A, q.b, q.c = A, np.zeros(m), np.zeros(n)
     dev = DeviceLp(A, q.b, q.c, gpu or GpuOptions())
-    rng = np.random.default_rng(seed)
-    v = rng.standard_normal(n)
-    v /= np.linalg.norm(v)
-    return dev.opnorm(v, tol=tol, max_iters=max_iters)
+    return dev.opnorm(_start_vector(n, seed), tol=tol, max_iters=max_iters)
