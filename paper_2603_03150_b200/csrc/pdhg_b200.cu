@@ -97,6 +97,11 @@ __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 #ifndef PDHG_L2_HINT
 #define PDHG_L2_HINT 0
 #endif
+// Two-point KKT checks gather both points' vectors from one interleaved copy
+// (k_pair, row_dot_pair); 0 = two separate gathers per entry.
+#ifndef PDHG_CHECK_PAIR
+#define PDHG_CHECK_PAIR 1
+#endif
 // Row reductions of the warp-owns-32-rows routines: 1 = per-pass partials
 // kept in registers and reduced once per warp by a reduce-scatter
 // (reduce_scatter_rows), 0 = butterfly + parking shuffle per pass.  Measured
@@ -1000,10 +1005,58 @@ struct CheckPts {
   const double* y[2];
   const double* zin[2];  // nullptr => z = max(0, c - A'y)
   double* zout[2];       // optional z output
+  const double2* pair;   // two-point checks: the gathered vectors interleaved
+                         // ((x0[j], x1[j]) or (y0[i], y1[i])), one 16-byte gather
+                         // per entry instead of two 8-byte ones
 };
 
+// row_dot for two right-hand sides stored interleaved: each accumulator sees
+// the same fma sequence as row_dot<V, 2> (bitwise-identical sums), but one
+// gather (one L2 sector) serves both points.
+template <int V>
+__device__ __forceinline__ void row_dot_pair(const RowSet& A, int s, int e, int lane,
+                                             const double2* __restrict__ xx, double* acc) {
+  constexpr int kU = V >= 16 ? 4 : 2;
+  acc[0] = 0.0;
+  acc[1] = 0.0;
+  for (int k = s + lane; k < e; k += kU * V) {
+    double a[kU];
+    int j[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int kk = k + u * V;
+      a[u] = kk < e ? ld_stream(A.val + kk) : 0.0;
+      j[u] = kk < e ? ld_stream(A.col + kk) : -1;
+    }
+    double2 xv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) xv[u] = j[u] >= 0 ? __ldg(xx + j[u]) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (j[u] >= 0) acc[0] = fma(a[u], xv[u].x, acc[0]);
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (j[u] >= 0) acc[1] = fma(a[u], xv[u].y, acc[1]);
+  }
+}
+
+template <int V, int NP, bool PAIR>
+__device__ __forceinline__ void check_row_dot(const RowSet& A, int s, int e, int lane,
+                                              const double* const* __restrict__ xin,
+                                              const double2* __restrict__ pair, double* acc) {
+  if constexpr (PAIR && NP == 2) row_dot_pair<V>(A, s, e, lane, pair, acc);
+  else row_dot<V, NP>(A, s, e, lane, xin, acc);
+}
+
+__global__ void k_pair(const double* __restrict__ a, const double* __restrict__ b,
+                       double2* __restrict__ out, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = make_double2(a[i], b[i]);
+}
+
 // Per-point primal-side terms over rows of A: r_p = b - A x (lp_core.py:436).
-template <int V, int NP>
+template <int V, int NP, bool PAIR = false>
 __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_primal(RowSet rs, const double* __restrict__ b,
                                                          CheckPts pts, double* __restrict__ partials) {
   __shared__ double red[kWarps];
@@ -1028,7 +1081,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_primal(RowSet 
   for (int h = blockIdx.x; h < rs.n_heavy; h += gridDim.x) {
     const int row = rs.heavy[h];
     double acc[NP], d[NP];
-    row_dot<kBlock, NP>(rs, rs.ptr[row], rs.ptr[row + 1], threadIdx.x, xin, acc);
+    check_row_dot<kBlock, NP, PAIR>(rs, rs.ptr[row], rs.ptr[row + 1], threadIdx.x, xin, pts.pair, acc);
 #pragma unroll
     for (int p = 0; p < NP; ++p) d[p] = block_sum(acc[p], red);
     if (threadIdx.x == 0) row_terms(row, d);
@@ -1046,7 +1099,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_primal(RowSet 
       if (e - s > rs.heavy_threshold) { valid = false; e = s; }
     }
     double acc[NP], d[NP];
-    row_dot<V, NP>(rs, s, e, lane, xin, acc);
+    check_row_dot<V, NP, PAIR>(rs, s, e, lane, xin, pts.pair, acc);
 #pragma unroll
     for (int p = 0; p < NP; ++p) d[p] = group_sum<V>(acc[p]);
     if (valid && lane == 0) row_terms(row, d);
@@ -1066,7 +1119,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_primal(RowSet 
 }
 
 // Per-point dual-side terms over rows of A' (lp_core.py:437,441,443; pdhg.py:114).
-template <int V, int NP>
+template <int V, int NP, bool PAIR = false>
 __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual(RowSet rs, const double* __restrict__ c,
                                                        CheckPts pts, double* __restrict__ partials) {
   __shared__ double red[kWarps];
@@ -1095,7 +1148,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual(RowSet rs
   for (int h = blockIdx.x; h < rs.n_heavy; h += gridDim.x) {
     const int row = rs.heavy[h];
     double acc[NP], d[NP];
-    row_dot<kBlock, NP>(rs, rs.ptr[row], rs.ptr[row + 1], threadIdx.x, yin, acc);
+    check_row_dot<kBlock, NP, PAIR>(rs, rs.ptr[row], rs.ptr[row + 1], threadIdx.x, yin, pts.pair, acc);
 #pragma unroll
     for (int p = 0; p < NP; ++p) d[p] = block_sum(acc[p], red);
     if (threadIdx.x == 0) row_terms(row, d);
@@ -1113,7 +1166,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual(RowSet rs
       if (e - s > rs.heavy_threshold) { valid = false; e = s; }
     }
     double acc[NP], d[NP];
-    row_dot<V, NP>(rs, s, e, lane, yin, acc);
+    check_row_dot<V, NP, PAIR>(rs, s, e, lane, yin, pts.pair, acc);
 #pragma unroll
     for (int p = 0; p < NP; ++p) d[p] = group_sum<V>(acc[p]);
     if (valid && lane == 0) row_terms(row, d);
@@ -1250,9 +1303,11 @@ struct CheckLaunch {
                  double* partials, cudaStream_t s) {
     if (primal) {
       if (np == 1) k_check_primal<V, 1><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
+      else if (pts.pair) k_check_primal<V, 2, true><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
       else k_check_primal<V, 2><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
     } else {
       if (np == 1) k_check_dual<V, 1><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
+      else if (pts.pair) k_check_dual<V, 2, true><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
       else k_check_dual<V, 2><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
     }
     return 0;
@@ -1286,6 +1341,7 @@ struct pdhg_ctx {
   // workspace carve
   double *x, *xe, *xbar, *xbest, *zbest, *tn1, *tn2;
   double *y, *ybar, *ybest, *tm1, *tm2;
+  double2 *px, *py;  // interleaved gather vectors of a two-point check
   double* partials;
   double* scalars;
   StepParams* P;
@@ -1329,6 +1385,7 @@ size_t carve_bytes(int32_t m, int32_t n) {
   b += align_up((size_t)kCheckBlocks * kMaxQ * 8 + 256);
   b += align_up(64 * 8 + 256);
   b += align_up(sizeof(StepParams) + 256);
+  b += align_up((size_t)n * 16 + 256) + align_up((size_t)m * 16 + 256);  // px, py
   return b;
 }
 
@@ -1566,6 +1623,8 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->partials = cv.take<double>((size_t)kCheckBlocks * kMaxQ);
   c->scalars = cv.take<double>(64);
   c->P = cv.take<StepParams>(1);
+  c->px = cv.take<double2>(n);
+  c->py = cv.take<double2>(m);
   c->coop_grid = 0;
   c->tiny = false;
   c->period_direct = prob->persistent == 3;
@@ -1770,6 +1829,18 @@ int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
     pd.x[p] = x + c->xo; pd.y[p] = y;
     pd.zin[p] = (specs[p] & PDHG_SPEC_BEST_Z) ? c->zbest + c->xo : nullptr;
     pd.zout[p] = nullptr;
+  }
+  if (npts == 2 && PDHG_CHECK_PAIR) {
+    // interleave the two points' gathered vectors (full padded length: the
+    // check gathers by global index): 0.5 GB of copies on config 4 buys one
+    // 16-byte gather per entry instead of two 8-byte ones
+    const double *x0, *y0, *x1, *y1;
+    point_xy(c, specs[0], &x0, &y0);
+    point_xy(c, specs[1], &x1, &y1);
+    k_pair<<<kCheckBlocks, kBlock, 0, c->stream>>>(x0, x1, c->px, c->nf);
+    k_pair<<<kCheckBlocks, kBlock, 0, c->stream>>>(y0, y1, c->py, c->mf);
+    pp.pair = c->px;
+    pd.pair = c->py;
   }
   CUDA_TRY(cudaMemsetAsync(c->partials, 0, (size_t)kCheckBlocks * kMaxQ * 8, c->stream));
   int rc = dispatch_lanes<CheckLaunch>(c->a_lanes, true, (int)npts, c->A, c->prob.b, pp, c->partials,
