@@ -102,6 +102,11 @@ __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 #ifndef PDHG_CHECK_PAIR
 #define PDHG_CHECK_PAIR 1
 #endif
+// Two-point checks over an operator with a sliced-ELL layout use it too
+// (k_check_dual_sell); 0 = the CSR-vector check kernel.
+#ifndef PDHG_CHECK_SELL
+#define PDHG_CHECK_SELL 1
+#endif
 // Row reductions of the warp-owns-32-rows routines: 1 = per-pass partials
 // kept in registers and reduced once per warp by a reduce-scatter
 // (reduce_scatter_rows), 0 = butterfly + parking shuffle per pass.  Measured
@@ -1048,6 +1053,36 @@ __device__ __forceinline__ void check_row_dot(const RowSet& A, int s, int e, int
   else row_dot<V, NP>(A, s, e, lane, xin, acc);
 }
 
+// sell_row_dot for an interleaved pair of vectors (two-point checks).
+__device__ __forceinline__ void sell_row_dot_pair(const SellSet& S, long long sl, int lane, int len,
+                                                  const double2* __restrict__ xx, double& a0,
+                                                  double& a1) {
+  constexpr int kU = PDHG_SELL_U;
+  const int width = S.width[sl];
+  const long long base = S.sptr[sl] + lane;
+  a0 = 0.0;
+  a1 = 0.0;
+  for (int k = 0; k < width; k += kU) {
+    double av[kU];
+    int jv[kU];
+    double2 xv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const bool on = k + u < len;
+      av[u] = on ? ld_stream(S.val + base + 32LL * (k + u)) : 0.0;
+      jv[u] = on ? ld_stream(S.col + base + 32LL * (k + u)) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) xv[u] = jv[u] >= 0 ? __ldg(xx + jv[u]) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (jv[u] >= 0) {
+        a0 = fma(av[u], xv[u].x, a0);
+        a1 = fma(av[u], xv[u].y, a1);
+      }
+  }
+}
+
 __global__ void k_pair(const double* __restrict__ a, const double* __restrict__ b,
                        double2* __restrict__ out, long long n) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -1173,6 +1208,65 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual(RowSet rs
   }
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
+    const double t0 = block_sum(rd2[p], red);
+    const double t1 = block_max(rdmax[p], red);
+    const double t2 = block_sum(cx[p], red);
+    const double t3 = block_sum(xz[p], red);
+    if (threadIdx.x == 0) {
+      double* o = partials + (size_t)blockIdx.x * kMaxQ + p * PDHG_NQ;
+      o[PDHG_Q_RD2] = t0;
+      o[PDHG_Q_RDMAX] = t1;
+      o[PDHG_Q_CX] = t2;
+      o[PDHG_Q_XZ] = t3;
+    }
+  }
+}
+
+// Two-point dual-side terms over the sliced-ELL layout of A' (lane = row,
+// every lane runs its row's epilogue, coalesced), gathering the interleaved
+// (y0, y1) pairs.  Same quantities and partials layout as k_check_dual.
+__global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual_sell(RowSet rs, SellSet S,
+                                                                        const double* __restrict__ c,
+                                                                        CheckPts pts,
+                                                                        double* __restrict__ partials) {
+  __shared__ double red[kWarps];
+  double rd2[2] = {0.0, 0.0}, rdmax[2] = {0.0, 0.0}, cx[2] = {0.0, 0.0}, xz[2] = {0.0, 0.0};
+  auto row_terms = [&](int j, const double* d) {
+    const double cj = c[j];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const double t = __dsub_rn(cj, d[p]);                 // c - A'y
+      const double z = pts.zin[p] ? pts.zin[p][j] : np_max0(t);
+      if (pts.zout[p]) pts.zout[p][j] = z;
+      const double r = __dsub_rn(t, z);                     // r_d = c - A'y - z
+      const double xj = pts.x[p][j];
+      rd2[p] = fma(r, r, rd2[p]);
+      rdmax[p] = nan_max(fabs(r), rdmax[p]);
+      cx[p] = fma(cj, xj, cx[p]);
+      xz[p] = fma(xj, z, xz[p]);
+    }
+  };
+  for (int h = blockIdx.x; h < rs.n_heavy; h += gridDim.x) {
+    const int row = rs.heavy[h];
+    double acc[2], d[2];
+    row_dot_pair<kBlock>(rs, rs.ptr[row], rs.ptr[row + 1], threadIdx.x, pts.pair, acc);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) d[p] = block_sum(acc[p], red);
+    if (threadIdx.x == 0) row_terms(row, d);
+  }
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * kWarps;
+  for (long long sl = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5; sl < S.nslices; sl += warps) {
+    const long long rl = sl * 32 + (S.perm ? S.perm[sl * 32 + lane] : lane);
+    int len = rl < rs.rows ? rs.ptr[rl + 1] - rs.ptr[rl] : -1;
+    const bool ok = len >= 0 && len <= rs.heavy_threshold;
+    if (!ok) len = 0;
+    double d[2];
+    sell_row_dot_pair(S, sl, lane, len, pts.pair, d[0], d[1]);
+    if (ok) row_terms((int)rl, d);
+  }
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
     const double t0 = block_sum(rd2[p], red);
     const double t1 = block_max(rdmax[p], red);
     const double t2 = block_sum(cx[p], red);
@@ -1846,9 +1940,14 @@ int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
   int rc = dispatch_lanes<CheckLaunch>(c->a_lanes, true, (int)npts, c->A, c->prob.b, pp, c->partials,
                                        c->stream);
   if (rc) return rc;
-  rc = dispatch_lanes<CheckLaunch>(c->at_lanes, false, (int)npts, c->At, c->prob.c, pd, c->partials,
-                                   c->stream);
-  if (rc) return rc;
+  if (pd.pair && c->has_sell[1] && PDHG_CHECK_SELL) {
+    k_check_dual_sell<<<kCheckBlocks, kBlock, 0, c->stream>>>(c->At, c->sell[1], c->prob.c, pd, c->partials);
+    CUDA_TRY(cudaGetLastError());
+  } else {
+    rc = dispatch_lanes<CheckLaunch>(c->at_lanes, false, (int)npts, c->At, c->prob.c, pd, c->partials,
+                                     c->stream);
+    if (rc) return rc;
+  }
   const int nq = npts * PDHG_NQ;
   k_reduce<<<nq, kBlock, 0, c->stream>>>(c->partials, kCheckBlocks, kMaxQ, nq, c->scalars);
   CUDA_TRY(cudaGetLastError());
