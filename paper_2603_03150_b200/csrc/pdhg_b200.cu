@@ -107,6 +107,10 @@ __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 #ifndef PDHG_CHECK_SELL
 #define PDHG_CHECK_SELL 1
 #endif
+#ifndef PDHG_CHECK_EARLY
+#define PDHG_CHECK_EARLY 1
+#endif
+
 // Row reductions of the warp-owns-32-rows routines: 1 = per-pass partials
 // kept in registers and reduced once per warp by a reduce-scatter
 // (reduce_scatter_rows), 0 = butterfly + parking shuffle per pass.  Measured
@@ -1102,15 +1106,20 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_primal(RowSet 
 #pragma unroll
   for (int p = 0; p < NP; ++p) xin[p] = pts.x[p];
 
-  auto row_terms = [&](int i, const double* d) {
-    const double bi = b[i];
+  auto row_terms_pre = [&](double bi, const double* yi, const double* d) {
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       const double r = __dsub_rn(bi, d[p]);
       rp2[p] = fma(r, r, rp2[p]);
       rpmax[p] = nan_max(fabs(r), rpmax[p]);
-      by[p] = fma(bi, pts.y[p][i], by[p]);
+      by[p] = fma(bi, yi[p], by[p]);
     }
+  };
+  auto row_terms = [&](int i, const double* d) {
+    double yi[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) yi[p] = pts.y[p][i];
+    row_terms_pre(b[i], yi, d);
   };
   // heavy rows: block per row, blocks take them round robin
   for (int h = blockIdx.x; h < rs.n_heavy; h += gridDim.x) {
@@ -1133,11 +1142,23 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_primal(RowSet 
       e = rs.ptr[row + 1];
       if (e - s > rs.heavy_threshold) { valid = false; e = s; }
     }
+    // the row's epilogue operands are independent of its dot: issued first
+    double bi = 0.0, yi[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) yi[p] = 0.0;
+    if (PDHG_CHECK_EARLY && valid && lane == 0) {
+      bi = b[row];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) yi[p] = pts.y[p][row];
+    }
     double acc[NP], d[NP];
     check_row_dot<V, NP, PAIR>(rs, s, e, lane, xin, pts.pair, acc);
 #pragma unroll
     for (int p = 0; p < NP; ++p) d[p] = group_sum<V>(acc[p]);
-    if (valid && lane == 0) row_terms(row, d);
+    if (valid && lane == 0) {
+      if (PDHG_CHECK_EARLY) row_terms_pre(bi, yi, d);
+      else row_terms(row, d);
+    }
   }
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
@@ -1165,20 +1186,25 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual(RowSet rs
 #pragma unroll
   for (int p = 0; p < NP; ++p) yin[p] = pts.y[p];
 
-  auto row_terms = [&](int j, const double* d) {
-    const double cj = c[j];
+  auto row_terms_pre = [&](int j, double cj, const double* xjs, const double* d) {
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       const double t = __dsub_rn(cj, d[p]);                 // c - A'y
       const double z = pts.zin[p] ? pts.zin[p][j] : np_max0(t);
       if (pts.zout[p]) pts.zout[p][j] = z;
       const double r = __dsub_rn(t, z);                     // r_d = c - A'y - z
-      const double xj = pts.x[p][j];
+      const double xj = xjs[p];
       rd2[p] = fma(r, r, rd2[p]);
       rdmax[p] = nan_max(fabs(r), rdmax[p]);
       cx[p] = fma(cj, xj, cx[p]);
       xz[p] = fma(xj, z, xz[p]);
     }
+  };
+  auto row_terms = [&](int j, const double* d) {
+    double xjs[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) xjs[p] = pts.x[p][j];
+    row_terms_pre(j, c[j], xjs, d);
   };
   for (int h = blockIdx.x; h < rs.n_heavy; h += gridDim.x) {
     const int row = rs.heavy[h];
@@ -1200,11 +1226,22 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual(RowSet rs
       e = rs.ptr[row + 1];
       if (e - s > rs.heavy_threshold) { valid = false; e = s; }
     }
+    double cj = 0.0, xjs[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) xjs[p] = 0.0;
+    if (PDHG_CHECK_EARLY && valid && lane == 0) {   // operands first, as in k_check_primal
+      cj = c[row];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) xjs[p] = pts.x[p][row];
+    }
     double acc[NP], d[NP];
     check_row_dot<V, NP, PAIR>(rs, s, e, lane, yin, pts.pair, acc);
 #pragma unroll
     for (int p = 0; p < NP; ++p) d[p] = group_sum<V>(acc[p]);
-    if (valid && lane == 0) row_terms(row, d);
+    if (valid && lane == 0) {
+      if (PDHG_CHECK_EARLY) row_terms_pre(row, cj, xjs, d);
+      else row_terms(row, d);
+    }
   }
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
