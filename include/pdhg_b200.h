@@ -207,6 +207,12 @@ int pdhg_save_best(pdhg_ctx* ctx, int32_t which, int32_t flags);
 /* Copy point spec (as in pdhg_check) to host arrays (any may be NULL).
  * z is max(0, c - A'y) unless PDHG_SPEC_BEST_Z selects the stored best z. */
 int pdhg_fetch(pdhg_ctx* ctx, int32_t spec, double* x_host, double* y_host, double* z_host);
+/* Device-side form of pdhg_fetch: computes the point's z on the device (into
+ * scratch, unless spec carries PDHG_SPEC_BEST_Z) and returns the device
+ * addresses of x, y, z (full padded lengths), queued on the context's stream
+ * without synchronising -- for callers with their own download path. */
+int pdhg_point_device(pdhg_ctx* ctx, int32_t spec, const double** x_dev, const double** y_dev,
+                      const double** z_dev);
 
 /* Device vectors of the context (full, padded length), for host-driven
  * exchanges between shards (NCCL all-gather or device copies). */

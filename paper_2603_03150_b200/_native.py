@@ -23,7 +23,7 @@ Q_RP2, Q_RPMAX, Q_BY, Q_RD2, Q_RDMAX, Q_CX, Q_XZ = range(7)
 EXPORTS = (
     "pdhg_abi_version", "pdhg_last_error", "pdhg_workspace_bytes", "pdhg_ctx_create",
     "pdhg_ctx_destroy", "pdhg_spmv", "pdhg_opnorm", "pdhg_reset", "pdhg_run_period",
-    "pdhg_check", "pdhg_restart", "pdhg_save_best", "pdhg_fetch", "pdhg_time_kernel",
+    "pdhg_check", "pdhg_restart", "pdhg_save_best", "pdhg_fetch", "pdhg_point_device", "pdhg_time_kernel",
     "pdhg_transpose_tmp_bytes", "pdhg_transpose_csr",
     "pdhg_psr_tmp_bytes", "pdhg_psr_plan", "pdhg_psr_build",
     "pdhg_check_device", "pdhg_vector", "pdhg_reduced_costs", "pdhg_set_step", "pdhg_half_step",
@@ -124,6 +124,7 @@ def load():
         _sig(lib, "pdhg_restart", C.c_int, vp, i32)
         _sig(lib, "pdhg_save_best", C.c_int, vp, i32, i32)
         _sig(lib, "pdhg_fetch", C.c_int, vp, i32, vp, vp, vp)
+        _sig(lib, "pdhg_point_device", C.c_int, vp, i32, vp, vp, vp)
         _sig(lib, "pdhg_time_kernel", C.c_int, vp, i32, i32, dbl, dbl, P(dbl))
         _sig(lib, "pdhg_transpose_tmp_bytes", szt, i64, i32, i32)
         _sig(lib, "pdhg_transpose_csr", C.c_int, i32, i32, i64, vp, vp, vp, vp, vp, vp, vp, szt, vp)

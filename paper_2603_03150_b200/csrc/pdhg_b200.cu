@@ -2095,6 +2095,20 @@ int pdhg_fetch(pdhg_ctx* c, int32_t spec, double* x_host, double* y_host, double
   return 0;
 }
 
+int pdhg_point_device(pdhg_ctx* c, int32_t spec, const double** x_dev, const double** y_dev,
+                      const double** z_dev) {
+  if (!c || !x_dev || !y_dev || !z_dev) return fail(PDHG_ERR_ARG, "null argument");
+  point_xy(c, spec, x_dev, y_dev);
+  if (spec & PDHG_SPEC_BEST_Z) {
+    *z_dev = c->zbest;
+  } else {
+    int rc = reduced_costs(c, spec, c->tn1 + c->xo);
+    if (rc) return rc;
+    *z_dev = c->tn1;
+  }
+  return 0;
+}
+
 void* pdhg_vector(pdhg_ctx* c, int32_t which) {
   if (!c) return nullptr;
   switch (which) {

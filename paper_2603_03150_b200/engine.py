@@ -414,11 +414,17 @@ class DeviceLp:
         N.check(self.lib.pdhg_save_best(self.ctx, which, flags))
 
     def fetch(self, spec: int, want_z: bool = True):
-        x = np.empty(self.n_full)
-        y = np.empty(self.m_full)
-        z = np.empty(self.n_full) if want_z else None
-        N.check(self.lib.pdhg_fetch(self.ctx, spec, x.ctypes.data, y.ctypes.data,
-                                    z.ctypes.data if want_z else None))
+        """Host copies of a point (full padded lengths): z computed on the device,
+        downloads through the pinned ring (hostio)."""
+        torch = _torch()
+        px, py, pz = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        N.check(self.lib.pdhg_point_device(self.ctx, spec, C.byref(px), C.byref(py), C.byref(pz)))
+        base = self.ws.data_ptr()
+        view = lambda ptr, k: self.ws[ptr - base:ptr - base + 8 * k].view(torch.float64)
+        with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+            x = hostio.d2h(view(px.value, self.n_full))
+            y = hostio.d2h(view(py.value, self.m_full))
+            z = hostio.d2h(view(pz.value, self.n_full)) if want_z else None
         return x, y, z
 
     def spmv(self, v: np.ndarray, transpose: bool = False) -> np.ndarray:
