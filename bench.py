@@ -184,7 +184,8 @@ def run_reference(args):
     rank, world, _ = _env_rank()
     if rank != 0:
         return 0
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    # all host threads the reference can use: scipy's csr_matvec and numpy's
+    # ufuncs are single-threaded; BLAS (the norms and dots) is left unrestricted
     inst = _instance(args.scale, args.seed)
     samples = []
     import numpy as np
@@ -213,7 +214,8 @@ def run_reference(args):
     value = 1.0 / per_iter
     sample = (f"{args.steps} pdhg_step calls + 1 scored check (2 points, amortised over "
               f"{CHECK_EVERY} iterations) of the oracle on config4 scale={args.scale}; "
-              "scipy csr_matvec single-threaded, OPENBLAS_NUM_THREADS=1")
+              f"scipy csr_matvec and numpy ufuncs single-threaded (1 core busy), BLAS threads "
+              f"unrestricted ({os.cpu_count()} host CPUs)")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_iter * 1e3, "higher_is_better": True,
