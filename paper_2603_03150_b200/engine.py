@@ -652,7 +652,7 @@ def run_pdhg(p, params=None, seed: int = 0, *, gpu: GpuOptions | None = None):
     t0 = time.monotonic()                                      # pdhg.py:177
     if p.A.nnz == 0:                                           # pdhg.py:87-88
         raise T.InvalidModelError("cannot estimate the norm of an empty matrix")
-    v0 = hostio._executor().submit(_start_vector, n, seed) if opts.opnorm is None else None
+    v0 = hostio.submit(_start_vector, n, seed) if opts.opnorm is None else None
     dev = device_lp(p, opts)
     t_layout = time.monotonic() - t0
     with dev.lock:

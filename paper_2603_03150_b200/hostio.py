@@ -44,6 +44,13 @@ def _executor():
         return _pool
 
 
+def submit(fn, *args):
+    """Run fn(*args) on the host thread pool, overlapped with device work
+    (e.g. the power iteration's start vector during the model upload);
+    returns a concurrent.futures.Future."""
+    return _executor().submit(fn, *args)
+
+
 class _Ring:
     def __init__(self, dev):
         import torch

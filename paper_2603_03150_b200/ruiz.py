@@ -74,7 +74,7 @@ def ruiz_equilibrate(p, max_iters: int = 20, tol: float = 1e-2, *, gpu=None, reg
         raise N.NativeError("ruiz_equilibrate needs a CUDA device; there is no CPU fallback")
     # the scaled matrix gets its own index arrays (as the reference's product
     # does): copied on a host thread while the device works
-    idx_copy = hostio._executor().submit(lambda: (A.indices.copy(), A.indptr.copy()))
+    idx_copy = hostio.submit(lambda: (A.indices.copy(), A.indptr.copy()))
     tm["host_checks_s"] = time.perf_counter() - t
     lib = N.load()
     opts = gpu or GpuOptions()
