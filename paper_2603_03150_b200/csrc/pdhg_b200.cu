@@ -1434,17 +1434,6 @@ int grid_rows(const RowSet& rs, int lanes) {
 }
 
 template <int V>
-struct StepLaunch {
-  static int run(bool primal, const StepArgs& a, int j, cudaStream_t s) {
-    const int g = grid_rows(a.rs, V);
-    if (g == 0) return 0;
-    if (primal) k_step<V, true><<<g, kBlock, 0, s>>>(a, j);
-    else k_step<V, false><<<g, kBlock, 0, s>>>(a, j);
-    return 0;
-  }
-};
-
-template <int V>
 struct SpmvLaunch {
   static int run(const RowSet& rs, const double* in, double* out, cudaStream_t s) {
     const int g = grid_rows(rs, V);
