@@ -724,7 +724,10 @@ def _run(T, dev: DeviceLp, p, params, seed, opts, t0, v0_future=None):
         if iterations >= params.max_kkt_passes:                # pdhg.py:185-187
             status = S.ITERATION_LIMIT
             break
-        if time.monotonic() - t0 > params.time_limit_s:        # pdhg.py:188-190
+        timed_out = time.monotonic() - t0 > params.time_limit_s   # pdhg.py:188-190
+        if hasattr(dev, "agree") and math.isfinite(params.time_limit_s):
+            timed_out = dev.agree(timed_out)    # shards stop together (clocks differ per rank)
+        if timed_out:
             status = S.TIME_LIMIT
             break
         k = min(check_every - iterations % check_every, int(params.max_kkt_passes) - iterations)

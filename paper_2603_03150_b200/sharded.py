@@ -395,6 +395,13 @@ class ShardedDevice:
             else:
                 self._ag("y")
 
+    def agree(self, flag: bool) -> bool:
+        """True on every rank if it is true on any (the time-limit exit): each
+        rank reads its own clock, the decision must be collective."""
+        with self._on_stream():
+            flags = self.comm.allgather_int([int(bool(flag))] * len(self.shards))
+        return any(flags)
+
     def _complete(self, spec: int):
         which = spec & 3
         xs = {N.PT_CUR: "x", N.PT_AVG: "xbar", N.PT_BEST: "xbest"}[which]

@@ -191,3 +191,55 @@ def test_loopback_failure_stops_every_shard(G):
     np.testing.assert_allclose(pt.x, opt.x, rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(pt.y, opt.y, rtol=1e-9, atol=1e-12)
     assert [sh.fail for sh in shards] == [335] * G   # every shard stopped there
+
+
+def _worker_time_limit(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    import time
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch.distributed as dist
+
+    from conftest import load_golden
+    from paper_2603_03150_b200 import engine
+    from paper_2603_03150_b200.lp_types import resolve
+    from paper_2603_03150_b200.sharded import ShardPlan, ShardedDevice, TorchComm
+    from shard_double import NumpyShard
+
+    if rank == 1:   # this rank's clock jumps 1,000 s after the run starts
+        real, calls = time.monotonic, [0]
+
+        def late():
+            calls[0] += 1
+            return real() + (1000.0 if calls[0] > 1 else 0.0)
+
+        engine.time.monotonic = late
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        gm = load_golden("config0_s0")
+        plan = ShardPlan(gm.A, world)
+        dev = ShardedDevice(plan, [NumpyShard(plan.block(rank, gm.A, gm.b, gm.c))], TorchComm(plan))
+        T = resolve()
+        pt, st = engine.run_on_device(dev, gm, T.PdhgParams(eps_rel=1e-12, time_limit_s=500.0))
+        q.put((rank, st.status.value, st.iterations))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_time_limit_is_collective():
+    """One rank past the time limit stops every rank at the same iteration
+    (ShardedDevice.agree) instead of leaving the others in a collective."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_time_limit, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == [(0, "TimeLimit", 0), (1, "TimeLimit", 0)]
