@@ -667,17 +667,28 @@ struct SellSet {
   const int* __restrict__ col;
   const double* __restrict__ val;
   const unsigned char* __restrict__ perm;  // lane -> row offset in the slice (nullptr = identity)
+  bool u_long = false;                     // mean row >= PDHG_SELL_U_MEAN: PDHG_SELL_U_LONG in flight
 };
 
+// Entries in flight per lane in the SELL row loop: PDHG_SELL_U for short
+// rows, PDHG_SELL_U_LONG for operators averaging >= PDHG_SELL_U_MEAN entries
+// per row (config 4's A', mean 20: 4 -> 6 takes the primal step 0.816 ->
+// 0.781 ms; config 3's A', mean 3, stays at 4: profiles/r01_pipeline.md).
 #ifndef PDHG_SELL_U
 #define PDHG_SELL_U 4
+#endif
+#ifndef PDHG_SELL_U_LONG
+#define PDHG_SELL_U_LONG 6
+#endif
+#ifndef PDHG_SELL_U_MEAN
+#define PDHG_SELL_U_MEAN 12
 #endif
 
 // Lane's row of slice sl: sequential sum over its len entries (kU entries'
 // loads in flight per round).
+template <int kU>
 __device__ __forceinline__ double sell_row_dot(const SellSet& S, long long sl, int lane, int len,
                                                const double* __restrict__ x) {
-  constexpr int kU = PDHG_SELL_U;
   const int width = S.width[sl];
   const long long base = S.sptr[sl] + lane;
   double acc = 0.0;
@@ -699,8 +710,6 @@ __device__ __forceinline__ double sell_row_dot(const SellSet& S, long long sl, i
   return acc;
 }
 
-template <bool PRIMAL>
-
 // 8 blocks per SM (32 registers) with the epilogue operands loaded after the
 // row loop: primal step 0.820 -> 0.812 ms on config 4; 6 blocks with early
 // loads measured 1.03 ms (profiles/r01_pipeline.md).
@@ -710,6 +719,7 @@ template <bool PRIMAL>
 #ifndef PDHG_SELL_LATE
 #define PDHG_SELL_LATE 1
 #endif
+template <bool PRIMAL, int kU>
 __global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_step_sell(StepArgs a, SellSet S, int j_in_period) {
   __shared__ double red[kWarps];
   pdl_enter();
@@ -748,7 +758,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_step_sell(StepArgs a
   }
   const bool ok = in_range && len <= a.rs.heavy_threshold;
   if (!ok) len = 0;
-  const double acc = sell_row_dot(S, sl, lane, len, a.gather);
+  const double acc = sell_row_dot<kU>(S, sl, lane, len, a.gather);
 
   if (PDHG_SELL_LATE && ok) {
     o1 = a.cb[rl];
@@ -991,6 +1001,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv(RowSet rs, const double* __rest
 
 // out = M in over the sliced-ELL layout (the power iteration's products when
 // the operator has one): the step kernel's row loop without the epilogue.
+template <int kU>
 __global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_spmv_sell(RowSet rs, SellSet S,
                                                                     const double* __restrict__ in,
                                                                     double* __restrict__ out) {
@@ -1011,7 +1022,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_spmv_sell(RowSet rs,
   int len = rl < rs.rows ? rs.ptr[rl + 1] - rs.ptr[rl] : -1;
   const bool ok = len >= 0 && len <= rs.heavy_threshold;
   if (!ok) len = 0;
-  const double acc = sell_row_dot(S, sl, lane, len, in);
+  const double acc = sell_row_dot<kU>(S, sl, lane, len, in);
   if (ok) out[rl] = acc;
 }
 
@@ -1083,10 +1094,10 @@ __device__ __forceinline__ void check_row_dot(const RowSet& A, int s, int e, int
 }
 
 // sell_row_dot for an interleaved pair of vectors (two-point checks).
+template <int kU>
 __device__ __forceinline__ void sell_row_dot_pair(const SellSet& S, long long sl, int lane, int len,
                                                   const double2* __restrict__ xx, double& a0,
                                                   double& a1) {
-  constexpr int kU = PDHG_SELL_U;
   const int width = S.width[sl];
   const long long base = S.sptr[sl] + lane;
   a0 = 0.0;
@@ -1287,6 +1298,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual(RowSet rs
 // Two-point dual-side terms over the sliced-ELL layout of A' (lane = row,
 // every lane runs its row's epilogue, coalesced), gathering the interleaved
 // (y0, y1) pairs.  Same quantities and partials layout as k_check_dual.
+template <int kU>
 __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual_sell(RowSet rs, SellSet S,
                                                                         const double* __restrict__ c,
                                                                         CheckPts pts,
@@ -1324,7 +1336,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual_sell(RowS
     const bool ok = len >= 0 && len <= rs.heavy_threshold;
     if (!ok) len = 0;
     double d[2];
-    sell_row_dot_pair(S, sl, lane, len, pts.pair, d[0], d[1]);
+    sell_row_dot_pair<kU>(S, sl, lane, len, pts.pair, d[0], d[1]);
     if (ok) row_terms((int)rl, d);
   }
 #pragma unroll
@@ -1691,8 +1703,11 @@ int launch_step(pdhg_ctx* c, bool primal, int j) {
   if (c->has_sell[k]) {
     const SellSet& S = c->sell[k];
     const int grid = a.rs.n_heavy + (int)(((long long)S.nslices * 32 + kBlock - 1) / kBlock);
-    return primal ? launch_ex(c, k_step_sell<true>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j)
-                  : launch_ex(c, k_step_sell<false>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
+    if (S.u_long)
+      return primal ? launch_ex(c, k_step_sell<true, PDHG_SELL_U_LONG>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j)
+                    : launch_ex(c, k_step_sell<false, PDHG_SELL_U_LONG>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
+    return primal ? launch_ex(c, k_step_sell<true, PDHG_SELL_U>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j)
+                  : launch_ex(c, k_step_sell<false, PDHG_SELL_U>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
   }
   return dispatch_lanes<StepLaunchEx>(lanes, c, primal, a, j, grid_rows(a.rs, lanes), win_base, win);
 }
@@ -1703,7 +1718,10 @@ int spmv(pdhg_ctx* c, bool transpose, const double* in, double* out) {
     const RowSet& rs = transpose ? c->At : c->A;
     const SellSet& S = c->sell[k];
     const int grid = rs.n_heavy + (int)(((long long)S.nslices * 32 + kBlock - 1) / kBlock);
-    if (grid > 0) k_spmv_sell<<<grid, kBlock, 0, c->stream>>>(rs, S, in, out);
+    if (grid > 0) {
+      if (S.u_long) k_spmv_sell<PDHG_SELL_U_LONG><<<grid, kBlock, 0, c->stream>>>(rs, S, in, out);
+      else k_spmv_sell<PDHG_SELL_U><<<grid, kBlock, 0, c->stream>>>(rs, S, in, out);
+    }
     CUDA_TRY(cudaGetLastError());
     return 0;
   }
@@ -1803,6 +1821,8 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
       }
       c->sell[k] = SellSet{q->rows, q->nslices, reinterpret_cast<const long long*>(q->sptr), q->width,
                            q->col, q->val, q->perm};
+      const long long ops_nnz = k == 0 ? prob->nnz : (prob->at_nnz > 0 ? prob->at_nnz : prob->nnz);
+      c->sell[k].u_long = q->rows > 0 && ops_nnz >= (long long)PDHG_SELL_U_MEAN * q->rows;
     }
   }
   for (int k = 0; k < 2; ++k) {
@@ -1997,7 +2017,12 @@ int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
                                        c->stream);
   if (rc) return rc;
   if (pd.pair && c->has_sell[1] && PDHG_CHECK_SELL) {
-    k_check_dual_sell<<<kCheckBlocks, kBlock, 0, c->stream>>>(c->At, c->sell[1], c->prob.c, pd, c->partials);
+    if (c->sell[1].u_long)
+      k_check_dual_sell<PDHG_SELL_U_LONG><<<kCheckBlocks, kBlock, 0, c->stream>>>(c->At, c->sell[1], c->prob.c, pd,
+                                                                                c->partials);
+    else
+      k_check_dual_sell<PDHG_SELL_U><<<kCheckBlocks, kBlock, 0, c->stream>>>(c->At, c->sell[1], c->prob.c, pd,
+                                                                           c->partials);
     CUDA_TRY(cudaGetLastError());
   } else {
     rc = dispatch_lanes<CheckLaunch>(c->at_lanes, false, (int)npts, c->At, c->prob.c, pd, c->partials,
