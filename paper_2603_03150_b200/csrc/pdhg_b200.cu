@@ -122,6 +122,15 @@ __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 #ifndef PDHG_PDL
 #define PDHG_PDL 2
 #endif
+// Entries in flight per lane: row_dot with V >= 16 lanes per row (4 -> 5:
+// config 4 dual step 0.956 -> 0.940 ms, config 2 110 -> 106 us; 6 spills)
+// and the pipelined V <= 8 routine.
+#ifndef PDHG_ROW_U16
+#define PDHG_ROW_U16 5
+#endif
+#ifndef PDHG_PIPE_U
+#define PDHG_PIPE_U 4
+#endif
 
 __device__ __forceinline__ void pdl_enter() {
 #if PDHG_PDL == 1
@@ -281,7 +290,7 @@ __device__ __forceinline__ void row_dot(const RowSet& A, int s, int e, int lane,
   // parallelism for the dependent gathers); the fma chain still runs in
   // entry order k, k+V, k+2V, ...  (V, kU) from tools/spmv_lab.cu on config 4
   // (profiles/r01_spmv_lab2.log): (16, 4) for mean-40 rows, (8, 2) for mean 20.
-  constexpr int kU = V >= 16 ? 4 : 2;
+  constexpr int kU = V >= 16 ? PDHG_ROW_U16 : 2;
 #pragma unroll
   for (int r = 0; r < NR; ++r) acc[r] = 0.0;
   for (int k = s + lane; k < e; k += kU * V) {
@@ -369,7 +378,7 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
                                                      const double* const* __restrict__ xin,
                                                      bool& ok) {
   constexpr int G = 32 / V;
-  constexpr int kU = 4;
+  constexpr int kU = PDHG_PIPE_U;
   const int sub = lane % V;
   const long long rl = row0 + lane;
   int my_s = 0, my_e = 0;
