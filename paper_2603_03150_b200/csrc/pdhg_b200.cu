@@ -131,6 +131,10 @@ __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 #ifndef PDHG_PIPE_U
 #define PDHG_PIPE_U 4
 #endif
+// row_dot_pair (two-point checks): entries in flight per lane for V >= 16
+#ifndef PDHG_PAIR_U16
+#define PDHG_PAIR_U16 4
+#endif
 
 __device__ __forceinline__ void pdl_enter() {
 #if PDHG_PDL == 1
@@ -1070,7 +1074,7 @@ struct CheckPts {
 template <int V>
 __device__ __forceinline__ void row_dot_pair(const RowSet& A, int s, int e, int lane,
                                              const double2* __restrict__ xx, double* acc) {
-  constexpr int kU = V >= 16 ? 4 : 2;
+  constexpr int kU = V >= 16 ? PDHG_PAIR_U16 : 2;
   acc[0] = 0.0;
   acc[1] = 0.0;
   for (int k = s + lane; k < e; k += kU * V) {
