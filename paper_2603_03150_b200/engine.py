@@ -58,9 +58,11 @@ class GpuOptions:
                      count stays within sell_max_pad x its nonzeros (near-uniform row
                      lengths), that has no PSR layout, and either short rows (mean <
                      sell_max_mean: config 3, steps 10-22 % faster) or >= sell_min_nnz
-                     entries (config 4's A': primal step 0.862 -> 0.820 ms; at 1.5-20M
-                     entries it measured neutral to 50 % slower).  Skewed rows (config 4's
-                     A: 4x padding) stay on CSR-vector.
+                     entries (with 6 entries in flight per lane: config 4's A' primal
+                     step 0.862 -> 0.780 ms, config 2's A' (18M) 81.6 -> 73.6 us,
+                     config 4 at 5 % (10M) 41.3 -> 35.6 us; at 1.5M entries it measured
+                     50 % slower).  Skewed rows (config 4's A: 4x padding) stay on
+                     CSR-vector.
     sell_sort:       "auto" | "on" | "off" -- order each slice's rows by length (lanes
                      active in a round form a prefix, so fetched sectors are full):
                      config 4's A' reads 3.55 instead of 3.85 GB per primal step (period
@@ -96,7 +98,7 @@ class GpuOptions:
     sell: str = "auto"
     sell_max_pad: float = 1.6
     sell_max_mean: float = 12.0
-    sell_min_nnz: int = 50_000_000
+    sell_min_nnz: int = 5_000_000
     sell_sort: str = "auto"
 
 
