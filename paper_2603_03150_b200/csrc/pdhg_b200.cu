@@ -992,7 +992,7 @@ __global__ void __launch_bounds__(psr::kThreads, 1) k_step_psr(PsrStepArgs a, in
 // ------------------------------------------------------------------ plain SpMV
 
 template <int V>
-__global__ void __launch_bounds__(kBlock) k_spmv(RowSet rs, const double* __restrict__ in,
+__global__ void __launch_bounds__(kBlock, step_min_blocks<V>()) k_spmv(RowSet rs, const double* __restrict__ in,
                                                  double* __restrict__ out) {
   __shared__ double red[kWarps];
   const double* xin[1] = {in};
