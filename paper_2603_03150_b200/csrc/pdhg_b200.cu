@@ -131,6 +131,10 @@ __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 #ifndef PDHG_PIPE_U
 #define PDHG_PIPE_U 4
 #endif
+// V >= 16 step kernels load their epilogue operands after the row loop
+#ifndef PDHG_LATE16
+#define PDHG_LATE16 1
+#endif
 // row_dot_pair (two-point checks): entries in flight per lane for V >= 16
 #ifndef PDHG_PAIR_U16
 #define PDHG_PAIR_U16 4
@@ -612,7 +616,7 @@ constexpr int step_min_blocks() { return V >= 16 ? 8 : (V <= 2 ? 6 : 4); }
 
 template <int V, bool PRIMAL, bool PEERS = false>
 __global__ void __launch_bounds__(kBlock, step_min_blocks<V>()) k_step(StepArgs a, int j_in_period) {
-  constexpr bool kLateEpi = V >= 16;
+  constexpr bool kLateEpi = V >= 16 && PDHG_LATE16;
   __shared__ double red[kWarps];
   pdl_enter();
   StepParams* P = a.P;
