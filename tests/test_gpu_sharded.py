@@ -204,3 +204,22 @@ def test_failure_single_gpu(eng):
     assert st.status.value == "NumericalFailure" and st.iterations == ost.iterations == 335
     np.testing.assert_allclose(pt.x, opt.x, rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(pt.y, opt.y, rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["loopback", "loopback_fused"])
+def test_sharded_sell_layouts_match_single_gpu(eng, kind):
+    """Shards whose operators run on the sliced-ELL kernels (step, check,
+    power iteration; 6 entries in flight for A', 4 for A) reproduce the
+    single-GPU SELL run: same iterations, iterates to 1e-9."""
+    from paper_2603_03150_b200.instances import config4
+    from paper_2603_03150_b200.sharded import run_pdhg_sharded
+
+    p = config4(scale=0.01, seed=21)
+    T = eng.types()
+    opts = eng.GpuOptions(sell="on", cache_layout=False)
+    params = T.PdhgParams(eps_rel=1e-12, max_kkt_passes=256)
+    p1, s1 = eng.run_pdhg(p, params, gpu=opts)
+    p2, s2 = run_pdhg_sharded(p, params, G=2, gpu=opts, comm_kind=kind)
+    assert s1.iterations == s2.iterations == 256 and s1.restarts == s2.restarts
+    np.testing.assert_allclose(p2.x, p1.x, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(p2.y, p1.y, rtol=1e-9, atol=1e-12)
