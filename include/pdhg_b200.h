@@ -137,6 +137,13 @@ typedef struct pdhg_problem {
    * 3: direct stream launches, no graph.  1 and 2 need CSR layouts and an
    * unsharded context (ignored otherwise). */
   int32_t persistent;
+  /* Medium rows (CSR step kernels only): rows of A / A' with light_max <
+   * length <= heavy threshold, listed in a_medium / at_medium, run one warp
+   * per row instead of sharing a warp-owns-32-rows pass.  0 = none. */
+  int32_t a_light_max, at_light_max;
+  int32_t a_n_medium, at_n_medium;
+  const int32_t* a_medium;
+  const int32_t* at_medium;
 } pdhg_problem;
 
 typedef struct pdhg_ctx pdhg_ctx;

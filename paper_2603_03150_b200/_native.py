@@ -79,6 +79,9 @@ class Problem(C.Structure):
         ("at_heavy_threshold", C.c_int32),
         ("a_sell", C.POINTER(Sell)), ("at_sell", C.POINTER(Sell)),
         ("persistent", C.c_int32),
+        ("a_light_max", C.c_int32), ("at_light_max", C.c_int32),
+        ("a_n_medium", C.c_int32), ("at_n_medium", C.c_int32),
+        ("a_medium", C.c_void_p), ("at_medium", C.c_void_p),
     ]
 
 

@@ -275,6 +275,13 @@ struct RowSet {
   int heavy_threshold;
   int n_heavy;
   const int* __restrict__ heavy;
+  // k_step only: rows with light_max < len <= heavy_threshold run one warp
+  // per row (medium list, kWarps rows per block) instead of V lanes in the
+  // warp-owns-32-rows path, whose warps a long row would hold for many
+  // dependent load rounds.  Other kernels treat them as light rows.
+  int light_max = 0x7fffffff;
+  int n_medium = 0;
+  const int* __restrict__ medium = nullptr;
 };
 
 // Partial dot of one row over lanes [lane, lane+V, ...]; NR right-hand sides
@@ -638,6 +645,20 @@ __global__ void __launch_bounds__(kBlock, step_min_blocks<V>()) k_step(StepArgs 
     }
     return;
   }
+  const int medium_blocks = (a.rs.n_medium + kWarps - 1) / kWarps;
+  if ((int)blockIdx.x < a.rs.n_heavy + medium_blocks) {  // one warp per medium row
+    const int h = ((int)blockIdx.x - a.rs.n_heavy) * kWarps + (int)(threadIdx.x >> 5);
+    if (h >= a.rs.n_medium) return;  // warp-uniform
+    const int row = a.rs.medium[h];
+    double acc[1];
+    row_dot<32, 1>(a.rs, a.rs.ptr[row], a.rs.ptr[row + 1], threadIdx.x & 31, xin, acc);
+    const double d = group_sum<32>(acc[0]);
+    if ((threadIdx.x & 31) == 0) {
+      if (PRIMAL) bcast_if<PEERS>(P, 0, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast_if<PEERS>(P, 1, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
+    }
+    return;
+  }
   // Light rows: a warp owns 32 consecutive rows.  It computes them in V
   // passes of 32/V rows (V lanes per row, fixed lane order), parks row k's
   // dot in lane k with one shuffle per pass, then all 32 lanes run the
@@ -645,11 +666,14 @@ __global__ void __launch_bounds__(kBlock, step_min_blocks<V>()) k_step(StepArgs 
   // traffic (v1 ran the epilogue on one lane in V: ncu showed ~110
   // instructions per 32 entries, profiles/r01_csr_epilogue.md).
   const int lane = threadIdx.x & 31;
-  const long long warp_id = ((long long)(blockIdx.x - a.rs.n_heavy) * kBlock + threadIdx.x) >> 5;
+  const long long warp_id =
+      ((long long)(blockIdx.x - a.rs.n_heavy - medium_blocks) * kBlock + threadIdx.x) >> 5;
   const long long row0 = warp_id * 32;
   if (row0 >= a.rs.rows) return;  // warp-uniform
   const long long rl = row0 + lane;
   const bool in_range = rl < a.rs.rows;
+  RowSet lrs = a.rs;  // the light path skips heavy and medium rows
+  lrs.heavy_threshold = min(a.rs.heavy_threshold, a.rs.light_max);
   // epilogue operands: coalesced, loaded before the SpMV (V <= 8) or after it
   // (V >= 16, so that fewer registers are live in the row loop)
   double o1 = 0.0, o2 = 0.0, o3 = 0.0;
@@ -659,7 +683,7 @@ __global__ void __launch_bounds__(kBlock, step_min_blocks<V>()) k_step(StepArgs 
     o3 = a.xbar[rl];
   }
   bool my_ok;
-  const double mine = warp_rows_dot<V>(a.rs, row0, lane, xin, my_ok);
+  const double mine = warp_rows_dot<V>(lrs, row0, lane, xin, my_ok);
   if (kLateEpi && in_range) {
     o1 = a.cb[rl];
     o2 = a.x[rl];
@@ -1462,6 +1486,11 @@ int grid_rows(const RowSet& rs, int lanes) {
   return rs.n_heavy + (int)((rs.rows + (long long)kBlock - 1) / kBlock);
 }
 
+// k_step's grid: heavy rows (a block each), medium rows (a warp each), light rows
+int grid_step(const RowSet& rs) {
+  return rs.n_heavy + (rs.n_medium + kWarps - 1) / kWarps + (int)((rs.rows + (long long)kBlock - 1) / kBlock);
+}
+
 template <int V>
 struct SpmvLaunch {
   static int run(const RowSet& rs, const double* in, double* out, cudaStream_t s) {
@@ -1726,7 +1755,7 @@ int launch_step(pdhg_ctx* c, bool primal, int j) {
     return primal ? launch_ex(c, k_step_sell<true, PDHG_SELL_U>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j)
                   : launch_ex(c, k_step_sell<false, PDHG_SELL_U>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
   }
-  return dispatch_lanes<StepLaunchEx>(lanes, c, primal, a, j, grid_rows(a.rs, lanes), win_base, win);
+  return dispatch_lanes<StepLaunchEx>(lanes, c, primal, a, j, grid_step(a.rs), win_base, win);
 }
 
 int spmv(pdhg_ctx* c, bool transpose, const double* in, double* out) {
@@ -1793,6 +1822,19 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->At = RowSet{prob->at_ptr, prob->at_col, prob->at_val, prob->n,
                  prob->at_heavy_threshold > 0 ? prob->at_heavy_threshold : prob->heavy_threshold,
                  prob->at_n_heavy, prob->at_heavy};
+  for (int k = 0; k < 2; ++k) {  // medium rows (k_step only; not with a PSR layout)
+    RowSet& rs = k == 0 ? c->A : c->At;
+    const int nmed = k == 0 ? prob->a_n_medium : prob->at_n_medium;
+    const int* med = k == 0 ? prob->a_medium : prob->at_medium;
+    const int lmax = k == 0 ? prob->a_light_max : prob->at_light_max;
+    const bool psr = (k == 0 ? prob->a_psr : prob->at_psr) != nullptr;
+    if (nmed < 0 || (nmed > 0 && (!med || lmax <= 0))) return fail(PDHG_ERR_ARG, "bad medium-row list");
+    if (nmed > 0 && !psr) {
+      rs.n_medium = nmed;
+      rs.medium = med;
+      rs.light_max = lmax;
+    }
+  }
   c->a_lanes = prob->a_lanes > 0 ? prob->a_lanes : auto_lanes(prob->nnz, prob->m);
   c->at_lanes = prob->at_lanes > 0 ? prob->at_lanes
                                     : auto_lanes(prob->at_nnz > 0 ? prob->at_nnz : prob->nnz, prob->n);

@@ -45,6 +45,13 @@ class GpuOptions:
                      operator: 32 x lanes per row, so a light warp never runs more
                      than ~8 dependent load rounds on one row; measured on config 1,
                      profiles/r01_pipeline.md).
+    medium_per_lane: CSR step kernels: rows longer than this many entries per lane
+                     (x lanes per row) but not heavy run one warp per row, so a
+                     long row does not hold a warp-owns-32-rows pass for many
+                     dependent load rounds.  -1 = auto: 8 for <= 8 lanes per row
+                     (config 1's dual step 12.1 -> 9.8 us), 16 for 16 lanes (config
+                     2's 104.6 -> 99.4 us; 8 would slow config 4's 944 -> 976 us);
+                     0 = off.
     opnorm:          override the power-iteration estimate (parity fallback).
     cache_layout:    keep the device layout of a model for repeated solves.
     psr:             "auto" | "on" | "off" -- panel-staged rows layout for the step
@@ -83,6 +90,7 @@ class GpuOptions:
     a_lanes: int = 0
     at_lanes: int = 0
     heavy_threshold: int = 0
+    medium_per_lane: int = -1
     opnorm: float | None = None
     cache_layout: bool = True
     psr: str = "off"
@@ -126,6 +134,18 @@ def _torch():
         raise N.NativeError("paper_2603_03150_b200 needs a CUDA device (B200, sm_100a); "
                             "there is no CPU fallback")
     return torch
+
+
+def _medium_list(torch, ptr, lanes: int, H: int, per_lane: int):
+    """Rows with per_lane*lanes < length <= H (row order) and that light limit."""
+    if per_lane < 0:
+        per_lane = 8 if lanes <= 8 else 16
+    light_max = per_lane * lanes
+    if per_lane <= 0 or lanes >= 32 or light_max >= H:
+        return torch.empty(0, dtype=torch.int32, device=ptr.device), 0
+    lens = ptr[1:] - ptr[:-1]
+    idx = torch.nonzero((lens > light_max) & (lens <= H)).flatten().to(torch.int32).contiguous()
+    return idx, light_max
 
 
 def _as_csr(A):
@@ -220,6 +240,9 @@ class DeviceLp:
                 self.heavy = (H, Ht)
                 self.a_heavy = torch.nonzero((self.a_ptr[1:] - self.a_ptr[:-1]) > H).flatten().to(torch.int32)
                 self.at_heavy = torch.nonzero((self.at_ptr[1:] - self.at_ptr[:-1]) > Ht).flatten().to(torch.int32)
+                self.a_medium, la = _medium_list(torch, self.a_ptr, self.a_lanes, H, opts.medium_per_lane)
+                self.at_medium, lt = _medium_list(torch, self.at_ptr, self.at_lanes, Ht, opts.medium_per_lane)
+                self.light_max = (la, lt)
                 self.psr_info = {}
                 self._psr = {}
                 for key, rows, cols, nz, ptr, col, val in (
@@ -271,6 +294,10 @@ class DeviceLp:
         p.a_sell = C.pointer(self._sell["A"][0]) if self._sell["A"] else None
         p.at_sell = C.pointer(self._sell["At"][0]) if self._sell["At"] else None
         p.a_n_heavy, p.at_n_heavy = self.a_heavy.numel(), self.at_heavy.numel()
+        p.a_light_max, p.at_light_max = self.light_max
+        p.a_n_medium, p.at_n_medium = self.a_medium.numel(), self.at_medium.numel()
+        p.a_medium = self.a_medium.data_ptr() if p.a_n_medium else None
+        p.at_medium = self.at_medium.data_ptr() if p.at_n_medium else None
         p.a_heavy = self.a_heavy.data_ptr() if p.a_n_heavy else None
         p.at_heavy = self.at_heavy.data_ptr() if p.at_n_heavy else None
         p.a_psr = C.pointer(self._psr["A"][0]) if self._psr["A"] else None

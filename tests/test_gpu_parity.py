@@ -38,6 +38,8 @@ LAYOUTS = {
     "persistent": dict(psr="off", sell="off", persistent="on"),
     "tiny": dict(psr="off", sell="off", persistent="tiny"),
     "csr_split2": dict(psr="off", sell="off", persistent="off", dual_split=2),
+    # every row longer than its lane count runs warp-per-row (the medium tier)
+    "csr_medium": dict(psr="off", sell="off", persistent="off", medium_per_lane=1),
     "psr_staged": dict(psr="on", psr_min_staged=1),
     "psr_remote": dict(psr="on", psr_min_staged=10**9),
 }
