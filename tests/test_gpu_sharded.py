@@ -223,3 +223,19 @@ def test_sharded_sell_layouts_match_single_gpu(eng, kind):
     assert s1.iterations == s2.iterations == 256 and s1.restarts == s2.restarts
     np.testing.assert_allclose(p2.x, p1.x, rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(p2.y, p1.y, rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["loopback", "loopback_fused"])
+def test_sharded_medium_rows_match_reference(eng, kind):
+    """Shards with every longer-than-lanes row on the warp-per-row tier
+    reproduce the golden run."""
+    from paper_2603_03150_b200.sharded import run_pdhg_sharded
+
+    gm = load_golden("config0_s0")
+    T = eng.types()
+    opts = eng.GpuOptions(sell="off", medium_per_lane=1)
+    pt, st = run_pdhg_sharded(gm, T.PdhgParams(eps_rel=1e-4), G=2, gpu=opts, comm_kind=kind)
+    r = gm.run("e4")
+    assert st.status.value == "Optimal"
+    assert st.iterations == int(r["iterations"]) and st.restarts == int(r["restarts"])
+    assert float(gm.c @ pt.x) == pytest.approx(float(r["obj"]), rel=1e-6)
