@@ -436,7 +436,9 @@ def run_ours(args):
                 "allocator": "warm: torch caching allocator holds the timing leg's freed device blocks"},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
-        "gpu_launches": args.steps * (2 * CHECK_EVERY + 3),
+        # per step: 2 step kernels per iteration + the check's k_pair x2,
+        # k_check_primal, k_check_dual(_sell), k_reduce (ncu launch list)
+        "gpu_launches": args.steps * (2 * CHECK_EVERY + 5),
         "setup_s": t_setup,
         "time_to_1e4": out,
     }
