@@ -148,14 +148,20 @@ typedef struct pdhg_problem {
 
 typedef struct pdhg_ctx pdhg_ctx;
 
+/* ABI version and the thread-local message of the last failing call (the
+ * reference raises Python exceptions instead; the Python host re-raises
+ * them as InvalidModelError / ValueError where pdhg.py / lp_core.py do). */
 int pdhg_abi_version(void);
 const char* pdhg_last_error(void);
 
 /* Device workspace the caller must provide (m, n: full vector lengths --
- * m_full, n_full when sharded). */
+ * m_full, n_full when sharded): x, xe, x̄, x_best, z_best, y, ȳ, y_best
+ * (PdhgState, pdhg.py:51-67) plus scratch, partials and step parameters. */
 size_t pdhg_workspace_bytes(int32_t m, int32_t n);
 
-/* Create / destroy an engine context bound to `stream` (a cudaStream_t). */
+/* Create / destroy an engine context bound to `stream` (a cudaStream_t):
+ * the device side of one run_pdhg call on one StandardLp (pdhg.py:162-258;
+ * the matrix layouts replace StandardLp.A / A_csc, lp_core.py:114-142). */
 int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_bytes,
                     void* stream, pdhg_ctx** out);
 int pdhg_ctx_destroy(pdhg_ctx* ctx);
@@ -214,10 +220,12 @@ int pdhg_save_best(pdhg_ctx* ctx, int32_t which, int32_t flags);
 /* Copy point spec (as in pdhg_check) to host arrays (any may be NULL).
  * z is max(0, c - A'y) unless PDHG_SPEC_BEST_Z selects the stored best z. */
 int pdhg_fetch(pdhg_ctx* ctx, int32_t spec, double* x_host, double* y_host, double* z_host);
-/* Device-side form of pdhg_fetch: computes the point's z on the device (into
- * scratch, unless spec carries PDHG_SPEC_BEST_Z) and returns the device
- * addresses of x, y, z (full padded lengths), queued on the context's stream
- * without synchronising -- for callers with their own download path. */
+/* Device-side form of pdhg_fetch (the KktPoint run_pdhg returns,
+ * pdhg.py:249-258, with z = extract_reduced_costs, pdhg.py:112-114):
+ * computes the point's z on the device (into scratch, unless spec carries
+ * PDHG_SPEC_BEST_Z) and returns the device addresses of x, y, z (full padded
+ * lengths), queued on the context's stream without synchronising -- for
+ * callers with their own download path. */
 int pdhg_point_device(pdhg_ctx* ctx, int32_t spec, const double** x_dev, const double** y_dev,
                       const double** z_dev);
 
@@ -238,11 +246,13 @@ int pdhg_point_device(pdhg_ctx* ctx, int32_t spec, const double** x_dev, const d
 #define PDHG_VEC_FAILWORD 12  /* the int64 first-failure iteration word of this context */
 void* pdhg_vector(pdhg_ctx* ctx, int32_t which);
 
-/* z = max(0, c - A'y) for this shard's rows of A' into z_slice (device). */
+/* z = max(0, c - A'y) for this shard's rows of A' into z_slice (device):
+ * extract_reduced_costs, pdhg.py:112-114. */
 int pdhg_reduced_costs(pdhg_ctx* ctx, int32_t spec, double* z_slice);
 
 /* Host-driven stepping (sharded execution exchanges vectors between the
- * half steps): set the step parameters of the next steps (as
+ * half steps; pdhg_step, pdhg.py:140-151, split at the x+ / y+ boundary):
+ * set the step parameters of the next steps (as
  * pdhg_run_period does), launch one primal (primal=1) or dual half step
  * number j, and read the first failing iteration (-1 = none, syncs). */
 int pdhg_set_step(pdhg_ctx* ctx, int64_t iter0, double tau_over_omega, double sigma_omega,
@@ -273,7 +283,8 @@ int pdhg_div(pdhg_ctx* ctx, const double* w, double* v, int64_t len, double s);
 int pdhg_time_kernel(pdhg_ctx* ctx, int32_t which, int32_t reps, double tau_over_omega,
                      double sigma_omega, double* avg_ms_out);
 
-/* Layout helper for the split dual step: split_out[(k-1)*m + i] = first
+/* Layout helper for the split dual step (A @ xe of pdhg.py:143 over column
+ * chunks): split_out[(k-1)*m + i] = first
  * entry of row i whose column is >= k*chunk, k = 1..K-1.  Rows must have
  * sorted columns; *unsorted_out = 1 reports a row that has not (then do not
  * split).  flag_dev: 4 bytes of device scratch. */
@@ -281,7 +292,8 @@ int pdhg_split_build(int32_t m, const int32_t* ptr, const int32_t* col, int32_t 
                      int32_t* split_out, int32_t* flag_dev, void* stream, int32_t* unsorted_out);
 
 /* Layout helper: A' (CSR of the transpose, = CSC of A with rows ascending
- * in each column, as scipy's tocsc) from CSR A, all on the device.
+ * in each column, as scipy's tocsc behind StandardLp.A_csc, lp_core.py:133-138)
+ * from CSR A, all on the device.
  * tmp must hold pdhg_transpose_tmp_bytes(nnz, m, n) bytes. */
 size_t pdhg_transpose_tmp_bytes(int64_t nnz, int32_t m, int32_t n);
 int pdhg_transpose_csr(int32_t m, int32_t n, int64_t nnz, const int32_t* a_ptr,
@@ -289,7 +301,8 @@ int pdhg_transpose_csr(int32_t m, int32_t n, int64_t nnz, const int32_t* a_ptr,
                        int32_t* at_col, double* at_val, void* tmp, size_t tmp_bytes,
                        void* stream);
 
-/* PSR layout build (device).  pdhg_psr_plan fixes the row-block size R and
+/* PSR layout build (device; an optional step layout for the products of
+ * pdhg.py:142-143).  pdhg_psr_plan fixes the row-block size R and
  * panel width W from the shape, counts entries per (row block, panel),
  * marks panels with >= min_staged entries as staged and returns the sizes
  * the caller must allocate: nblk, ntiles, and the number of entries that
@@ -388,7 +401,9 @@ int pdhg_violation(int32_t m, int32_t n, const int32_t* a_ptr, const int32_t* a_
                    double* out_host);
 
 
-/* Sliced-ELL build (device): plan writes width (nslices = ceil(rows/32)) and
+/* Sliced-ELL build (device; the step / check / power-iteration layout of the
+ * products at pdhg.py:89-109,142-143 for near-uniform rows): plan writes
+ * width (nslices = ceil(rows/32)) and
  * sptr (nslices+1) and returns the slot count; optionally sort orders each
  * slice's rows by length (perm: lane -> row offset, inv: row offset -> lane,
  * both nslices*32 bytes); the caller allocates slots-sized col/val and calls
