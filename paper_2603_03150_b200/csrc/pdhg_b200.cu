@@ -135,6 +135,10 @@ __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 #ifndef PDHG_LATE16
 #define PDHG_LATE16 1
 #endif
+// Two-point A-side check in the warp-owns-32-rows shape (k_check_primal_rows)
+#ifndef PDHG_CHECK_ROWS
+#define PDHG_CHECK_ROWS 1
+#endif
 // row_dot_pair (two-point checks): entries in flight per lane for V >= 16
 #ifndef PDHG_PAIR_U16
 #define PDHG_PAIR_U16 4
@@ -1171,6 +1175,86 @@ __global__ void k_pair(const double* __restrict__ a, const double* __restrict__ 
     out[i] = make_double2(a[i], b[i]);
 }
 
+// Two-point primal-side terms in the step kernel's shape: a warp owns 32
+// consecutive rows (grid-strided over a fixed grid), computes them in V
+// passes of 32/V rows with row_dot_pair + group_sum (so every row's two dots
+// are exactly k_check_primal's), parks row k's dots in lane k and runs the
+// epilogue on all 32 lanes with coalesced b / y loads.
+template <int V>
+__global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_primal_rows(RowSet rs, const double* __restrict__ b,
+                                                                         CheckPts pts,
+                                                                         double* __restrict__ partials) {
+  __shared__ double red[kWarps];
+  constexpr int G = 32 / V;
+  double rp2[2] = {0.0, 0.0}, rpmax[2] = {0.0, 0.0}, by[2] = {0.0, 0.0};
+  auto row_terms_pre = [&](double bi, double y0, double y1, double d0, double d1) {
+    const double r0 = __dsub_rn(bi, d0), r1 = __dsub_rn(bi, d1);
+    rp2[0] = fma(r0, r0, rp2[0]);
+    rp2[1] = fma(r1, r1, rp2[1]);
+    rpmax[0] = nan_max(fabs(r0), rpmax[0]);
+    rpmax[1] = nan_max(fabs(r1), rpmax[1]);
+    by[0] = fma(bi, y0, by[0]);
+    by[1] = fma(bi, y1, by[1]);
+  };
+  for (int h = blockIdx.x; h < rs.n_heavy; h += gridDim.x) {
+    const int row = rs.heavy[h];
+    double acc[2], d[2];
+    row_dot_pair<kBlock>(rs, rs.ptr[row], rs.ptr[row + 1], threadIdx.x, pts.pair, acc);
+    d[0] = block_sum(acc[0], red);
+    d[1] = block_sum(acc[1], red);
+    if (threadIdx.x == 0) row_terms_pre(b[row], pts.y[0][row], pts.y[1][row], d[0], d[1]);
+  }
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = (long long)gridDim.x * kWarps;
+  const long long ngroups = (rs.rows + 31) / 32;
+  for (long long gw = (long long)blockIdx.x * kWarps + (threadIdx.x >> 5); gw < ngroups; gw += nwarps) {
+    const long long rl = gw * 32 + lane;
+    bool ok = rl < rs.rows;
+    int my_s = 0, my_e = 0;
+    if (ok) {
+      my_s = rs.ptr[rl];
+      my_e = rs.ptr[rl + 1];
+      if (my_e - my_s > rs.heavy_threshold) ok = false;
+    }
+    if (!ok) my_e = my_s;
+    double bi = 0.0, y0 = 0.0, y1 = 0.0;
+    if (ok) {
+      bi = b[rl];
+      y0 = pts.y[0][rl];
+      y1 = pts.y[1][rl];
+    }
+    double m0 = 0.0, m1 = 0.0;
+#pragma unroll 1
+    for (int pass = 0; pass < V; ++pass) {
+      const int src = pass * G + lane / V;
+      const int s0 = __shfl_sync(0xffffffffu, my_s, src);
+      const int e0 = __shfl_sync(0xffffffffu, my_e, src);
+      double acc[2];
+      row_dot_pair<V>(rs, s0, e0, lane % V, pts.pair, acc);
+      const double d0 = group_sum<V>(acc[0]), d1 = group_sum<V>(acc[1]);
+      const int from = ((lane - pass * G) & (G - 1)) * V;
+      const double g0 = __shfl_sync(0xffffffffu, d0, from), g1 = __shfl_sync(0xffffffffu, d1, from);
+      if (lane / G == pass) {
+        m0 = g0;
+        m1 = g1;
+      }
+    }
+    if (ok) row_terms_pre(bi, y0, y1, m0, m1);
+  }
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const double t0 = block_sum(rp2[p], red);
+    const double t1 = block_max(rpmax[p], red);
+    const double t2 = block_sum(by[p], red);
+    if (threadIdx.x == 0) {
+      double* o = partials + (size_t)blockIdx.x * kMaxQ + p * PDHG_NQ;
+      o[PDHG_Q_RP2] = t0;
+      o[PDHG_Q_RPMAX] = t1;
+      o[PDHG_Q_BY] = t2;
+    }
+  }
+}
+
 // Per-point primal-side terms over rows of A: r_p = b - A x (lp_core.py:436).
 template <int V, int NP, bool PAIR = false>
 __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_primal(RowSet rs, const double* __restrict__ b,
@@ -1506,6 +1590,8 @@ struct CheckLaunch {
                  double* partials, cudaStream_t s) {
     if (primal) {
       if (np == 1) k_check_primal<V, 1><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
+      else if (pts.pair && V >= 16 && PDHG_CHECK_ROWS)
+        k_check_primal_rows<(V >= 16 ? V : 16)><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
       else if (pts.pair) k_check_primal<V, 2, true><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
       else k_check_primal<V, 2><<<kCheckBlocks, kBlock, 0, s>>>(rs, bc, pts, partials);
     } else {
