@@ -123,8 +123,13 @@ def auto_lanes(nnz: int, rows: int) -> int:
 
 
 def heavy_threshold(lanes: int) -> int:
-    """Auto heavy-row threshold for an operator processed with `lanes` lanes per row."""
-    return max(32, 32 * lanes)
+    """Auto heavy-row threshold for an operator processed with `lanes` lanes per row.
+
+    Rows between 8-16 entries per lane and this threshold run warp-per-row
+    (the medium tier), so only rows of >= 128 entries need a whole block:
+    config 1 (2 lanes) dual step 10.5 -> 8.7 us with 128 instead of 64;
+    16 lanes keeps 512 (1,024 measured 7 % slower on config 2)."""
+    return max(128, 32 * lanes)
 
 
 def _torch():
