@@ -8,8 +8,9 @@ lp_core.py:145-166, ``TerminationCheck`` lp_core.py:180-206,
 ``StandardLp`` lp_core.py:106-142), so callers such as the reference's
 ``hybrid_solve`` and its IPM warm start consume our results unchanged.
 Otherwise (e.g. on a GPU box without the reference) field-for-field mirrors
-are used.  ``SolveStats`` gains one defaulted field, ``history`` (one dict
-per KKT check), which every existing field keeps around.
+are used.  ``SolveStats`` gains two defaulted fields, ``history`` (one dict
+per KKT check) and ``timings`` (wall seconds of the engine's phases); every
+existing field is unchanged.
 """
 
 from __future__ import annotations
