@@ -12,12 +12,17 @@ metric through the public drop-in call ``run_pdhg(p, params)`` on host
 arrays: layout upload + device transpose + power iteration + K*64
 iterations + result download, all inside the timed region.
 
-``--impl reference`` times the CPU oracle (oracle/pdhg_port.py: the
-reference's numpy/scipy run_pdhg restated, pinned bit-for-bit against the
-reference in tests/test_oracle_golden.py) on the same instance: per-step
-samples of pdhg_step plus one scored check amortised over 64 iterations.
-The reference path is single-threaded (scipy csr_matvec); BLAS is pinned to
-one thread.
+``--impl reference`` times the reference's own CPU implementation of the
+path: the UNMODIFIED ``hybridlp`` package installed by ``oracle/make_ref.sh``
+into oracle/_ref/site (its ``pdhg_step``, pdhg.py:140-151, and its two-point
+``_score`` + ``check_relative_termination`` check, pdhg.py:201-204) on the
+same instance, with OPENBLAS/OMP threads pinned to 1 (scipy's csr_matvec is
+single-threaded).  A step is the same unit in both arms, one
+period of 64 iterations plus the check; on the CPU it is extrapolated from a
+bounded sample (K pdhg_step calls + one check), stated in
+``cpu_baseline.sample``.  Without oracle/_ref (not built) it falls back to
+the oracle port (oracle/pdhg_port.py, pinned bit-for-bit to the reference),
+``kind: "port"``.
 
 Inputs (4.8 GB of matrix) are far larger than the 126 MB L2, so no L2 flush
 is needed between steps.
@@ -40,6 +45,36 @@ sys.path.insert(0, str(ROOT))
 METRIC = "PDHG iters/s and time-to-1e-4 rel KKT; achieved HBM GB/s vs B200 peak"
 UNIT = "iter/s"
 CHECK_EVERY = 64
+NOMINAL_HBM_GBS = 8000.0   # north_star: "roughly 8 TB/s per B200"
+
+
+def _config(m: int, n: int, nnz: int, scale: float, seed: int) -> dict:
+    """The `config` object, identical in both arms (same instance, same step)."""
+    return {"workload": f"config4 (m={m}, n={n}, nnz={nnz}) PDHG period = {CHECK_EVERY} iterations "
+                        f"+ KKT check (pdhg.py:140-151, 198-204)",
+            "scale": scale, "seed": seed,
+            "l2": (f"no flush: {24 * nnz / 1e9:.1f} GB matrix (A and A') > 126 MB L2 (inputs larger than L2)"
+                   if 24 * nnz > 4 * 126e6 else "no flush (small scaled instance; L2-resident)")}
+
+
+def _cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _reference_ttk_iterations():
+    """Iterations the REAL reference needed to reach 1e-4 on this instance
+    (tests/golden/run_config4_s1.json, oracle/make_golden_runs.py), or None."""
+    f = ROOT / "tests" / "golden" / "run_config4_s1.json"
+    try:
+        return int(json.loads(f.read_text())["iterations"])
+    except Exception:
+        return None
 
 
 def _env_rank():
@@ -150,82 +185,119 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_sample(inst, steps: int = 3) -> dict:
-    """Oracle (reference numpy/scipy path, 1 thread) per-iteration time on `inst`."""
+def _pin_host_threads() -> None:
+    """The reference path is single-threaded (scipy csr_matvec); pin BLAS and
+    OpenMP to one thread for its norms/dots too.  Effective
+    when called before numpy is first imported (the reference arm)."""
+    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+
+
+def _reference_impl():
+    """(module-like namespace, kind): the unmodified reference package from
+    oracle/_ref/site when built (oracle/make_ref.sh), else the oracle port."""
+    site = ROOT / "oracle" / "_ref" / "site"
+    if (site / "hybridlp" / "pdhg.py").exists():
+        if str(site) not in sys.path:
+            sys.path.insert(0, str(site))
+        import hybridlp
+        from hybridlp import lp_core, pdhg
+
+        if not str(Path(hybridlp.__file__).resolve()).startswith(str(site.resolve())):
+            raise RuntimeError(f"hybridlp resolved outside oracle/_ref: {hybridlp.__file__}")
+
+        class R:
+            kind = "reference"
+            where = "hybridlp (unmodified reference, oracle/_ref/site)"
+            model = staticmethod(lambda A, b, c: lp_core.StandardLp(A, b, c))
+            step = staticmethod(pdhg.pdhg_step)
+            score = staticmethod(pdhg._score)
+            term = staticmethod(lp_core.check_relative_termination)
+            State = pdhg.PdhgState
+        return R
+    import oracle
+    from oracle.pdhg_port import Model, PdhgState, _score, check_relative_termination
+
+    class P:
+        kind = "port"
+        where = "oracle/pdhg_port.py (reference restated, pinned bit-for-bit)"
+        model = staticmethod(Model)
+        step = staticmethod(oracle.pdhg_step)
+        score = staticmethod(_score)
+        term = staticmethod(check_relative_termination)
+        State = PdhgState
+    return P
+
+
+def cpu_sample(inst, steps: int = 3, warmup: int = 1) -> dict:
+    """The reference's CPU path on `inst`: `steps` timed pdhg_step calls (after
+    `warmup` untimed ones) and one two-point check (pdhg.py:201-204), i.e. one
+    period = 64 steps + 1 check, extrapolated from the sample."""
     import numpy as np
 
-    import oracle
-    from oracle.pdhg_port import KktPoint, Model, PdhgState, _score, check_relative_termination
-
-    p = Model(inst.A, inst.b, inst.c)
+    R = _reference_impl()
+    p = R.model(inst.A, inst.b, inst.c)
     t = time.perf_counter()
-    p.A_csc  # the reference builds the CSC copy lazily on first at_y (lp_core.py:133-138)
+    p.A_csc  # the reference builds its CSC copy lazily on first at_y (lp_core.py:133-138)
     t_csc = time.perf_counter() - t
-    st = PdhgState(x=np.zeros(p.n), y=np.zeros(p.m), avg_x=np.zeros(p.n), avg_y=np.zeros(p.m),
-                   avg_weight=0.0, tau=0.5 / 40.0, sigma=0.5 / 40.0, omega=1.0, iterations=0,
-                   restarts=0, restart_x=None, restart_y=None, restart_score=1.0)
-    oracle.pdhg_step(st, p)  # warm
-    t = time.perf_counter()
+    st = R.State(x=np.zeros(p.n), y=np.zeros(p.m), avg_x=np.zeros(p.n), avg_y=np.zeros(p.m),
+                 avg_weight=0.0, tau=0.5 / 40.0, sigma=0.5 / 40.0, omega=1.0, iterations=0,
+                 restarts=0, restart_x=None, restart_y=None, restart_score=1.0)
+    for _ in range(max(1, warmup)):
+        R.step(st, p)
+    samples = []
     for _ in range(steps):
-        oracle.pdhg_step(st, p)
-    t_step = (time.perf_counter() - t) / steps
+        t = time.perf_counter()
+        R.step(st, p)
+        samples.append(time.perf_counter() - t)
     t = time.perf_counter()
-    cur_pt, _, _ = _score(p, st.x, st.y)
-    avg_pt, _, _ = _score(p, st.avg_x, st.avg_y)
-    check_relative_termination(p, cur_pt, 1e-4)
-    check_relative_termination(p, avg_pt, 1e-4)
+    cur_pt, _, _ = R.score(p, st.x, st.y)
+    avg_pt, _, _ = R.score(p, st.avg_x, st.avg_y)
+    R.term(p, cur_pt, 1e-4)
+    R.term(p, avg_pt, 1e-4)
     t_check = time.perf_counter() - t
+    t_step = sum(samples) / len(samples)
     per_iter = t_step + t_check / CHECK_EVERY
     return {"per_iter_s": per_iter, "step_s": t_step, "check_s": t_check, "tocsc_s": t_csc,
-            "steps": steps}
+            "steps": steps, "step_s_samples": samples, "kind": R.kind, "impl": R.where}
+
+
+def _cpu_baseline(cs: dict, m: int, n: int, nnz: int) -> dict:
+    value = 1.0 / cs["per_iter_s"]
+    ref_its = _reference_ttk_iterations()
+    out = {"value": value, "unit": UNIT, "cores": 1, "kind": cs["kind"],
+           "sample": (f"{cs['impl']} on the same config4 instance (m={m}, n={n}, nnz={nnz}): "
+                      f"{cs['steps']} timed pdhg_step calls ({cs['step_s']:.3f} s each) + one two-point "
+                      f"check ({cs['check_s']:.2f} s) amortised over {CHECK_EVERY} iterations; "
+                      f"OPENBLAS/OMP threads = 1 (scipy csr_matvec is single-threaded)"),
+           "host": {"cpu_model": _cpu_model(), "nproc": os.cpu_count(), "active_cores": 1},
+           "ms_per_period": (CHECK_EVERY * cs["step_s"] + cs["check_s"]) * 1e3}
+    if ref_its:
+        out["time_to_1e4_s"] = {"value": ref_its * cs["per_iter_s"], "iterations": ref_its,
+                                "note": "extrapolated: iterations the real reference took to reach 1e-4 "
+                                        "on this instance (tests/golden/run_config4_s1.json) x the "
+                                        "sampled seconds per iteration"}
+    return out
 
 
 def run_reference(args):
     rank, world, _ = _env_rank()
     if rank != 0:
         return 0
-    # all host threads the reference can use: scipy's csr_matvec and numpy's
-    # ufuncs are single-threaded; BLAS (the norms and dots) is left unrestricted
+    _pin_host_threads()
     inst = _instance(args.scale, args.seed)
-    samples = []
-    import numpy as np
-
-    import oracle
-    from oracle.pdhg_port import Model, PdhgState, _score, check_relative_termination
-
-    p = Model(inst.A, inst.b, inst.c)
-    p.A_csc
-    st = PdhgState(x=np.zeros(p.n), y=np.zeros(p.m), avg_x=np.zeros(p.n), avg_y=np.zeros(p.m),
-                   avg_weight=0.0, tau=0.5 / 40.0, sigma=0.5 / 40.0, omega=1.0, iterations=0,
-                   restarts=0, restart_x=None, restart_y=None, restart_score=1.0)
-    for _ in range(args.warmup):
-        oracle.pdhg_step(st, p)
-    t = time.perf_counter()
-    cur_pt, _, _ = _score(p, st.x, st.y)
-    avg_pt, _, _ = _score(p, st.avg_x, st.avg_y)
-    check_relative_termination(p, cur_pt, 1e-4)
-    check_relative_termination(p, avg_pt, 1e-4)
-    t_check = time.perf_counter() - t
-    for _ in range(args.steps):
-        t = time.perf_counter()
-        oracle.pdhg_step(st, p)
-        samples.append(time.perf_counter() - t)
-    per_iter = sum(samples) / len(samples) + t_check / CHECK_EVERY
-    value = 1.0 / per_iter
-    sample = (f"{args.steps} pdhg_step calls + 1 scored check (2 points, amortised over "
-              f"{CHECK_EVERY} iterations) of the oracle on config4 scale={args.scale}; "
-              f"scipy csr_matvec and numpy ufuncs single-threaded (1 core busy), BLAS threads "
-              f"unrestricted ({os.cpu_count()} host CPUs)")
+    cs = cpu_sample(inst, steps=args.steps, warmup=args.warmup)
+    cpu = _cpu_baseline(cs, inst.m, inst.n, inst.nnz)
+    value = cpu["value"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": per_iter * 1e3, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": cpu["ms_per_period"], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": f"config4 (m={inst.m}, n={inst.n}, nnz={inst.nnz}) PDHG iteration",
-                   "scale": args.scale, "seed": args.seed},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "config": _config(inst.m, inst.n, inst.nnz, args.scale, args.seed),
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "step_s_samples": samples, "check_s": t_check,
+        "step_s_samples": cs["step_s_samples"], "check_s": cs["check_s"],
     }
     print(json.dumps(line))
     return 0
@@ -276,15 +348,40 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # the product's period call (engine._run): the graph of 64 iterations and
+    # the two-point check, one host synchronisation per period
+    period = getattr(dev, "run_period_check", None)
     with ClockSampler(local) as clk:
         ev0.record(s)
         for _ in range(args.steps):
-            fail = dev.run_period(CHECK_EVERY, it, step, step, float(it))
-            dev.check(N.PT_CUR, N.PT_AVG)
+            if period is not None:
+                fail, _ = period(CHECK_EVERY, it, step, step, float(it), N.PT_CUR, N.PT_AVG)
+            else:
+                fail = dev.run_period(CHECK_EVERY, it, step, step, float(it))
+                dev.check(N.PT_CUR, N.PT_AVG)
             it += CHECK_EVERY
         ev1.record(s)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
+    # where a period's time goes (after the timed region, same sustained state):
+    # events around the graph of 64 iterations and around the check
+    breakdown = None
+    if world == 1:
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(3)]
+        for e in evs:
+            e[0].record(s)
+            dev.run_period(CHECK_EVERY, it, step, step, float(it))
+            e[1].record(s)
+            dev.check(N.PT_CUR, N.PT_AVG)
+            e[2].record(s)
+            it += CHECK_EVERY
+        torch.cuda.synchronize()
+        g_ms = [e[0].elapsed_time(e[1]) for e in evs]
+        c_ms = [e[1].elapsed_time(e[2]) for e in evs]
+        breakdown = {"graph_64_iterations_ms": statistics.median(g_ms),
+                     "check_ms": statistics.median(c_ms),
+                     "method": "3 periods after the timed region: CUDA events around the period graph "
+                               "and around the two-point check (run_period + check, 2 host syncs)"}
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -327,6 +424,7 @@ def run_ours(args):
     iter_ms = ms_per_step / CHECK_EVERY
     roofline = {"bound": "hbm", "kernel": f"k_step<{'primal' if top == 'primal' else 'dual'}>",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "frac_nominal": achieved / NOMINAL_HBM_GBS,
                 "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
                 "kernels_ms": tk, "kernels_ms_method": (
@@ -342,6 +440,15 @@ def run_ours(args):
     # the timing leg's device memory goes back to torch's caching allocator
     # (not to the driver): the e2e call below reuses it, as repeated calls in
     # one serving process do (reported as e2e.allocator)
+    def _op_layout(key, lanes):
+        if getattr(kdev, "_psr", {}).get(key):
+            return "psr"
+        if getattr(kdev, "_sell", {}).get(key):
+            return "sliced-ELL"
+        return f"csr-vector ({lanes} lanes/row)"
+
+    layout_name = {"A (dual step)": _op_layout("A", kdev.a_lanes),
+                   "A' (primal step)": _op_layout("At", kdev.at_lanes)}
     del dev, kdev
 
     # ---- e2e through the public drop-in call, host arrays in, host arrays out
@@ -397,6 +504,7 @@ def run_ours(args):
         out = {"status": st2.status.value, "iterations": st2.iterations, "restarts": st2.restarts,
                "pdhg_wall_s": wall2, "ruiz_s": t_ruiz, "ruiz_passes": info.applied_iterations,
                "total_s": t_ruiz + wall2, "ruiz_phases_s": dict(eng.ruiz.last_timings),
+               "reference_iterations": _reference_ttk_iterations(),
                "note": "device Ruiz (bit-identical to transform.py:35-77) + run_pdhg to eps_rel=1e-4"
                        + (f", sharded over {world} GPUs" if world > 1 else "")}
         if args.ttk_unscaled and world == 1:
@@ -406,29 +514,23 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
         cs = cpu_sample(inst, steps=args.cpu_steps)
-        cpu = {"value": 1.0 / cs["per_iter_s"], "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": (f"oracle (reference numpy/scipy path) on the same config4 instance: "
-                          f"{cs['steps']} pdhg_step calls ({cs['step_s']:.3f} s each) + one scored "
-                          f"check ({cs['check_s']:.2f} s) amortised over 64 iterations; 1 thread"),
-               "detail": cs}
+        cpu = _cpu_baseline(cs, m, n, nnz)
     if rank != 0:
         return 0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config4 (m={m}, n={n}, nnz={nnz}) PDHG period = 64 iterations + KKT check",
-                   "scale": args.scale, "seed": args.seed,
-                   "l2": "no flush: 4.8 GB matrix > 126 MB L2 (inputs larger than L2)",
-                   "parallelism": ((f"A rows / A' rows sharded x{world}, equal nnz; " +
+        "config": _config(m, n, nnz, args.scale, args.seed),
+        "layout": {"parallelism": ((f"A rows / A' rows sharded x{world}, equal nnz; " +
                                     ("xe / y pushed to peers by the step epilogues (symmetric memory, "
                                      "NVLink stores) + stream barrier" if args.comm == "peer" else
                                      "NCCL all-gather of xe and y per iteration"))
                                    if world > 1 else "1 GPU"),
-                   "kernel_layout": "psr" if args.psr == "on" else "csr-vector"},
+                   "kernel_layout": layout_name},
         "roofline": roofline,
+        "period_breakdown": breakdown,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / K,
                 "d2h_bytes_per_step": d2h / K, "iterations": st.iterations,
                 "wall_s": wall_e2e, "timings": getattr(st, "timings", None),

@@ -30,11 +30,12 @@ from paper_2603_03150_b200.instances import config1_general, config3_general  # 
 
 def main(which: str, scale: float = 1.0):
     t0 = time.perf_counter()
-    if which == "config2":   # built directly in standard form (instances.config2)
-        from paper_2603_03150_b200.instances import config2
+    if which in ("config2", "config4"):   # built directly in standard form
+        from paper_2603_03150_b200 import instances
 
-        inst = config2(scale)
+        inst = getattr(instances, which)(scale)
         p = hybridlp.StandardLp(inst.A, inst.b, inst.c)
+        del inst
     else:
         g = (config1_general if which == "config1" else config3_general)(scale).to_reference()
         t0 = time.perf_counter()
@@ -42,11 +43,20 @@ def main(which: str, scale: float = 1.0):
     t1 = time.perf_counter()
     s, info = hybridlp.ruiz_equilibrate(p)
     t2 = time.perf_counter()
+    orig_score, n_scores = hybridlp.pdhg._score, [0]
+
+    def score(pp, x, y):     # progress line every 16 checks (pdhg.py:154-159 unchanged)
+        n_scores[0] += 1
+        if n_scores[0] % 32 == 0:
+            print(f"  {which}: check {n_scores[0] // 2} ({time.perf_counter() - t2:.0f} s)", flush=True)
+        return orig_score(pp, x, y)
+
+    hybridlp.pdhg._score = score
     pt, st = hybridlp.run_pdhg(s, hybridlp.PdhgParams(eps_rel=1e-4))
     t3 = time.perf_counter()
     term = st.termination
     out = {
-        "instance": f"{which}{'' if which == 'config2' else '_general'}(scale={scale})", "m_std": p.m, "n_std": p.n, "nnz_std": int(p.A.nnz),
+        "instance": f"{which}{'' if which in ('config2', 'config4') else '_general'}(scale={scale})", "m_std": p.m, "n_std": p.n, "nnz_std": int(p.A.nnz),
         "status": st.status.value, "iterations": st.iterations, "restarts": st.restarts,
         "objective_scaled": float(s.c @ pt.x), "max_violation": st.max_violation,
         "termination": [term.primal_lhs, term.primal_rhs, term.dual_lhs, term.dual_rhs,

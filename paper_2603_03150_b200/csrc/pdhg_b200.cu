@@ -1624,6 +1624,7 @@ size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct pdhg_ctx {
   pdhg_problem prob;
+  int device;          // the CUDA device of `stream`; every ABI entry runs on it (DevGuard)
   RowSet A, At;
   int a_lanes, at_lanes;
   cudaStream_t stream;
@@ -1882,6 +1883,23 @@ int sumsq_host(pdhg_ctx* c, const double* v, int len, double* out) {
 
 }  // namespace
 
+namespace {
+// Every ABI entry that takes a context runs on the context's device, whatever
+// device is current in the calling thread (restored on return).
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    int cur = -1;
+    if (dev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess)
+      prev = cur;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+#define CTX_DEVICE_GUARD(c) DevGuard dev_guard_((c) ? (c)->device : -1)
+
 extern "C" {
 
 int pdhg_abi_version(void) { return PDHG_ABI_VERSION; }
@@ -1900,7 +1918,13 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
     return fail(PDHG_ERR_ARG, "shard slice outside the full vectors");
   if (workspace_bytes < carve_bytes(mf, nf))
     return fail(PDHG_ERR_ARG, "workspace too small");
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(PDHG_ERR_CUDA, "cudaGetDevice failed");
+  if (stream && cudaStreamGetDevice((cudaStream_t)stream, &dev) != cudaSuccess)
+    return fail(PDHG_ERR_CUDA, "cudaStreamGetDevice failed");
+  DevGuard guard(dev);  // ctx_create reads device attributes and sets kernel attributes on it
   pdhg_ctx* c = new pdhg_ctx();
+  c->device = dev;
   c->prob = *prob;
   c->stream = (cudaStream_t)stream;
   c->A = RowSet{prob->a_ptr, prob->a_col, prob->a_val, prob->m, prob->heavy_threshold,
@@ -2014,6 +2038,7 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
 
 int pdhg_ctx_destroy(pdhg_ctx* c) {
   if (!c) return 0;
+  CTX_DEVICE_GUARD(c);
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   cudaFreeHost(c->P_host);
   cudaFreeHost(c->scal_host);
@@ -2022,6 +2047,7 @@ int pdhg_ctx_destroy(pdhg_ctx* c) {
 }
 
 int pdhg_spmv(pdhg_ctx* c, int transpose, const double* in, double* out) {
+  CTX_DEVICE_GUARD(c);
   if (!c || !in || !out) return fail(PDHG_ERR_ARG, "null argument");
   int rc = spmv(c, transpose != 0, in, out);
   if (rc) return rc;
@@ -2031,6 +2057,7 @@ int pdhg_spmv(pdhg_ctx* c, int transpose, const double* in, double* out) {
 
 int pdhg_opnorm(pdhg_ctx* c, const double* v0_host, double tol, int32_t max_iters, double* lam_out,
                 int32_t* iters_out) {
+  CTX_DEVICE_GUARD(c);
   // pdhg.py:80-109.  v (tn1) <- v0; loop: w (tn2) = A'(A v); ||w||; v = w/||w||.
   if (!c || !v0_host || !lam_out) return fail(PDHG_ERR_ARG, "null argument");
   if (c->mf != c->prob.m || c->nf != c->prob.n)
@@ -2069,6 +2096,7 @@ int pdhg_opnorm(pdhg_ctx* c, const double* v0_host, double tol, int32_t max_iter
 }
 
 int pdhg_reset(pdhg_ctx* c) {
+  CTX_DEVICE_GUARD(c);
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
   const size_t nb = (size_t)c->nf * 8, mb = (size_t)c->mf * 8;
   CUDA_TRY(cudaMemsetAsync(c->x, 0, nb, c->stream));
@@ -2081,6 +2109,7 @@ int pdhg_reset(pdhg_ctx* c) {
 
 int pdhg_run_period(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_over_omega,
                     double sigma_omega, double w0, int64_t* fail_iter_out) {
+  CTX_DEVICE_GUARD(c);
   if (!c || iters < 0) return fail(PDHG_ERR_ARG, "bad argument");
   StepParams& h = *c->P_host;
   h.tau_w = tau_over_omega;
@@ -2105,6 +2134,7 @@ int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs);
 int pdhg_run_period_check(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_over_omega,
                           double sigma_omega, double w0, int32_t npts, const int32_t* specs,
                           int64_t* fail_iter_out, double* out_host) {
+  CTX_DEVICE_GUARD(c);
   // run_period + check with one host synchronisation: the graph of the
   // period, the check kernels and both device-to-host copies are queued
   // back to back on the stream.
@@ -2133,6 +2163,7 @@ int pdhg_run_period_check(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_
 }
 
 int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
+  CTX_DEVICE_GUARD(c);
   if (!c || !specs || npts < 1 || npts > 2) return fail(PDHG_ERR_ARG, "bad argument");
   // primal side (rows of A): gathers full x, row-indexed y slice;
   // dual side (rows of A'): gathers full y, row-indexed x / z slices.
@@ -2181,6 +2212,7 @@ int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
 }
 
 int pdhg_check(pdhg_ctx* c, int32_t npts, const int32_t* specs, double* out_host) {
+  CTX_DEVICE_GUARD(c);
   if (!out_host) return fail(PDHG_ERR_ARG, "null out_host");
   int rc = pdhg_check_device(c, npts, specs);
   if (rc) return rc;
@@ -2193,6 +2225,7 @@ int pdhg_check(pdhg_ctx* c, int32_t npts, const int32_t* specs, double* out_host
 }
 
 int pdhg_restart(pdhg_ctx* c, int32_t which) {
+  CTX_DEVICE_GUARD(c);
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
   const size_t nb = (size_t)c->nf * 8, mb = (size_t)c->mf * 8;
   if (which == PDHG_PT_CUR) {
@@ -2220,6 +2253,7 @@ int reduced_costs(pdhg_ctx* c, int32_t spec, double* z_slice) {
 }
 
 int pdhg_save_best(pdhg_ctx* c, int32_t which, int32_t flags) {
+  CTX_DEVICE_GUARD(c);
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
   const double *x, *y;
   point_xy(c, which, &x, &y);
@@ -2235,6 +2269,7 @@ int pdhg_save_best(pdhg_ctx* c, int32_t which, int32_t flags) {
 }
 
 int pdhg_fetch(pdhg_ctx* c, int32_t spec, double* x_host, double* y_host, double* z_host) {
+  CTX_DEVICE_GUARD(c);
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
   const double *x, *y;
   point_xy(c, spec, &x, &y);
@@ -2256,6 +2291,7 @@ int pdhg_fetch(pdhg_ctx* c, int32_t spec, double* x_host, double* y_host, double
 
 int pdhg_point_device(pdhg_ctx* c, int32_t spec, const double** x_dev, const double** y_dev,
                       const double** z_dev) {
+  CTX_DEVICE_GUARD(c);
   if (!c || !x_dev || !y_dev || !z_dev) return fail(PDHG_ERR_ARG, "null argument");
   point_xy(c, spec, x_dev, y_dev);
   if (spec & PDHG_SPEC_BEST_Z) {
@@ -2289,11 +2325,13 @@ void* pdhg_vector(pdhg_ctx* c, int32_t which) {
 }
 
 int pdhg_reduced_costs(pdhg_ctx* c, int32_t spec, double* z_slice) {
+  CTX_DEVICE_GUARD(c);
   if (!c || !z_slice) return fail(PDHG_ERR_ARG, "null argument");
   return reduced_costs(c, spec, z_slice);
 }
 
 int pdhg_set_step(pdhg_ctx* c, int64_t iter0, double tau_over_omega, double sigma_omega, double w0) {
+  CTX_DEVICE_GUARD(c);
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
   CUDA_TRY(cudaStreamSynchronize(c->stream));  // the pinned staging struct is reused
   StepParams& h = *c->P_host;
@@ -2304,6 +2342,7 @@ int pdhg_set_step(pdhg_ctx* c, int64_t iter0, double tau_over_omega, double sigm
 }
 
 int pdhg_half_step(pdhg_ctx* c, int32_t primal, int32_t j) {
+  CTX_DEVICE_GUARD(c);
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
   int rc = launch_step(c, primal != 0, j);
   if (rc) return rc;
@@ -2312,6 +2351,7 @@ int pdhg_half_step(pdhg_ctx* c, int32_t primal, int32_t j) {
 }
 
 int pdhg_set_peers(pdhg_ctx* c, int32_t which, const double* const* peers_dev, int32_t npeers) {
+  CTX_DEVICE_GUARD(c);
   if (!c || which < 0 || which > 2 || npeers < 0 || (npeers > 0 && !peers_dev))
     return fail(PDHG_ERR_ARG, "set_peers: bad argument");
   if (which == 2) {  // peers' fail words (pdhg_vector(peer, PDHG_VEC_FAILWORD))
@@ -2334,6 +2374,7 @@ int pdhg_set_peers(pdhg_ctx* c, int32_t which, const double* const* peers_dev, i
 }
 
 int pdhg_fail_iter(pdhg_ctx* c, int64_t* fail_iter_out) {
+  CTX_DEVICE_GUARD(c);
   if (!c || !fail_iter_out) return fail(PDHG_ERR_ARG, "null argument");
   CUDA_TRY(cudaMemcpyAsync(&c->P_host->fail_iter, &c->P->fail_iter, sizeof(long long),
                            cudaMemcpyDeviceToHost, c->stream));
@@ -2343,6 +2384,7 @@ int pdhg_fail_iter(pdhg_ctx* c, int64_t* fail_iter_out) {
 }
 
 int pdhg_sumsq(pdhg_ctx* c, const double* v, int64_t len, double* out_dev) {
+  CTX_DEVICE_GUARD(c);
   if (!c || !v || !out_dev || len < 0 || len >= INT_MAX) return fail(PDHG_ERR_ARG, "bad argument");
   k_sumsq<<<kCheckBlocks, kBlock, 0, c->stream>>>(v, (int)len, c->partials);
   k_reduce<<<1, kBlock, 0, c->stream>>>(c->partials, kCheckBlocks, 1, 1, out_dev);
@@ -2351,6 +2393,7 @@ int pdhg_sumsq(pdhg_ctx* c, const double* v, int64_t len, double* out_dev) {
 }
 
 int pdhg_div(pdhg_ctx* c, const double* w, double* v, int64_t len, double s) {
+  CTX_DEVICE_GUARD(c);
   if (!c || !w || !v || len < 0 || len >= INT_MAX) return fail(PDHG_ERR_ARG, "bad argument");
   if (len > 0) k_div<<<(unsigned)((len + kBlock - 1) / kBlock), kBlock, 0, c->stream>>>(w, v, s, (int)len);
   CUDA_TRY(cudaGetLastError());
@@ -2359,6 +2402,7 @@ int pdhg_div(pdhg_ctx* c, const double* w, double* v, int64_t len, double s) {
 
 int pdhg_time_kernel(pdhg_ctx* c, int32_t which, int32_t reps, double tau_over_omega,
                      double sigma_omega, double* avg_ms_out) {
+  CTX_DEVICE_GUARD(c);
   if (!c || reps < 1 || !avg_ms_out) return fail(PDHG_ERR_ARG, "bad argument");
   StepParams& h = *c->P_host;
   h.tau_w = tau_over_omega; h.sigma_w = sigma_omega; h.w0 = 0.0; h.iter0 = 0; h.fail_iter = LLONG_MAX;

@@ -118,6 +118,18 @@ def ruiz_equilibrate(p, max_iters: int = 20, tol: float = 1e-2, *, gpu=None, reg
     tm["download_s"] = time.perf_counter() - t
     t = time.perf_counter()
     indices, indptr = idx_copy.result()
+    dropped = False
+    if applied.value > 0 and not np.all(data != 0.0):
+        # the reference rebuilds A as diags(r) @ A @ diags(c) (transform.py:69);
+        # scipy's csr_matmat keeps only nonzero products, so stored zeros (and
+        # products that underflow to zero) leave the structure.  Same here, in
+        # row order; the device layout is then built from the compacted arrays.
+        keep = data != 0.0
+        counts = np.add.reduceat(keep.astype(np.int64), indptr[:-1]) if data.size else np.zeros(0, np.int64)
+        counts[np.diff(indptr) == 0] = 0
+        indptr = np.concatenate([[0], np.cumsum(counts)]).astype(indptr.dtype)
+        data, indices = data[keep], indices[keep]
+        dropped = True
     S = sp.csr_matrix((data, indices, indptr), shape=A.shape)
     b = row_scale * np.asarray(p.b, dtype=float)                    # transform.py:75
     c = col_scale * np.asarray(p.c, dtype=float)
@@ -127,7 +139,7 @@ def ruiz_equilibrate(p, max_iters: int = 20, tol: float = 1e-2, *, gpu=None, reg
     t = time.perf_counter()
     if register_layout:
         lay = DeviceLp(scaled.A, scaled.b, scaled.c, opts,
-                       device_arrays=(ptr, col, val), stream=stream)
+                       device_arrays=None if dropped else (ptr, col, val), stream=stream)
         _cache_register(scaled, lay, opts)
         torch.cuda.synchronize(dev)
     tm["layout_s"] = time.perf_counter() - t

@@ -55,13 +55,18 @@ Y_SPACE = ("y", "ybar", "ybest", "tm1")
 
 
 def _cuts(counts_ptr: np.ndarray, G: int) -> np.ndarray:
-    """G+1 monotone cut points over rows with ~equal entries (ptr = cumulative counts)."""
+    """G+1 strictly increasing cut points over rows with ~equal entries
+    (ptr = cumulative counts).  Every shard owns at least one row: a row
+    holding >= nnz/G entries (a dense linking row) would otherwise give two
+    shards the same cut and one of them no rows."""
     total = int(counts_ptr[-1])
     rows = counts_ptr.size - 1
+    if rows < G:
+        raise ValueError(f"cannot shard {rows} rows over {G} shards")
     cuts = [0]
     for g in range(1, G):
         c = int(np.searchsorted(counts_ptr, g * total / G, side="left"))
-        cuts.append(min(max(c, cuts[-1]), rows))
+        cuts.append(min(max(c, cuts[-1] + 1), rows - (G - g)))
     cuts.append(rows)
     return np.asarray(cuts, dtype=np.int64)
 
@@ -474,7 +479,8 @@ def build_sharded(p, G: int, comm_kind: str = "loopback", opts=None, group=None)
     plan = ShardPlan(p.A, G)
     if comm_kind in ("loopback", "loopback_fused"):
         comm = LoopbackComm(plan, fused=comm_kind == "loopback_fused")
-        stream = torch.cuda.Stream()
+        dev = torch.device("cuda", torch.cuda.current_device() if opts.device is None else opts.device)
+        stream = torch.cuda.Stream(dev)
         shards = [DeviceLp(blk.A, blk.b, blk.c, opts, shard=blk, stream=stream)
                   for blk in (plan.block(g, p.A, p.b, p.c) for g in range(G))]
     elif comm_kind in ("torch", "torch_peer"):

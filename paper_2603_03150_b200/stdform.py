@@ -39,11 +39,26 @@ _device_csr: dict[int, tuple] = {}
 _lock = threading.Lock()
 
 
+def _host_fingerprint(A):
+    """What must still hold for the device arrays to describe ``p.A``: the same
+    matrix object, shape, nnz and host buffers (a reassigned or resized p.A
+    invalidates the device copy)."""
+    try:
+        return (id(A), tuple(A.shape), int(A.nnz), A.data.ctypes.data, A.indices.ctypes.data,
+                A.indptr.ctypes.data)
+    except AttributeError:
+        return None
+
+
 def device_csr(p):
-    """(indptr, indices, data) device tensors of a model built by to_standard_form, or None."""
+    """(indptr, indices, data) device tensors of a model built by to_standard_form,
+    or None (unknown model, or its host matrix changed since it was built)."""
     with _lock:
         ent = _device_csr.get(id(p))
     if ent is None or ent[0]() is not p:
+        return None
+    fp = _host_fingerprint(getattr(p, "A", None))
+    if fp is None or fp != ent[2]:
         return None
     return ent[1]
 
@@ -54,8 +69,9 @@ def _register(p, arrays) -> None:
         ref = weakref.ref(p, lambda _r, k=key: _device_csr.pop(k, None))
     except TypeError:
         return
+    fp = _host_fingerprint(getattr(p, "A", None))
     with _lock:
-        _device_csr[key] = (ref, arrays)
+        _device_csr[key] = (ref, arrays, fp)
 
 
 def _canonical_csr(A):

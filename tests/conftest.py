@@ -21,7 +21,7 @@ def pytest_configure(config):
 
 
 GOLDEN_NAMES = sorted(p.stem for p in GOLDEN.glob("*.npz")
-                      if not p.stem.startswith(("ruiz_", "stdform_", "center")))
+                      if not p.stem.startswith(("ruiz_", "stdform_", "center", "full_")))
 RUIZ_NAMES = sorted(p.stem for p in GOLDEN.glob("ruiz_*.npz"))
 
 

@@ -1,0 +1,132 @@
+"""Full-size parity on the headline configurations against the REAL reference.
+
+tests/golden/full_config{4,2}.npz were written by oracle/make_golden_full.py,
+which ran the unmodified reference (hybridlp.run_pdhg, pdhg.py:162-258) on
+the full-size seeded instances in the build container: config 4 (5M x 10M,
+199.9M nnz, seed 4 -- the bench instance) and config 2 (500k x 1.15M,
+17.9M nnz, heavy rows up to ~42k entries, seed 2).  The GPU box regenerates
+the instances from the seeds and runs the engine with its OWN power
+iteration (no opnorm override) and default GpuOptions, and compares:
+
+  * estimate_opnorm (pdhg.py:80-109) to 1e-9 relative;
+  * iterates k = 1, 2, 64 (before the check), 65, 100 -- x, y, avg_x, avg_y:
+    4,096 fixed sampled entries each to 1e-9 relative, and the 2-norms;
+  * the iteration-64 check (pdhg.py:198-247): both scores, the restart
+    decision and the state after it (the candidate copied into x, y and the
+    averages, the new omega through iterate 65).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, dtype=float), np.asarray(b, dtype=float)
+    return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
+
+
+def _golden(name):
+    path = GOLDEN / f"full_{name}.npz"
+    if not path.exists():
+        pytest.skip(f"{path.name} not generated (oracle/make_golden_full.py)")
+    return np.load(path)
+
+
+@pytest.fixture(scope="module")
+def eng():
+    import paper_2603_03150_b200 as e
+
+    return e
+
+
+def _instance(name):
+    from paper_2603_03150_b200 import instances
+
+    return instances.config4(1.0, seed=4) if name == "config4" else instances.config2(1.0, seed=2)
+
+
+def _state(eng, p, k, check_every):
+    """Run the engine for k iterations and return the device's current and
+    averaged iterates (the reference's state after iteration k)."""
+    from paper_2603_03150_b200 import _native as N
+
+    T = eng.types()
+    pt, st = eng.run_pdhg(p, T.PdhgParams(eps_rel=1e-12, max_kkt_passes=k, check_every=check_every))
+    dev = eng.device_lp(p, eng.GpuOptions())
+    x, y, _ = dev.fetch(N.PT_CUR, want_z=False)
+    ax, ay, _ = dev.fetch(N.PT_AVG, want_z=False)
+    return st, {"x": x[:p.n], "y": y[:p.m], "avg_x": ax[:p.n], "avg_y": ay[:p.m]}
+
+
+def _compare(g, tag, vecs):
+    ix, iy = g["sample_x"], g["sample_y"]
+    for name, v in vecs.items():
+        idx = ix if name.endswith("x") else iy
+        err = _rel(v[idx], g[f"{tag}_{name}_s"])
+        assert err <= TOL, (tag, name, err)
+        nrm, ref = float(np.linalg.norm(v)), float(g[f"{tag}_{name}_norm"])
+        assert abs(nrm - ref) <= TOL * max(1.0, ref), (tag, name, nrm, ref)
+
+
+@pytest.mark.parametrize("name", ["config4", "config2"])
+def test_full_size_against_reference(eng, name):
+    g = _golden(name)
+    p = _instance(name)
+    assert (p.m, p.n, p.nnz) == (int(g["m"]), int(g["n"]), int(g["nnz"]))
+    if name == "config2":   # the heavy-row path really runs, with default options
+        dev = eng.device_lp(p, eng.GpuOptions())
+        lens = np.diff(p.A.indptr)
+        assert lens.max() > 10_000
+        assert dev._prob.a_n_heavy > 0
+    # the engine's own power iteration, the reference's start vector
+    lam = eng.estimate_opnorm(p.A)
+    assert abs(lam - float(g["opnorm"])) <= TOL * float(g["opnorm"]), (lam, float(g["opnorm"]))
+
+    for k in (1, 2, 100):
+        _, vecs = _state(eng, p, k, 64)
+        _compare(g, f"k{k}", vecs)
+    # iteration 64 before its check, then the check's decision and its result
+    _, vecs = _state(eng, p, 64, 10**6)
+    _compare(g, "k64", vecs)
+    st, vecs = _state(eng, p, 64, 64)
+    _compare(g, "post64", vecs)
+    assert st.restarts == int(g["post64_restarts"])
+    rec = st.history[-1]
+    assert rec["iteration"] == 64 and rec["restart"] == (int(g["post64_restarts"]) == 1)
+    assert abs(rec["cur_max_violation"] - float(g["score64_cur"])) <= TOL * float(g["score64_cur"])
+    assert abs(rec["avg_max_violation"] - float(g["score64_avg"])) <= TOL * float(g["score64_avg"])
+    _, vecs = _state(eng, p, 65, 64)     # the new omega (clip(|r_p|/|r_d|)) drives step 65
+    _compare(g, "k65", vecs)
+    eng.clear_cache()
+
+
+@pytest.mark.parametrize("name", ["config4", "config2"])
+def test_full_size_run_to_1e4_against_reference(eng, name):
+    """The pipeline the bench times -- device Ruiz (bit-identical to
+    transform.py:35-77) then run_pdhg to eps_rel=1e-4 -- against the real
+    reference's own full run on the same instance (oracle/make_golden_runs.py):
+    same status, iteration count within +-5 %, objective within 1e-6."""
+    import json
+
+    f = GOLDEN / f"run_{name}_s1.json"
+    if not f.exists():
+        pytest.skip(f"{f.name} not generated (oracle/make_golden_runs.py {name})")
+    ref = json.loads(f.read_text())
+    T = eng.types()
+    p = _instance(name)
+    scaled, info = eng.ruiz_equilibrate(p)
+    assert info.applied_iterations == ref["ruiz_passes"]
+    pt, st = eng.run_pdhg(scaled, T.PdhgParams(eps_rel=1e-4, time_limit_s=600))
+    assert st.status.value == ref["status"] == "Optimal"
+    assert abs(st.iterations - ref["iterations"]) <= 0.05 * ref["iterations"], (st.iterations, ref)
+    obj = float(np.dot(scaled.c, pt.x))
+    assert abs(obj - ref["objective_scaled"]) <= 1e-6 * max(1.0, abs(ref["objective_scaled"]))
+    eng.clear_cache()

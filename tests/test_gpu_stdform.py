@@ -143,3 +143,22 @@ def test_config1_pipeline_matches_oracle(eng):
     assert v.max_violation <= 10 * max(ov.max_violation, 1e-6)
     # general-model objective within 1e-6 relative of the oracle's
     assert abs(g.c @ x - g.c @ ox) <= 1e-6 * max(1.0, abs(g.c @ ox))
+
+
+def test_device_copy_invalidated_when_host_matrix_changes(eng):
+    """stdform.device_csr serves the resident device matrix only while p.A is
+    the matrix it was built from (a reassigned p.A must not be read
+    through stale device arrays)."""
+    from paper_2603_03150_b200 import stdform
+
+    _, g = load("lp1")
+    p, _ = eng.to_standard_form(g)
+    assert stdform.device_csr(p) is not None
+    p.A = sp.csr_matrix(p.A, copy=True)        # same values, new host buffers
+    assert stdform.device_csr(p) is None
+    # the Ruiz pass then uploads the new host matrix and still matches the oracle
+    import oracle
+
+    S, info = eng.ruiz_equilibrate(p)
+    S_o, info_o = oracle.ruiz_equilibrate(p)
+    np.testing.assert_array_equal(info.row_scale, info_o.row_scale)

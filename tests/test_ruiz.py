@@ -121,3 +121,72 @@ def test_empty_column_rejected():
     p.A = A
     with pytest.raises(ValueError, match="column 3 has no nonzero entries"):
         eng.ruiz_equilibrate(p)
+
+
+def _stored_zero_model():
+    """A model whose A stores explicit zeros (MPS files can): 3 of them."""
+    rng = np.random.default_rng(41)
+    A = sp.random(30, 50, density=0.2, random_state=rng, format="csr")
+    A.data = rng.standard_normal(A.nnz) * rng.uniform(0.1, 30.0, A.nnz)
+    for r in range(30):                    # every row / column nonzero
+        A[r, r] = 1.0 + r
+    for j in range(30, 50):
+        A[j - 30, j] = 2.0
+    A = sp.csr_matrix(A)
+    A.data[[0, 7, 19]] = 0.0               # stored zeros, not eliminated
+    p = type("P", (), {})()
+    p.A, p.b, p.c = A, rng.standard_normal(30), rng.standard_normal(50)
+    return p
+
+
+def test_oracle_ruiz_drops_stored_zeros_like_reference():
+    """scipy's diags @ A @ diags drops stored zeros (transform.py:69): the
+    restatement must do the same as the live reference (build container)."""
+    import sys
+    from pathlib import Path
+
+    import oracle
+
+    ref = Path("/root/reference/pkg/src")
+    p = _stored_zero_model()
+    S, info = oracle.ruiz_equilibrate(p)
+    assert info.applied_iterations > 0
+    assert S.A.nnz == p.A.nnz - 3 and np.all(S.A.data != 0.0)
+    if not ref.exists():
+        pytest.skip("reference tree not available (GPU box)")
+    sys.path.insert(0, str(ref))
+    try:
+        import hybridlp
+
+        R, rinfo = hybridlp.ruiz_equilibrate(hybridlp.StandardLp(p.A, p.b, p.c))
+    finally:
+        sys.path.remove(str(ref))
+    np.testing.assert_array_equal(info.row_scale, rinfo.row_scale)
+    got, want = _canon(S.A), _canon(R.A)
+    np.testing.assert_array_equal(got.indptr, want.indptr)
+    np.testing.assert_array_equal(got.indices, want.indices)
+    np.testing.assert_array_equal(got.data, want.data)
+
+
+@pytest.mark.gpu
+def test_device_ruiz_drops_stored_zeros():
+    """Device Ruiz on a matrix with stored zeros: structure, values and scales
+    equal to the restatement (hence the reference), and PDHG runs on it."""
+    import oracle
+    import paper_2603_03150_b200 as eng
+
+    p = _stored_zero_model()
+    S_o, info_o = oracle.ruiz_equilibrate(p)
+    S, info = eng.ruiz_equilibrate(p)
+    np.testing.assert_array_equal(info.row_scale, info_o.row_scale)
+    np.testing.assert_array_equal(info.col_scale, info_o.col_scale)
+    got, want = _canon(S.A), _canon(S_o.A)
+    assert got.nnz == want.nnz == p.A.nnz - 3
+    np.testing.assert_array_equal(got.indptr, want.indptr)
+    np.testing.assert_array_equal(got.indices, want.indices)
+    np.testing.assert_array_equal(got.data, want.data)
+    T = eng.types()
+    pt, st = eng.run_pdhg(S, T.PdhgParams(eps_rel=1e-12, max_kkt_passes=64))
+    opt, ost = oracle.run_pdhg(S_o, oracle.PdhgParams(eps_rel=1e-12, max_kkt_passes=64))
+    assert st.iterations == ost.iterations == 64
+    np.testing.assert_allclose(pt.x, opt.x, rtol=0, atol=1e-9 * max(1.0, np.abs(opt.x).max()))

@@ -243,3 +243,51 @@ def test_gloo_time_limit_is_collective():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res == [(0, "TimeLimit", 0), (1, "TimeLimit", 0)]
+
+
+def dense_row_model():
+    """config0_s0 plus one dense linking row over every column (a budget row
+    holding more than nnz/G entries): equal-nnz cuts would collide on it."""
+    gm = load_golden("config0_s0")
+    rng = np.random.default_rng(3)
+    dense = sp.csr_matrix(rng.uniform(0.5, 1.5, (1, gm.n)))
+    A = sp.vstack([dense, gm.A], format="csr")
+    x0 = np.abs(rng.standard_normal(gm.n)) * (rng.random(gm.n) < 0.5)
+    b = np.concatenate([dense @ x0, gm.b])
+    return Model(A, b, gm.c.copy())
+
+
+@pytest.mark.parametrize("G", [16, 24])
+def test_shard_plan_dense_row_gives_no_empty_shard(G):
+    p = dense_row_model()
+    assert p.A.getnnz(axis=1)[0] >= 2 * p.A.nnz / G      # the dense row spans two cut targets
+    plan = ShardPlan(p.A, G)
+    assert np.all(np.diff(plan.rcut) >= 1) and np.all(np.diff(plan.ccut) >= 1)
+    for g in range(G):
+        blk = plan.block(g, p.A, p.b, p.c)
+        assert blk.A.shape[0] >= 1 and blk.At.shape[0] >= 1
+
+
+def test_shard_plan_rejects_more_shards_than_rows():
+    A = sp.csr_matrix(np.ones((2, 5)))
+    with pytest.raises(ValueError, match="cannot shard 2 rows over 3 shards"):
+        ShardPlan(A, 3)
+
+
+def test_loopback_dense_row_matches_oracle():
+    """The sharded engine (16 numpy shards, loopback) on the dense-row model."""
+    from shard_double import NumpyShard
+
+    from paper_2603_03150_b200 import engine
+    from paper_2603_03150_b200.lp_types import resolve
+
+    p = dense_row_model()
+    plan = ShardPlan(p.A, 16)
+    shards = [NumpyShard(plan.block(g, p.A, p.b, p.c)) for g in range(16)]
+    dev = ShardedDevice(plan, shards, LoopbackComm(plan))
+    T = resolve()
+    pt, st = engine.run_on_device(dev, p, T.PdhgParams(eps_rel=1e-4, max_kkt_passes=640))
+    opt, ost = oracle.run_pdhg(p, oracle.PdhgParams(eps_rel=1e-4, max_kkt_passes=640))
+    assert st.status.value == ost.status.value
+    assert st.iterations == ost.iterations and st.restarts == ost.restarts
+    np.testing.assert_allclose(pt.x, opt.x, rtol=1e-9, atol=1e-12)
