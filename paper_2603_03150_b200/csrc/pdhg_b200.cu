@@ -713,7 +713,16 @@ struct SellSet {
   const double* __restrict__ val;
   const unsigned char* __restrict__ perm;  // lane -> row offset in the slice (nullptr = identity)
   bool u_long = false;                     // mean row >= PDHG_SELL_U_MEAN: PDHG_SELL_U_LONG in flight
+  int win = 0;                             // > 0: rows sorted inside windows of win (= kBlock) rows;
+                                           // perm maps sorted position -> row offset in the window
+  const int* __restrict__ slen = nullptr;  // win > 0: light length of each sorted position
 };
+
+// Row of lane `lane` of slice sl (natural, slice-sorted or window-sorted layout).
+__device__ __forceinline__ long long sell_row(const SellSet& S, long long sl, int lane) {
+  if (S.win > 0) return (sl * 32 / S.win) * S.win + S.perm[sl * 32 + lane];
+  return sl * 32 + (S.perm ? S.perm[sl * 32 + lane] : lane);
+}
 
 // Entries in flight per lane in the SELL row loop: PDHG_SELL_U for short
 // rows, PDHG_SELL_U_LONG for operators averaging >= PDHG_SELL_U_MEAN entries
@@ -814,6 +823,56 @@ __global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_step_sell(StepArgs a
     const int row = (int)rl;
     if (PRIMAL) bcast(P, 0, row, primal_epi_pre(row, acc, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
     else bcast(P, 1, row, dual_epi_pre(row, acc, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
+  }
+}
+
+// Step over the window-sorted sliced ELL (S.win == kBlock): block = one window
+// of kBlock consecutive rows whose rows were sorted by length (SELL-C-sigma),
+// warp w = slice w of the window, each lane one (permuted) row summed
+// sequentially in entry order like k_step_sell.  The row dots meet in shared
+// memory at their natural offsets, and after one barrier thread t runs the
+// epilogue of row window*kBlock + t -- coalesced operands and stores, exactly
+// the k_step epilogue.  Heavy rows: a block each (first n_heavy blocks).
+template <bool PRIMAL, int kU>
+__global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_step_sellw(StepArgs a, SellSet S, int j_in_period) {
+  __shared__ double red[kWarps];
+  __shared__ double dots[kBlock];
+  pdl_enter();
+  StepParams* P = a.P;
+  const long long iter = P->iter0 + j_in_period + 1;
+  if (P->fail_iter < iter) return;
+  const double w = P->w0 + (double)(j_in_period + 1);
+  const double step = PRIMAL ? P->tau_w : P->sigma_w;
+  if ((int)blockIdx.x < a.rs.n_heavy) {
+    const double* xin[1] = {a.gather};
+    const int row = a.rs.heavy[blockIdx.x];
+    const int s = a.rs.ptr[row], e = a.rs.ptr[row + 1];
+    double acc[1];
+    row_dot<kBlock, 1>(a.rs, s, e, threadIdx.x, xin, acc);
+    const double d = block_sum(acc[0], red);
+    if (threadIdx.x == 0) {
+      if (PRIMAL) bcast(P, 0, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast(P, 1, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
+    }
+    return;
+  }
+  const long long win = (long long)blockIdx.x - a.rs.n_heavy;
+  const int lane = threadIdx.x & 31;
+  const long long sl = win * kWarps + (threadIdx.x >> 5);
+  const long long q = win * kBlock + threadIdx.x;  // sorted position
+  if (sl < S.nslices) {                             // warp-uniform
+    const int len = S.slen[q];
+    const double acc = sell_row_dot<kU>(S, sl, lane, len, a.gather);
+    dots[S.perm[q]] = acc;
+  }
+  __syncthreads();
+  const long long rl = win * kBlock + threadIdx.x;  // natural row
+  if (rl < a.rs.rows && a.rs.ptr[rl + 1] - a.rs.ptr[rl] <= a.rs.heavy_threshold) {
+    const double o1 = a.cb[rl], o2 = a.x[rl], o3 = a.xbar[rl];
+    const int row = (int)rl;
+    const double d = dots[threadIdx.x];
+    if (PRIMAL) bcast(P, 0, row, primal_epi_pre(row, d, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
+    else bcast(P, 1, row, dual_epi_pre(row, d, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
   }
 }
 
@@ -1063,7 +1122,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_spmv_sell(RowSet rs,
   const int lane = threadIdx.x & 31;
   const long long sl = ((long long)(blockIdx.x - rs.n_heavy) * kBlock + threadIdx.x) >> 5;
   if (sl >= S.nslices) return;  // warp-uniform
-  const long long rl = sl * 32 + (S.perm ? S.perm[sl * 32 + lane] : lane);
+  const long long rl = sell_row(S, sl, lane);
   int len = rl < rs.rows ? rs.ptr[rl + 1] - rs.ptr[rl] : -1;
   const bool ok = len >= 0 && len <= rs.heavy_threshold;
   if (!ok) len = 0;
@@ -1456,7 +1515,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual_sell(RowS
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * kWarps;
   for (long long sl = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5; sl < S.nslices; sl += warps) {
-    const long long rl = sl * 32 + (S.perm ? S.perm[sl * 32 + lane] : lane);
+    const long long rl = sell_row(S, sl, lane);
     int len = rl < rs.rows ? rs.ptr[rl + 1] - rs.ptr[rl] : -1;
     const bool ok = len >= 0 && len <= rs.heavy_threshold;
     if (!ok) len = 0;
@@ -1836,6 +1895,13 @@ int launch_step(pdhg_ctx* c, bool primal, int j) {
   if (c->has_sell[k]) {
     const SellSet& S = c->sell[k];
     const int grid = a.rs.n_heavy + (int)(((long long)S.nslices * 32 + kBlock - 1) / kBlock);
+    if (S.win > 0) {  // one block per window of kBlock rows (grid above: same count)
+      if (S.u_long)
+        return primal ? launch_ex(c, k_step_sellw<true, PDHG_SELL_U_LONG>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j)
+                      : launch_ex(c, k_step_sellw<false, PDHG_SELL_U_LONG>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
+      return primal ? launch_ex(c, k_step_sellw<true, PDHG_SELL_U>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j)
+                    : launch_ex(c, k_step_sellw<false, PDHG_SELL_U>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
+    }
     if (S.u_long)
       return primal ? launch_ex(c, k_step_sell<true, PDHG_SELL_U_LONG>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j)
                     : launch_ex(c, k_step_sell<false, PDHG_SELL_U_LONG>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
@@ -1988,8 +2054,14 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
         delete c;
         return fail(PDHG_ERR_ARG, "sell layout does not match the operator");
       }
+      if (q->win != 0 && (q->win != kBlock || !q->perm || !q->slen)) {
+        delete c;
+        return fail(PDHG_ERR_ARG, "window-sorted sell layout needs win == 256, perm and slen");
+      }
       c->sell[k] = SellSet{q->rows, q->nslices, reinterpret_cast<const long long*>(q->sptr), q->width,
                            q->col, q->val, q->perm};
+      c->sell[k].win = q->win;
+      c->sell[k].slen = q->slen;
       const long long ops_nnz = k == 0 ? prob->nnz : (prob->at_nnz > 0 ? prob->at_nnz : prob->nnz);
       c->sell[k].u_long = q->rows > 0 && ops_nnz >= (long long)PDHG_SELL_U_MEAN * q->rows;
     }

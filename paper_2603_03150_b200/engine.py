@@ -70,6 +70,14 @@ class GpuOptions:
                      config 4 at 5 % (10M) 41.3 -> 35.6 us; at 1.5M entries it measured
                      50 % slower).  Skewed rows (config 4's A: 4x padding) stay on
                      CSR-vector.
+    sell_window:     "auto" | "on" | "off" -- window-sorted sliced ELL (SELL-C-sigma,
+                     csrc/sell_build.cu k_sellw_sort): rows sorted by length inside
+                     windows of 256 rows, the step kernel a block per window with a
+                     shared-memory dot exchange so the epilogue stays coalesced
+                     (k_step_sellw).  Lets skewed operators use SELL: config 4's A
+                     pads 1.45x instead of 4.1x.  auto: operators with >= sell_min_nnz
+                     entries.  Rows longer than sell_window_heavy entries are
+                     processed block per row (the operator's heavy threshold).
     sell_sort:       "auto" | "on" | "off" -- order each slice's rows by length (lanes
                      active in a round form a prefix, so fetched sectors are full):
                      config 4's A' reads 3.55 instead of 3.85 GB per primal step (period
@@ -108,6 +116,8 @@ class GpuOptions:
     sell_max_mean: float = 12.0
     sell_min_nnz: int = 5_000_000
     sell_sort: str = "auto"
+    sell_window: str = "auto"
+    sell_window_heavy: int = 256
 
 
 def auto_lanes(nnz: int, rows: int) -> int:
@@ -151,6 +161,13 @@ def _medium_list(torch, ptr, lanes: int, H: int, per_lane: int):
     lens = ptr[1:] - ptr[:-1]
     idx = torch.nonzero((lens > light_max) & (lens <= H)).flatten().to(torch.int32).contiguous()
     return idx, light_max
+
+
+def _want_window(opts: GpuOptions, nnz: int, pers_req: str = "off") -> bool:
+    """Window-sorted sliced ELL for an operator with `nnz` entries (GpuOptions.sell_window)."""
+    if opts.sell == "off" or opts.psr != "off" or pers_req in ("on", "tiny") or nnz <= 0:
+        return False
+    return opts.sell_window == "on" or (opts.sell_window == "auto" and nnz >= opts.sell_min_nnz)
 
 
 def _as_csr(A):
@@ -242,6 +259,14 @@ class DeviceLp:
                 self.at_lanes = int(opts.at_lanes) or auto_lanes(self.at_nnz, n)
                 H = int(opts.heavy_threshold) or heavy_threshold(self.a_lanes)
                 Ht = int(opts.heavy_threshold) or heavy_threshold(self.at_lanes)
+                # window-sorted SELL: rows longer than sell_window_heavy run block per
+                # row, so no window holds a slice wider than that
+                self.sell_window = {k: _want_window(opts, nz, pers_req=opts.persistent)
+                                    for k, nz in (("A", nnz), ("At", self.at_nnz))}
+                if self.sell_window["A"]:
+                    H = min(H, int(opts.sell_window_heavy))
+                if self.sell_window["At"]:
+                    Ht = min(Ht, int(opts.sell_window_heavy))
                 self.heavy = (H, Ht)
                 self.a_heavy = torch.nonzero((self.a_ptr[1:] - self.a_ptr[:-1]) > H).flatten().to(torch.int32)
                 self.at_heavy = torch.nonzero((self.at_ptr[1:] - self.at_ptr[:-1]) > Ht).flatten().to(torch.int32)
@@ -325,10 +350,10 @@ class DeviceLp:
         self._scal = (C.c_double * (2 * N.NQ))()
 
     def _build_sell(self, torch, dev, key, rows, nnz, ptr, col, val, H, opts):
-        """Plan + fill the sliced-ELL layout of one operator on the device (or None)."""
+        """Plan + fill the sliced-ELL layout of one operator on the device (or None):
+        window-sorted (SELL-C-sigma) when enabled for this operator, else slices of
+        32 natural (optionally slice-sorted) rows."""
         if opts.sell == "off" or rows <= 0 or nnz <= 0:
-            return None
-        if opts.sell == "auto" and nnz / rows >= opts.sell_max_mean and nnz < opts.sell_min_nnz:
             return None
         lib = self.lib
         sptr_ = self.stream.cuda_stream
@@ -338,6 +363,32 @@ class DeviceLp:
         tb = lib.pdhg_sell_tmp_bytes(rows)
         tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=dev)
         slots = C.c_int64()
+        win = 256
+        if self.sell_window.get(key):
+            nw = (rows + win - 1) // win
+            perm = torch.empty(nw * win, dtype=torch.uint8, device=dev)
+            inv = torch.empty(nw * win, dtype=torch.uint8, device=dev)
+            slen = torch.empty(nw * win, dtype=torch.int32, device=dev)
+            N.check(lib.pdhg_sell_plan_window(rows, ptr.data_ptr(), int(H), win, perm.data_ptr(),
+                                              inv.data_ptr(), slen.data_ptr(), width.data_ptr(),
+                                              sp.data_ptr(), tmp.data_ptr(), tb, sptr_, C.byref(slots)))
+            pad = slots.value / max(1, nnz)
+            self.sell_info[key] = {"slots": slots.value, "pad": pad, "used": False, "window": win}
+            scol = torch.empty(max(slots.value, 1), dtype=torch.int32, device=dev)
+            sval = torch.empty(max(slots.value, 1), dtype=torch.float64, device=dev)
+            N.check(lib.pdhg_sell_fill_window(rows, ptr.data_ptr(), col.data_ptr(), val.data_ptr(),
+                                              int(H), win, sp.data_ptr(), inv.data_ptr(),
+                                              scol.data_ptr(), sval.data_ptr(), sptr_))
+            d = N.Sell()
+            d.rows, d.nslices = rows, ns
+            d.sptr, d.width, d.col, d.val = sp.data_ptr(), width.data_ptr(), scol.data_ptr(), sval.data_ptr()
+            d.perm, d.win, d.slen = perm.data_ptr(), win, slen.data_ptr()
+            self.stream.synchronize()
+            del inv
+            self.sell_info[key].update(used=True, sorted=True)
+            return (d, (width, sp, scol, sval, perm, slen))
+        if opts.sell == "auto" and nnz / rows >= opts.sell_max_mean and nnz < opts.sell_min_nnz:
+            return None
         N.check(lib.pdhg_sell_plan(rows, ptr.data_ptr(), int(H), width.data_ptr(), sp.data_ptr(),
                                    tmp.data_ptr(), tb, sptr_, C.byref(slots)))
         pad = slots.value / max(1, nnz)
@@ -359,6 +410,7 @@ class DeviceLp:
         d.rows, d.nslices = rows, ns
         d.sptr, d.width, d.col, d.val = sp.data_ptr(), width.data_ptr(), scol.data_ptr(), sval.data_ptr()
         d.perm = perm.data_ptr() if perm is not None else None
+        d.win, d.slen = 0, None
         self.stream.synchronize()
         del inv
         self.sell_info[key]["used"] = True

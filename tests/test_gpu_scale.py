@@ -37,14 +37,18 @@ def c2small():
     return config2(scale=0.02, seed=12)   # 10k x ~23k, heavy-tailed rows (up to 1000)
 
 
-@pytest.mark.parametrize("psr", ["off", "on"])
-def test_iterates_scaled_config4(eng, c4small, psr):
+SCALED_LAYOUTS = {"default": {}, "psr": dict(psr="on"), "window": dict(sell_window="on")}
+
+
+@pytest.mark.parametrize("layout", sorted(SCALED_LAYOUTS))
+def test_iterates_scaled_config4(eng, c4small, layout):
     """First 100 iterates (incl. the iteration-64 check/restart) to 1e-9."""
     from paper_2603_03150_b200 import _native as N
 
     T = eng.types()
     p = c4small
-    opts = eng.GpuOptions(psr=psr)
+    psr = "on" if layout == "psr" else "off"
+    opts = eng.GpuOptions(**SCALED_LAYOUTS[layout])
     rec = {}
     keep = {1, 2, 17, 63, 64, 65, 100}
     oracle.run_pdhg(Model(p.A, p.b, p.c), oracle.PdhgParams(eps_rel=1e-12, max_kkt_passes=100),
@@ -57,6 +61,8 @@ def test_iterates_scaled_config4(eng, c4small, psr):
         dev = eng.device_lp(p, opts)
         if psr == "on":
             assert dev.psr_info["A"]["used"] and dev.psr_info["At"]["used"]
+        if layout == "window":
+            assert dev.sell_info["A"].get("window") and dev.sell_info["At"].get("window")
         x, y, _ = dev.fetch(N.PT_CUR, want_z=False)
         ax, ay, _ = dev.fetch(N.PT_AVG, want_z=False)
         ox, oy, oax, oay = rec[k]
