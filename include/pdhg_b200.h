@@ -92,13 +92,6 @@ typedef struct pdhg_sell {
   const double* val;     /* slots */
   const uint8_t* perm;   /* optional (rows rounded up to 32): lane -> row offset in its
                             slice, rows sorted by length inside each slice (NULL = identity) */
-  /* window-sorted form (win > 0, = 256): rows sorted by length inside windows of
-   * `win` rows; perm (rows rounded up to win) maps sorted position -> row offset
-   * in its window and slen holds the sorted rows' light lengths.  The step
-   * kernel runs one block per window and exchanges the row dots through shared
-   * memory, so its epilogue stays coalesced in natural row order. */
-  int32_t win;
-  const int32_t* slen;
 } pdhg_sell;
 
 typedef struct pdhg_problem {
@@ -423,17 +416,16 @@ int pdhg_sell_sort(int32_t rows, const int32_t* ptr, int32_t heavy_threshold, ui
 int pdhg_sell_fill(int32_t rows, const int32_t* ptr, const int32_t* col, const double* val,
                    int32_t heavy_threshold, const int64_t* sptr, const uint8_t* inv, int32_t* scol,
                    double* sval, void* stream);
-/* Window-sorted plan (SELL-C-sigma, sigma = window = 256 rows): sorts each
- * window's rows by light length (descending, stable) and writes perm / inv /
- * slen ((rows rounded up to 256) entries each), width and sptr as
- * pdhg_sell_plan does; tmp as pdhg_sell_tmp_bytes.  fill_window copies the
- * entries to their window-sorted slots. */
-int pdhg_sell_plan_window(int32_t rows, const int32_t* ptr, int32_t heavy_threshold, int32_t window,
-                          uint8_t* perm, uint8_t* inv, int32_t* slen, int32_t* width, int64_t* sptr,
-                          void* tmp, size_t tmp_bytes, void* stream, int64_t* slots_out);
-int pdhg_sell_fill_window(int32_t rows, const int32_t* ptr, const int32_t* col, const double* val,
-                          int32_t heavy_threshold, int32_t window, const int64_t* sptr, const uint8_t* inv,
-                          int32_t* scol, double* sval, void* stream);
+
+/* Row relabelling of a CSR matrix on the device (GpuOptions.row_order =
+ * "length": the rows of A -- the y-space -- sorted by length inside windows so
+ * the dual step's sliced-ELL slices hold rows of equal length).  New row r is
+ * old row perm[r], entries keep their order; new_ptr (rows+1) holds the
+ * scanned permuted lengths.  The LP is the same one with its constraints
+ * renumbered: b is permuted alike and y is mapped back on every download. */
+int pdhg_permute_rows(int32_t rows, const int32_t* perm, const int32_t* ptr, const int32_t* col,
+                      const double* val, const int32_t* new_ptr, int32_t* new_col, double* new_val,
+                      void* stream);
 
 
 /* IPM hand-off (warmstart.py:62-107): center_toward_target

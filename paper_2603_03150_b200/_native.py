@@ -33,7 +33,7 @@ EXPORTS = (
     "pdhg_lift_bound_duals", "pdhg_max0", "pdhg_violation_tmp_bytes", "pdhg_violation",
     "pdhg_sell_tmp_bytes", "pdhg_sell_plan", "pdhg_sell_fill", "pdhg_sell_sort", "pdhg_set_peers",
     "pdhg_run_period_check", "pdhg_center_toward_target", "pdhg_dot_tmp_bytes", "pdhg_dot",
-    "pdhg_sell_plan_window", "pdhg_sell_fill_window",
+    "pdhg_permute_rows",
 )
 
 VEC = {name: i for i, name in enumerate(
@@ -58,7 +58,7 @@ class Sell(C.Structure):
 
     _fields_ = [("rows", C.c_int32), ("nslices", C.c_int32), ("sptr", C.c_void_p),
                 ("width", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p),
-                ("perm", C.c_void_p), ("win", C.c_int32), ("slen", C.c_void_p)]
+                ("perm", C.c_void_p)]
 
 
 class Problem(C.Structure):
@@ -174,9 +174,7 @@ def load():
         _sig(lib, "pdhg_sell_plan", C.c_int, i32, vp, i32, vp, vp, vp, szt, vp, P(i64))
         _sig(lib, "pdhg_sell_sort", C.c_int, i32, vp, i32, vp, vp, vp)
         _sig(lib, "pdhg_sell_fill", C.c_int, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp)
-        _sig(lib, "pdhg_sell_plan_window", C.c_int, i32, vp, i32, i32, vp, vp, vp, vp, vp, vp, szt, vp,
-             P(i64))
-        _sig(lib, "pdhg_sell_fill_window", C.c_int, i32, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp)
+        _sig(lib, "pdhg_permute_rows", C.c_int, i32, vp, vp, vp, vp, vp, vp, vp, vp)
         _sig(lib, "pdhg_violation", C.c_int, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
              vp, szt, vp, P(dbl))
         if lib.pdhg_abi_version() != ABI_VERSION:

@@ -713,14 +713,10 @@ struct SellSet {
   const double* __restrict__ val;
   const unsigned char* __restrict__ perm;  // lane -> row offset in the slice (nullptr = identity)
   bool u_long = false;                     // mean row >= PDHG_SELL_U_MEAN: PDHG_SELL_U_LONG in flight
-  int win = 0;                             // > 0: rows sorted inside windows of win (= kBlock) rows;
-                                           // perm maps sorted position -> row offset in the window
-  const int* __restrict__ slen = nullptr;  // win > 0: light length of each sorted position
 };
 
-// Row of lane `lane` of slice sl (natural, slice-sorted or window-sorted layout).
+// Row of lane `lane` of slice sl (natural or slice-sorted layout).
 __device__ __forceinline__ long long sell_row(const SellSet& S, long long sl, int lane) {
-  if (S.win > 0) return (sl * 32 / S.win) * S.win + S.perm[sl * 32 + lane];
   return sl * 32 + (S.perm ? S.perm[sl * 32 + lane] : lane);
 }
 
@@ -823,56 +819,6 @@ __global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_step_sell(StepArgs a
     const int row = (int)rl;
     if (PRIMAL) bcast(P, 0, row, primal_epi_pre(row, acc, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
     else bcast(P, 1, row, dual_epi_pre(row, acc, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
-  }
-}
-
-// Step over the window-sorted sliced ELL (S.win == kBlock): block = one window
-// of kBlock consecutive rows whose rows were sorted by length (SELL-C-sigma),
-// warp w = slice w of the window, each lane one (permuted) row summed
-// sequentially in entry order like k_step_sell.  The row dots meet in shared
-// memory at their natural offsets, and after one barrier thread t runs the
-// epilogue of row window*kBlock + t -- coalesced operands and stores, exactly
-// the k_step epilogue.  Heavy rows: a block each (first n_heavy blocks).
-template <bool PRIMAL, int kU>
-__global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_step_sellw(StepArgs a, SellSet S, int j_in_period) {
-  __shared__ double red[kWarps];
-  __shared__ double dots[kBlock];
-  pdl_enter();
-  StepParams* P = a.P;
-  const long long iter = P->iter0 + j_in_period + 1;
-  if (P->fail_iter < iter) return;
-  const double w = P->w0 + (double)(j_in_period + 1);
-  const double step = PRIMAL ? P->tau_w : P->sigma_w;
-  if ((int)blockIdx.x < a.rs.n_heavy) {
-    const double* xin[1] = {a.gather};
-    const int row = a.rs.heavy[blockIdx.x];
-    const int s = a.rs.ptr[row], e = a.rs.ptr[row + 1];
-    double acc[1];
-    row_dot<kBlock, 1>(a.rs, s, e, threadIdx.x, xin, acc);
-    const double d = block_sum(acc[0], red);
-    if (threadIdx.x == 0) {
-      if (PRIMAL) bcast(P, 0, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
-      else bcast(P, 1, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
-    }
-    return;
-  }
-  const long long win = (long long)blockIdx.x - a.rs.n_heavy;
-  const int lane = threadIdx.x & 31;
-  const long long sl = win * kWarps + (threadIdx.x >> 5);
-  const long long q = win * kBlock + threadIdx.x;  // sorted position
-  if (sl < S.nslices) {                             // warp-uniform
-    const int len = S.slen[q];
-    const double acc = sell_row_dot<kU>(S, sl, lane, len, a.gather);
-    dots[S.perm[q]] = acc;
-  }
-  __syncthreads();
-  const long long rl = win * kBlock + threadIdx.x;  // natural row
-  if (rl < a.rs.rows && a.rs.ptr[rl + 1] - a.rs.ptr[rl] <= a.rs.heavy_threshold) {
-    const double o1 = a.cb[rl], o2 = a.x[rl], o3 = a.xbar[rl];
-    const int row = (int)rl;
-    const double d = dots[threadIdx.x];
-    if (PRIMAL) bcast(P, 0, row, primal_epi_pre(row, d, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
-    else bcast(P, 1, row, dual_epi_pre(row, d, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
   }
 }
 
@@ -1122,7 +1068,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_spmv_sell(RowSet rs,
   const int lane = threadIdx.x & 31;
   const long long sl = ((long long)(blockIdx.x - rs.n_heavy) * kBlock + threadIdx.x) >> 5;
   if (sl >= S.nslices) return;  // warp-uniform
-  const long long rl = sell_row(S, sl, lane);
+  const long long rl = sl * 32 + (S.perm ? S.perm[sl * 32 + lane] : lane);
   int len = rl < rs.rows ? rs.ptr[rl + 1] - rs.ptr[rl] : -1;
   const bool ok = len >= 0 && len <= rs.heavy_threshold;
   if (!ok) len = 0;
@@ -1539,6 +1485,79 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual_sell(RowS
   }
 }
 
+// Two-point A-side check over the sliced-ELL layout of A: lane per row, both
+// points' dots from one 16-byte gather per entry, the row terms of
+// k_check_primal_rows (r_p = b - A x, |r_p|^2, max |r_p|, b'y) accumulated per
+// thread and reduced in a fixed order.  No lane reductions: ~0.1 instead of
+// ~0.3 L1 wavefronts per entry besides the gather.
+template <int kU>
+__global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_primal_sell(RowSet rs, SellSet S,
+                                                                          const double* __restrict__ b,
+                                                                          CheckPts pts,
+                                                                          double* __restrict__ partials) {
+  __shared__ double red[kWarps];
+  double rp2[2] = {0.0, 0.0}, rpmax[2] = {0.0, 0.0}, by[2] = {0.0, 0.0};
+  auto row_terms = [&](long long i, const double* d) {
+    const double bi = b[i];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const double r = __dsub_rn(bi, d[p]);
+      rp2[p] = fma(r, r, rp2[p]);
+      rpmax[p] = nan_max(fabs(r), rpmax[p]);
+      by[p] = fma(bi, pts.y[p][i], by[p]);
+    }
+  };
+  for (int h = blockIdx.x; h < rs.n_heavy; h += gridDim.x) {
+    const int row = rs.heavy[h];
+    double acc[2], d[2];
+    row_dot_pair<kBlock>(rs, rs.ptr[row], rs.ptr[row + 1], threadIdx.x, pts.pair, acc);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) d[p] = block_sum(acc[p], red);
+    if (threadIdx.x == 0) row_terms(row, d);
+  }
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * kWarps;
+  for (long long sl = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5; sl < S.nslices; sl += warps) {
+    const long long rl = sell_row(S, sl, lane);
+    int len = rl < rs.rows ? rs.ptr[rl + 1] - rs.ptr[rl] : -1;
+    const bool ok = len >= 0 && len <= rs.heavy_threshold;
+    if (!ok) len = 0;
+    double d[2];
+    sell_row_dot_pair<kU>(S, sl, lane, len, pts.pair, d[0], d[1]);
+    if (ok) row_terms(rl, d);
+  }
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const double t0 = block_sum(rp2[p], red);
+    const double t1 = block_max(rpmax[p], red);
+    const double t2 = block_sum(by[p], red);
+    if (threadIdx.x == 0) {
+      double* o = partials + (size_t)blockIdx.x * kMaxQ + p * PDHG_NQ;
+      o[PDHG_Q_RP2] = t0;
+      o[PDHG_Q_RPMAX] = t1;
+      o[PDHG_Q_BY] = t2;
+    }
+  }
+}
+
+// Row relabelling of a CSR matrix (warp per new row): new row r is old row
+// perm[r]; new_ptr must already hold the scanned lengths.  Entries keep their
+// order inside each row.
+__global__ void k_permute_rows(int rows, const int* __restrict__ perm, const int* __restrict__ ptr,
+                               const int* __restrict__ col, const double* __restrict__ val,
+                               const int* __restrict__ new_ptr, int* __restrict__ new_col,
+                               double* __restrict__ new_val) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  const int o = perm[w];
+  const int s = ptr[o], e = ptr[o + 1], d = new_ptr[w];
+  for (int k = lane; k < e - s; k += 32) {
+    new_col[d + k] = col[s + k];
+    new_val[d + k] = val[s + k];
+  }
+}
+
 // One block per quantity: combine per-block partials in a fixed order.
 __global__ void __launch_bounds__(kBlock) k_reduce(const double* __restrict__ partials, int nblk,
                                                    int stride, int nq, double* __restrict__ out) {
@@ -1895,13 +1914,6 @@ int launch_step(pdhg_ctx* c, bool primal, int j) {
   if (c->has_sell[k]) {
     const SellSet& S = c->sell[k];
     const int grid = a.rs.n_heavy + (int)(((long long)S.nslices * 32 + kBlock - 1) / kBlock);
-    if (S.win > 0) {  // one block per window of kBlock rows (grid above: same count)
-      if (S.u_long)
-        return primal ? launch_ex(c, k_step_sellw<true, PDHG_SELL_U_LONG>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j)
-                      : launch_ex(c, k_step_sellw<false, PDHG_SELL_U_LONG>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
-      return primal ? launch_ex(c, k_step_sellw<true, PDHG_SELL_U>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j)
-                    : launch_ex(c, k_step_sellw<false, PDHG_SELL_U>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
-    }
     if (S.u_long)
       return primal ? launch_ex(c, k_step_sell<true, PDHG_SELL_U_LONG>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j)
                     : launch_ex(c, k_step_sell<false, PDHG_SELL_U_LONG>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
@@ -2054,14 +2066,8 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
         delete c;
         return fail(PDHG_ERR_ARG, "sell layout does not match the operator");
       }
-      if (q->win != 0 && (q->win != kBlock || !q->perm || !q->slen)) {
-        delete c;
-        return fail(PDHG_ERR_ARG, "window-sorted sell layout needs win == 256, perm and slen");
-      }
       c->sell[k] = SellSet{q->rows, q->nslices, reinterpret_cast<const long long*>(q->sptr), q->width,
                            q->col, q->val, q->perm};
-      c->sell[k].win = q->win;
-      c->sell[k].slen = q->slen;
       const long long ops_nnz = k == 0 ? prob->nnz : (prob->at_nnz > 0 ? prob->at_nnz : prob->nnz);
       c->sell[k].u_long = q->rows > 0 && ops_nnz >= (long long)PDHG_SELL_U_MEAN * q->rows;
     }
@@ -2261,9 +2267,20 @@ int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
     pd.pair = c->py;
   }
   CUDA_TRY(cudaMemsetAsync(c->partials, 0, (size_t)kCheckBlocks * kMaxQ * 8, c->stream));
-  int rc = dispatch_lanes<CheckLaunch>(c->a_lanes, true, (int)npts, c->A, c->prob.b, pp, c->partials,
-                                       c->stream);
-  if (rc) return rc;
+  int rc = 0;
+  if (pp.pair && c->has_sell[0] && PDHG_CHECK_SELL) {
+    if (c->sell[0].u_long)
+      k_check_primal_sell<PDHG_SELL_U_LONG><<<kCheckBlocks, kBlock, 0, c->stream>>>(c->A, c->sell[0], c->prob.b,
+                                                                                  pp, c->partials);
+    else
+      k_check_primal_sell<PDHG_SELL_U><<<kCheckBlocks, kBlock, 0, c->stream>>>(c->A, c->sell[0], c->prob.b, pp,
+                                                                             c->partials);
+    CUDA_TRY(cudaGetLastError());
+  } else {
+    rc = dispatch_lanes<CheckLaunch>(c->a_lanes, true, (int)npts, c->A, c->prob.b, pp, c->partials,
+                                     c->stream);
+    if (rc) return rc;
+  }
   if (pd.pair && c->has_sell[1] && PDHG_CHECK_SELL) {
     if (c->sell[1].u_long)
       k_check_dual_sell<PDHG_SELL_U_LONG><<<kCheckBlocks, kBlock, 0, c->stream>>>(c->At, c->sell[1], c->prob.c, pd,
@@ -2551,6 +2568,19 @@ int pdhg_transpose_csr(int32_t m, int32_t n, int64_t nnz, const int32_t* a_ptr, 
   } else {
     CUDA_TRY(cudaMemsetAsync(at_ptr, 0, (size_t)(n + 1) * 4, s));
   }
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// Row relabelling (GpuOptions.row_order): new row r = old row perm[r]; the
+// caller scans the permuted lengths into new_ptr (rows+1) first.
+int pdhg_permute_rows(int32_t rows, const int32_t* perm, const int32_t* ptr, const int32_t* col,
+                      const double* val, const int32_t* new_ptr, int32_t* new_col, double* new_val,
+                      void* stream) {
+  if (rows <= 0 || !perm || !ptr || !col || !val || !new_ptr || !new_col || !new_val)
+    return fail(PDHG_ERR_ARG, "permute_rows: bad argument");
+  k_permute_rows<<<(unsigned)(((long long)rows * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      rows, perm, ptr, col, val, new_ptr, new_col, new_val);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

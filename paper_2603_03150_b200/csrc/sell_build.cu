@@ -109,68 +109,6 @@ __global__ void k_sell_fill(int rows, const int* __restrict__ ptr, const int* __
   }
 }
 
-// Window-sorted form (SELL-C-sigma, C = 32, sigma = W = the step kernel's
-// block): block per window of W consecutive rows; the rows are sorted by light
-// length, descending and stable (cub block radix sort), heavy rows counting as
-// empty and rows past the end sorting last.  Sorted position q of window w is
-// lane q % 32 of slice w*W/32 + q/32, so a slice holds rows of similar
-// length: config 4's A (lognormal, mean 40) pads 1.6x instead of 4.1x with
-// per-slice sorting, and the matrix stream of the step kernel costs ~0.13
-// instead of ~0.22 L1 wavefronts per entry (CSR-vector) with no shuffles.
-// perm[w*W + q] = row offset in the window, inv[w*W + offset] = q,
-// slen[w*W + q] = light length (0 for heavy / missing rows), width[slice] =
-// its first (longest) row, w32[slice] = 32 * width (scanned to sptr).
-template <int W>
-__global__ void __launch_bounds__(W) k_sellw_sort(int rows, const int* __restrict__ ptr, int heavy,
-                                                  unsigned char* __restrict__ perm,
-                                                  unsigned char* __restrict__ inv, int* __restrict__ slen,
-                                                  int* __restrict__ width, long long* __restrict__ w32) {
-  using Sort = cub::BlockRadixSort<int, W, 1, int>;
-  __shared__ typename Sort::TempStorage tmp;
-  const long long base = (long long)blockIdx.x * W;
-  const long long r = base + threadIdx.x;
-  int key[1] = {-1};
-  int val[1] = {(int)threadIdx.x};
-  if (r < rows) {
-    const int l = ptr[r + 1] - ptr[r];
-    key[0] = l > heavy ? 0 : l;
-  }
-  Sort(tmp).SortDescending(key, val);  // blocked arrangement: thread t holds sorted position t
-  const int q = threadIdx.x;
-  perm[base + q] = (unsigned char)val[0];
-  inv[base + val[0]] = (unsigned char)q;
-  const int len = key[0] < 0 ? 0 : key[0];
-  slen[base + q] = len;
-  const int ns = (rows + 31) / 32;
-  const long long sl = (base + q) / 32;
-  if ((q & 31) == 0 && sl < ns) {
-    width[sl] = len;
-    w32[sl] = 32LL * len;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) w32[ns] = 0;
-}
-
-// warp per row: copies the row's entries to its (window-sorted) slot column
-template <int W>
-__global__ void k_sellw_fill(int rows, const int* __restrict__ ptr, const int* __restrict__ col,
-                             const double* __restrict__ val, int heavy, const long long* __restrict__ sptr,
-                             const unsigned char* __restrict__ inv, int* __restrict__ scol,
-                             double* __restrict__ sval) {
-  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= rows) return;
-  const int r = (int)w;
-  const int s = ptr[r], e = ptr[r + 1];
-  if (e - s > heavy) return;
-  const int q = inv[r];
-  const long long sl = (long long)(r / W) * (W / 32) + q / 32;
-  const long long base = sptr[sl] + (q & 31);
-  for (int k = lane; k < e - s; k += 32) {
-    scol[base + 32LL * k] = col[s + k];
-    sval[base + 32LL * k] = val[s + k];
-  }
-}
-
 size_t cub_bytes(int len) {
   size_t b = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b, (long long*)nullptr, (long long*)nullptr, len);
@@ -217,42 +155,6 @@ int pdhg_sell_fill(int32_t rows, const int32_t* ptr, const int32_t* col, const d
   if (rows <= 0 || !ptr || !sptr || !scol || !sval) return set_error(PDHG_ERR_ARG, "sell_fill: bad argument");
   cudaStream_t s = (cudaStream_t)stream;
   k_sell_fill<<<(unsigned)(((long long)rows * 32 + 255) / 256), 256, 0, s>>>(
-      rows, ptr, col, val, heavy_threshold, reinterpret_cast<const long long*>(sptr), inv, scol, sval);
-  SELL_TRY(cudaGetLastError());
-  return 0;
-}
-
-int pdhg_sell_plan_window(int32_t rows, const int32_t* ptr, int32_t heavy_threshold, int32_t window,
-                          uint8_t* perm, uint8_t* inv, int32_t* slen, int32_t* width, int64_t* sptr,
-                          void* tmp, size_t tmp_bytes, void* stream, int64_t* slots_out) {
-  if (rows <= 0 || !ptr || !perm || !inv || !slen || !width || !sptr || !tmp || !slots_out)
-    return set_error(PDHG_ERR_ARG, "sell_plan_window: bad argument");
-  if (window != 256) return set_error(PDHG_ERR_ARG, "sell_plan_window: window must be 256");
-  if (tmp_bytes < pdhg_sell_tmp_bytes(rows)) return set_error(PDHG_ERR_ARG, "sell_plan_window: tmp too small");
-  cudaStream_t s = (cudaStream_t)stream;
-  const int ns = (rows + 31) / 32;
-  const int nwin = (rows + 255) / 256;
-  long long* w32 = reinterpret_cast<long long*>(sptr);
-  k_sellw_sort<256><<<nwin, 256, 0, s>>>(rows, ptr, heavy_threshold, perm, inv, slen, width, w32);
-  SELL_TRY(cudaGetLastError());
-  size_t b = tmp_bytes;
-  SELL_TRY(cub::DeviceScan::ExclusiveSum(tmp, b, w32, w32, ns + 1, s));
-  long long tot = 0;
-  SELL_TRY(cudaMemcpyAsync(&tot, w32 + ns, 8, cudaMemcpyDeviceToHost, s));
-  SELL_TRY(cudaStreamSynchronize(s));
-  SELL_TRY(cudaGetLastError());
-  *slots_out = tot;
-  return 0;
-}
-
-int pdhg_sell_fill_window(int32_t rows, const int32_t* ptr, const int32_t* col, const double* val,
-                          int32_t heavy_threshold, int32_t window, const int64_t* sptr, const uint8_t* inv,
-                          int32_t* scol, double* sval, void* stream) {
-  if (rows <= 0 || !ptr || !sptr || !inv || !scol || !sval)
-    return set_error(PDHG_ERR_ARG, "sell_fill_window: bad argument");
-  if (window != 256) return set_error(PDHG_ERR_ARG, "sell_fill_window: window must be 256");
-  cudaStream_t s = (cudaStream_t)stream;
-  k_sellw_fill<256><<<(unsigned)(((long long)rows * 32 + 255) / 256), 256, 0, s>>>(
       rows, ptr, col, val, heavy_threshold, reinterpret_cast<const long long*>(sptr), inv, scol, sval);
   SELL_TRY(cudaGetLastError());
   return 0;

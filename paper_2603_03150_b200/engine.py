@@ -70,14 +70,15 @@ class GpuOptions:
                      config 4 at 5 % (10M) 41.3 -> 35.6 us; at 1.5M entries it measured
                      50 % slower).  Skewed rows (config 4's A: 4x padding) stay on
                      CSR-vector.
-    sell_window:     "auto" | "on" | "off" -- window-sorted sliced ELL (SELL-C-sigma,
-                     csrc/sell_build.cu k_sellw_sort): rows sorted by length inside
-                     windows of 256 rows, the step kernel a block per window with a
-                     shared-memory dot exchange so the epilogue stays coalesced
-                     (k_step_sellw).  Lets skewed operators use SELL: config 4's A
-                     pads 1.45x instead of 4.1x.  auto: operators with >= sell_min_nnz
-                     entries.  Rows longer than sell_window_heavy entries are
-                     processed block per row (the operator's heavy threshold).
+    row_order:       "auto" | "length" | "natural" -- "length" renumbers the rows of A
+                     (the constraints: b, y) by decreasing length inside windows of
+                     row_order_window rows on the device, so consecutive rows -- one
+                     sliced-ELL slice -- have equal lengths and the dual step runs on
+                     sliced ELL without padding (config 4's A: 4.1x padded in natural
+                     order, ~1.03x renumbered).  y is mapped back on every
+                     download, so results are the same LP's.  auto: unsharded operators
+                     with >= sell_min_nnz entries whose natural-order padding exceeds
+                     sell_max_pad.
     sell_sort:       "auto" | "on" | "off" -- order each slice's rows by length (lanes
                      active in a round form a prefix, so fetched sectors are full):
                      config 4's A' reads 3.55 instead of 3.85 GB per primal step (period
@@ -116,8 +117,8 @@ class GpuOptions:
     sell_max_mean: float = 12.0
     sell_min_nnz: int = 5_000_000
     sell_sort: str = "auto"
-    sell_window: str = "auto"
-    sell_window_heavy: int = 256
+    row_order: str = "auto"
+    row_order_window: int = 65536
 
 
 def auto_lanes(nnz: int, rows: int) -> int:
@@ -163,11 +164,27 @@ def _medium_list(torch, ptr, lanes: int, H: int, per_lane: int):
     return idx, light_max
 
 
-def _want_window(opts: GpuOptions, nnz: int, pers_req: str = "off") -> bool:
-    """Window-sorted sliced ELL for an operator with `nnz` entries (GpuOptions.sell_window)."""
-    if opts.sell == "off" or opts.psr != "off" or pers_req in ("on", "tiny") or nnz <= 0:
+def _slice_pad(torch, ptr, H: int) -> float:
+    """Padded slots / entries of the natural-order sliced ELL of a CSR operator
+    (rows longer than H excluded, as the SELL plan does)."""
+    lens = (ptr[1:] - ptr[:-1]).to(torch.int64)
+    lens = torch.where(lens > H, torch.zeros_like(lens), lens)
+    rows = lens.numel()
+    pad_rows = (-rows) % 32
+    if pad_rows:
+        lens = torch.cat([lens, torch.zeros(pad_rows, dtype=lens.dtype, device=lens.device)])
+    slots = 32 * int(lens.view(-1, 32).max(dim=1).values.sum())
+    return slots / max(1, int(lens.sum()))
+
+
+def _want_row_order(torch, opts, ptr, nnz: int, H: int) -> bool:
+    if opts.row_order == "length":
+        return True
+    if opts.row_order != "auto" or opts.sell == "off" or opts.psr != "off" or nnz < opts.sell_min_nnz:
         return False
-    return opts.sell_window == "on" or (opts.sell_window == "auto" and nnz >= opts.sell_min_nnz)
+    if opts.persistent not in ("off", "auto") or int(opts.dual_split) > 1:
+        return False
+    return _slice_pad(torch, ptr, H) > opts.sell_max_pad
 
 
 def _as_csr(A):
@@ -237,6 +254,12 @@ class DeviceLp:
                 self.c = t(c, np.float64)
                 self.stream.synchronize()
                 t_up = time.monotonic()
+                self.row_perm = self.row_inv = None
+                if shard is None and m > 1:
+                    lanes0 = int(opts.a_lanes) or auto_lanes(nnz, m)
+                    H0 = int(opts.heavy_threshold) or heavy_threshold(lanes0)
+                    if _want_row_order(torch, opts, self.a_ptr, nnz, H0):
+                        self._renumber_rows(torch, dev, m, nnz, int(opts.row_order_window))
                 sptr = self.stream.cuda_stream
                 tmp = None
                 if At is None:
@@ -259,14 +282,6 @@ class DeviceLp:
                 self.at_lanes = int(opts.at_lanes) or auto_lanes(self.at_nnz, n)
                 H = int(opts.heavy_threshold) or heavy_threshold(self.a_lanes)
                 Ht = int(opts.heavy_threshold) or heavy_threshold(self.at_lanes)
-                # window-sorted SELL: rows longer than sell_window_heavy run block per
-                # row, so no window holds a slice wider than that
-                self.sell_window = {k: _want_window(opts, nz, pers_req=opts.persistent)
-                                    for k, nz in (("A", nnz), ("At", self.at_nnz))}
-                if self.sell_window["A"]:
-                    H = min(H, int(opts.sell_window_heavy))
-                if self.sell_window["At"]:
-                    Ht = min(Ht, int(opts.sell_window_heavy))
                 self.heavy = (H, Ht)
                 self.a_heavy = torch.nonzero((self.a_ptr[1:] - self.a_ptr[:-1]) > H).flatten().to(torch.int32)
                 self.at_heavy = torch.nonzero((self.at_ptr[1:] - self.at_ptr[:-1]) > Ht).flatten().to(torch.int32)
@@ -349,11 +364,37 @@ class DeviceLp:
         self._fin = weakref.finalize(self, self.lib.pdhg_ctx_destroy, ctx)
         self._scal = (C.c_double * (2 * N.NQ))()
 
+    def _renumber_rows(self, torch, dev, m: int, nnz: int, window: int):
+        """Renumber A's rows by decreasing length inside windows of `window` rows
+        (stable): new row r = old row row_perm[r].  A, b are permuted on the
+        device; y-space results are mapped back through row_inv."""
+        lens = (self.a_ptr[1:] - self.a_ptr[:-1]).to(torch.int64)
+        top = int(lens.max()) + 1
+        win = torch.arange(m, device=dev, dtype=torch.int64) // max(1, window)
+        key = win * (top + 1) + (top - lens)
+        perm = torch.sort(key, stable=True).indices
+        new_ptr = torch.zeros(m + 1, dtype=torch.int32, device=dev)
+        new_ptr[1:] = torch.cumsum(lens[perm], 0).to(torch.int32)
+        new_col = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        new_val = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+        perm32 = perm.to(torch.int32)
+        N.check(self.lib.pdhg_permute_rows(m, perm32.data_ptr(), self.a_ptr.data_ptr(), self.a_col.data_ptr(),
+                                           self.a_val.data_ptr(), new_ptr.data_ptr(), new_col.data_ptr(),
+                                           new_val.data_ptr(), self.stream.cuda_stream))
+        self.b = self.b[perm].contiguous()
+        inv = torch.empty_like(perm)
+        inv[perm] = torch.arange(m, device=dev, dtype=torch.int64)
+        self.stream.synchronize()
+        self.a_ptr, self.a_col, self.a_val = new_ptr, new_col, new_val
+        self.row_perm, self.row_inv = perm, inv
+        self._row_perm_host = perm.cpu().numpy()
+        self._row_inv_host = inv.cpu().numpy()
+
     def _build_sell(self, torch, dev, key, rows, nnz, ptr, col, val, H, opts):
-        """Plan + fill the sliced-ELL layout of one operator on the device (or None):
-        window-sorted (SELL-C-sigma) when enabled for this operator, else slices of
-        32 natural (optionally slice-sorted) rows."""
+        """Plan + fill the sliced-ELL layout of one operator on the device (or None)."""
         if opts.sell == "off" or rows <= 0 or nnz <= 0:
+            return None
+        if opts.sell == "auto" and nnz / rows >= opts.sell_max_mean and nnz < opts.sell_min_nnz:
             return None
         lib = self.lib
         sptr_ = self.stream.cuda_stream
@@ -363,32 +404,6 @@ class DeviceLp:
         tb = lib.pdhg_sell_tmp_bytes(rows)
         tmp = torch.empty(max(tb, 1), dtype=torch.uint8, device=dev)
         slots = C.c_int64()
-        win = 256
-        if self.sell_window.get(key):
-            nw = (rows + win - 1) // win
-            perm = torch.empty(nw * win, dtype=torch.uint8, device=dev)
-            inv = torch.empty(nw * win, dtype=torch.uint8, device=dev)
-            slen = torch.empty(nw * win, dtype=torch.int32, device=dev)
-            N.check(lib.pdhg_sell_plan_window(rows, ptr.data_ptr(), int(H), win, perm.data_ptr(),
-                                              inv.data_ptr(), slen.data_ptr(), width.data_ptr(),
-                                              sp.data_ptr(), tmp.data_ptr(), tb, sptr_, C.byref(slots)))
-            pad = slots.value / max(1, nnz)
-            self.sell_info[key] = {"slots": slots.value, "pad": pad, "used": False, "window": win}
-            scol = torch.empty(max(slots.value, 1), dtype=torch.int32, device=dev)
-            sval = torch.empty(max(slots.value, 1), dtype=torch.float64, device=dev)
-            N.check(lib.pdhg_sell_fill_window(rows, ptr.data_ptr(), col.data_ptr(), val.data_ptr(),
-                                              int(H), win, sp.data_ptr(), inv.data_ptr(),
-                                              scol.data_ptr(), sval.data_ptr(), sptr_))
-            d = N.Sell()
-            d.rows, d.nslices = rows, ns
-            d.sptr, d.width, d.col, d.val = sp.data_ptr(), width.data_ptr(), scol.data_ptr(), sval.data_ptr()
-            d.perm, d.win, d.slen = perm.data_ptr(), win, slen.data_ptr()
-            self.stream.synchronize()
-            del inv
-            self.sell_info[key].update(used=True, sorted=True)
-            return (d, (width, sp, scol, sval, perm, slen))
-        if opts.sell == "auto" and nnz / rows >= opts.sell_max_mean and nnz < opts.sell_min_nnz:
-            return None
         N.check(lib.pdhg_sell_plan(rows, ptr.data_ptr(), int(H), width.data_ptr(), sp.data_ptr(),
                                    tmp.data_ptr(), tb, sptr_, C.byref(slots)))
         pad = slots.value / max(1, nnz)
@@ -399,6 +414,8 @@ class DeviceLp:
         sval = torch.empty(max(slots.value, 1), dtype=torch.float64, device=dev)
         perm = inv = None
         sort = opts.sell_sort if isinstance(opts.sell_sort, str) else ("on" if opts.sell_sort else "off")
+        if key == "A" and self.row_perm is not None:
+            sort = "off"     # already ordered by length (row_order)
         if sort == "on" or (sort == "auto" and nnz / rows >= 12):
             perm = torch.empty(ns * 32, dtype=torch.uint8, device=dev)
             inv = torch.empty(ns * 32, dtype=torch.uint8, device=dev)
@@ -410,7 +427,6 @@ class DeviceLp:
         d.rows, d.nslices = rows, ns
         d.sptr, d.width, d.col, d.val = sp.data_ptr(), width.data_ptr(), scol.data_ptr(), sval.data_ptr()
         d.perm = perm.data_ptr() if perm is not None else None
-        d.win, d.slen = 0, None
         self.stream.synchronize()
         del inv
         self.sell_info[key]["used"] = True
@@ -509,17 +525,25 @@ class DeviceLp:
         view = lambda ptr, k: self.ws[ptr - base:ptr - base + 8 * k].view(torch.float64)
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             x = hostio.d2h(view(px.value, self.n_full))
-            y = hostio.d2h(view(py.value, self.m_full))
+            yv = view(py.value, self.m_full)
+            if self.row_perm is not None:     # renumbered constraints -> the caller's order
+                yv = yv.index_select(0, self.row_inv)
+            y = hostio.d2h(yv)
             z = hostio.d2h(view(pz.value, self.n_full)) if want_z else None
         return x, y, z
 
     def spmv(self, v: np.ndarray, transpose: bool = False) -> np.ndarray:
         """A @ v or A' @ v through the device SpMV (the 1e-12 parity gate)."""
         torch = _torch()
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        if transpose and self.row_perm is not None:
+            v = np.ascontiguousarray(v[self._row_perm_host])
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
-            vin = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(self.device)
+            vin = torch.from_numpy(v).to(self.device)
             out = torch.empty(self.n if transpose else self.m, dtype=torch.float64, device=self.device)
             N.check(self.lib.pdhg_spmv(self.ctx, 1 if transpose else 0, vin.data_ptr(), out.data_ptr()))
+            if not transpose and self.row_perm is not None:
+                out = out.index_select(0, self.row_inv)
             self.stream.synchronize()
             return out.cpu().numpy()
 

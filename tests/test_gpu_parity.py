@@ -33,14 +33,12 @@ def eng():
 # with every entry staged in shared-memory panels or gathered from global memory
 LAYOUTS = {
     "csr": dict(psr="off", sell="off", persistent="off"),
-    "sell": dict(psr="off", sell="on", sell_sort="off", sell_window="off", persistent="off"),
-    "sell_sorted": dict(psr="off", sell="on", sell_sort="on", sell_window="off", persistent="off"),
-    # rows sorted by length inside windows of 256 rows, block-per-window step with
-    # the shared-memory dot exchange (k_step_sellw); _h8: rows over 8 entries go
-    # block per row, so heavy rows and window slices meet in one launch
-    "sell_window": dict(psr="off", sell="on", sell_window="on", persistent="off"),
-    "sell_window_h8": dict(psr="off", sell="on", sell_window="on", sell_window_heavy=8,
-                           persistent="off"),
+    "sell": dict(psr="off", sell="on", sell_sort="off", persistent="off"),
+    "sell_sorted": dict(psr="off", sell="on", sell_sort="on", persistent="off"),
+    # constraints renumbered by length inside windows of 64 rows (row_order),
+    # sliced ELL on the renumbered A; y mapped back on download
+    "sell_rows": dict(psr="off", sell="on", sell_sort="off", persistent="off", row_order="length",
+                      row_order_window=64),
     "persistent": dict(psr="off", sell="off", persistent="on"),
     "tiny": dict(psr="off", sell="off", persistent="tiny"),
     "csr_split2": dict(psr="off", sell="off", persistent="off", dual_split=2),

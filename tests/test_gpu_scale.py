@@ -37,7 +37,7 @@ def c2small():
     return config2(scale=0.02, seed=12)   # 10k x ~23k, heavy-tailed rows (up to 1000)
 
 
-SCALED_LAYOUTS = {"default": {}, "psr": dict(psr="on"), "window": dict(sell_window="on")}
+SCALED_LAYOUTS = {"default": {}, "psr": dict(psr="on"), "rows": dict(row_order="length")}
 
 
 @pytest.mark.parametrize("layout", sorted(SCALED_LAYOUTS))
@@ -61,8 +61,8 @@ def test_iterates_scaled_config4(eng, c4small, layout):
         dev = eng.device_lp(p, opts)
         if psr == "on":
             assert dev.psr_info["A"]["used"] and dev.psr_info["At"]["used"]
-        if layout == "window":
-            assert dev.sell_info["A"].get("window") and dev.sell_info["At"].get("window")
+        if layout == "rows":
+            assert dev.row_perm is not None and dev.sell_info["A"]["used"]
         x, y, _ = dev.fetch(N.PT_CUR, want_z=False)
         ax, ay, _ = dev.fetch(N.PT_AVG, want_z=False)
         ox, oy, oax, oay = rec[k]
@@ -106,9 +106,10 @@ def test_heavy_rows_config2(eng, c2small, psr):
     assert dev._prob.a_n_heavy > 0
 
 
-def test_spmv_scaled_1e12(eng, c4small):
+@pytest.mark.parametrize("layout", sorted(SCALED_LAYOUTS))
+def test_spmv_scaled_1e12(eng, c4small, layout):
     p = c4small
-    dev = eng.device_lp(p, eng.GpuOptions())
+    dev = eng.device_lp(p, eng.GpuOptions(**SCALED_LAYOUTS[layout]))
     rng = np.random.default_rng(5)
     v = rng.standard_normal(p.n)
     w = rng.standard_normal(p.m)

@@ -42,7 +42,9 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_abi_version_and_error_channel(lib):
-    assert lib.pdhg_abi_version() == 1
+    from paper_2603_03150_b200 import _native
+
+    assert lib.pdhg_abi_version() == _native.ABI_VERSION == 2
     assert isinstance(lib.pdhg_last_error(), bytes)
 
 

@@ -41,12 +41,11 @@ def main():
         "sell": dict(psr="off", sell="on"),
         "sell_unsorted": dict(psr="off", sell="on", sell_sort="off"),
         "auto": dict(),
-        "nowindow": dict(sell_window="off"),
-        "window": dict(sell_window="on"),
-        "window_h128": dict(sell_window="on", sell_window_heavy=128),
-        "window_h192": dict(sell_window="on", sell_window_heavy=192),
-        "window_h512": dict(sell_window="on", sell_window_heavy=512),
-        "window_dual": dict(sell_window="on", sell="auto"),
+        "natural": dict(row_order="natural"),
+        "rows": dict(row_order="length"),
+        "rows_w4k": dict(row_order="length", row_order_window=4096),
+        "rows_global": dict(row_order="length", row_order_window=10**9),
+        "rows_h1k": dict(row_order="length", heavy_threshold=1024),
         "direct": dict(graphs=False),
         "auto_sorted": dict(sell_sort="on"),
         "auto_unsorted": dict(sell_sort="off"),
