@@ -417,6 +417,12 @@ int pdhg_sell_fill(int32_t rows, const int32_t* ptr, const int32_t* col, const d
                    int32_t heavy_threshold, const int64_t* sptr, const uint8_t* inv, int32_t* scol,
                    double* sval, void* stream);
 
+/* Feature bits of the loaded build: 1 = the experiment layouts (PSR panels,
+ * persistent period kernels, L2 persisting windows), compiled only with
+ * -DPDHG_EXPERIMENTAL=1 (python -m paper_2603_03150_b200.build --experimental);
+ * the product build rejects them in pdhg_ctx_create / pdhg_psr_*. */
+int pdhg_features(void);
+
 /* Row relabelling of a CSR matrix on the device (GpuOptions.row_order =
  * "length": the rows of A -- the y-space -- sorted by length inside windows so
  * the dual step's sliced-ELL slices hold rows of equal length).  New row r is

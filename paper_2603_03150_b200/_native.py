@@ -8,10 +8,13 @@ sm_100a kernels behind this ABI.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libpdhg_b200.so"
+# the product build; PDHG_B200_LIB points at another build of the same ABI
+# (e.g. the experiment build: python -m paper_2603_03150_b200.build --experimental)
+LIB_PATH = Path(os.environ.get("PDHG_B200_LIB") or Path(__file__).resolve().parent / "libpdhg_b200.so")
 
 PT_CUR, PT_AVG, PT_BEST = 0, 1, 2
 SPEC_BEST_Z = 16
@@ -33,7 +36,7 @@ EXPORTS = (
     "pdhg_lift_bound_duals", "pdhg_max0", "pdhg_violation_tmp_bytes", "pdhg_violation",
     "pdhg_sell_tmp_bytes", "pdhg_sell_plan", "pdhg_sell_fill", "pdhg_sell_sort", "pdhg_set_peers",
     "pdhg_run_period_check", "pdhg_center_toward_target", "pdhg_dot_tmp_bytes", "pdhg_dot",
-    "pdhg_permute_rows",
+    "pdhg_permute_rows", "pdhg_features",
 )
 
 VEC = {name: i for i, name in enumerate(
@@ -175,12 +178,22 @@ def load():
         _sig(lib, "pdhg_sell_sort", C.c_int, i32, vp, i32, vp, vp, vp)
         _sig(lib, "pdhg_sell_fill", C.c_int, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp)
         _sig(lib, "pdhg_permute_rows", C.c_int, i32, vp, vp, vp, vp, vp, vp, vp, vp)
+        _sig(lib, "pdhg_features", C.c_int)
         _sig(lib, "pdhg_violation", C.c_int, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
              vp, szt, vp, P(dbl))
         if lib.pdhg_abi_version() != ABI_VERSION:
             raise NativeError("libpdhg_b200.so ABI version mismatch")
         _lib = lib
         return lib
+
+
+FEATURE_EXPERIMENTAL = 1
+
+
+def experimental() -> bool:
+    """True when the loaded library is the experiment build (PSR, persistent
+    periods, L2 windows; measured slower, not in the product build)."""
+    return bool(load().pdhg_features() & FEATURE_EXPERIMENTAL)
 
 
 def check(rc: int) -> None:

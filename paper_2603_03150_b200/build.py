@@ -18,8 +18,11 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpdhg_b200.so"
-SOURCES = [CSRC / "pdhg_b200.cu", CSRC / "psr_build.cu", CSRC / "ruiz.cu", CSRC / "stdform.cu", CSRC / "finish.cu",
+SOURCES = [CSRC / "pdhg_b200.cu", CSRC / "ruiz.cu", CSRC / "stdform.cu", CSRC / "finish.cu",
            CSRC / "sell_build.cu"]
+# the experiment build adds the PSR builders (measured slower)
+EXPERIMENT_SOURCES = [CSRC / "psr_build.cu"]
+EXPERIMENT_LIB = ROOT / "tools" / "_libs" / "libpdhg_b200_exp.so"
 HEADERS = [ROOT / "include" / "pdhg_b200.h"] + sorted(CSRC.glob("*.cuh"))
 
 NVCC_FLAGS = [
@@ -41,7 +44,7 @@ def _stale() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    return any(p.stat().st_mtime > t for p in SOURCES + HEADERS)
+    return any(p.stat().st_mtime > t for p in SOURCES + EXPERIMENT_SOURCES + HEADERS)
 
 
 def _run(cmd, verbose):
@@ -62,12 +65,15 @@ def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: 
         return LIB
     from concurrent.futures import ThreadPoolExecutor
 
+    experimental = any(d.startswith("PDHG_EXPERIMENTAL") and not d.endswith("=0") for d in defines)
+    sources = SOURCES + (EXPERIMENT_SOURCES if experimental else [])
     objdir = PKG / ("_obj" if not defines else "_obj_" + "_".join(d.replace("=", "") for d in defines))
     objdir.mkdir(exist_ok=True)
+    lib.parent.mkdir(parents=True, exist_ok=True)
     flags = [f for f in NVCC_FLAGS if f != "-shared"] + [f"-D{d}" for d in defines]
-    objs = [objdir / (src.stem + ".o") for src in SOURCES]
+    objs = [objdir / (src.stem + ".o") for src in sources]
     cmds = [[nvcc(), *flags, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
-            for src, obj in zip(SOURCES, objs)]
+            for src, obj in zip(sources, objs)]
     with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
         list(ex.map(lambda c: _run(c, verbose), cmds))
     _run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *map(str, objs),
@@ -79,5 +85,8 @@ def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: 
 if __name__ == "__main__":
     defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
     outs = [a[len("--out="):] for a in sys.argv[1:] if a.startswith("--out=")]
+    if "--experimental" in sys.argv:   # PSR + persistent periods + L2 windows, own .so
+        defs = defs + ("PDHG_EXPERIMENTAL=1",)
+        outs = outs or [str(EXPERIMENT_LIB)]
     print(build(force="--force" in sys.argv, verbose=True, defines=defs,
                 out=Path(outs[0]) if outs else None))

@@ -23,9 +23,12 @@
 //   k_reduce        fixed-order combine of the per-block partials.
 //   k_spmv / k_div  power iteration (pdhg.py:80-109) and the 1e-12 SpMV gate.
 #include "../../include/pdhg_b200.h"
+#if PDHG_EXPERIMENTAL
 #include "psr.cuh"
+#endif
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
@@ -69,6 +72,16 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
+// Layouts and period modes that were built, parity-tested and measured
+// SLOWER than the default path (profiles/r01_pipeline.md, r01_psr_notes.md):
+// panel-staged rows (PSR, csrc/psr.cuh + psr_build.cu), the cooperative and
+// single-block period kernels, L2 persisting windows.  Compiled only into the
+// experiment build (python -m paper_2603_03150_b200.build --experimental);
+// the product library holds the reachable kernels only.
+#ifndef PDHG_EXPERIMENTAL
+#define PDHG_EXPERIMENTAL 0
+#endif
+
 #ifndef PDHG_CHECK_BPS
 #define PDHG_CHECK_BPS 4
 #endif
@@ -822,6 +835,7 @@ __global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_step_sell(StepArgs a
   }
 }
 
+#if PDHG_EXPERIMENTAL  // persistent period kernels
 // ------------------------------------------------- persistent period kernel
 //
 // One cooperative launch runs a whole period (up to the next KKT check):
@@ -935,6 +949,8 @@ __global__ void __launch_bounds__(kTinyBlock, 1) k_period_tiny(StepArgs pa, Step
   }
 }
 
+#endif  // PDHG_EXPERIMENTAL (persistent period kernels)
+
 // Dual step split by column chunks (split-K over the columns of A): pass k
 // sums each row's entries whose column lies in chunk k, so the xe gathers
 // of a pass come from an L2-sized window of the 80 MB vector instead of all
@@ -987,6 +1003,7 @@ __global__ void __launch_bounds__(kBlock) k_dual_split(StepArgs a, int j_in_peri
   else a.partial[rl] = d;
 }
 
+#if PDHG_EXPERIMENTAL  // PSR step
 // PSR step: persistent CTAs (one per SM) walk row blocks; the SpMV lands in
 // shared memory (psr::block_spmv), then the same epilogue as k_step.
 struct PsrStepArgs {
@@ -1025,6 +1042,8 @@ __global__ void __launch_bounds__(psr::kThreads, 1) k_step_psr(PsrStepArgs a, in
     });
   }
 }
+
+#endif  // PDHG_EXPERIMENTAL (PSR step)
 
 // ------------------------------------------------------------------ plain SpMV
 
@@ -1722,8 +1741,10 @@ struct pdhg_ctx {
   bool has_psr[2];     // [0] = A (dual), [1] = A' (primal)
   bool has_sell[2];    // same indexing
   SellSet sell[2];
+#if PDHG_EXPERIMENTAL
   psr::Layout psr_l[2];
   size_t psr_smem[2];
+#endif
   int l2_persist, l2_maxwin;
   int l2_mask;         // bit0: window on y for the primal step, bit1: on xe for the dual step
   int coop_grid;       // > 0: periods run as one cooperative k_period launch of this many blocks
@@ -1873,6 +1894,10 @@ int launch_period(pdhg_ctx* c, int iters) {
 }
 
 int launch_period_persistent(pdhg_ctx* c, int iters) {
+#if !PDHG_EXPERIMENTAL
+  (void)iters;
+  return fail(PDHG_ERR_STATE, "persistent period kernels need the experiment build (PDHG_EXPERIMENTAL)");
+#else
   StepArgs pa = step_args(c, true), da = step_args(c, false);
   int va = c->at_lanes, vd = c->a_lanes;
   if (c->tiny) {
@@ -1884,6 +1909,7 @@ int launch_period_persistent(pdhg_ctx* c, int iters) {
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_period, dim3(c->coop_grid), dim3(kBlock), args, 0,
                                        c->stream));
   return 0;
+#endif
 }
 
 int launch_step(pdhg_ctx* c, bool primal, int j) {
@@ -1900,6 +1926,7 @@ int launch_step(pdhg_ctx* c, bool primal, int j) {
   const void* win_base = (c->l2_mask & (primal ? 1 : 2)) ? a.gather : nullptr;
   const int lanes = primal ? c->at_lanes : c->a_lanes;
   const int k = primal ? 1 : 0;
+#if PDHG_EXPERIMENTAL
   if (c->has_psr[k]) {
     PsrStepArgs pa{c->psr_l[k], a.gather, a.cb, a.x, a.xe, a.xbar, a.P};
     const int grid = std::min(c->psr_l[k].nblk, 148);
@@ -1911,6 +1938,7 @@ int launch_step(pdhg_ctx* c, bool primal, int j) {
     // heavy rows: block per row through the CSR kernel (grid = n_heavy => no light rows)
     return dispatch_lanes<StepLaunchEx>(lanes, c, primal, a, j, a.rs.n_heavy, win_base, win);
   }
+#endif
   if (c->has_sell[k]) {
     const SellSet& S = c->sell[k];
     const int grid = a.rs.n_heavy + (int)(((long long)S.nslices * 32 + kBlock - 1) / kBlock);
@@ -1978,6 +2006,15 @@ struct DevGuard {
 }  // namespace
 #define CTX_DEVICE_GUARD(c) DevGuard dev_guard_((c) ? (c)->device : -1)
 
+namespace {
+// NVTX range over one ABI call (period, check, power iteration): the host-side
+// timeline of a run in Nsight Systems (header-only NVTX v3; no-op without a tool).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+
 extern "C" {
 
 int pdhg_abi_version(void) { return PDHG_ABI_VERSION; }
@@ -2043,6 +2080,15 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->coop_grid = 0;
   c->tiny = false;
   c->period_direct = prob->persistent == 3;
+  c->has_psr[0] = c->has_psr[1] = false;
+  c->l2_mask = c->l2_persist = c->l2_maxwin = 0;
+#if !PDHG_EXPERIMENTAL
+  if (prob->persistent == 1 || prob->persistent == 2 || prob->a_psr || prob->at_psr || (prob->l2_persist & 3)) {
+    delete c;
+    return fail(PDHG_ERR_ARG, "PSR layouts, persistent periods and L2 windows need the experiment build "
+                              "(PDHG_EXPERIMENTAL)");
+  }
+#else
   if (prob->persistent == 2 && !prob->a_sell && !prob->at_sell && !prob->a_psr && !prob->at_psr &&
       prob->a_nsplit <= 1 && mf == prob->m && nf == prob->n) {
     c->tiny = true;
@@ -2057,6 +2103,7 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
     cudaGetLastError();
     if (coop && per_sm > 0) c->coop_grid = nsm * per_sm;
   }
+#endif
   for (int k = 0; k < 2; ++k) {
     const pdhg_sell* q = k == 0 ? prob->a_sell : prob->at_sell;
     c->has_sell[k] = q != nullptr;
@@ -2072,6 +2119,7 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
       c->sell[k].u_long = q->rows > 0 && ops_nnz >= (long long)PDHG_SELL_U_MEAN * q->rows;
     }
   }
+#if PDHG_EXPERIMENTAL
   for (int k = 0; k < 2; ++k) {
     const pdhg_psr* q = k == 0 ? prob->a_psr : prob->at_psr;
     c->has_psr[k] = q != nullptr;
@@ -2102,6 +2150,7 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
     cudaFuncSetAttribute(k_step_psr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaGetLastError();
   }
+#endif
   cudaError_t e1 = cudaMallocHost(&c->P_host, sizeof(StepParams));
   cudaError_t e2 = cudaMallocHost(&c->scal_host, 64 * sizeof(double));
   if (e1 != cudaSuccess || e2 != cudaSuccess) {
@@ -2136,6 +2185,7 @@ int pdhg_spmv(pdhg_ctx* c, int transpose, const double* in, double* out) {
 int pdhg_opnorm(pdhg_ctx* c, const double* v0_host, double tol, int32_t max_iters, double* lam_out,
                 int32_t* iters_out) {
   CTX_DEVICE_GUARD(c);
+  NvtxRange nvtx_range_("pdhg_opnorm");
   // pdhg.py:80-109.  v (tn1) <- v0; loop: w (tn2) = A'(A v); ||w||; v = w/||w||.
   if (!c || !v0_host || !lam_out) return fail(PDHG_ERR_ARG, "null argument");
   if (c->mf != c->prob.m || c->nf != c->prob.n)
@@ -2188,6 +2238,7 @@ int pdhg_reset(pdhg_ctx* c) {
 int pdhg_run_period(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_over_omega,
                     double sigma_omega, double w0, int64_t* fail_iter_out) {
   CTX_DEVICE_GUARD(c);
+  NvtxRange nvtx_range_("pdhg_period");
   if (!c || iters < 0) return fail(PDHG_ERR_ARG, "bad argument");
   StepParams& h = *c->P_host;
   h.tau_w = tau_over_omega;
@@ -2213,6 +2264,7 @@ int pdhg_run_period_check(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_
                           double sigma_omega, double w0, int32_t npts, const int32_t* specs,
                           int64_t* fail_iter_out, double* out_host) {
   CTX_DEVICE_GUARD(c);
+  NvtxRange nvtx_range_("pdhg_period_check");
   // run_period + check with one host synchronisation: the graph of the
   // period, the check kernels and both device-to-host copies are queued
   // back to back on the stream.
@@ -2242,6 +2294,7 @@ int pdhg_run_period_check(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_
 
 int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
   CTX_DEVICE_GUARD(c);
+  NvtxRange nvtx_range_("pdhg_check");
   if (!c || !specs || npts < 1 || npts > 2) return fail(PDHG_ERR_ARG, "bad argument");
   // primal side (rows of A): gathers full x, row-indexed y slice;
   // dual side (rows of A'): gathers full y, row-indexed x / z slices.
@@ -2584,5 +2637,24 @@ int pdhg_permute_rows(int32_t rows, const int32_t* perm, const int32_t* ptr, con
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
+
+// Feature bits of this build: 1 = the experiment layouts (PSR, persistent
+// periods, L2 windows; PDHG_EXPERIMENTAL).
+int pdhg_features(void) { return PDHG_EXPERIMENTAL ? 1 : 0; }
+
+#if !PDHG_EXPERIMENTAL
+// The PSR builders live in psr_build.cu, compiled into the experiment build
+// only; the product library keeps the symbols and reports the missing layout.
+size_t pdhg_psr_tmp_bytes(int32_t, int32_t, int64_t) { return 0; }
+int pdhg_psr_plan(int32_t, int32_t, int64_t, const int32_t*, const int32_t*, int32_t, int32_t, void*, size_t,
+                  void*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int64_t*, int64_t*) {
+  return fail(PDHG_ERR_ARG, "PSR layouts need the experiment build (PDHG_EXPERIMENTAL)");
+}
+int pdhg_psr_build(int32_t, int32_t, int64_t, const int32_t*, const int32_t*, const double*, int32_t, void*,
+                   size_t, void*, int32_t*, int32_t*, int32_t*, uint16_t*, double*, uint16_t*, int32_t*,
+                   uint8_t*) {
+  return fail(PDHG_ERR_ARG, "PSR layouts need the experiment build (PDHG_EXPERIMENTAL)");
+}
+#endif
 
 }  // extern "C"

@@ -299,7 +299,11 @@ class DeviceLp:
                 if pers == "auto":
                     pers = ("tiny" if nnz <= opts.tiny_max_nnz and m + n <= opts.tiny_max_rows
                             and shard is None and opts.psr == "off" and int(opts.dual_split) <= 1
-                            else "off")
+                            and N.experimental() else "off")
+                if (pers in ("on", "tiny") or int(opts.l2_persist) & 3) and not N.experimental():
+                    raise N.NativeError(f"persistent={pers!r} / l2_persist need the experiment build of "
+                                        "libpdhg_b200 (both measured slower; python -m "
+                                        "paper_2603_03150_b200.build --experimental)")
                 self.persistent_mode = pers
                 self._sell = {}
                 self.sell_info = {}
@@ -437,6 +441,12 @@ class DeviceLp:
         """Plan + build the PSR layout of one operator on the device (or None)."""
         if opts.psr == "off" or (opts.psr == "auto" and rows < opts.psr_min_rows):
             return None
+        if not N.experimental():
+            if opts.psr == "auto":
+                return None
+            raise N.NativeError("psr='on' needs the experiment build of libpdhg_b200 (PSR was measured "
+                                "slower; python -m paper_2603_03150_b200.build --experimental and "
+                                "PDHG_B200_LIB=tools/_libs/libpdhg_b200_exp.so)")
         lib = self.lib
         sptr = self.stream.cuda_stream
         tb = lib.pdhg_psr_tmp_bytes(rows, cols, nnz)

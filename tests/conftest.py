@@ -64,3 +64,12 @@ def golden(request):
 
 def load_golden(name: str) -> GoldenModel:
     return GoldenModel(name)
+
+
+def skip_unless_experimental(what: str = "layout") -> None:
+    """PSR layouts, persistent periods and L2 windows exist only in the
+    experiment build of the library (measured slower)."""
+    from paper_2603_03150_b200 import _native
+
+    if not _native.experimental():
+        pytest.skip(f"{what}: experiment build only (PDHG_B200_LIB=tools/_libs/libpdhg_b200_exp.so)")

@@ -49,7 +49,16 @@ LAYOUTS = {
 }
 
 
+# layouts compiled only into the experiment build (measured slower)
+EXPERIMENTAL = {"persistent", "tiny", "psr_staged", "psr_remote"}
+
+
 def _opts(eng, layout):
+    if layout in EXPERIMENTAL:
+        from paper_2603_03150_b200 import _native
+
+        if not _native.experimental():
+            pytest.skip(f"{layout}: experiment build only (PDHG_B200_LIB=tools/_libs/libpdhg_b200_exp.so)")
     return eng.GpuOptions(**LAYOUTS[layout])
 
 

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
+from conftest import skip_unless_experimental
 from oracle.pdhg_port import KktPoint, Model, PdhgState
 
 pytestmark = pytest.mark.gpu
@@ -37,7 +38,8 @@ def c2small():
     return config2(scale=0.02, seed=12)   # 10k x ~23k, heavy-tailed rows (up to 1000)
 
 
-SCALED_LAYOUTS = {"default": {}, "psr": dict(psr="on"), "rows": dict(row_order="length")}
+SCALED_LAYOUTS = {"default": {}, "psr": dict(psr="on"),
+                  "rows": dict(row_order="length", sell="on", sell_sort="off")}
 
 
 @pytest.mark.parametrize("layout", sorted(SCALED_LAYOUTS))
@@ -48,6 +50,8 @@ def test_iterates_scaled_config4(eng, c4small, layout):
     T = eng.types()
     p = c4small
     psr = "on" if layout == "psr" else "off"
+    if psr == "on":
+        skip_unless_experimental("psr")
     opts = eng.GpuOptions(**SCALED_LAYOUTS[layout])
     rec = {}
     keep = {1, 2, 17, 63, 64, 65, 100}
@@ -72,6 +76,7 @@ def test_iterates_scaled_config4(eng, c4small, layout):
 
 def test_psr_and_csr_agree_full_run(eng, c4small):
     """Both layouts reach 1e-4 with the same iteration count; the point passes KKT."""
+    skip_unless_experimental("psr")
     T = eng.types()
     p = c4small
     runs = {}
@@ -90,6 +95,8 @@ def test_heavy_rows_config2(eng, c2small, psr):
     """Heavy-tailed rows (block-per-row path) against the oracle, 100 iterates."""
     from paper_2603_03150_b200 import _native as N
 
+    if psr == "on":
+        skip_unless_experimental("psr")
     T = eng.types()
     p = c2small
     opts = eng.GpuOptions(psr=psr, heavy_threshold=128, psr_min_rows=1)
@@ -109,6 +116,8 @@ def test_heavy_rows_config2(eng, c2small, psr):
 @pytest.mark.parametrize("layout", sorted(SCALED_LAYOUTS))
 def test_spmv_scaled_1e12(eng, c4small, layout):
     p = c4small
+    if layout == "psr":
+        skip_unless_experimental("psr")
     dev = eng.device_lp(p, eng.GpuOptions(**SCALED_LAYOUTS[layout]))
     rng = np.random.default_rng(5)
     v = rng.standard_normal(p.n)

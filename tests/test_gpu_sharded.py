@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import oracle
-from conftest import load_golden
+from conftest import load_golden, skip_unless_experimental
 from oracle.pdhg_port import KktPoint, Model
 
 pytestmark = pytest.mark.gpu
@@ -31,6 +31,8 @@ def eng():
 def test_loopback_shards_match_reference(eng, G, name, eps, limit, psr):
     from paper_2603_03150_b200.sharded import run_pdhg_sharded
 
+    if psr == "on":
+        skip_unless_experimental("psr")
     gm = load_golden(name)
     T = eng.types()
     opts = eng.GpuOptions(psr=psr, psr_min_staged=1)
@@ -112,6 +114,8 @@ def test_fused_allgather_matches_copy_allgather(eng, G, psr):
     after each half step: the same arithmetic, so bitwise-identical results."""
     from paper_2603_03150_b200.sharded import run_pdhg_sharded
 
+    if psr == "on":
+        skip_unless_experimental("psr")
     gm = load_golden("config0_s0")
     T = eng.types()
     opts = eng.GpuOptions(psr=psr, psr_min_staged=1)
