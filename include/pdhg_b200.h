@@ -144,6 +144,13 @@ typedef struct pdhg_problem {
   int32_t a_n_medium, at_n_medium;
   const int32_t* a_medium;
   const int32_t* at_medium;
+  /* Split primal step (rows of A'), as a_nsplit / a_split for the dual step:
+   * at_nsplit passes over per-row entry ranges, at_split = (at_nsplit-1)
+   * arrays of n split points.  Sharded contexts use 2 passes for both steps
+   * (local-slot entries first) so that the all-gather of the other shards'
+   * slices overlaps pass 0 (pdhg_half_step_pass). */
+  int32_t at_nsplit;
+  const int32_t* at_split;
 } pdhg_problem;
 
 typedef struct pdhg_ctx pdhg_ctx;
@@ -258,6 +265,10 @@ int pdhg_reduced_costs(pdhg_ctx* ctx, int32_t spec, double* z_slice);
 int pdhg_set_step(pdhg_ctx* ctx, int64_t iter0, double tau_over_omega, double sigma_omega,
                   double w0);
 int pdhg_half_step(pdhg_ctx* ctx, int32_t primal, int32_t j);
+/* One pass of a split half step (pass < 0: all passes).  An operator that is
+ * not split runs whole at pass 0 and launches nothing at later passes, so a
+ * host can always issue pass 0, (wait for the all-gather), pass 1. */
+int pdhg_half_step_pass(pdhg_ctx* ctx, int32_t primal, int32_t j, int32_t pass);
 /* Fused all-gather: from now on the primal (which = 0) / dual (which = 1)
  * step's epilogue also stores every new xe / y value into the full vector
  * of each of npeers peers, at this shard's slot (peers_dev: device array of

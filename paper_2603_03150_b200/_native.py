@@ -36,7 +36,7 @@ EXPORTS = (
     "pdhg_lift_bound_duals", "pdhg_max0", "pdhg_violation_tmp_bytes", "pdhg_violation",
     "pdhg_sell_tmp_bytes", "pdhg_sell_plan", "pdhg_sell_fill", "pdhg_sell_sort", "pdhg_set_peers",
     "pdhg_run_period_check", "pdhg_center_toward_target", "pdhg_dot_tmp_bytes", "pdhg_dot",
-    "pdhg_permute_rows", "pdhg_features",
+    "pdhg_permute_rows", "pdhg_features", "pdhg_half_step_pass",
 )
 
 VEC = {name: i for i, name in enumerate(
@@ -86,6 +86,7 @@ class Problem(C.Structure):
         ("a_light_max", C.c_int32), ("at_light_max", C.c_int32),
         ("a_n_medium", C.c_int32), ("at_n_medium", C.c_int32),
         ("a_medium", C.c_void_p), ("at_medium", C.c_void_p),
+        ("at_nsplit", C.c_int32), ("at_split", C.c_void_p),
     ]
 
 
@@ -179,6 +180,7 @@ def load():
         _sig(lib, "pdhg_sell_fill", C.c_int, i32, vp, vp, vp, i32, vp, vp, vp, vp, vp)
         _sig(lib, "pdhg_permute_rows", C.c_int, i32, vp, vp, vp, vp, vp, vp, vp, vp)
         _sig(lib, "pdhg_features", C.c_int)
+        _sig(lib, "pdhg_half_step_pass", C.c_int, vp, i32, i32, i32)
         _sig(lib, "pdhg_violation", C.c_int, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
              vp, szt, vp, P(dbl))
         if lib.pdhg_abi_version() != ABI_VERSION:

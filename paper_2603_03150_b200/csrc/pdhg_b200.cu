@@ -951,15 +951,18 @@ __global__ void __launch_bounds__(kTinyBlock, 1) k_period_tiny(StepArgs pa, Step
 
 #endif  // PDHG_EXPERIMENTAL (persistent period kernels)
 
-// Dual step split by column chunks (split-K over the columns of A): pass k
-// sums each row's entries whose column lies in chunk k, so the xe gathers
-// of a pass come from an L2-sized window of the 80 MB vector instead of all
-// of it (v4 profile: the unsplit dual step moved 1.67x its algorithmic
-// bytes, the scattered gathers missing L2).  Passes run in order; a row's
-// sum is ((chunk 0) + chunk 1) + ...: fixed, bitwise reproducible.  Heavy
-// rows (whole rows, block per row) go with the last pass.
-template <int V>
-__global__ void __launch_bounds__(kBlock) k_dual_split(StepArgs a, int j_in_period, int pass,
+// A step split into passes over per-row entry ranges (split-K): pass k sums
+// each row's entries [split[k-1][r], split[k][r]) (split[-1] = ptr[r],
+// split[K-1] = ptr[r+1]) into a per-row partial, and the last pass adds its
+// part and runs the epilogue; a row's sum is ((part 0) + part 1) + ...:
+// fixed, bitwise reproducible.  Heavy rows run whole (block per row) with
+// the last pass.  Two uses: the multi-GPU overlap (a shard's rows hold their
+// local-slot entries first, so pass 0 needs only this shard's slice of the
+// gathered vector and runs while the all-gather of the other slices is in
+// flight -- DESIGN.md §6), and split-K of the dual step over column chunks
+// of A (GpuOptions.dual_split, measured slower on one GPU).
+template <int V, bool PRIMAL>
+__global__ void __launch_bounds__(kBlock) k_step_split(StepArgs a, int j_in_period, int pass,
                                                        int n_heavy_now) {
   __shared__ double red[kWarps];
   pdl_enter();
@@ -967,7 +970,7 @@ __global__ void __launch_bounds__(kBlock) k_dual_split(StepArgs a, int j_in_peri
   const long long iter = P->iter0 + j_in_period + 1;
   if (P->fail_iter < iter) return;
   const double w = P->w0 + (double)(j_in_period + 1);
-  const double step = P->sigma_w;
+  const double step = PRIMAL ? P->tau_w : P->sigma_w;
   const double* xin[1] = {a.gather};
   const bool last = pass == a.nsplit - 1;
   if ((int)blockIdx.x < n_heavy_now) {
@@ -975,7 +978,10 @@ __global__ void __launch_bounds__(kBlock) k_dual_split(StepArgs a, int j_in_peri
     double acc[1];
     row_dot<kBlock, 1>(a.rs, a.rs.ptr[row], a.rs.ptr[row + 1], threadIdx.x, xin, acc);
     const double d = block_sum(acc[0], red);
-    if (threadIdx.x == 0) bcast(P, 1, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
+    if (threadIdx.x == 0) {
+      if (PRIMAL) bcast(P, 0, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast(P, 1, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
+    }
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -999,8 +1005,13 @@ __global__ void __launch_bounds__(kBlock) k_dual_split(StepArgs a, int j_in_peri
   const double dot = warp_rows_dot_seg<V>(a.rs, sp, ep, row0, lane, xin, ok);
   if (!ok) return;
   const double d = pass > 0 ? part + dot : dot;
-  if (last) bcast(P, 1, (int)rl, dual_epi_pre((int)rl, d, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
-  else a.partial[rl] = d;
+  if (!last) {
+    a.partial[rl] = d;
+    return;
+  }
+  const int row = (int)rl;
+  if (PRIMAL) bcast(P, 0, row, primal_epi_pre(row, d, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
+  else bcast(P, 1, row, dual_epi_pre(row, d, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
 }
 
 #if PDHG_EXPERIMENTAL  // PSR step
@@ -1816,11 +1827,13 @@ int launch_ex(const pdhg_ctx* c, K kernel, dim3 grid, dim3 block, size_t smem, c
 
 template <int V>
 struct SplitLaunch {
-  static int run(const pdhg_ctx* c, const StepArgs& a, int j) {
-    for (int pass = 0; pass < a.nsplit; ++pass) {
+  // passes [p0, p1) of a split step
+  static int run(const pdhg_ctx* c, bool primal, const StepArgs& a, int j, int p0, int p1) {
+    for (int pass = p0; pass < p1; ++pass) {
       const int nh = pass == a.nsplit - 1 ? a.rs.n_heavy : 0;
       const int g = nh + (int)((a.rs.rows + (long long)kBlock - 1) / kBlock);
-      int rc = launch_ex(c, k_dual_split<V>, dim3(g), dim3(kBlock), 0, nullptr, 0, a, j, pass, nh);
+      int rc = primal ? launch_ex(c, k_step_split<V, true>, dim3(g), dim3(kBlock), 0, nullptr, 0, a, j, pass, nh)
+                      : launch_ex(c, k_step_split<V, false>, dim3(g), dim3(kBlock), 0, nullptr, 0, a, j, pass, nh);
       if (rc) return rc;
     }
     return 0;
@@ -1912,16 +1925,25 @@ int launch_period_persistent(pdhg_ctx* c, int iters) {
 #endif
 }
 
-int launch_step(pdhg_ctx* c, bool primal, int j) {
+int launch_step_pass(pdhg_ctx* c, bool primal, int j, int pass);
+
+int launch_step(pdhg_ctx* c, bool primal, int j) { return launch_step_pass(c, primal, j, -1); }
+
+// One half step, or one pass of a split half step (pass < 0: all passes; an
+// unsplit operator runs whole at pass 0 and nothing at later passes).
+int launch_step_pass(pdhg_ctx* c, bool primal, int j, int pass) {
   // gathers read the full (padded) vectors; the rows a shard owns are
   // written through pointers offset to its slice
   StepArgs a = step_args(c, primal);
-  if (!primal && c->prob.a_nsplit > 1 && !c->has_psr[0]) {
-    a.split = c->prob.a_split;
-    a.nsplit = c->prob.a_nsplit;
-    a.partial = c->tm2;
-    return dispatch_lanes<SplitLaunch>(c->a_lanes, c, a, j);
+  const int nsplit = primal ? c->prob.at_nsplit : c->prob.a_nsplit;
+  if (nsplit > 1 && !c->has_psr[primal ? 1 : 0]) {
+    a.split = primal ? c->prob.at_split : c->prob.a_split;
+    a.nsplit = nsplit;
+    a.partial = primal ? c->tn2 : c->tm2;
+    const int p0 = pass < 0 ? 0 : pass, p1 = pass < 0 ? nsplit : std::min(pass + 1, nsplit);
+    return dispatch_lanes<SplitLaunch>(primal ? c->at_lanes : c->a_lanes, c, primal, a, j, p0, p1);
   }
+  if (pass > 0) return 0;
   const size_t win = (size_t)(primal ? c->mf : c->nf) * 8;
   const void* win_base = (c->l2_mask & (primal ? 1 : 2)) ? a.gather : nullptr;
   const int lanes = primal ? c->at_lanes : c->a_lanes;
@@ -2077,6 +2099,10 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->P = cv.take<StepParams>(1);
   c->px = cv.take<double2>(n);
   c->py = cv.take<double2>(m);
+  if ((prob->a_nsplit > 1 && !prob->a_split) || (prob->at_nsplit > 1 && !prob->at_split)) {
+    delete c;
+    return fail(PDHG_ERR_ARG, "split step without split points");
+  }
   c->coop_grid = 0;
   c->tiny = false;
   c->period_direct = prob->persistent == 3;
@@ -2487,6 +2513,15 @@ int pdhg_half_step(pdhg_ctx* c, int32_t primal, int32_t j) {
   CTX_DEVICE_GUARD(c);
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
   int rc = launch_step(c, primal != 0, j);
+  if (rc) return rc;
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int pdhg_half_step_pass(pdhg_ctx* c, int32_t primal, int32_t j, int32_t pass) {
+  CTX_DEVICE_GUARD(c);
+  if (!c) return fail(PDHG_ERR_ARG, "null ctx");
+  int rc = launch_step_pass(c, primal != 0, j, pass);
   if (rc) return rc;
   CUDA_TRY(cudaGetLastError());
   return 0;

@@ -307,10 +307,18 @@ class DeviceLp:
                 self.persistent_mode = pers
                 self._sell = {}
                 self.sell_info = {}
+                # split steps (sharded local-first blocks, overlapped schedule): pass 0 =
+                # each row's local-slot entries, pass 1 = the rest + epilogue (CSR kernels)
+                self.split_local = {"A": None, "At": None}
+                if shard is not None and getattr(shard, "a_nloc", None) is not None:
+                    for key, ptr, nloc in (("A", self.a_ptr, shard.a_nloc), ("At", self.at_ptr, shard.at_nloc)):
+                        nl = torch.from_numpy(np.ascontiguousarray(nloc, dtype=np.int32)).to(dev)
+                        self.split_local[key] = (ptr[:-1] + nl).contiguous()
                 for key, rows, nz, ptr, col, val, Hk in (
                         ("A", m, nnz, self.a_ptr, self.a_col, self.a_val, H),
                         ("At", n, self.at_nnz, self.at_ptr, self.at_col, self.at_val, Ht)):
-                    self._sell[key] = None if (self._psr[key] or pers in ("tiny", "on")) else \
+                    self._sell[key] = None if (self._psr[key] or pers in ("tiny", "on")
+                                               or self.split_local[key] is not None) else \
                         self._build_sell(torch, dev, key, rows, nz, ptr, col, val, Hk, opts)
                 self.stream.synchronize()
                 t_sell = time.monotonic()
@@ -356,6 +364,10 @@ class DeviceLp:
         p.at_nnz = self.at_nnz
         p.a_nsplit = self.nsplit
         p.a_split = self.a_split.data_ptr() if self.a_split is not None else None
+        if self.split_local["A"] is not None:
+            p.a_nsplit, p.a_split = 2, self.split_local["A"].data_ptr()
+        if self.split_local["At"] is not None:
+            p.at_nsplit, p.at_split = 2, self.split_local["At"].data_ptr()
         self._prob = p
         ctx = C.c_void_p()
         N.check(self.lib.pdhg_ctx_create(C.byref(p), self.ws.data_ptr(), ws_bytes,
@@ -597,6 +609,11 @@ class DeviceLp:
 
     def half_step(self, primal: bool, j: int):
         N.check(self.lib.pdhg_half_step(self.ctx, 1 if primal else 0, int(j)))
+
+    def half_step_pass(self, primal: bool, j: int, pass_: int):
+        """Pass 0 (local-slot entries) or pass 1 (the rest + epilogue) of a split
+        half step; an unsplit operator runs whole at pass 0."""
+        N.check(self.lib.pdhg_half_step_pass(self.ctx, 1 if primal else 0, int(j), int(pass_)))
 
     def fail_iter(self) -> int:
         f = C.c_int64()

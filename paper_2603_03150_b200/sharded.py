@@ -71,6 +71,20 @@ def _cuts(counts_ptr: np.ndarray, G: int) -> np.ndarray:
     return np.asarray(cuts, dtype=np.int64)
 
 
+def _local_first(M: sp.csr_matrix, lo: int, hi: int):
+    """Reorder each row's entries: columns in [lo, hi) first, then the rest,
+    each part keeping its order; returns (matrix, per-row count of the first part)."""
+    rows = M.shape[0]
+    lens = np.diff(M.indptr)
+    rid = np.repeat(np.arange(rows, dtype=np.int64), lens)
+    remote = (M.indices < lo) | (M.indices >= hi)
+    order = np.argsort(rid * 2 + remote, kind="stable")
+    nloc = np.bincount(rid[~remote], minlength=rows).astype(np.int32)
+    out = sp.csr_matrix((M.data[order], M.indices[order], M.indptr.copy()), shape=M.shape)
+    out.has_sorted_indices = False
+    return out, nloc
+
+
 @dataclass
 class ShardBlock:
     """What shard g needs: its A rows, its A' rows, b/c slices and slice offsets."""
@@ -84,6 +98,11 @@ class ShardBlock:
     n_full: int
     y_off: int
     x_off: int
+    # local_first blocks: each row holds its entries in this shard's own slot
+    # range first (a_nloc / at_nloc of them), then the others, each part in
+    # column order -- the split steps' pass 0 / pass 1
+    a_nloc: np.ndarray | None = None
+    at_nloc: np.ndarray | None = None
 
 
 class ShardPlan:
@@ -108,18 +127,31 @@ class ShardPlan:
         self.yslot = (rg * self.maxR + np.arange(self.m) - self.rcut[rg]).astype(np.int64)
         self.xslot = (cg * self.maxC + np.arange(self.n) - self.ccut[cg]).astype(np.int64)
 
-    def block(self, g: int, A, b, c) -> ShardBlock:
-        A = sp.csr_matrix(A)
+    def block(self, g: int, A, b, c, local_first: bool = False) -> ShardBlock:
+        """Shard g's rows of A and of A' (slot-indexed).  ``local_first``: each
+        row's entries in g's own slot range first (for the overlapped
+        schedule's split steps), with their counts in a_nloc / at_nloc."""
+        A = A if sp.isspmatrix_csr(A) else sp.csr_matrix(A)
         r0, r1 = int(self.rcut[g]), int(self.rcut[g + 1])
         c0, c1 = int(self.ccut[g]), int(self.ccut[g + 1])
         Ar = A[r0:r1]
         Ag = sp.csr_matrix((Ar.data, self.xslot[Ar.indices].astype(np.int32), Ar.indptr),
                            shape=(r1 - r0, self.n_full))
-        Ac = A[:, c0:c1].tocsc()   # CSC of the column block = CSR of its transpose
-        Atg = sp.csr_matrix((Ac.data, self.yslot[Ac.indices].astype(np.int32), Ac.indptr),
+        # CSC of A once per plan (column blocks are then contiguous ranges) =
+        # CSR of the transpose's row blocks
+        if getattr(self, "_csc_of", None) is not A:
+            self._csc, self._csc_of = A.tocsc(), A
+        Acsc = self._csc
+        s0, s1 = int(Acsc.indptr[c0]), int(Acsc.indptr[c1])
+        Atg = sp.csr_matrix((Acsc.data[s0:s1], self.yslot[Acsc.indices[s0:s1]].astype(np.int32),
+                             (Acsc.indptr[c0:c1 + 1] - s0).astype(Acsc.indptr.dtype)),
                             shape=(c1 - c0, self.m_full))
-        return ShardBlock(g, Ag, Atg, np.asarray(b, float)[r0:r1], np.asarray(c, float)[c0:c1],
-                          self.m_full, self.n_full, g * self.maxR, g * self.maxC)
+        blk = ShardBlock(g, Ag, Atg, np.asarray(b, float)[r0:r1], np.asarray(c, float)[c0:c1],
+                         self.m_full, self.n_full, g * self.maxR, g * self.maxC)
+        if local_first:
+            blk.A, blk.a_nloc = _local_first(Ag, g * self.maxC, (g + 1) * self.maxC)
+            blk.At, blk.at_nloc = _local_first(Atg, g * self.maxR, (g + 1) * self.maxR)
+        return blk
 
     def slice_len(self, space: str) -> int:
         return self.maxC if space == "x" else self.maxR
@@ -278,10 +310,21 @@ def _combine(rows: np.ndarray, npts: int) -> list[np.ndarray]:
 class ShardedDevice:
     """G shards behind engine._run's device interface (see module doc)."""
 
-    def __init__(self, plan: ShardPlan, shards, comm, graph: bool = True):
+    def __init__(self, plan: ShardPlan, shards, comm, graph: bool = True, overlap: str = "off"):
+        """overlap: "on" -- split half steps (local-first blocks) with each
+        all-gather on a side stream, overlapping pass 0 (DESIGN.md §6);
+        "serial" -- the same split kernels and all-gathers on one stream (the
+        bitwise reference for "on"); "off" -- unsplit half steps."""
+        if overlap not in ("off", "on", "serial"):
+            raise ValueError(f"overlap must be 'off', 'on' or 'serial', not {overlap!r}")
         self.plan = plan
         self.shards = list(shards)   # local shard backends, in comm.local order
         self.comm = comm
+        self.overlap = overlap
+        if overlap == "on" and (getattr(comm, "fused", False)
+                                or any(getattr(sh, "stream", None) is None for sh in self.shards)):
+            self.overlap = "serial"   # fused stores / CPU doubles: no side stream to overlap on
+        self._comm_stream = None
         self.m, self.n = plan.m, plan.n
         # a period (kernels + all-gathers) is captured once per length and
         # replayed, like the single-GPU engine's graphs; the symmetric-memory
@@ -378,8 +421,63 @@ class ShardedDevice:
         self._graphs[iters] = g
         return g
 
+    def _side_stream(self):
+        import torch
+
+        if self._comm_stream is None:
+            self._comm_stream = torch.cuda.Stream(self.shards[0].stream.device)
+        return self._comm_stream
+
+    def _period_split(self, iters: int):
+        """Split half steps.  overlap="on": per half step, pass 0 (the shard's
+        local-slot entries) runs while the other shards' slices of the vector it
+        just produced are all-gathered on a side stream; pass 1 (remote entries
+        + epilogue) waits for that all-gather.  "serial": the same on one stream."""
+        import contextlib
+
+        import torch
+
+        side = self.overlap == "on"
+        main = self.shards[0].stream
+        comm = self._side_stream() if side else None
+        pending = None                  # event: last all-gather (of y) done on the side stream
+
+        def gather(name):
+            if not side:
+                self._ag(name)
+                return None
+            ev = torch.cuda.Event()
+            ev.record(main)
+            comm.wait_event(ev)
+            with torch.cuda.stream(comm):
+                self.comm.allgather(self.shards, name)
+            done = torch.cuda.Event()
+            done.record(comm)
+            return done
+
+        with torch.cuda.stream(main) if main is not None else contextlib.nullcontext():
+            for j in range(iters):
+                for sh in self.shards:
+                    sh.half_step_pass(True, j, 0)
+                if pending is not None:
+                    main.wait_event(pending)
+                for sh in self.shards:
+                    sh.half_step_pass(True, j, 1)
+                done_x = gather("xe")
+                for sh in self.shards:
+                    sh.half_step_pass(False, j, 0)
+                if done_x is not None:
+                    main.wait_event(done_x)
+                for sh in self.shards:
+                    sh.half_step_pass(False, j, 1)
+                pending = gather("y")
+            if pending is not None:
+                main.wait_event(pending)
+
     def _period_body(self, iters: int):
         """The kernels and all-gathers of one period, queued on the shards' stream."""
+        if self.overlap in ("on", "serial") and iters > 0:
+            return self._period_split(iters)
         fused = getattr(self.comm, "fused", False)
         if fused and iters > 0:         # every rank has reset its fail word (set_step)
             with self._on_stream():
@@ -465,27 +563,34 @@ def _to_like(a: np.ndarray, like):
 # ----------------------------------------------------------- entry points
 
 
-def build_sharded(p, G: int, comm_kind: str = "loopback", opts=None, group=None):
+def build_sharded(p, G: int, comm_kind: str = "loopback", opts=None, group=None, overlap: str = "auto"):
     """ShardedDevice for StandardLp ``p`` over G shards of CUDA contexts.
 
     comm_kind="loopback": all G shards on the current device (one process);
     comm_kind="torch": this process's shard (rank) of a torch.distributed job.
+    overlap: "on" / "serial" / "off" (ShardedDevice); "auto" = "on" for the
+    NCCL all-gather mode ("torch"), "off" otherwise.
     """
     import torch
 
     from .engine import DeviceLp, GpuOptions
 
     opts = opts or GpuOptions()
+    if overlap == "auto":
+        overlap = "on" if comm_kind == "torch" else "off"
+    split = overlap in ("on", "serial") and comm_kind in ("loopback", "torch")
+    if not split:
+        overlap = "off"
     plan = ShardPlan(p.A, G)
     if comm_kind in ("loopback", "loopback_fused"):
         comm = LoopbackComm(plan, fused=comm_kind == "loopback_fused")
         dev = torch.device("cuda", torch.cuda.current_device() if opts.device is None else opts.device)
         stream = torch.cuda.Stream(dev)
         shards = [DeviceLp(blk.A, blk.b, blk.c, opts, shard=blk, stream=stream)
-                  for blk in (plan.block(g, p.A, p.b, p.c) for g in range(G))]
+                  for blk in (plan.block(g, p.A, p.b, p.c, local_first=split) for g in range(G))]
     elif comm_kind in ("torch", "torch_peer"):
         comm = TorchComm(plan, group, fused=comm_kind == "torch_peer")
-        blk = plan.block(comm.rank, p.A, p.b, p.c)
+        blk = plan.block(comm.rank, p.A, p.b, p.c, local_first=split)
         alloc = comm.symmetric_workspace if comm.fused else None
         shards = [DeviceLp(blk.A, blk.b, blk.c, opts, shard=blk, ws_alloc=alloc)]
     else:
@@ -494,11 +599,11 @@ def build_sharded(p, G: int, comm_kind: str = "loopback", opts=None, group=None)
         comm.connect_peers(shards)
     if hasattr(comm, "connect_fail"):
         comm.connect_fail(shards)   # loopback: same device; torch_peer: NVLink atomics
-    return ShardedDevice(plan, shards, comm)
+    return ShardedDevice(plan, shards, comm, overlap=overlap)
 
 
 def run_pdhg_sharded(p, params=None, seed: int = 0, *, G: int, comm_kind: str = "loopback",
-                     gpu=None, group=None):
+                     gpu=None, group=None, overlap: str = "auto"):
     """run_pdhg (pdhg.py:162-258) over G shards; same results contract."""
     import threading
     import time
@@ -516,6 +621,107 @@ def run_pdhg_sharded(p, params=None, seed: int = 0, *, G: int, comm_kind: str = 
     t0 = time.monotonic()
     if p.A.nnz == 0:
         raise T.InvalidModelError("cannot estimate the norm of an empty matrix")
-    dev = build_sharded(p, G, comm_kind, opts, group)
+    dev = build_sharded(p, G, comm_kind, opts, group, overlap=overlap)
+    dev.lock = threading.Lock()
+    return engine._run(T, dev, p, params, seed, opts, t0)
+
+
+# ------------------------------------------------- per-rank blocks (no full model)
+
+
+def plan_state(plan: ShardPlan) -> dict:
+    """What a rank needs of the plan without the matrix (cuts, slots, sizes)."""
+    return {k: getattr(plan, k) for k in ("G", "m", "n", "nnz", "rcut", "ccut", "maxR", "maxC",
+                                          "m_full", "n_full", "yslot", "xslot")}
+
+
+def plan_from_state(state: dict) -> ShardPlan:
+    plan = ShardPlan.__new__(ShardPlan)
+    for k, v in state.items():
+        setattr(plan, k, v)
+    return plan
+
+
+def save_block(path, plan: ShardPlan, blk: ShardBlock, b_full, c_full) -> None:
+    """One rank's block + the plan's state, as an uncompressed .npz (e.g. under
+    /dev/shm): ranks then load only their own rows instead of every rank
+    generating and slicing the whole model."""
+    arrays = {f"plan_{k}": np.asarray(v) for k, v in plan_state(plan).items()}
+    for key, M in (("A", blk.A), ("At", blk.At)):
+        arrays[f"{key}_data"], arrays[f"{key}_indices"] = M.data, M.indices
+        arrays[f"{key}_indptr"], arrays[f"{key}_shape"] = M.indptr, np.asarray(M.shape)
+    for k in ("b", "c"):
+        arrays[k] = getattr(blk, k)
+    for k in ("a_nloc", "at_nloc"):
+        if getattr(blk, k) is not None:
+            arrays[k] = getattr(blk, k)
+    arrays["meta"] = np.asarray([blk.g, blk.m_full, blk.n_full, blk.y_off, blk.x_off])
+    arrays["b_full"], arrays["c_full"] = np.asarray(b_full, float), np.asarray(c_full, float)
+    np.savez(path, **arrays)
+
+
+def load_block(path):
+    """(plan, block, b_full, c_full) from save_block's file."""
+    z = np.load(path)
+    state = {k[len("plan_"):]: (z[k].item() if z[k].ndim == 0 else z[k]) for k in z.files
+             if k.startswith("plan_")}
+    plan = plan_from_state(state)
+    mats = {key: sp.csr_matrix((z[f"{key}_data"], z[f"{key}_indices"], z[f"{key}_indptr"]),
+                               shape=tuple(z[f"{key}_shape"])) for key in ("A", "At")}
+    for M in mats.values():
+        M.has_sorted_indices = False     # local-first blocks are not column-sorted
+    g, m_full, n_full, y_off, x_off = (int(v) for v in z["meta"])
+    blk = ShardBlock(g, mats["A"], mats["At"], z["b"], z["c"], m_full, n_full, y_off, x_off,
+                     z["a_nloc"] if "a_nloc" in z.files else None,
+                     z["at_nloc"] if "at_nloc" in z.files else None)
+    return plan, blk, z["b_full"], z["c_full"]
+
+
+def build_sharded_from_block(plan: ShardPlan, blk: ShardBlock, comm_kind: str = "torch", opts=None,
+                             group=None, overlap: str = "auto"):
+    """This rank's ShardedDevice from its own block (torch.distributed job)."""
+    from .engine import DeviceLp, GpuOptions
+
+    opts = opts or GpuOptions()
+    if comm_kind not in ("torch", "torch_peer"):
+        raise ValueError("build_sharded_from_block is for one shard per process")
+    comm = TorchComm(plan, group, fused=comm_kind == "torch_peer")
+    if comm.rank != blk.g:
+        raise ValueError(f"block {blk.g} loaded on rank {comm.rank}")
+    if overlap == "auto":
+        overlap = "on" if comm_kind == "torch" and blk.a_nloc is not None else "off"
+    if overlap != "off" and blk.a_nloc is None:
+        raise ValueError("the overlapped schedule needs a local_first block")
+    alloc = comm.symmetric_workspace if comm.fused else None
+    shards = [DeviceLp(blk.A, blk.b, blk.c, opts, shard=blk, ws_alloc=alloc)]
+    if comm.fused:
+        comm.connect_peers(shards)
+    return ShardedDevice(plan, shards, comm, overlap=overlap)
+
+
+def run_pdhg_sharded_block(plan: ShardPlan, blk: ShardBlock, b_full, c_full, params=None, seed: int = 0, *,
+                           comm_kind: str = "torch", gpu=None, group=None, overlap: str = "auto"):
+    """run_pdhg (pdhg.py:162-258) from this rank's block; same results contract.
+    The host loop reads only b and c of the whole model (its norms)."""
+    import threading
+    import time
+
+    from . import engine
+    from .lp_types import resolve
+
+    T = resolve()
+    opts = gpu or engine.GpuOptions()
+    if params is None:
+        params = T.PdhgParams()
+    if plan.m == 0 or plan.n == 0:
+        raise T.InvalidModelError("pdhg requires a nonempty model")
+    t0 = time.monotonic()
+
+    class _Model:   # what engine._run reads of the StandardLp
+        pass
+
+    p = _Model()
+    p.b, p.c = np.asarray(b_full, float), np.asarray(c_full, float)
+    dev = build_sharded_from_block(plan, blk, comm_kind, opts, group, overlap)
     dev.lock = threading.Lock()
     return engine._run(T, dev, p, params, seed, opts, t0)

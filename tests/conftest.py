@@ -66,6 +66,20 @@ def load_golden(name: str) -> GoldenModel:
     return GoldenModel(name)
 
 
+def experimental_build() -> bool:
+    """Is the loaded library the experiment build?  (Collection-time: the
+    experiment-only parametrizations are left out of the product build's run.)"""
+    try:
+        from paper_2603_03150_b200 import _native
+
+        return _native.experimental()
+    except Exception:
+        return False
+
+
+EXPERIMENTAL_BUILD = experimental_build()
+
+
 def skip_unless_experimental(what: str = "layout") -> None:
     """PSR layouts, persistent periods and L2 windows exist only in the
     experiment build of the library (measured slower)."""

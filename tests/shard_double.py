@@ -35,6 +35,22 @@ class NumpyShard:
         self.params = None
         self.fail = -1
         self.fail_peers = []
+        # local_first blocks (split steps): each row's first nloc entries are the
+        # shard's own slots -- pass 0 sums them, pass 1 the rest + epilogue
+        self.split = {}
+        for key, M, nloc in (("A", self.A, getattr(blk, "a_nloc", None)),
+                             ("At", self.At, getattr(blk, "at_nloc", None))):
+            if nloc is not None:
+                pos = np.arange(M.nnz) - np.repeat(M.indptr[:-1], np.diff(M.indptr))
+                first = pos < np.repeat(np.asarray(nloc), np.diff(M.indptr))
+                rid = np.repeat(np.arange(M.shape[0]), np.diff(M.indptr))
+
+                def part(mask, M=M, rid=rid):
+                    ptr = np.concatenate([[0], np.cumsum(np.bincount(rid[mask], minlength=M.shape[0]))])
+                    return sp.csr_matrix((M.data[mask], M.indices[mask], ptr), shape=M.shape)
+
+                self.split[key] = (part(first), part(~first))
+        self.partial = {}
 
     def vec(self, name):
         return torch.from_numpy(self.v[name])
@@ -53,7 +69,22 @@ class NumpyShard:
         self.params = (int(iter0), tau_w, sigma_w, w0)
         self.fail = -1
 
-    def half_step(self, primal, j):
+    def half_step_pass(self, primal, j, pass_):
+        """Split half step (pdhg_half_step_pass): pass 0 = local-slot entries,
+        pass 1 = the rest, added to the pass-0 partial, + the epilogue."""
+        key = "At" if primal else "A"
+        if key not in self.split:
+            if pass_ == 0:
+                self.half_step(primal, j)
+            return
+        loc, rem = self.split[key]
+        v = self.v["y"] if primal else self.v["xe"]
+        if pass_ == 0:
+            self.partial[key] = loc @ v
+            return
+        self.half_step(primal, j, dot=self.partial.pop(key) + rem @ v)
+
+    def half_step(self, primal, j, dot=None):
         iter0, tau_w, sigma_w, w0 = self.params
         it = iter0 + j + 1
         if self.fail >= 0 and self.fail < it:
@@ -62,14 +93,16 @@ class NumpyShard:
         if primal:
             xs = self._xs()
             x = self.v["x"][xs].copy()
-            xn = np.maximum(0.0, x - tau_w * (self.c - self.At @ self.v["y"]))
+            aty = self.At @ self.v["y"] if dot is None else dot
+            xn = np.maximum(0.0, x - tau_w * (self.c - aty))
             self.v["x"][xs] = xn
             self.v["xe"][xs] = 2.0 * xn - x
             self.v["xbar"][xs] += (xn - self.v["xbar"][xs]) / w
             bad = not np.all(np.isfinite(xn))
         else:
             ys = self._ys()
-            yn = self.v["y"][ys] + sigma_w * (self.b - self.A @ self.v["xe"])
+            ax = self.A @ self.v["xe"] if dot is None else dot
+            yn = self.v["y"][ys] + sigma_w * (self.b - ax)
             self.v["y"][ys] = yn
             self.v["ybar"][ys] += (yn - self.v["ybar"][ys]) / w
             bad = not np.all(np.isfinite(yn))

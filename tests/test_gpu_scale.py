@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
-from conftest import skip_unless_experimental
+from conftest import EXPERIMENTAL_BUILD, skip_unless_experimental
 from oracle.pdhg_port import KktPoint, Model, PdhgState
 
 pytestmark = pytest.mark.gpu
@@ -38,8 +38,10 @@ def c2small():
     return config2(scale=0.02, seed=12)   # 10k x ~23k, heavy-tailed rows (up to 1000)
 
 
-SCALED_LAYOUTS = {"default": {}, "psr": dict(psr="on"),
-                  "rows": dict(row_order="length", sell="on", sell_sort="off")}
+SCALED_LAYOUTS = {"default": {}, "rows": dict(row_order="length", sell="on", sell_sort="off")}
+if EXPERIMENTAL_BUILD:
+    SCALED_LAYOUTS["psr"] = dict(psr="on")
+PSR_PARAMS = ["off", "on"] if EXPERIMENTAL_BUILD else ["off"]
 
 
 @pytest.mark.parametrize("layout", sorted(SCALED_LAYOUTS))
@@ -74,6 +76,7 @@ def test_iterates_scaled_config4(eng, c4small, layout):
         assert _rel(ax, oax) <= 1e-9 and _rel(ay, oay) <= 1e-9, k
 
 
+@pytest.mark.skipif(not EXPERIMENTAL_BUILD, reason="PSR: experiment build only")
 def test_psr_and_csr_agree_full_run(eng, c4small):
     """Both layouts reach 1e-4 with the same iteration count; the point passes KKT."""
     skip_unless_experimental("psr")
@@ -90,7 +93,7 @@ def test_psr_and_csr_agree_full_run(eng, c4small):
     assert runs["on"][1] == pytest.approx(runs["off"][1], rel=1e-6)
 
 
-@pytest.mark.parametrize("psr", ["off", "on"])
+@pytest.mark.parametrize("psr", PSR_PARAMS)
 def test_heavy_rows_config2(eng, c2small, psr):
     """Heavy-tailed rows (block-per-row path) against the oracle, 100 iterates."""
     from paper_2603_03150_b200 import _native as N

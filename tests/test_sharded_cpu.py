@@ -291,3 +291,100 @@ def test_loopback_dense_row_matches_oracle():
     assert st.status.value == ost.status.value
     assert st.iterations == ost.iterations and st.restarts == ost.restarts
     np.testing.assert_allclose(pt.x, opt.x, rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("G", [2, 3, 5])
+def test_local_first_blocks(G):
+    """local_first blocks: the same entries per row, the shard's own slot range
+    first (a_nloc / at_nloc of them), each part in column order."""
+    gm = load_golden("config0_s0")
+    plan = ShardPlan(gm.A, G)
+    for g in range(G):
+        ref = plan.block(g, gm.A, gm.b, gm.c)
+        blk = plan.block(g, gm.A, gm.b, gm.c, local_first=True)
+        for M, R, nloc, lo, hi in ((blk.A, ref.A, blk.a_nloc, g * plan.maxC, (g + 1) * plan.maxC),
+                                   (blk.At, ref.At, blk.at_nloc, g * plan.maxR, (g + 1) * plan.maxR)):
+            np.testing.assert_array_equal(M.indptr, R.indptr)
+            assert nloc.shape == (M.shape[0],)
+            for r in range(M.shape[0]):
+                s, e = M.indptr[r], M.indptr[r + 1]
+                cols, vals = M.indices[s:e], M.data[s:e]
+                k = int(nloc[r])
+                assert np.all((cols[:k] >= lo) & (cols[:k] < hi))
+                assert not np.any((cols[k:] >= lo) & (cols[k:] < hi))
+                assert np.all(np.diff(cols[:k]) > 0) and np.all(np.diff(cols[k:]) > 0)
+                order = np.argsort(cols, kind="stable")
+                np.testing.assert_array_equal(cols[order], R.indices[s:e])
+                np.testing.assert_array_equal(vals[order], R.data[s:e])
+
+
+def _block_worker(rank, world, port, name, eps, limit, tmpdir, q):
+    """One rank: loads ONLY its own block (written by rank 0 with save_block),
+    runs the split-step schedule ("serial" on CPU) over gloo."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch.distributed as dist
+
+    from conftest import load_golden
+    from paper_2603_03150_b200 import engine
+    from paper_2603_03150_b200.lp_types import resolve
+    from paper_2603_03150_b200.sharded import (ShardPlan, ShardedDevice, TorchComm, load_block,
+                                               save_block)
+    from shard_double import NumpyShard
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        path = Path(tmpdir) / f"block_{rank}.npz"
+        if rank == 0:
+            gm = load_golden(name)
+            plan = ShardPlan(gm.A, world)
+            for g in range(world):
+                save_block(Path(tmpdir) / f"block_{g}.npz", plan,
+                           plan.block(g, gm.A, gm.b, gm.c, local_first=True), gm.b, gm.c)
+            del gm, plan
+        dist.barrier()
+        plan, blk, b_full, c_full = load_block(path)
+        assert blk.g == rank and blk.a_nloc is not None
+
+        class P:
+            pass
+
+        p = P()
+        p.b, p.c = b_full, c_full
+        dev = ShardedDevice(plan, [NumpyShard(blk)], TorchComm(plan), overlap="on")
+        assert dev.overlap == "serial"      # CPU doubles: no side stream
+        T = resolve()
+        pt, st = engine.run_on_device(dev, p, T.PdhgParams(eps_rel=eps, max_kkt_passes=limit))
+        q.put((rank, st.status.value, st.iterations, st.restarts, pt.x, pt.y, pt.z))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,eps,limit", [("config0_s0", 1e-4, 200_000),
+                                            ("eq_10x18_s7_ruiz", 1e-12, 200)])
+def test_gloo_two_ranks_from_saved_blocks_split_schedule(name, eps, limit, tmp_path):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_block_worker, args=(r, 2, port, name, eps, limit, str(tmp_path), q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    gm = load_golden(name)
+    opt, ost = oracle.run_pdhg(Model(gm.A, gm.b, gm.c),
+                               oracle.PdhgParams(eps_rel=eps, max_kkt_passes=limit))
+    (_, s0, it0, rs0, x0, y0, z0), (_, s1, it1, rs1, x1, y1, z1) = res
+    assert (s0, it0, rs0) == (s1, it1, rs1)
+    np.testing.assert_array_equal(x0, x1)
+    assert s0 == ost.status.value and it0 == ost.iterations and rs0 == ost.restarts
+    np.testing.assert_allclose(x0, opt.x, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(y0, opt.y, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(z0, opt.z, rtol=1e-9, atol=1e-12)
