@@ -303,6 +303,78 @@ def run_reference(args):
     return 0
 
 
+def _shard_blocks(args, world: int, rank: int, local: int, eng, opts) -> dict:
+    """Rank 0: generate config 4, equilibrate it on its GPU (device Ruiz), cut
+    both into local-first per-rank blocks (sharded.ShardPlan) and write them to
+    /dev/shm; every rank: load only its own two blocks.  Returns the loaded
+    (plan, block, b, c) pairs and rank 0's Ruiz time."""
+    import shutil
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_03150_b200.sharded import ShardPlan, load_block, save_block
+
+    shm = Path("/dev/shm") / f"pdhg_bench_{os.environ.get('MASTER_PORT', '0')}"
+    meta = [None]
+    if rank == 0:
+        shm.mkdir(parents=True, exist_ok=True)
+        inst = _instance(args.scale, args.seed)
+        for tag, model in (("unscaled", inst), ("scaled", None)):
+            if model is None:
+                if not args.ttk:
+                    break
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                model, info = eng.ruiz_equilibrate(inst, gpu=opts, register_layout=False)
+                torch.cuda.synchronize()
+                meta[0] = {"ruiz_s": time.perf_counter() - t0, "ruiz_passes": info.applied_iterations,
+                           "ruiz_phases": dict(eng.ruiz.last_timings)}
+            plan = ShardPlan(model.A, world)
+            for g in range(world):
+                save_block(shm / f"{tag}_{g}.npz", plan,
+                           plan.block(g, model.A, model.b, model.c, local_first=True), model.b, model.c)
+            del plan
+        del inst
+        if torch.cuda.is_available():
+            torch.cuda.empty_cache()
+    dist.broadcast_object_list(meta, src=0)
+    out = {"unscaled": load_block(shm / f"unscaled_{rank}.npz")}
+    if args.ttk:
+        out["scaled"] = load_block(shm / f"scaled_{rank}.npz")
+        out.update(meta[0])
+    dist.barrier()
+    if rank == 0:
+        shutil.rmtree(shm, ignore_errors=True)
+    return out
+
+
+def _host_rss_gb() -> float:
+    import resource
+
+    return resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6   # KB -> GB (Linux)
+
+
+def _allgather_ms(dev, reps: int = 32) -> dict:
+    """Average time of the per-iteration all-gathers of xe and y alone (CUDA
+    events on the shard stream), i.e. the exchange the overlap hides."""
+    import torch
+
+    s = dev.shards[0].stream
+    out = {}
+    for name in ("xe", "y"):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            dev.comm.allgather(dev.shards, name)
+            e0.record(s)
+            for _ in range(reps):
+                dev.comm.allgather(dev.shards, name)
+            e1.record(s)
+        torch.cuda.synchronize()
+        out[name] = e0.elapsed_time(e1) / reps
+    return out
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -315,18 +387,29 @@ def run_ours(args):
     import paper_2603_03150_b200 as eng
     from paper_2603_03150_b200 import _native as N
 
-    inst = _instance(args.scale, args.seed)  # every rank builds the same LP; N>1 shards it
     T = eng.types()
-    m, n, nnz = inst.m, inst.n, inst.nnz
-    ab = algorithmic_bytes(m, n, nnz)
     opts = eng.GpuOptions(cache_layout=False, psr=args.psr)
+    comm_kind = "torch_peer" if args.comm == "peer" else "torch"
+    blocks = None
+    if world > 1:
+        # rank 0 generates the LP (and its device-Ruiz-scaled twin for the run to
+        # 1e-4), cuts it into per-rank blocks and writes them to /dev/shm; every
+        # rank then holds only its own rows (no per-rank copy of the whole model)
+        blocks = _shard_blocks(args, world, rank, local, eng, opts)
+        plan, blk, b_full, c_full = blocks["unscaled"]
+        m, n, nnz = plan.m, plan.n, plan.nnz
+        inst = None
+    else:
+        inst = _instance(args.scale, args.seed)
+        m, n, nnz = inst.m, inst.n, inst.nnz
+    ab = algorithmic_bytes(m, n, nnz)
 
     # ---- device-resident timing: K periods of 64 iterations + check
     t_setup = time.perf_counter()
     if world > 1:
-        from paper_2603_03150_b200.sharded import build_sharded
+        from paper_2603_03150_b200.sharded import build_sharded_from_block
 
-        dev = build_sharded(inst, world, "torch_peer" if args.comm == "peer" else "torch", opts)
+        dev = build_sharded_from_block(plan, blk, comm_kind, opts, overlap=args.overlap)
         kdev = dev.shards[0]   # this rank's shard context (kernel timing)
     else:
         dev = kdev = eng.DeviceLp(inst.A, inst.b, inst.c, opts)
@@ -409,6 +492,16 @@ def run_ours(args):
     else:
         tk = {"primal": kdev.time_kernel(0, reps, step, step), "dual": kdev.time_kernel(1, reps, step, step)}
         tk_isolated = dict(tk)
+    comm_info = None
+    if world > 1:
+        ag = _allgather_ms(dev)
+        comm_info = {"overlap": dev.overlap, "comm": comm_kind,
+                     "allgather_ms_per_iteration": {"xe": ag["xe"], "y": ag["y"], "sum": ag["xe"] + ag["y"]},
+                     "allgather_bytes_received_per_rank": 8 * (plan.n_full + plan.m_full) * (world - 1) // world,
+                     "pass0_entries_fraction": {
+                         "A": float(blk.a_nloc.sum()) / max(1, blk.A.nnz) if blk.a_nloc is not None else None,
+                         "At": float(blk.at_nloc.sum()) / max(1, blk.At.nnz) if blk.at_nloc is not None else None},
+                     "method": "32 all-gathers of each vector alone, CUDA events on the shard stream (rank 0)"}
     top = max(tk, key=tk.get)
     peaks = _peaks()
     peak = peaks["hbm_gbs"] if peaks else 6650.0
@@ -459,10 +552,12 @@ def run_ours(args):
     e0.record()
     t0 = time.perf_counter()
     if world > 1:
-        from paper_2603_03150_b200.sharded import run_pdhg_sharded
+        from paper_2603_03150_b200.sharded import run_pdhg_sharded_block
 
-        pt, st = run_pdhg_sharded(inst, params, G=world, gpu=opts,
-                                  comm_kind="torch_peer" if args.comm == "peer" else "torch")
+        # the public entry from this rank's host block (upload, layout, power
+        # iteration, K*64 iterations, download), every rank at once
+        pt, st = run_pdhg_sharded_block(plan, blk, b_full, c_full, params, gpu=opts,
+                                        comm_kind=comm_kind, overlap=args.overlap)
     else:
         pt, st = eng.run_pdhg(inst, params, gpu=opts)
     e1.record()
@@ -484,29 +579,37 @@ def run_ours(args):
         # (its device layout is handed over, no second upload).  At N > 1 every
         # rank equilibrates the whole model (bit-identical), then the sharded
         # run; times are the max over ranks.
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        scaled, info = eng.ruiz_equilibrate(inst, gpu=opts, register_layout=world == 1)
-        torch.cuda.synchronize()
-        t_ruiz = time.perf_counter() - t0
         ttk_params = T.PdhgParams(eps_rel=1e-4, time_limit_s=args.ttk_limit)
         if world > 1:
-            from paper_2603_03150_b200.sharded import run_pdhg_sharded
+            from paper_2603_03150_b200.sharded import run_pdhg_sharded_block
 
-            pt2, st2 = run_pdhg_sharded(scaled, ttk_params, G=world, gpu=opts,
-                                        comm_kind="torch_peer" if args.comm == "peer" else "torch")
-            tt = torch.tensor([t_ruiz, st2.wall_seconds], dtype=torch.float64, device="cuda")
+            splan, sblk, sb, sc = blocks["scaled"]
+            t_ruiz, passes = blocks["ruiz_s"], blocks["ruiz_passes"]
+            pt2, st2 = run_pdhg_sharded_block(splan, sblk, sb, sc, ttk_params, gpu=opts,
+                                              comm_kind=comm_kind, overlap=args.overlap)
+            tt = torch.tensor([st2.wall_seconds], dtype=torch.float64, device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t_ruiz, wall2 = float(tt[0]), float(tt[1])
+            wall2 = float(tt[0])
+
+            class _I:
+                applied_iterations = passes
+            info = _I()
         else:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            scaled, info = eng.ruiz_equilibrate(inst, gpu=opts, register_layout=True)
+            torch.cuda.synchronize()
+            t_ruiz = time.perf_counter() - t0
             pt2, st2 = eng.run_pdhg(scaled, ttk_params, gpu=opts)
             wall2 = st2.wall_seconds
         out = {"status": st2.status.value, "iterations": st2.iterations, "restarts": st2.restarts,
                "pdhg_wall_s": wall2, "ruiz_s": t_ruiz, "ruiz_passes": info.applied_iterations,
-               "total_s": t_ruiz + wall2, "ruiz_phases_s": dict(eng.ruiz.last_timings),
+               "total_s": t_ruiz + wall2,
+               "ruiz_phases_s": dict(eng.ruiz.last_timings) if world == 1 else blocks.get("ruiz_phases"),
                "reference_iterations": _reference_ttk_iterations(),
                "note": "device Ruiz (bit-identical to transform.py:35-77) + run_pdhg to eps_rel=1e-4"
-                       + (f", sharded over {world} GPUs" if world > 1 else "")}
+                       + (f", sharded over {world} GPUs (Ruiz once on rank 0's GPU, blocks to "
+                          f"/dev/shm)" if world > 1 else "")}
         if args.ttk_unscaled and world == 1:
             pt3, st3 = eng.run_pdhg(inst, T.PdhgParams(eps_rel=1e-4, time_limit_s=args.ttk_limit), gpu=opts)
             out["unscaled"] = {"status": st3.status.value, "iterations": st3.iterations,
@@ -516,7 +619,14 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cs = cpu_sample(inst, steps=args.cpu_steps)
         cpu = _cpu_baseline(cs, m, n, nnz)
+    rss_max = _host_rss_gb()
+    if world > 1:
+        t = torch.tensor([rss_max], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        rss_max = float(t.item())
     if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
         return 0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -538,11 +648,15 @@ def run_ours(args):
                 "allocator": "warm: torch caching allocator holds the timing leg's freed device blocks"},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
-        # per step: 2 step kernels per iteration + the check's k_pair x2,
-        # k_check_primal, k_check_dual(_sell), k_reduce (ncu launch list)
-        "gpu_launches": args.steps * (2 * CHECK_EVERY + 5),
+        # per step: 2 step kernels per iteration (4 with the split steps of the
+        # overlapped multi-GPU schedule) + the check's k_pair x2,
+        # k_check_primal(_sell), k_check_dual(_sell), k_reduce (ncu launch list)
+        "gpu_launches": args.steps * ((4 if comm_info and comm_info["overlap"] != "off" else 2)
+                                      * CHECK_EVERY + 5),
         "setup_s": t_setup,
         "time_to_1e4": out,
+        "multi_gpu": comm_info,
+        "host_rss_gb_max_over_ranks": rss_max,
     }
     print(json.dumps(line))
     if world > 1:
@@ -567,6 +681,9 @@ def main():
     ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
                     help="N>1: all-gather xe/y with NCCL after each half step, or push them "
                          "from the step epilogues to the peers' symmetric memory")
+    ap.add_argument("--overlap", default="auto", choices=["auto", "on", "serial", "off"],
+                    help="N>1 NCCL mode: split half steps with the all-gather overlapping pass 0 "
+                         "(on/auto), the same split kernels in line (serial), or unsplit (off)")
     ap.add_argument("--psr", default="off", choices=["off", "on", "auto"],
                     help="step-kernel layout (off = CSR-vector, the measured fastest)")
     args = ap.parse_args()

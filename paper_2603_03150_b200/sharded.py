@@ -678,8 +678,9 @@ def load_block(path):
 
 
 def build_sharded_from_block(plan: ShardPlan, blk: ShardBlock, comm_kind: str = "torch", opts=None,
-                             group=None, overlap: str = "auto"):
-    """This rank's ShardedDevice from its own block (torch.distributed job)."""
+                             group=None, overlap: str = "auto", shard_factory=None):
+    """This rank's ShardedDevice from its own block (torch.distributed job).
+    ``shard_factory(blk)``: a stand-in shard backend (CPU tests' numpy double)."""
     from .engine import DeviceLp, GpuOptions
 
     opts = opts or GpuOptions()
@@ -693,14 +694,16 @@ def build_sharded_from_block(plan: ShardPlan, blk: ShardBlock, comm_kind: str = 
     if overlap != "off" and blk.a_nloc is None:
         raise ValueError("the overlapped schedule needs a local_first block")
     alloc = comm.symmetric_workspace if comm.fused else None
-    shards = [DeviceLp(blk.A, blk.b, blk.c, opts, shard=blk, ws_alloc=alloc)]
+    shards = [shard_factory(blk) if shard_factory is not None
+              else DeviceLp(blk.A, blk.b, blk.c, opts, shard=blk, ws_alloc=alloc)]
     if comm.fused:
         comm.connect_peers(shards)
     return ShardedDevice(plan, shards, comm, overlap=overlap)
 
 
 def run_pdhg_sharded_block(plan: ShardPlan, blk: ShardBlock, b_full, c_full, params=None, seed: int = 0, *,
-                           comm_kind: str = "torch", gpu=None, group=None, overlap: str = "auto"):
+                           comm_kind: str = "torch", gpu=None, group=None, overlap: str = "auto",
+                           shard_factory=None):
     """run_pdhg (pdhg.py:162-258) from this rank's block; same results contract.
     The host loop reads only b and c of the whole model (its norms)."""
     import threading
@@ -722,6 +725,6 @@ def run_pdhg_sharded_block(plan: ShardPlan, blk: ShardBlock, b_full, c_full, par
 
     p = _Model()
     p.b, p.c = np.asarray(b_full, float), np.asarray(c_full, float)
-    dev = build_sharded_from_block(plan, blk, comm_kind, opts, group, overlap)
+    dev = build_sharded_from_block(plan, blk, comm_kind, opts, group, overlap, shard_factory)
     dev.lock = threading.Lock()
     return engine._run(T, dev, p, params, seed, opts, t0)

@@ -388,3 +388,60 @@ def test_gloo_two_ranks_from_saved_blocks_split_schedule(name, eps, limit, tmp_p
     np.testing.assert_allclose(x0, opt.x, rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(y0, opt.y, rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(z0, opt.z, rtol=1e-9, atol=1e-12)
+
+
+def _bench_blocks_worker(rank, world, port, q):
+    """bench.py's N>1 plumbing on CPU: rank 0 writes the per-rank blocks of a
+    scaled config 4, every rank loads only its own and runs
+    run_pdhg_sharded_block (numpy shard double, split schedule) over gloo."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    import types
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch.distributed as dist
+
+    import bench
+    import paper_2603_03150_b200 as eng
+    from paper_2603_03150_b200.sharded import run_pdhg_sharded_block
+    from shard_double import NumpyShard
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        args = types.SimpleNamespace(scale=0.0005, seed=4, ttk=False)
+        blocks = bench._shard_blocks(args, world, rank, 0, eng, None)
+        plan, blk, b, c = blocks["unscaled"]
+        T = eng.types()
+        pt, st = run_pdhg_sharded_block(plan, blk, b, c, T.PdhgParams(eps_rel=1e-12, max_kkt_passes=128),
+                                        comm_kind="torch", overlap="on", shard_factory=NumpyShard)
+        q.put((rank, blk.g, blk.A.shape[0], st.iterations, pt.x, pt.y, bench._host_rss_gb()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_block_files_two_ranks():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_blocks_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, g0, rows0, it0, x0, y0, rss0), (r1, g1, rows1, it1, x1, y1, rss1) = res
+    assert (g0, g1) == (0, 1) and rows0 > 0 and rows1 > 0
+    assert it0 == it1 == 128
+    np.testing.assert_array_equal(x0, x1)
+    from paper_2603_03150_b200.instances import config4
+
+    inst = config4(scale=0.0005, seed=4)
+    assert rows0 + rows1 == inst.m
+    opt, ost = oracle.run_pdhg(Model(inst.A, inst.b, inst.c),
+                               oracle.PdhgParams(eps_rel=1e-12, max_kkt_passes=128))
+    np.testing.assert_allclose(x0, opt.x, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(y0, opt.y, rtol=1e-9, atol=1e-12)
+    assert rss0 > 0 and rss1 > 0
