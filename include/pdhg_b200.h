@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PDHG_ABI_VERSION 2
+#define PDHG_ABI_VERSION 3
 
 /* Error codes. */
 #define PDHG_OK 0
@@ -92,6 +92,7 @@ typedef struct pdhg_sell {
   const double* val;     /* slots */
   const uint8_t* perm;   /* optional (rows rounded up to 32): lane -> row offset in its
                             slice, rows sorted by length inside each slice (NULL = identity) */
+  int64_t nslots;        /* slots (sptr[nslices]); 0 = unknown (bounds-checked build only) */
 } pdhg_sell;
 
 typedef struct pdhg_problem {
@@ -431,8 +432,13 @@ int pdhg_sell_fill(int32_t rows, const int32_t* ptr, const int32_t* col, const d
 /* Feature bits of the loaded build: 1 = the experiment layouts (PSR panels,
  * persistent period kernels, L2 persisting windows), compiled only with
  * -DPDHG_EXPERIMENTAL=1 (python -m paper_2603_03150_b200.build --experimental);
- * the product build rejects them in pdhg_ctx_create / pdhg_psr_*. */
+ * the product build rejects them in pdhg_ctx_create / pdhg_psr_*.
+ * 2 = bounds-checked build (-DPDHG_BOUNDS_CHECK=1, --checked). */
 int pdhg_features(void);
+/* Bounds-checked build: out-of-bounds index count since the last call (and
+ * the first index with its bound); resets the count.  Product build:
+ * PDHG_ERR_STATE. */
+int pdhg_debug_oob(int64_t* count, int64_t* first_index, int64_t* first_bound);
 
 /* Row relabelling of a CSR matrix on the device (GpuOptions.row_order =
  * "length": the rows of A -- the y-space -- sorted by length inside windows so

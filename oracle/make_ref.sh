@@ -30,6 +30,7 @@ mkdir -p "$OUT.tmp"
 python -m pip install --quiet --no-index --no-deps --no-build-isolation \
   --find-links /opt/wheelhouse --target "$OUT.tmp/site" "$SCRATCH/pkg" >&2
 cp -r "$REF/tests" "$OUT.tmp/tests"
+chmod -R u+w "$OUT.tmp"
 find "$OUT.tmp" -name __pycache__ -prune -exec rm -rf {} +
 rm -rf "$OUT"
 mv "$OUT.tmp" "$OUT"

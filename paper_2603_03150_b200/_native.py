@@ -36,7 +36,7 @@ EXPORTS = (
     "pdhg_lift_bound_duals", "pdhg_max0", "pdhg_violation_tmp_bytes", "pdhg_violation",
     "pdhg_sell_tmp_bytes", "pdhg_sell_plan", "pdhg_sell_fill", "pdhg_sell_sort", "pdhg_set_peers",
     "pdhg_run_period_check", "pdhg_center_toward_target", "pdhg_dot_tmp_bytes", "pdhg_dot",
-    "pdhg_permute_rows", "pdhg_features", "pdhg_half_step_pass",
+    "pdhg_permute_rows", "pdhg_features", "pdhg_half_step_pass", "pdhg_debug_oob",
 )
 
 VEC = {name: i for i, name in enumerate(
@@ -61,7 +61,7 @@ class Sell(C.Structure):
 
     _fields_ = [("rows", C.c_int32), ("nslices", C.c_int32), ("sptr", C.c_void_p),
                 ("width", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p),
-                ("perm", C.c_void_p)]
+                ("perm", C.c_void_p), ("nslots", C.c_int64)]
 
 
 class Problem(C.Structure):
@@ -104,7 +104,7 @@ def _sig(lib, name, restype, *argtypes):
     f.argtypes = list(argtypes)
 
 
-ABI_VERSION = 2   # include/pdhg_b200.h PDHG_ABI_VERSION
+ABI_VERSION = 3   # include/pdhg_b200.h PDHG_ABI_VERSION
 
 
 def load():
@@ -181,6 +181,7 @@ def load():
         _sig(lib, "pdhg_permute_rows", C.c_int, i32, vp, vp, vp, vp, vp, vp, vp, vp)
         _sig(lib, "pdhg_features", C.c_int)
         _sig(lib, "pdhg_half_step_pass", C.c_int, vp, i32, i32, i32)
+        _sig(lib, "pdhg_debug_oob", C.c_int, P(i64), P(i64), P(i64))
         _sig(lib, "pdhg_violation", C.c_int, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
              vp, szt, vp, P(dbl))
         if lib.pdhg_abi_version() != ABI_VERSION:
@@ -190,6 +191,19 @@ def load():
 
 
 FEATURE_EXPERIMENTAL = 1
+FEATURE_BOUNDS_CHECK = 2
+
+
+def bounds_checked() -> bool:
+    return bool(load().pdhg_features() & FEATURE_BOUNDS_CHECK)
+
+
+def debug_oob() -> tuple[int, int, int]:
+    """(count, first index, its bound) of out-of-bounds loads since the last call
+    (bounds-checked build only; resets the count)."""
+    n, i, b = C.c_int64(), C.c_int64(), C.c_int64()
+    check(load().pdhg_debug_oob(C.byref(n), C.byref(i), C.byref(b)))
+    return int(n.value), int(i.value), int(b.value)
 
 
 def experimental() -> bool:

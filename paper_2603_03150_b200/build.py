@@ -23,6 +23,7 @@ SOURCES = [CSRC / "pdhg_b200.cu", CSRC / "ruiz.cu", CSRC / "stdform.cu", CSRC / 
 # the experiment build adds the PSR builders (measured slower)
 EXPERIMENT_SOURCES = [CSRC / "psr_build.cu"]
 EXPERIMENT_LIB = ROOT / "tools" / "_libs" / "libpdhg_b200_exp.so"
+CHECKED_LIB = ROOT / "tools" / "_libs" / "libpdhg_b200_checked.so"
 HEADERS = [ROOT / "include" / "pdhg_b200.h"] + sorted(CSRC.glob("*.cuh"))
 
 NVCC_FLAGS = [
@@ -88,5 +89,8 @@ if __name__ == "__main__":
     if "--experimental" in sys.argv:   # PSR + persistent periods + L2 windows, own .so
         defs = defs + ("PDHG_EXPERIMENTAL=1",)
         outs = outs or [str(EXPERIMENT_LIB)]
+    if "--checked" in sys.argv:        # device-side bounds checks on every gather / stream load
+        defs = defs + ("PDHG_BOUNDS_CHECK=1",)
+        outs = outs or [str(CHECKED_LIB)]
     print(build(force="--force" in sys.argv, verbose=True, defines=defs,
                 out=Path(outs[0]) if outs else None))

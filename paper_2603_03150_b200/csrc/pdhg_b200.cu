@@ -82,6 +82,28 @@ constexpr int kWarps = kBlock / 32;
 #define PDHG_EXPERIMENTAL 0
 #endif
 
+// Bounds-checked build (python -m paper_2603_03150_b200.build --checked;
+// compute-sanitizer is not available on the GPU pool): every gathered-vector
+// index, matrix-stream index and sliced-ELL slot is checked against its bound
+// before the load; a violation is counted (pdhg_debug_oob), the first one kept,
+// and the load is redirected to index 0 so the run continues without a fault.
+#ifndef PDHG_BOUNDS_CHECK
+#define PDHG_BOUNDS_CHECK 0
+#endif
+#if PDHG_BOUNDS_CHECK
+__device__ unsigned long long g_oob_count;
+__device__ long long g_oob_first[2];
+__device__ __noinline__ void oob_hit(long long i, long long n) {
+  if (atomicAdd(&g_oob_count, 1ULL) == 0ULL) {
+    g_oob_first[0] = i;
+    g_oob_first[1] = n;
+  }
+}
+#define CHK(i, n) (((unsigned long long)(long long)(i) < (unsigned long long)(long long)(n)) ? (i) : (oob_hit((i), (n)), 0))
+#else
+#define CHK(i, n) (i)
+#endif
+
 #ifndef PDHG_CHECK_BPS
 #define PDHG_CHECK_BPS 4
 #endif
@@ -299,6 +321,8 @@ struct RowSet {
   int light_max = 0x7fffffff;
   int n_medium = 0;
   const int* __restrict__ medium = nullptr;
+  int ncols = 0x7fffffff;                // gathered-vector length (bounds-checked build)
+  long long nnz = 0x7fffffffffffffffLL;  // entries (bounds-checked build)
 };
 
 // Partial dot of one row over lanes [lane, lane+V, ...]; NR right-hand sides
@@ -331,14 +355,14 @@ __device__ __forceinline__ void row_dot(const RowSet& A, int s, int e, int lane,
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int kk = k + u * V;
-      a[u] = kk < e ? ld_stream(A.val + kk) : 0.0;
-      j[u] = kk < e ? ld_stream(A.col + kk) : -1;
+      a[u] = kk < e ? ld_stream(A.val + CHK(kk, A.nnz)) : 0.0;
+      j[u] = kk < e ? ld_stream(A.col + CHK(kk, A.nnz)) : -1;
     }
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       double xv[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) xv[u] = j[u] >= 0 ? gather_ld<COH>(xin[r] + j[u]) : 0.0;
+      for (int u = 0; u < kU; ++u) xv[u] = j[u] >= 0 ? gather_ld<COH>(xin[r] + CHK(j[u], A.ncols)) : 0.0;
 #pragma unroll
       for (int u = 0; u < kU; ++u)
         if (j[u] >= 0) acc[r] = fma(a[u], xv[u], acc[r]);
@@ -428,8 +452,8 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
 #pragma unroll
   for (int u = 0; u < kU; ++u) {
     const int kk = s + sub + u * V;
-    ac[u] = kk < e ? ld_stream(rs.val + kk) : 0.0;
-    jc[u] = kk < e ? ld_stream(rs.col + kk) : -1;
+    ac[u] = kk < e ? ld_stream(rs.val + CHK(kk, rs.nnz)) : 0.0;
+    jc[u] = kk < e ? ld_stream(rs.col + CHK(kk, rs.nnz)) : -1;
   }
 #if PDHG_RS_PIPE
   double accs[V];
@@ -450,12 +474,12 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int kk = sn + sub + u * V;
-      an[u] = kk < en ? ld_stream(rs.val + kk) : 0.0;
-      jn[u] = kk < en ? ld_stream(rs.col + kk) : -1;
+      an[u] = kk < en ? ld_stream(rs.val + CHK(kk, rs.nnz)) : 0.0;
+      jn[u] = kk < en ? ld_stream(rs.col + CHK(kk, rs.nnz)) : -1;
     }
     double xv[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) xv[u] = jc[u] >= 0 ? gather_ld<COH>(x + jc[u]) : 0.0;
+    for (int u = 0; u < kU; ++u) xv[u] = jc[u] >= 0 ? gather_ld<COH>(x + CHK(jc[u], rs.ncols)) : 0.0;
     double acc = 0.0;
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -466,11 +490,11 @@ __device__ __forceinline__ double warp_rows_dot_pipe(const RowSet& rs, long long
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int kk = k + u * V;
-        a2[u] = kk < e ? ld_stream(rs.val + kk) : 0.0;
-        j2[u] = kk < e ? ld_stream(rs.col + kk) : -1;
+        a2[u] = kk < e ? ld_stream(rs.val + CHK(kk, rs.nnz)) : 0.0;
+        j2[u] = kk < e ? ld_stream(rs.col + CHK(kk, rs.nnz)) : -1;
       }
 #pragma unroll
-      for (int u = 0; u < kU; ++u) x2[u] = j2[u] >= 0 ? gather_ld<COH>(x + j2[u]) : 0.0;
+      for (int u = 0; u < kU; ++u) x2[u] = j2[u] >= 0 ? gather_ld<COH>(x + CHK(j2[u], rs.ncols)) : 0.0;
 #pragma unroll
       for (int u = 0; u < kU; ++u)
         if (j2[u] >= 0) acc = fma(a2[u], x2[u], acc);
@@ -726,6 +750,8 @@ struct SellSet {
   const double* __restrict__ val;
   const unsigned char* __restrict__ perm;  // lane -> row offset in the slice (nullptr = identity)
   bool u_long = false;                     // mean row >= PDHG_SELL_U_MEAN: PDHG_SELL_U_LONG in flight
+  int ncols = 0x7fffffff;                  // gathered-vector length (bounds-checked build)
+  long long nslots = 0x7fffffffffffffffLL; // slots (bounds-checked build)
 };
 
 // Row of lane `lane` of slice sl (natural or slice-sorted layout).
@@ -761,11 +787,11 @@ __device__ __forceinline__ double sell_row_dot(const SellSet& S, long long sl, i
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const bool on = k + u < len;
-      av[u] = on ? ld_stream(S.val + base + 32LL * (k + u)) : 0.0;
-      jv[u] = on ? ld_stream(S.col + base + 32LL * (k + u)) : -1;
+      av[u] = on ? ld_stream(S.val + CHK(base + 32LL * (k + u), S.nslots)) : 0.0;
+      jv[u] = on ? ld_stream(S.col + CHK(base + 32LL * (k + u), S.nslots)) : -1;
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) xv[u] = jv[u] >= 0 ? ld_gather(x + jv[u]) : 0.0;
+    for (int u = 0; u < kU; ++u) xv[u] = jv[u] >= 0 ? ld_gather(x + CHK(jv[u], S.ncols)) : 0.0;
 #pragma unroll
     for (int u = 0; u < kU; ++u)
       if (jv[u] >= 0) acc = fma(av[u], xv[u], acc);
@@ -1150,12 +1176,12 @@ __device__ __forceinline__ void row_dot_pair(const RowSet& A, int s, int e, int 
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int kk = k + u * V;
-      a[u] = kk < e ? ld_stream(A.val + kk) : 0.0;
-      j[u] = kk < e ? ld_stream(A.col + kk) : -1;
+      a[u] = kk < e ? ld_stream(A.val + CHK(kk, A.nnz)) : 0.0;
+      j[u] = kk < e ? ld_stream(A.col + CHK(kk, A.nnz)) : -1;
     }
     double2 xv[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) xv[u] = j[u] >= 0 ? __ldg(xx + j[u]) : make_double2(0.0, 0.0);
+    for (int u = 0; u < kU; ++u) xv[u] = j[u] >= 0 ? __ldg(xx + CHK(j[u], A.ncols)) : make_double2(0.0, 0.0);
 #pragma unroll
     for (int u = 0; u < kU; ++u)
       if (j[u] >= 0) acc[0] = fma(a[u], xv[u].x, acc[0]);
@@ -1189,11 +1215,11 @@ __device__ __forceinline__ void sell_row_dot_pair(const SellSet& S, long long sl
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const bool on = k + u < len;
-      av[u] = on ? ld_stream(S.val + base + 32LL * (k + u)) : 0.0;
-      jv[u] = on ? ld_stream(S.col + base + 32LL * (k + u)) : -1;
+      av[u] = on ? ld_stream(S.val + CHK(base + 32LL * (k + u), S.nslots)) : 0.0;
+      jv[u] = on ? ld_stream(S.col + CHK(base + 32LL * (k + u), S.nslots)) : -1;
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) xv[u] = jv[u] >= 0 ? __ldg(xx + jv[u]) : make_double2(0.0, 0.0);
+    for (int u = 0; u < kU; ++u) xv[u] = jv[u] >= 0 ? __ldg(xx + CHK(jv[u], S.ncols)) : make_double2(0.0, 0.0);
 #pragma unroll
     for (int u = 0; u < kU; ++u)
       if (jv[u] >= 0) {
@@ -2069,6 +2095,10 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->At = RowSet{prob->at_ptr, prob->at_col, prob->at_val, prob->n,
                  prob->at_heavy_threshold > 0 ? prob->at_heavy_threshold : prob->heavy_threshold,
                  prob->at_n_heavy, prob->at_heavy};
+  c->A.ncols = prob->n_full > 0 ? prob->n_full : prob->n;   // gathers xe (x-space)
+  c->A.nnz = prob->nnz;
+  c->At.ncols = prob->m_full > 0 ? prob->m_full : prob->m;  // gathers y (y-space)
+  c->At.nnz = prob->at_nnz > 0 ? prob->at_nnz : prob->nnz;
   for (int k = 0; k < 2; ++k) {  // medium rows (k_step only; not with a PSR layout)
     RowSet& rs = k == 0 ? c->A : c->At;
     const int nmed = k == 0 ? prob->a_n_medium : prob->at_n_medium;
@@ -2143,6 +2173,8 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
                            q->col, q->val, q->perm};
       const long long ops_nnz = k == 0 ? prob->nnz : (prob->at_nnz > 0 ? prob->at_nnz : prob->nnz);
       c->sell[k].u_long = q->rows > 0 && ops_nnz >= (long long)PDHG_SELL_U_MEAN * q->rows;
+      c->sell[k].ncols = k == 0 ? c->A.ncols : c->At.ncols;
+      c->sell[k].nslots = q->nslots > 0 ? q->nslots : 0x7fffffffffffffffLL;
     }
   }
 #if PDHG_EXPERIMENTAL
@@ -2675,7 +2707,7 @@ int pdhg_permute_rows(int32_t rows, const int32_t* perm, const int32_t* ptr, con
 
 // Feature bits of this build: 1 = the experiment layouts (PSR, persistent
 // periods, L2 windows; PDHG_EXPERIMENTAL).
-int pdhg_features(void) { return PDHG_EXPERIMENTAL ? 1 : 0; }
+int pdhg_features(void) { return (PDHG_EXPERIMENTAL ? 1 : 0) | (PDHG_BOUNDS_CHECK ? 2 : 0); }
 
 #if !PDHG_EXPERIMENTAL
 // The PSR builders live in psr_build.cu, compiled into the experiment build
@@ -2691,5 +2723,27 @@ int pdhg_psr_build(int32_t, int32_t, int64_t, const int32_t*, const int32_t*, co
   return fail(PDHG_ERR_ARG, "PSR layouts need the experiment build (PDHG_EXPERIMENTAL)");
 }
 #endif
+
+// Bounds-checked build only (PDHG_BOUNDS_CHECK): out-of-bounds loads seen
+// since the last call (count, first index, its bound); resets the counter.
+// Returns PDHG_ERR_STATE in the product build.
+int pdhg_debug_oob(int64_t* count, int64_t* first_index, int64_t* first_bound) {
+#if PDHG_BOUNDS_CHECK
+  unsigned long long n = 0;
+  long long first[2] = {0, 0};
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpyFromSymbol(&n, g_oob_count, sizeof(n)));
+  CUDA_TRY(cudaMemcpyFromSymbol(first, g_oob_first, sizeof(first)));
+  const unsigned long long zero = 0;
+  CUDA_TRY(cudaMemcpyToSymbol(g_oob_count, &zero, sizeof(zero)));
+  if (count) *count = (int64_t)n;
+  if (first_index) *first_index = first[0];
+  if (first_bound) *first_bound = first[1];
+  return 0;
+#else
+  (void)count; (void)first_index; (void)first_bound;
+  return fail(PDHG_ERR_STATE, "pdhg_debug_oob needs the bounds-checked build (PDHG_BOUNDS_CHECK)");
+#endif
+}
 
 }  // extern "C"

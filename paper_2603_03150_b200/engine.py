@@ -443,6 +443,7 @@ class DeviceLp:
         d.rows, d.nslices = rows, ns
         d.sptr, d.width, d.col, d.val = sp.data_ptr(), width.data_ptr(), scol.data_ptr(), sval.data_ptr()
         d.perm = perm.data_ptr() if perm is not None else None
+        d.nslots = slots.value
         self.stream.synchronize()
         del inv
         self.sell_info[key]["used"] = True

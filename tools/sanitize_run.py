@@ -21,13 +21,29 @@ from conftest import load_golden  # noqa: E402
 from paper_2603_03150_b200.instances import config2, config4  # noqa: E402
 from paper_2603_03150_b200.sharded import run_pdhg_sharded  # noqa: E402
 
+from paper_2603_03150_b200 import _native as N  # noqa: E402
+
 T = eng.types()
 done = []
+CHECKED = N.bounds_checked()     # PDHG_B200_LIB=tools/_libs/libpdhg_b200_checked.so
+oob_total = 0
+
+
+def oob(tag):
+    """Out-of-bounds loads the checked build saw since the last call."""
+    global oob_total
+    if not CHECKED:
+        return None
+    n, i, b = N.debug_oob()
+    oob_total += n
+    if n:
+        print(f"OUT OF BOUNDS after {tag}: {n} loads, first index {i} >= bound {b}", flush=True)
+    return n
 
 
 def run(tag, p, opts=None, **kw):
     pt, st = eng.run_pdhg(p, T.PdhgParams(**kw), gpu=opts or eng.GpuOptions())
-    done.append((tag, st.status.value, st.iterations))
+    done.append((tag, st.status.value, st.iterations, oob(tag)))
 
 
 gm = load_golden("config0_s0")
@@ -50,7 +66,7 @@ dev.spmv(np.ones(c4.m), transpose=True)
 for kind, ov in (("loopback", "off"), ("loopback_fused", "off"), ("loopback", "on"), ("loopback", "serial")):
     pt, st = run_pdhg_sharded(gm, T.PdhgParams(eps_rel=1e-12, max_kkt_passes=130), G=3, comm_kind=kind,
                               overlap=ov)
-    done.append((f"sharded G=3 {kind} overlap={ov}", st.status.value, st.iterations))
+    done.append((f"sharded G=3 {kind} overlap={ov}", st.status.value, st.iterations, oob(kind)))
 scaled, info = eng.ruiz_equilibrate(c4)
 run("config4 0.2% after device Ruiz", scaled, eps_rel=1e-12, max_kkt_passes=64)
 from paper_2603_03150_b200.instances import config1_general  # noqa: E402
@@ -59,7 +75,7 @@ g = config1_general(scale=0.002)
 p, fmap = eng.to_standard_form(g)
 s2, info2 = eng.ruiz_equilibrate(p)
 pt, st = eng.run_pdhg(s2, T.PdhgParams(eps_rel=1e-12, max_kkt_passes=64))
-done.append(("config1 0.2% stdform+ruiz", st.status.value, st.iterations))
+done.append(("config1 0.2% stdform+ruiz", st.status.value, st.iterations, oob("config1")))
 from paper_2603_03150_b200 import finish  # noqa: E402
 
 up = finish.unscale_point(info2, pt)
@@ -67,6 +83,11 @@ gp = finish.restrict_point(g, fmap, up)
 vs = finish.violation_summary(p, up)
 cs = finish.centered_start(up)
 done.append(("finishing: unscale, restrict, violation, centered_start", float(vs.max_violation), len(gp[0])))
+dev.spmv(np.ones(c4.n))
+oob("spmv")
 for d in done:
     print(d)
-print(f"sanitize workload ok: {len(done)} runs")
+print(f"sanitize workload ok: {len(done)} runs; bounds-checked build: {CHECKED}; "
+      f"out-of-bounds loads: {oob_total if CHECKED else 'n/a'}")
+if CHECKED and oob_total:
+    sys.exit(9)
