@@ -186,6 +186,7 @@ class LoopbackComm:
             others = [o for h, o in enumerate(shards) if h != g]
             if others:
                 s.connect_fail(others)
+        self.fail_connected = True
 
     def barrier(self, shards):
         pass   # one stream: stream order is the barrier
@@ -393,7 +394,51 @@ class ShardedDevice:
         for s in self.shards:
             s.reset()
 
+    def _shared_fail(self) -> bool:
+        """Do the shards see each other's fail words during a period?  (fused
+        peer stores carry them over NVLink; loopback shards after connect_fail)"""
+        return bool(getattr(self.comm, "fused", False) or getattr(self.comm, "fail_connected", False)
+                    or self.plan.G == 1)
+
+    def _snapshot(self):
+        """Each shard's own slices of the iterate vectors at the period start."""
+        snap = []
+        with self._on_stream():
+            for s in self.shards:
+                xs, ys = slice(s.x_off, s.x_off + s.n), slice(s.y_off, s.y_off + s.m)
+                snap.append({nm: s.vec(nm)[xs if nm in X_SPACE else ys].clone()
+                             for nm in ("x", "xe", "xbar", "y", "ybar")})
+        return snap
+
+    def _restore(self, snap):
+        with self._on_stream():
+            for s, d in zip(self.shards, snap):
+                xs, ys = slice(s.x_off, s.x_off + s.n), slice(s.y_off, s.y_off + s.m)
+                for nm, t in d.items():
+                    s.vec(nm)[xs if nm in X_SPACE else ys].copy_(t)
+        self._ag("y")           # the full y every shard gathers in the first primal step
+
     def run_period(self, iters: int, iter0: int, tau_w: float, sigma_w: float, w0: float) -> int:
+        # Without shared fail words (the NCCL all-gather mode) a shard does not
+        # see another's non-finite iterate until the period ends, and keeps
+        # stepping.  Then the period is replayed from a snapshot of its start up
+        # to the failing iteration exactly, so every shard stops there as on one
+        # GPU (pdhg.py:194-196) -- deterministic kernels make the replay the
+        # same arithmetic.  The snapshot is five slice copies per period.
+        snap = self._snapshot() if iters > 0 and not self._shared_fail() else None
+        fail = self._run_period(iters, iter0, tau_w, sigma_w, w0)
+        if snap is not None and fail >= 0:
+            self._restore(snap)
+            for s in self.shards:
+                s.set_step(iter0, tau_w, sigma_w, w0)
+            self._period_body(fail - iter0)
+            with self._on_stream():
+                fails = self.comm.allgather_int([s.fail_iter() for s in self.shards])
+            bad = [f for f in fails if f >= 0]
+            fail = min(bad) if bad else fail
+        return fail
+
+    def _run_period(self, iters: int, iter0: int, tau_w: float, sigma_w: float, w0: float) -> int:
         for s in self.shards:
             s.set_step(iter0, tau_w, sigma_w, w0)
         if self.graph and iters > 0 and iters in self._seen:

@@ -309,3 +309,38 @@ def test_overlap_config4_instance_matches_single_gpu(eng):
     plan = ShardPlan(p.A, 4)
     blk = plan.block(1, p.A, p.b, p.c, local_first=True)
     assert blk.a_nloc.sum() > 0.6 * blk.A.nnz and blk.at_nloc.sum() > 0.6 * blk.At.nnz
+
+
+@pytest.mark.parametrize("G", [2, 3])
+@pytest.mark.parametrize("overlap", ["off", "on"])
+def test_failure_replay_without_shared_fail_words(eng, G, overlap):
+    """CUDA shards whose fail words are NOT connected (the NCCL all-gather
+    mode's situation): the period with the non-finite iterate is replayed from
+    its start up to iteration 335, so every shard stops there and the running
+    averages equal the shared-fail-word run's bit for bit."""
+    from test_sharded_cpu import failing_block_model
+
+    from paper_2603_03150_b200.engine import DeviceLp, run_on_device
+    from paper_2603_03150_b200.sharded import LoopbackComm, ShardedDevice, ShardPlan, build_sharded
+
+    import torch
+
+    p = failing_block_model()
+    T = eng.types()
+    params = T.PdhgParams(eps_rel=1e-6, max_kkt_passes=500)
+    ref = build_sharded(p, G, comm_kind="loopback", overlap="serial" if overlap == "on" else "off")
+    pr, sr = run_on_device(ref, p, params)
+    plan = ShardPlan(p.A, G)
+    stream = torch.cuda.Stream()
+    split = overlap == "on"
+    shards = [DeviceLp(b.A, b.b, b.c, eng.GpuOptions(), shard=b, stream=stream)
+              for b in (plan.block(g, p.A, p.b, p.c, local_first=split) for g in range(G))]
+    dev = ShardedDevice(plan, shards, LoopbackComm(plan), overlap=overlap)   # no connect_fail
+    assert not dev._shared_fail()
+    pt, st = run_on_device(dev, p, params)
+    assert st.status.value == sr.status.value == "NumericalFailure"
+    assert st.iterations == sr.iterations == 335
+    assert pt.x.tobytes() == pr.x.tobytes() and pt.y.tobytes() == pr.y.tobytes()
+    for a, b in zip(dev.shards, ref.shards):
+        for nm in ("xbar", "ybar"):
+            assert a.vec(nm).cpu().numpy().tobytes() == b.vec(nm).cpu().numpy().tobytes(), nm

@@ -445,3 +445,73 @@ def test_bench_block_files_two_ranks():
     np.testing.assert_allclose(x0, opt.x, rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(y0, opt.y, rtol=1e-9, atol=1e-12)
     assert rss0 > 0 and rss1 > 0
+
+
+def _fail_worker(rank, world, port, overlap, q):
+    """gloo world: the NCCL-style all-gather mode, whose ranks do not share fail
+    words -- a non-finite iterate on one rank must still stop every rank at
+    the reference's iteration with the reference's failure-exit point."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch.distributed as dist
+
+    from paper_2603_03150_b200 import engine
+    from paper_2603_03150_b200.lp_types import resolve
+    from paper_2603_03150_b200.sharded import ShardPlan, ShardedDevice, TorchComm
+    from shard_double import NumpyShard
+    from test_sharded_cpu import failing_block_model
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = failing_block_model()
+        plan = ShardPlan(p.A, world)
+        sh = NumpyShard(plan.block(rank, p.A, p.b, p.c, local_first=overlap != "off"))
+        dev = ShardedDevice(plan, [sh], TorchComm(plan), overlap=overlap)
+        T = resolve()
+        pt, st = engine.run_on_device(dev, p, T.PdhgParams(eps_rel=1e-6, max_kkt_passes=500))
+        q.put((rank, st.status.value, st.iterations, pt.x, pt.y, pt.z, sh.fail,
+               float(sh.v["xbar"].sum()), float(sh.v["ybar"].sum())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("overlap", ["off", "on"])
+def test_gloo_failure_stops_every_rank(overlap):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fail_worker, args=(r, 2, port, overlap, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    p = failing_block_model()
+    opt, ost = oracle.run_pdhg(p, oracle.PdhgParams(eps_rel=1e-6, max_kkt_passes=500))
+    assert ost.status.value == "NumericalFailure" and ost.iterations == 335
+    for rank, status, its, x, y, z, fail, xbs, ybs in res:
+        assert status == ost.status.value and its == ost.iterations
+        np.testing.assert_allclose(x, opt.x, rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(y, opt.y, rtol=1e-9, atol=1e-12)
+    # the rank that did not fail stopped at the failing iteration too: its running
+    # averages are the single-process ones (checked against a loopback run with
+    # shared fail words)
+    from shard_double import NumpyShard
+
+    from paper_2603_03150_b200 import engine
+    from paper_2603_03150_b200.lp_types import resolve
+
+    plan = ShardPlan(p.A, 2)
+    shards = [NumpyShard(plan.block(g, p.A, p.b, p.c)) for g in range(2)]
+    comm = LoopbackComm(plan)
+    comm.connect_fail(shards)
+    engine.run_on_device(ShardedDevice(plan, shards, comm), p,
+                         resolve().PdhgParams(eps_rel=1e-6, max_kkt_passes=500))
+    for (rank, *_, xbs, ybs), sh in zip(res, shards):
+        assert xbs == pytest.approx(float(sh.v["xbar"].sum()), rel=1e-12, abs=1e-300, nan_ok=True)
+        assert ybs == pytest.approx(float(sh.v["ybar"].sum()), rel=1e-12, abs=1e-300, nan_ok=True)
