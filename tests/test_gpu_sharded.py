@@ -10,9 +10,9 @@ import pytest
 
 import oracle
 from conftest import EXPERIMENTAL_BUILD, load_golden, skip_unless_experimental
+from oracle.pdhg_port import KktPoint, Model
 
 PSR_PARAMS = ["off", "on"] if EXPERIMENTAL_BUILD else ["off"]
-from oracle.pdhg_port import KktPoint, Model
 
 pytestmark = pytest.mark.gpu
 
