@@ -619,6 +619,12 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cs = cpu_sample(inst, steps=args.cpu_steps)
         cpu = _cpu_baseline(cs, m, n, nnz)
+        if "time_to_1e4_s" not in cpu and out is not None and out.get("status") == "Optimal":
+            its = int(out["iterations"])
+            cpu["time_to_1e4_s"] = {"value": its * cs["per_iter_s"], "iterations": its,
+                                    "note": "extrapolated: this run's GPU iteration count to 1e-4 x the "
+                                            "reference's sampled seconds per iteration (the reference's "
+                                            "own count, once tests/golden/run_config4_s1.json exists)"}
     rss_max = _host_rss_gb()
     if world > 1:
         t = torch.tensor([rss_max], dtype=torch.float64, device="cuda")
