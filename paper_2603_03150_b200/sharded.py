@@ -253,7 +253,10 @@ class TorchComm:
 
     def barrier(self, shards):
         """Stream-ordered cross-GPU barrier: the next half step starts after every
-        rank's epilogue stores (symmetric-memory signal pads, release/acquire)."""
+        rank's epilogue stores.  torch's symmetric-memory barrier is a kernel on
+        the current stream: each rank sets its slot in every peer's signal pad
+        and waits for every peer's slot in its own (release / acquire, the
+        waiter resets the slot), so it is captured into the period graph."""
         self.symm.barrier(channel=0)
 
     def allgather(self, shards, name: str):
@@ -327,11 +330,12 @@ class ShardedDevice:
             self.overlap = "serial"   # fused stores / CPU doubles: no side stream to overlap on
         self._comm_stream = None
         self.m, self.n = plan.m, plan.n
-        # a period (kernels + all-gathers) is captured once per length and
-        # replayed, like the single-GPU engine's graphs; the symmetric-memory
-        # barrier of the torch_peer path stays eager
-        self.graph = (graph and all(getattr(sh, "stream", None) is not None for sh in self.shards)
-                      and not (isinstance(comm, TorchComm) and comm.fused))
+        # a period (kernels + all-gathers or peer stores + barriers) is captured
+        # once per length and replayed, like the single-GPU engine's graphs
+        # the fused peer-store mode is captured too: its barrier is a device-side
+        # kernel on the stream (symmetric-memory signal pads, each slot set by
+        # the peer and reset by its waiter -- replay-safe), not a host wait
+        self.graph = graph and all(getattr(sh, "stream", None) is not None for sh in self.shards)
         self._graphs = {}
         self._seen = set()
 

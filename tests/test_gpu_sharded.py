@@ -171,6 +171,14 @@ def test_torch_peer_world1(eng):
         r = gm.run("e4")
         assert st.status.value == "Optimal"
         assert st.iterations == int(r["iterations"]) and st.restarts == int(r["restarts"])
+        # the fused path's periods (peer stores + device-side barriers) replay as graphs
+        from paper_2603_03150_b200.engine import run_on_device
+        from paper_2603_03150_b200.sharded import build_sharded
+
+        dev = build_sharded(gm, 1, comm_kind="torch_peer")
+        pt2, st2 = run_on_device(dev, gm, T.PdhgParams(eps_rel=1e-4))
+        assert dev.graph and dev._graphs, "torch_peer periods were not captured"
+        assert st2.iterations == st.iterations and pt2.x.tobytes() == pt.x.tobytes()
     finally:
         dist.destroy_process_group()
 
