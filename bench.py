@@ -381,9 +381,13 @@ def run_ours(args):
     import torch.distributed as dist
 
     rank, world, local = _env_rank()
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
+    if world > 1:
+        import datetime
+
+        # rank 0 generates and cuts the 200M-entry model while the others wait
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(minutes=30))
     import paper_2603_03150_b200 as eng
     from paper_2603_03150_b200 import _native as N
 

@@ -78,7 +78,9 @@ class GpuOptions:
                      order, ~1.03x renumbered).  y is mapped back on every
                      download, so results are the same LP's.  auto: unsharded operators
                      with >= sell_min_nnz entries whose natural-order padding exceeds
-                     sell_max_pad.
+                     sell_max_pad and at most row_order_max_tail of whose entries sit
+                     in rows longer than 4x the mean (lane-per-row slices run a long
+                     row on one lane: config 2's power-law rows stay on CSR-vector).
     sell_sort:       "auto" | "on" | "off" -- order each slice's rows by length (lanes
                      active in a round form a prefix, so fetched sectors are full):
                      config 4's A' reads 3.55 instead of 3.85 GB per primal step (period
@@ -119,6 +121,7 @@ class GpuOptions:
     sell_sort: str = "auto"
     row_order: str = "auto"
     row_order_window: int = 65536
+    row_order_max_tail: float = 0.15
 
 
 def auto_lanes(nnz: int, rows: int) -> int:
@@ -183,6 +186,15 @@ def _want_row_order(torch, opts, ptr, nnz: int, H: int) -> bool:
     if opts.row_order != "auto" or opts.sell == "off" or opts.psr != "off" or nnz < opts.sell_min_nnz:
         return False
     if opts.persistent not in ("off", "auto") or int(opts.dual_split) > 1:
+        return False
+    # heavy-tailed operators stay on CSR-vector: lane-per-row sliced ELL runs a
+    # long row on one lane (config 2's power-law A, 52 % of its entries in rows
+    # over 4x the mean: 10.1 -> 15.3 s to 1e-4 renumbered); config 4's
+    # lognormal A has 9 % there
+    lens = (ptr[1:] - ptr[:-1]).to(torch.int64)
+    mean = float(nnz) / max(1, lens.numel())
+    tail = float(lens[lens > 4 * mean].sum()) / max(1, nnz)
+    if tail > opts.row_order_max_tail:
         return False
     return _slice_pad(torch, ptr, H) > opts.sell_max_pad
 
