@@ -315,7 +315,11 @@ def _shard_blocks(args, world: int, rank: int, local: int, eng, opts) -> dict:
 
     from paper_2603_03150_b200.sharded import ShardPlan, load_block, save_block
 
-    shm = Path("/dev/shm") / f"pdhg_bench_{os.environ.get('MASTER_PORT', '0')}"
+    need = 2 * 30e9 * max(args.scale, 0.01)          # both models' blocks (~24 B/entry + vectors)
+    root = Path("/dev/shm")
+    if not root.is_dir() or shutil.disk_usage(root).free < need:
+        root = Path(os.environ.get("TMPDIR", "/tmp"))
+    shm = root / f"pdhg_bench_{os.environ.get('MASTER_PORT', '0')}"
     meta = [None]
     if rank == 0:
         shm.mkdir(parents=True, exist_ok=True)
