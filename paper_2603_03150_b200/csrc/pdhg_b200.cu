@@ -808,8 +808,21 @@ __device__ __forceinline__ double sell_row_dot(const SellSet& S, long long sl, i
 #ifndef PDHG_SELL_LATE
 #define PDHG_SELL_LATE 1
 #endif
+// The dual step over long rows (config 4's renumbered A, ~40 entries per row
+// with a long tail) keeps PDHG_SELL_U_DUAL entries in flight per lane at 6
+// blocks per SM (40 registers): its gathers of the 80 MB xe miss L2 more
+// often than the primal step's of the 40 MB y, so it wants more memory-level
+// parallelism per warp -- dual 0.55 -> 0.51 ms, iteration -2 % on config 4 at
+// 50 % scale with the primal step unchanged (tools/lib_ab.py,
+// profiles/r02_sell_unroll.log).
+#ifndef PDHG_SELL_U_DUAL
+#define PDHG_SELL_U_DUAL 10
+#endif
 template <bool PRIMAL, int kU>
-__global__ void __launch_bounds__(kBlock, PDHG_SELL_MINB) k_step_sell(StepArgs a, SellSet S, int j_in_period) {
+constexpr int sell_min_blocks() { return (!PRIMAL && kU > PDHG_SELL_U_LONG) ? 6 : PDHG_SELL_MINB; }
+
+template <bool PRIMAL, int kU>
+__global__ void __launch_bounds__(kBlock, (sell_min_blocks<PRIMAL, kU>())) k_step_sell(StepArgs a, SellSet S, int j_in_period) {
   __shared__ double red[kWarps];
   pdl_enter();
   StepParams* P = a.P;
@@ -1992,7 +2005,7 @@ int launch_step_pass(pdhg_ctx* c, bool primal, int j, int pass) {
     const int grid = a.rs.n_heavy + (int)(((long long)S.nslices * 32 + kBlock - 1) / kBlock);
     if (S.u_long)
       return primal ? launch_ex(c, k_step_sell<true, PDHG_SELL_U_LONG>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j)
-                    : launch_ex(c, k_step_sell<false, PDHG_SELL_U_LONG>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
+                    : launch_ex(c, k_step_sell<false, PDHG_SELL_U_DUAL>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
     return primal ? launch_ex(c, k_step_sell<true, PDHG_SELL_U>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j)
                   : launch_ex(c, k_step_sell<false, PDHG_SELL_U>, dim3(grid), dim3(kBlock), 0, win_base, win, a, S, j);
   }
