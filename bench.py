@@ -550,7 +550,7 @@ def run_ours(args):
 
     layout_name = {"A (dual step)": _op_layout("A", kdev.a_lanes),
                    "A' (primal step)": _op_layout("At", kdev.at_lanes)}
-    del dev, kdev
+    del dev, kdev, period    # (the bound method would keep the timing leg's layout alive)
 
     # ---- e2e through the public drop-in call, host arrays in, host arrays out
     K = args.steps
