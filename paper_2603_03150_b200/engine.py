@@ -415,8 +415,7 @@ class DeviceLp:
         self.stream.synchronize()
         self.a_ptr, self.a_col, self.a_val = new_ptr, new_col, new_val
         self.row_perm, self.row_inv = perm, inv
-        self._row_perm_host = perm.cpu().numpy()
-        self._row_inv_host = inv.cpu().numpy()
+        self._row_perm_host = None      # host copy made on first use (spmv gates only)
 
     def _build_sell(self, torch, dev, key, rows, nnz, ptr, col, val, H, opts):
         """Plan + fill the sliced-ELL layout of one operator on the device (or None)."""
@@ -572,6 +571,8 @@ class DeviceLp:
         torch = _torch()
         v = np.ascontiguousarray(v, dtype=np.float64)
         if transpose and self.row_perm is not None:
+            if self._row_perm_host is None:
+                self._row_perm_host = self.row_perm.cpu().numpy()
             v = np.ascontiguousarray(v[self._row_perm_host])
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             vin = torch.from_numpy(v).to(self.device)
