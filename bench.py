@@ -430,9 +430,13 @@ def run_ours(args):
     step = 1.0 / (1.05 * lam)
     dev.reset()
     it = 0
+    # engine._run hands each two-point check's A'y of the current point to the
+    # next period's first primal step when nothing restarts (check_dot)
+    reuse = (lambda: dev.use_check_dot(0)) if getattr(dev, "check_dot", False) else (lambda: None)
     for _ in range(args.warmup):
         dev.run_period(CHECK_EVERY, it, step, step, float(it))
         dev.check(N.PT_CUR, N.PT_AVG)
+        reuse()
         it += CHECK_EVERY
     s = kdev.stream
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -450,6 +454,7 @@ def run_ours(args):
             else:
                 fail = dev.run_period(CHECK_EVERY, it, step, step, float(it))
                 dev.check(N.PT_CUR, N.PT_AVG)
+            reuse()
             it += CHECK_EVERY
         ev1.record(s)
         torch.cuda.synchronize()
@@ -465,6 +470,7 @@ def run_ours(args):
             e[1].record(s)
             dev.check(N.PT_CUR, N.PT_AVG)
             e[2].record(s)
+            reuse()
             it += CHECK_EVERY
         torch.cuda.synchronize()
         g_ms = [e[0].elapsed_time(e[1]) for e in evs]
@@ -555,28 +561,36 @@ def run_ours(args):
     # ---- e2e through the public drop-in call, host arrays in, host arrays out
     K = args.steps
     params = T.PdhgParams(eps_rel=1e-12, max_kkt_passes=K * CHECK_EVERY)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    t0 = time.perf_counter()
-    if world > 1:
-        from paper_2603_03150_b200.sharded import run_pdhg_sharded_block
+    # each call is a whole solve from host arrays (fresh layout, cache_layout
+    # off); --e2e-reps calls, the median is reported (the first pays whatever
+    # device allocations the caching allocator cannot serve from its pool)
+    e2e_runs = []
+    for _ in range(max(1, args.e2e_reps)):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        t0 = time.perf_counter()
+        if world > 1:
+            from paper_2603_03150_b200.sharded import run_pdhg_sharded_block
 
-        # the public entry from this rank's host block (upload, layout, power
-        # iteration, K*64 iterations, download), every rank at once
-        pt, st = run_pdhg_sharded_block(plan, blk, b_full, c_full, params, gpu=opts,
-                                        comm_kind=comm_kind, overlap=args.overlap)
-    else:
-        pt, st = eng.run_pdhg(inst, params, gpu=opts)
-    e1.record()
-    torch.cuda.synchronize()
-    wall_e2e = time.perf_counter() - t0
-    e2e_ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = st.iterations / (e2e_ms / 1e3)
+            # the public entry from this rank's host block (upload, layout, power
+            # iteration, K*64 iterations, download), every rank at once
+            pt, st = run_pdhg_sharded_block(plan, blk, b_full, c_full, params, gpu=opts,
+                                            comm_kind=comm_kind, overlap=args.overlap)
+        else:
+            pt, st = eng.run_pdhg(inst, params, gpu=opts)
+        e1.record()
+        torch.cuda.synchronize()
+        wall_e2e = time.perf_counter() - t0
+        e2e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([e2e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e_runs.append((st.iterations / (e2e_ms / 1e3), wall_e2e, st))
+        del pt
+    e2e_runs_sorted = sorted(e2e_runs, key=lambda r: r[0])
+    e2e_value, wall_e2e, st = e2e_runs_sorted[len(e2e_runs_sorted) // 2]
     h2d = 12 * nnz + 4 * (m + 1) + 8 * (m + n) + 8 * n
     d2h = 8 * (2 * n + m)
 
@@ -658,7 +672,9 @@ def run_ours(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / K,
                 "d2h_bytes_per_step": d2h / K, "iterations": st.iterations,
                 "wall_s": wall_e2e, "timings": getattr(st, "timings", None),
-                "note": "run_pdhg(StandardLp on host) incl. upload, transpose, opnorm",
+                "runs_iter_s": [round(r[0], 2) for r in e2e_runs],
+                "note": f"run_pdhg(StandardLp on host) incl. upload, transpose, opnorm; median of "
+                        f"{len(e2e_runs)} calls",
                 "allocator": "warm: torch caching allocator holds the timing leg's freed device blocks"},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
@@ -687,6 +703,7 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--seed", type=int, default=4)
     ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--e2e-reps", type=int, default=3, help="public-API calls for e2e (median reported)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ttk", action=argparse.BooleanOptionalAction, default=True,
                     help="also run to eps_rel=1e-4 (time-to-1e-4, part of the metric; --no-ttk skips)")

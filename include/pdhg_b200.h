@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PDHG_ABI_VERSION 3
+#define PDHG_ABI_VERSION 4
 
 /* Error codes. */
 #define PDHG_OK 0
@@ -211,6 +211,22 @@ int pdhg_check(pdhg_ctx* ctx, int32_t npts, const int32_t* specs, double* out_ho
  * (pdhg_vector(ctx, PDHG_VEC_SCALARS)) without synchronising -- sharded
  * hosts all-gather them and combine per-shard partials in rank order. */
 int pdhg_check_device(pdhg_ctx* ctx, int32_t npts, const int32_t* specs);
+
+/* Check -> next step reuse.  With check_dot enabled (needs the sliced-ELL
+ * layout of A' and one GPU, else PDHG_ERR_STATE), a two-point check also
+ * leaves A'y of both checked points in the workspace.  The iterate the next
+ * period starts from has one of those y's: the current point's when the
+ * check does not restart or restarts to it, the average's after a restart to
+ * the average (pdhg.py:234-240).  pdhg_use_check_dot(slot) (0 = first checked
+ * point, 1 = second) makes the next period's first primal step
+ * (pdhg.py:142-147) take that A'y instead of recomputing it -- the check's
+ * dual side runs the primal step's own row loop, so the step's result is
+ * bit for bit the same.  Valid only right after such a check (restart and
+ * save_best in between are fine); any other call that moves the iterates
+ * drops the dots.  Replaces the repeated `p.at_y(state.y)` of the first
+ * pdhg_step after _score (pdhg.py:142, 201-204). */
+int pdhg_check_dot_enable(pdhg_ctx* ctx, int32_t on);
+int pdhg_use_check_dot(pdhg_ctx* ctx, int32_t slot);
 
 /* Restart at point `which` (CUR or AVG): x, y, avg_x, avg_y <- that point
  * (pdhg.py:235-238). */

@@ -8,6 +8,11 @@ under tests/golden/, so the GPU tests can compare iteration counts and
 objectives at full size without the reference:
 
     PYTHONDONTWRITEBYTECODE=1 OPENBLAS_NUM_THREADS=1 python oracle/make_golden_runs.py config1
+    ... python oracle/make_golden_runs.py config4 1.0 nolimit
+
+The third argument ``nolimit`` passes ``time_limit_s=1e9`` (the reference's
+default of 10,000 s, pdhg.py:36, stops config 2 at ~48k and config 4 at ~7k
+iterations on one core) and writes ``run_<config>_s<scale>_nolimit.json``.
 """
 
 from __future__ import annotations
@@ -28,7 +33,7 @@ import hybridlp  # noqa: E402
 from paper_2603_03150_b200.instances import config1_general, config3_general  # noqa: E402
 
 
-def main(which: str, scale: float = 1.0):
+def main(which: str, scale: float = 1.0, nolimit: bool = False):
     t0 = time.perf_counter()
     if which in ("config2", "config4"):   # built directly in standard form
         from paper_2603_03150_b200 import instances
@@ -52,7 +57,8 @@ def main(which: str, scale: float = 1.0):
         return orig_score(pp, x, y)
 
     hybridlp.pdhg._score = score
-    pt, st = hybridlp.run_pdhg(s, hybridlp.PdhgParams(eps_rel=1e-4))
+    params = hybridlp.PdhgParams(eps_rel=1e-4, time_limit_s=1e9) if nolimit else hybridlp.PdhgParams(eps_rel=1e-4)
+    pt, st = hybridlp.run_pdhg(s, params)
     t3 = time.perf_counter()
     term = st.termination
     out = {
@@ -64,11 +70,13 @@ def main(which: str, scale: float = 1.0):
         "ruiz_passes": info.applied_iterations,
         "seconds": {"to_standard_form": t1 - t0, "ruiz": t2 - t1, "run_pdhg": t3 - t2},
         "numpy": np.__version__, "threads": "OPENBLAS_NUM_THREADS=1",
+        "time_limit_s": params.time_limit_s,
     }
-    path = ROOT / "tests" / "golden" / f"run_{which}_s{scale:g}.json"
+    path = ROOT / "tests" / "golden" / f"run_{which}_s{scale:g}{'_nolimit' if nolimit else ''}.json"
     path.write_text(json.dumps(out, indent=1))
     print(json.dumps(out))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 1.0)
+    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 1.0,
+         len(sys.argv) > 3 and sys.argv[3] == "nolimit")

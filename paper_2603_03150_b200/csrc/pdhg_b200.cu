@@ -874,6 +874,28 @@ __global__ void __launch_bounds__(kBlock, (sell_min_blocks<PRIMAL, kU>())) k_ste
   }
 }
 
+// The first primal step of a period right after a two-point check that left
+// A'y of both checked points in the workspace (pdhg_use_check_dot): the
+// next iterate's y is one of them (the current point, or the average after a
+// restart to it), and k_check_dual_sell computed its row dots with exactly
+// the primal step's fma sequence (sell_row_dot / row_dot + block_sum, same
+// entry order), so this epilogue-only pass gives the step's result bit for
+// bit without its SpMV (config 4: one of 64 primal SpMVs per period).
+__global__ void __launch_bounds__(kBlock) k_primal_from_dot(StepArgs a, const double2* __restrict__ dots,
+                                                            int slot, int j_in_period) {
+  pdl_enter();
+  StepParams* P = a.P;
+  const long long iter = P->iter0 + j_in_period + 1;
+  if (P->fail_iter < iter) return;
+  const double w = P->w0 + (double)(j_in_period + 1);
+  const long long i = (long long)blockIdx.x * kBlock + threadIdx.x;
+  if (i >= a.rs.rows) return;
+  const double2 d = dots[i];
+  const int row = (int)i;
+  bcast(P, 0, row, primal_epi_pre(row, slot ? d.y : d.x, a.cb[i], a.x[i], a.xbar[i], a.x, a.xe, a.xbar, P->tau_w,
+                                  w, iter, P));
+}
+
 #if PDHG_EXPERIMENTAL  // persistent period kernels
 // ------------------------------------------------- persistent period kernel
 //
@@ -1172,6 +1194,8 @@ struct CheckPts {
   const double2* pair;   // two-point checks: the gathered vectors interleaved
                          // ((x0[j], x1[j]) or (y0[i], y1[i])), one 16-byte gather
                          // per entry instead of two 8-byte ones
+  double2* dout;         // dual side, optional: each row's two dots (A'y0, A'y1)
+                         // -- the next period's first primal step (pdhg_use_check_dot)
 };
 
 // row_dot for two right-hand sides stored interleaved: each accumulator sees
@@ -1525,7 +1549,10 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual_sell(RowS
     row_dot_pair<kBlock>(rs, rs.ptr[row], rs.ptr[row + 1], threadIdx.x, pts.pair, acc);
 #pragma unroll
     for (int p = 0; p < 2; ++p) d[p] = block_sum(acc[p], red);
-    if (threadIdx.x == 0) row_terms(row, d);
+    if (threadIdx.x == 0) {
+      row_terms(row, d);
+      if (pts.dout) pts.dout[row] = make_double2(d[0], d[1]);
+    }
   }
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * kWarps;
@@ -1536,7 +1563,10 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_dual_sell(RowS
     if (!ok) len = 0;
     double d[2];
     sell_row_dot_pair<kU>(S, sl, lane, len, pts.pair, d[0], d[1]);
-    if (ok) row_terms((int)rl, d);
+    if (ok) {
+      row_terms((int)rl, d);
+      if (pts.dout) pts.dout[rl] = make_double2(d[0], d[1]);
+    }
   }
 #pragma unroll
   for (int p = 0; p < 2; ++p) {
@@ -1802,6 +1832,12 @@ struct pdhg_ctx {
   bool period_direct;  // periods launched kernel by kernel instead of as a graph
   double* const* peers[2];  // fused all-gather targets: [0] xe (primal), [1] y (dual)
   int npeers[2];
+  // check -> next primal step reuse (pdhg_check_dot_enable / pdhg_use_check_dot):
+  // a two-point check leaves A'y of both points interleaved in px (free once the
+  // check's A side has run; rebuilt by the next check's k_pair)
+  bool check_dot = false;  // enabled for this context
+  bool dots_ready = false; // px holds the last two-point check's A'y pairs
+  int first_dot = -1;      // armed: the next period's first primal step uses px[.].{x,y}
 };
 
 namespace {
@@ -1914,23 +1950,38 @@ int launch_step(pdhg_ctx* c, bool primal, int j);
 
 // The iterations of one period: a cooperative / single-block kernel, direct
 // stream launches (period_direct), or a CUDA graph captured once per length.
+// First primal step of a period from the last check's A'y (slot 0 / 1).
+int launch_primal_from_dot(pdhg_ctx* c, int slot, int j) {
+  const StepArgs a = step_args(c, true);
+  const int grid = (int)(((long long)a.rs.rows + kBlock - 1) / kBlock);
+  return launch_ex(c, k_primal_from_dot, dim3(grid), dim3(kBlock), 0, nullptr, 0, a,
+                   (const double2*)(c->px + c->xo), slot, j);
+}
+
 int launch_period(pdhg_ctx* c, int iters) {
+  // an armed check-dot slot is consumed by this period (or dropped)
+  const int first = c->first_dot;
+  c->first_dot = -1;
+  c->dots_ready = false;
   if (iters <= 0) return 0;
   if (c->coop_grid > 0) return launch_period_persistent(c, iters);
   int rc = 0;
+  auto primal0 = [&](int j) { return (j == 0 && first >= 0) ? launch_primal_from_dot(c, first, 0)
+                                                            : launch_step(c, true, j); };
   if (c->period_direct) {
     for (int j = 0; j < iters && !rc; ++j) {
-      rc = launch_step(c, true, j);
+      rc = primal0(j);
       if (!rc) rc = launch_step(c, false, j);
     }
     return rc;
   }
-  auto it = c->graphs.find(iters);
+  const int key = iters + (first + 1) * (1 << 28);  // graphs per (length, first step)
+  auto it = c->graphs.find(key);
   if (it == c->graphs.end()) {
     cudaGraph_t g;
     CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     for (int j = 0; j < iters && !rc; ++j) {
-      rc = launch_step(c, true, j);
+      rc = primal0(j);
       if (!rc) rc = launch_step(c, false, j);
     }
     cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
@@ -1939,7 +1990,7 @@ int launch_period(pdhg_ctx* c, int iters) {
     cudaGraphExec_t ex;
     CUDA_TRY(cudaGraphInstantiate(&ex, g, 0));
     cudaGraphDestroy(g);
-    it = c->graphs.emplace(iters, ex).first;
+    it = c->graphs.emplace(key, ex).first;
   }
   CUDA_TRY(cudaGraphLaunch(it->second, c->stream));
   return 0;
@@ -2256,6 +2307,7 @@ int pdhg_spmv(pdhg_ctx* c, int transpose, const double* in, double* out) {
 int pdhg_opnorm(pdhg_ctx* c, const double* v0_host, double tol, int32_t max_iters, double* lam_out,
                 int32_t* iters_out) {
   CTX_DEVICE_GUARD(c);
+  if (c) { c->first_dot = -1; c->dots_ready = false; }  // state changes: no check dots
   NvtxRange nvtx_range_("pdhg_opnorm");
   // pdhg.py:80-109.  v (tn1) <- v0; loop: w (tn2) = A'(A v); ||w||; v = w/||w||.
   if (!c || !v0_host || !lam_out) return fail(PDHG_ERR_ARG, "null argument");
@@ -2298,6 +2350,8 @@ int pdhg_reset(pdhg_ctx* c) {
   CTX_DEVICE_GUARD(c);
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
   const size_t nb = (size_t)c->nf * 8, mb = (size_t)c->mf * 8;
+  c->first_dot = -1;
+  c->dots_ready = false;
   CUDA_TRY(cudaMemsetAsync(c->x, 0, nb, c->stream));
   CUDA_TRY(cudaMemsetAsync(c->xe, 0, nb, c->stream));
   CUDA_TRY(cudaMemsetAsync(c->xbar, 0, nb, c->stream));
@@ -2390,6 +2444,12 @@ int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
     pp.pair = c->px;
     pd.pair = c->py;
   }
+  // A'y of both points for the next period's first primal step: written into
+  // px by the dual side, which runs after the A side has finished gathering px
+  const bool dots = c->check_dot && pd.pair && c->has_sell[1] && PDHG_CHECK_SELL;
+  pd.dout = dots ? c->px + c->xo : nullptr;
+  c->first_dot = -1;
+  c->dots_ready = false;
   CUDA_TRY(cudaMemsetAsync(c->partials, 0, (size_t)kCheckBlocks * kMaxQ * 8, c->stream));
   int rc = 0;
   if (pp.pair && c->has_sell[0] && PDHG_CHECK_SELL) {
@@ -2421,6 +2481,34 @@ int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
   const int nq = npts * PDHG_NQ;
   k_reduce<<<nq, kBlock, 0, c->stream>>>(c->partials, kCheckBlocks, kMaxQ, nq, c->scalars);
   CUDA_TRY(cudaGetLastError());
+  c->dots_ready = dots;
+  return 0;
+}
+
+int pdhg_check_dot_enable(pdhg_ctx* c, int32_t on) {
+  CTX_DEVICE_GUARD(c);
+  if (!c) return fail(PDHG_ERR_ARG, "null ctx");
+  c->first_dot = -1;
+  c->dots_ready = false;
+  if (!on) {
+    c->check_dot = false;
+    return 0;
+  }
+  // the check's dual side must run the primal step's own row loop (sliced ELL
+  // of A'), on one GPU (no peers: the from-dot step has no fused all-gather)
+  if (!c->has_sell[1] || !PDHG_CHECK_SELL || c->npeers[0] > 0 || c->has_psr[1] || c->coop_grid > 0 ||
+      c->prob.at_nsplit > 1)
+    return fail(PDHG_ERR_STATE, "check_dot: needs the sliced-ELL layout of A' on one GPU");
+  c->check_dot = true;
+  return 0;
+}
+
+int pdhg_use_check_dot(pdhg_ctx* c, int32_t slot) {
+  CTX_DEVICE_GUARD(c);
+  if (!c || slot < 0 || slot > 1) return fail(PDHG_ERR_ARG, "use_check_dot: bad argument");
+  if (!c->dots_ready) return fail(PDHG_ERR_STATE, "use_check_dot: the last call was not a two-point check "
+                                                  "with check_dot enabled");
+  c->first_dot = slot;
   return 0;
 }
 
@@ -2556,6 +2644,7 @@ int pdhg_set_step(pdhg_ctx* c, int64_t iter0, double tau_over_omega, double sigm
 
 int pdhg_half_step(pdhg_ctx* c, int32_t primal, int32_t j) {
   CTX_DEVICE_GUARD(c);
+  if (c) { c->first_dot = -1; c->dots_ready = false; }  // state changes: no check dots
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
   int rc = launch_step(c, primal != 0, j);
   if (rc) return rc;
@@ -2565,6 +2654,7 @@ int pdhg_half_step(pdhg_ctx* c, int32_t primal, int32_t j) {
 
 int pdhg_half_step_pass(pdhg_ctx* c, int32_t primal, int32_t j, int32_t pass) {
   CTX_DEVICE_GUARD(c);
+  if (c) { c->first_dot = -1; c->dots_ready = false; }  // state changes: no check dots
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
   int rc = launch_step_pass(c, primal != 0, j, pass);
   if (rc) return rc;
@@ -2574,6 +2664,7 @@ int pdhg_half_step_pass(pdhg_ctx* c, int32_t primal, int32_t j, int32_t pass) {
 
 int pdhg_set_peers(pdhg_ctx* c, int32_t which, const double* const* peers_dev, int32_t npeers) {
   CTX_DEVICE_GUARD(c);
+  if (c && which == 0 && npeers > 0) { c->check_dot = false; c->first_dot = -1; c->dots_ready = false; }
   if (!c || which < 0 || which > 2 || npeers < 0 || (npeers > 0 && !peers_dev))
     return fail(PDHG_ERR_ARG, "set_peers: bad argument");
   if (which == 2) {  // peers' fail words (pdhg_vector(peer, PDHG_VEC_FAILWORD))
@@ -2625,6 +2716,7 @@ int pdhg_div(pdhg_ctx* c, const double* w, double* v, int64_t len, double s) {
 int pdhg_time_kernel(pdhg_ctx* c, int32_t which, int32_t reps, double tau_over_omega,
                      double sigma_omega, double* avg_ms_out) {
   CTX_DEVICE_GUARD(c);
+  if (c) { c->first_dot = -1; c->dots_ready = false; }  // state changes: no check dots
   if (!c || reps < 1 || !avg_ms_out) return fail(PDHG_ERR_ARG, "bad argument");
   StepParams& h = *c->P_host;
   h.tau_w = tau_over_omega; h.sigma_w = sigma_omega; h.w0 = 0.0; h.iter0 = 0; h.fail_iter = LLONG_MAX;

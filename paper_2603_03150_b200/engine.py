@@ -95,6 +95,11 @@ class GpuOptions:
                      (profiles/r01_pipeline.md); CSR layouts, unsharded.
     l2_persist:      bit mask: 1 = pin y in L2 for the primal step, 2 = pin xe for the
                      dual step (persisting access-policy window; L2 holds 79 MB persisting).
+    check_dot:       reuse A'y of the checked points (both computed by the two-point
+                     check) as the SpMV of the next period's first primal step
+                     (pdhg_use_check_dot; bit-identical iterates).  Applies when A' has a
+                     sliced-ELL layout, unsharded: config 4 skips one of the 64 primal
+                     SpMVs of every period.
     """
 
     device: int | None = None
@@ -122,6 +127,7 @@ class GpuOptions:
     row_order: str = "auto"
     row_order_window: int = 65536
     row_order_max_tail: float = 0.15
+    check_dot: bool = True
 
 
 def auto_lanes(nnz: int, rows: int) -> int:
@@ -385,6 +391,9 @@ class DeviceLp:
         N.check(self.lib.pdhg_ctx_create(C.byref(p), self.ws.data_ptr(), ws_bytes,
                                          self.stream.cuda_stream, C.byref(ctx)))
         self.ctx = ctx
+        # check -> first primal step reuse (sliced ELL of A', one GPU)
+        self.check_dot = bool(opts.check_dot and shard is None and p.at_sell
+                              and self.lib.pdhg_check_dot_enable(ctx, 1) == 0)
         t_end = time.monotonic()
         self.timings = {"upload_s": t_up - t_start, "layout_s": t_end - t_up,
                         "layout_detail": {"transpose_s": t_tr - t_up, "psr_sell_s": t_sell - t_tr,
@@ -536,6 +545,12 @@ class DeviceLp:
                                                C.byref(f), self._scal))
         flat = np.frombuffer(self._scal, dtype=np.float64, count=len(specs) * N.NQ).copy()
         return int(f.value), [flat[k * N.NQ:(k + 1) * N.NQ] for k in range(len(specs))]
+
+    def use_check_dot(self, slot: int) -> None:
+        """The next period's first primal step takes A'y of point `slot` of the
+        last two-point check (0 = first spec, 1 = second) -- see
+        pdhg_use_check_dot in include/pdhg_b200.h."""
+        N.check(self.lib.pdhg_use_check_dot(self.ctx, int(slot)))
 
     def check(self, *specs: int) -> list[np.ndarray]:
         arr = (C.c_int32 * len(specs))(*specs)
@@ -939,11 +954,13 @@ def _run(T, dev: DeviceLp, p, params, seed, opts, t0, v0_future=None):
                 dev.save_best(N.PT_AVG, N.BEST_Z)
                 best_live_avg = True
 
+        restarted = False
         if cand_sum.max_violation <= params.restart_beta * restart_score:  # pdhg.py:234-247
             if best_live_avg:  # the average array best_pt aliases is rebound: freeze it
                 dev.save_best(N.PT_AVG, N.BEST_XY)
                 best_live_avg = False
             dev.restart(cand)
+            restarted = True
             avg_weight = 0.0
             rp, rd = cand_s.rp_norm, cand_s.rd_norm
             if rp > 0.0 and rd > 0.0:
@@ -951,6 +968,10 @@ def _run(T, dev: DeviceLp, p, params, seed, opts, t0, v0_future=None):
             restart_score = cand_sum.max_violation
             restarts += 1
             rec["restart"] = True
+        if getattr(dev, "check_dot", False):
+            # the next iterate's y is the current point's, or the average's after
+            # a restart to it: the check already holds its A'y (pdhg_use_check_dot)
+            dev.use_check_dot(1 if (restarted and cand == N.PT_AVG) else 0)
 
     # failure exit (pdhg.py:249-258): best point, re-checked with its own z
     tm["iterate_s"] = time.monotonic() - t_it

@@ -1,0 +1,361 @@
+// gather4_lab.cu -- lab (not product): does moving the SpMV's gathers off the
+// LSU / L1 miss path onto the TMA unit (Blackwell's
+// cp.async.bulk.tensor.2d.tile::gather4: four 2D rows by index into shared
+// memory) or widening the matrix stream to 128-bit loads raise the
+// sliced-ELL dual step's rate on a config-4-like matrix?
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
+//        tools/gather4_lab.cu -o tools/gather4_lab -lcuda
+//   tools/gather4_lab [m=5000000] [W=40] [reps=20]
+//
+// Matrix: m rows x n = 2m columns, every row W entries (sorted by column):
+// 70 % within +-50k of column 2i (wrapped), 30 % uniform -- config 4's
+// pattern (BASELINE.json configs[4]) at a fixed row length.  Sliced ELL:
+// slice s = rows 32s..32s+31, entry k of lane l at s*32*W + 32k + l (the
+// product layout, csrc/sell_build.cu).  Kernels compute y = A x only.
+//
+//   ldg    : the product's row loop (sell_row_dot, kU entries in flight)
+//   ldg128 : values in lane pairs (double2) and indices in lane quads (int4):
+//            one 128-bit load per 2 values / 4 indices
+//   g4_32  : gathers by TMA gather4 of 32-byte rows (x viewed as [n/4][4]),
+//            S entry columns in flight per warp, one mbarrier per stage
+//   g4_16  : the same with 16-byte rows (x as [n/2][2])
+// All variants sum each row sequentially in entry order: bitwise equal y.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) {                                                                   \
+      fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e_));       \
+      exit(1);                                                                                 \
+    }                                                                                          \
+  } while (0)
+
+__device__ __forceinline__ uint64_t mix(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// row i's W columns (sorted) and values; stored in both layouts
+__global__ void k_gen(int m, int n, int W, int* col, double* val, int2* colq /*int4 view*/, double2* valp) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  int c[64];
+  double v[64];
+  for (int k = 0; k < W; ++k) {
+    const uint64_t h = mix(((uint64_t)i << 8) + k);
+    long long cc;
+    if ((h & 1023) < 717) cc = 2 * i + (long long)((h >> 10) % 100001) - 50000;
+    else cc = (long long)((h >> 10) % (uint64_t)n);
+    cc %= n;
+    if (cc < 0) cc += n;
+    c[k] = (int)cc;
+    v[k] = (double)((h >> 40) & 0xffffff) / 8388608.0 - 1.0;
+  }
+  for (int a = 1; a < W; ++a) {  // insertion sort by column
+    int cj = c[a];
+    double vj = v[a];
+    int b = a - 1;
+    while (b >= 0 && c[b] > cj) {
+      c[b + 1] = c[b];
+      v[b + 1] = v[b];
+      --b;
+    }
+    c[b + 1] = cj;
+    v[b + 1] = vj;
+  }
+  const long long s = i >> 5, l = i & 31;
+  const long long base = s * 32 * W;
+  for (int k = 0; k < W; ++k) {
+    col[base + 32LL * k + l] = c[k];
+    val[base + 32LL * k + l] = v[k];
+  }
+  // 128-bit layouts: values pair p = (k/2): valp[s*16*W + p*32 + l] = {v[2p], v[2p+1]}
+  for (int p = 0; p < W / 2; ++p) valp[s * 16 * W + p * 32 + l] = make_double2(v[2 * p], v[2 * p + 1]);
+  int4* cq = reinterpret_cast<int4*>(colq);
+  for (int q = 0; q < W / 4; ++q) cq[s * 8 * W + q * 32 + l] = make_int4(c[4 * q], c[4 * q + 1], c[4 * q + 2], c[4 * q + 3]);
+}
+
+__global__ void k_fillx(long long n, double* x) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = (double)(mix(i * 7 + 3) >> 11) / 9007199254740992.0 - 0.5;
+}
+
+// ----------------------------------------------------------------- ldg
+template <int kU>
+__global__ void __launch_bounds__(256, 6) k_ldg(int m, int W, const int* __restrict__ col,
+                                                const double* __restrict__ val, const double* __restrict__ x,
+                                                double* __restrict__ y) {
+  const long long sl = ((long long)blockIdx.x * 256 + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (sl * 32 >= m) return;
+  const long long base = sl * 32 * W + lane;
+  double acc = 0.0;
+  for (int k = 0; k < W; k += kU) {
+    double av[kU], xv[kU];
+    int jv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const bool on = k + u < W;
+      av[u] = on ? __ldcs(val + base + 32LL * (k + u)) : 0.0;
+      jv[u] = on ? __ldcs(col + base + 32LL * (k + u)) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) xv[u] = jv[u] >= 0 ? __ldg(x + jv[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (jv[u] >= 0) acc = fma(av[u], xv[u], acc);
+  }
+  y[sl * 32 + lane] = acc;
+}
+
+// ----------------------------------------------------------------- ldg128
+// kQ quads (4 entries) in flight per lane; W % 4 == 0
+template <int kQ>
+__global__ void __launch_bounds__(256, 6) k_ldg128(int m, int W, const int4* __restrict__ colq,
+                                                   const double2* __restrict__ valp,
+                                                   const double* __restrict__ x, double* __restrict__ y) {
+  const long long sl = ((long long)blockIdx.x * 256 + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (sl * 32 >= m) return;
+  const int4* cq = colq + sl * 8 * W + lane;
+  const double2* vp = valp + sl * 16 * W + lane;
+  double acc = 0.0;
+  const int nq = W / 4;
+  for (int q = 0; q < nq; q += kQ) {
+    int4 c[kQ];
+    double2 a0[kQ], a1[kQ];
+    double xv[kQ][4];
+#pragma unroll
+    for (int u = 0; u < kQ; ++u) {
+      const bool on = q + u < nq;
+      c[u] = on ? __ldcs(cq + 32LL * (q + u)) : make_int4(-1, -1, -1, -1);
+      a0[u] = on ? __ldcs(vp + 64LL * (q + u)) : make_double2(0, 0);
+      a1[u] = on ? __ldcs(vp + 64LL * (q + u) + 32) : make_double2(0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kQ; ++u) {
+      xv[u][0] = c[u].x >= 0 ? __ldg(x + c[u].x) : 0.0;
+      xv[u][1] = c[u].y >= 0 ? __ldg(x + c[u].y) : 0.0;
+      xv[u][2] = c[u].z >= 0 ? __ldg(x + c[u].z) : 0.0;
+      xv[u][3] = c[u].w >= 0 ? __ldg(x + c[u].w) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kQ; ++u)
+      if (c[u].x >= 0) {
+        acc = fma(a0[u].x, xv[u][0], acc);
+        acc = fma(a0[u].y, xv[u][1], acc);
+        acc = fma(a1[u].x, xv[u][2], acc);
+        acc = fma(a1[u].y, xv[u][3], acc);
+      }
+  }
+  y[sl * 32 + lane] = acc;
+}
+
+// ----------------------------------------------------------------- gather4
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(saddr(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void g4(void* dst, const CUtensorMap* tm, uint64_t* bar, int r0, int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(saddr(dst)),
+      "l"(tm), "r"(saddr(bar)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+
+// EW = doubles per gathered row (4: 32 B, 2: 16 B); S stages per warp; NW warps per block
+template <int EW, int S, int NW>
+__global__ void __launch_bounds__(NW * 32) k_g4(const __grid_constant__ CUtensorMap tm, int m, int W,
+                                                const int* __restrict__ col, const double* __restrict__ val,
+                                                double* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int kStage = 32 * EW * 8;  // bytes per entry column of a warp
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* ring = smem + (size_t)wib * S * kStage;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)NW * S * kStage) + wib * S;
+  if (lane == 0)
+    for (int s = 0; s < S; ++s) mbar_init(bars + s, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const long long sl = (long long)blockIdx.x * NW + wib;
+  if (sl * 32 >= m) return;
+  const long long base = sl * 32 * W + lane;
+  constexpr int kSh = EW == 4 ? 2 : 1;
+  int cq[S];
+  double av[S];
+  auto issue = [&](int k, int s) {
+    // k < W guaranteed by caller
+    const int c = __ldcs(col + base + 32LL * k);
+    av[s] = __ldcs(val + base + 32LL * k);
+    cq[s] = c;
+    const int r = c >> kSh;
+    const int g = lane & ~3;
+    const int r0 = __shfl_sync(0xffffffffu, r, g), r1 = __shfl_sync(0xffffffffu, r, g + 1);
+    const int r2 = __shfl_sync(0xffffffffu, r, g + 2), r3 = __shfl_sync(0xffffffffu, r, g + 3);
+    if (lane == 0) mbar_expect_tx(bars + s, kStage);
+    __syncwarp();
+    if ((lane & 3) == 0) g4(ring + s * kStage + (lane >> 2) * (4 * EW * 8), &tm, bars + s, r0, r1, r2, r3);
+  };
+  double acc = 0.0;
+  uint32_t phase = 0;  // bit s: parity of stage s
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+    if (s < W) issue(s, s);
+  for (int k0 = 0; k0 < W; k0 += S) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int k = k0 + s;
+      if (k < W) {
+        mbar_wait(bars + s, (phase >> s) & 1);
+        phase ^= 1u << s;
+        const double xv =
+            *reinterpret_cast<const double*>(ring + s * kStage + lane * (EW * 8) + (cq[s] & (EW - 1)) * 8);
+        acc = fma(av[s], xv, acc);
+        __syncwarp();
+        if (k + S < W) issue(k + S, s);
+      }
+    }
+  }
+  y[sl * 32 + lane] = acc;
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static CUtensorMap make_map(double* x, long long n, int ew) {
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof tm);
+  cuuint64_t dims[2] = {(cuuint64_t)ew, (cuuint64_t)(n / ew)};
+  cuuint64_t strides[1] = {(cuuint64_t)ew * 8};
+  cuuint32_t box[2] = {(cuuint32_t)ew, 1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, x, dims, strides, box, es,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    const char* s = nullptr;
+    cuGetErrorString(r, &s);
+    fprintf(stderr, "cuTensorMapEncodeTiled(ew=%d): %s\n", ew, s ? s : "?");
+    exit(1);
+  }
+  return tm;
+}
+
+template <typename F>
+static float time_it(F f, int reps) {
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  for (int i = 0; i < 3; ++i) f();
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(a));
+  for (int i = 0; i < reps; ++i) f();
+  CK(cudaEventRecord(b));
+  CK(cudaEventSynchronize(b));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  CK(cudaGetLastError());
+  return ms / reps;
+}
+
+int main(int argc, char** argv) {
+  const int m = argc > 1 ? atoi(argv[1]) : 5000000;
+  const int W = argc > 2 ? atoi(argv[2]) : 40;
+  const int reps = argc > 3 ? atoi(argv[3]) : 20;
+  const long long n = 2LL * m;
+  const long long nnz = (long long)m * W;
+  if (m % 32 || W % 4 || W > 64) {
+    fprintf(stderr, "m %% 32 == 0, W %% 4 == 0, W <= 64\n");
+    return 1;
+  }
+  int *col, *colq;
+  double *val, *x, *y0, *y1;
+  double2* valp;
+  CK(cudaMalloc(&col, nnz * 4));
+  CK(cudaMalloc(&colq, nnz * 4));
+  CK(cudaMalloc(&val, nnz * 8));
+  CK(cudaMalloc(&valp, nnz * 8));
+  CK(cudaMalloc(&x, n * 8));
+  CK(cudaMalloc(&y0, (size_t)m * 8));
+  CK(cudaMalloc(&y1, (size_t)m * 8));
+  k_gen<<<(m + 127) / 128, 128>>>(m, (int)n, W, col, val, reinterpret_cast<int2*>(colq), valp);
+  k_fillx<<<(unsigned)((n + 255) / 256), 256>>>(n, x);
+  CK(cudaDeviceSynchronize());
+  std::vector<double> h0(m), h1(m);
+  const double alg = 12.0 * nnz + 8.0 * n + 8.0 * m;  // stream + compulsory x + y
+  printf("{\"m\": %d, \"n\": %lld, \"W\": %d, \"nnz\": %lld}\n", m, n, W, nnz);
+  auto report = [&](const char* name, float ms, bool check) {
+    bool same = true;
+    if (check) {
+      CK(cudaMemcpy(h1.data(), y1, (size_t)m * 8, cudaMemcpyDeviceToHost));
+      same = memcmp(h0.data(), h1.data(), (size_t)m * 8) == 0;
+    }
+    printf("{\"kernel\": \"%s\", \"ms\": %.4f, \"Gentries_s\": %.1f, \"alg_GBs\": %.0f, \"bitwise_equal\": %s}\n", name,
+           ms, nnz / (ms * 1e6), alg / (ms * 1e6), same ? "true" : "false");
+    fflush(stdout);
+  };
+  const unsigned gw = (unsigned)((m / 32 * 32 + 255) / 256);
+  float t;
+  t = time_it([&] { k_ldg<10><<<gw, 256>>>(m, W, col, val, x, y0); }, reps);
+  CK(cudaMemcpy(h0.data(), y0, (size_t)m * 8, cudaMemcpyDeviceToHost));
+  report("ldg_u10", t, false);
+  t = time_it([&] { k_ldg<8><<<gw, 256>>>(m, W, col, val, x, y1); }, reps);
+  report("ldg_u8", t, true);
+  t = time_it([&] { k_ldg128<2><<<gw, 256>>>(m, W, reinterpret_cast<int4*>(colq), valp, x, y1); }, reps);
+  report("ldg128_q2", t, true);
+  t = time_it([&] { k_ldg128<3><<<gw, 256>>>(m, W, reinterpret_cast<int4*>(colq), valp, x, y1); }, reps);
+  report("ldg128_q3", t, true);
+
+  CUtensorMap tm4 = make_map(x, n, 4), tm2 = make_map(x, n, 2);
+  auto run_g4 = [&](auto kern, const CUtensorMap& tm, int ew, int S, int NW, const char* name) {
+    const size_t sm = (size_t)NW * S * (32 * ew * 8) + (size_t)NW * S * 8;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const unsigned g = (unsigned)((m / 32 + NW - 1) / NW);
+    CK(cudaMemset(y1, 0, (size_t)m * 8));
+    float tt = time_it([&] { kern<<<g, NW * 32, sm>>>(tm, m, W, col, val, y1); }, reps);
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NW * 32, sm));
+    char nm[96];
+    snprintf(nm, sizeof nm, "%s_S%d_NW%d_occ%d", name, S, NW, nb);
+    report(nm, tt, true);
+  };
+  run_g4(k_g4<4, 4, 8>, tm4, 4, 4, 8, "g4_32");
+  run_g4(k_g4<4, 8, 8>, tm4, 4, 8, 8, "g4_32");
+  run_g4(k_g4<4, 4, 4>, tm4, 4, 4, 4, "g4_32");
+  run_g4(k_g4<4, 8, 4>, tm4, 4, 8, 4, "g4_32");
+  run_g4(k_g4<2, 4, 8>, tm2, 2, 4, 8, "g4_16");
+  run_g4(k_g4<2, 8, 8>, tm2, 2, 8, 8, "g4_16");
+  run_g4(k_g4<2, 12, 8>, tm2, 2, 12, 8, "g4_16");
+  run_g4(k_g4<2, 8, 4>, tm2, 2, 8, 4, "g4_16");
+  // ldg again (clock drift check)
+  t = time_it([&] { k_ldg<10><<<gw, 256>>>(m, W, col, val, x, y1); }, reps);
+  report("ldg_u10_again", t, true);
+  return 0;
+}
