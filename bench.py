@@ -385,8 +385,17 @@ def run_ours(args):
     import torch.distributed as dist
 
     rank, world, local = _env_rank()
+    # --sharded: the N > 1 path (rank-0 block files, sharded engine, NCCL
+    # all-gathers, overlap schedule) also on a world of one -- a smoke test of
+    # the multi-GPU bench on a one-GPU box, not a measurement
+    sharded = world > 1 or args.sharded
+    if sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
     torch.cuda.set_device(local)
-    if world > 1:
+    if sharded:
         import datetime
 
         # rank 0 generates and cuts the 200M-entry model while the others wait
@@ -399,7 +408,7 @@ def run_ours(args):
     opts = eng.GpuOptions(cache_layout=False, psr=args.psr)
     comm_kind = "torch_peer" if args.comm == "peer" else "torch"
     blocks = None
-    if world > 1:
+    if sharded:
         # rank 0 generates the LP (and its device-Ruiz-scaled twin for the run to
         # 1e-4), cuts it into per-rank blocks and writes them to /dev/shm; every
         # rank then holds only its own rows (no per-rank copy of the whole model)
@@ -414,7 +423,7 @@ def run_ours(args):
 
     # ---- device-resident timing: K periods of 64 iterations + check
     t_setup = time.perf_counter()
-    if world > 1:
+    if sharded:
         from paper_2603_03150_b200.sharded import build_sharded_from_block
 
         dev = build_sharded_from_block(plan, blk, comm_kind, opts, overlap=args.overlap)
@@ -440,7 +449,7 @@ def run_ours(args):
         it += CHECK_EVERY
     s = kdev.stream
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
+    if sharded:
         dist.barrier()
     torch.cuda.synchronize()
     # the product's period call (engine._run): the graph of 64 iterations and
@@ -462,7 +471,7 @@ def run_ours(args):
     # where a period's time goes (after the timed region, same sustained state):
     # events around the graph of 64 iterations and around the check
     breakdown = None
-    if world == 1:
+    if not sharded:
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(3)]
         for e in evs:
             e[0].record(s)
@@ -479,7 +488,7 @@ def run_ours(args):
                      "check_ms": statistics.median(c_ms),
                      "method": "3 periods after the timed region: CUDA events around the period graph "
                                "and around the two-point check (run_period + check, 2 host syncs)"}
-    if world > 1:
+    if sharded:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -487,14 +496,14 @@ def run_ours(args):
     iters = args.steps * CHECK_EVERY
     value = iters / (ms / 1e3)   # iterations of the one LP per second, all ranks together
     ms_per_step = ms / args.steps
-    if world > 1:   # kernel roofline below is for this rank's shard
+    if sharded:   # kernel roofline below is for this rank's shard
         ab = algorithmic_bytes(kdev.m, kdev.n, kdev.nnz)
         ab["primal"] = 12 * kdev.at_nnz + 4 * (kdev.n + 1) + 8 * kdev.m_full + 48 * kdev.n
         ab["dual"] = 12 * kdev.nnz + 4 * (kdev.m + 1) + 8 * kdev.n_full + 40 * kdev.m
 
     # ---- per-kernel timing for the roofline (CUDA events on the engine stream)
     reps = 20
-    if world == 1:
+    if not sharded:
         # live: one more period right after the timed region, in the same
         # sustained (power-capped) state, launched kernel by kernel with an
         # event pair around every launch -- the in-sequence duration of each
@@ -507,7 +516,7 @@ def run_ours(args):
         tk = {"primal": kdev.time_kernel(0, reps, step, step), "dual": kdev.time_kernel(1, reps, step, step)}
         tk_isolated = dict(tk)
     comm_info = None
-    if world > 1:
+    if sharded:
         ag = _allgather_ms(dev)
         comm_info = {"overlap": dev.overlap, "comm": comm_kind,
                      "allgather_ms_per_iteration": {"xe": ag["xe"], "y": ag["y"], "sum": ag["xe"] + ag["y"]},
@@ -537,7 +546,7 @@ def run_ours(args):
                 "kernels_ms": tk, "kernels_ms_method": (
                     "average of 64 in-sequence launches each, CUDA events on the engine stream, "
                     "one period launched kernel by kernel right after the timed region"
-                    if world == 1 else "pdhg_time_kernel: 20 repeated launches, CUDA events"),
+                    if not sharded else "pdhg_time_kernel: 20 repeated launches, CUDA events"),
                 "kernels_ms_isolated": tk_isolated, "algorithmic_bytes": ab,
                 # the units that bind (ncu capture, profiles/traffic.json): every gather of the
                 # 40/80 MB vector is a 32 B L2 sector, so L1TEX / L2-slice throughput, not DRAM,
@@ -570,7 +579,7 @@ def run_ours(args):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         t0 = time.perf_counter()
-        if world > 1:
+        if sharded:
             from paper_2603_03150_b200.sharded import run_pdhg_sharded_block
 
             # the public entry from this rank's host block (upload, layout, power
@@ -583,7 +592,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         wall_e2e = time.perf_counter() - t0
         e2e_ms = e0.elapsed_time(e1)
-        if world > 1:
+        if sharded:
             t = torch.tensor([e2e_ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
@@ -602,7 +611,7 @@ def run_ours(args):
         # rank equilibrates the whole model (bit-identical), then the sharded
         # run; times are the max over ranks.
         ttk_params = T.PdhgParams(eps_rel=1e-4, time_limit_s=args.ttk_limit)
-        if world > 1:
+        if sharded:
             from paper_2603_03150_b200.sharded import run_pdhg_sharded_block
 
             splan, sblk, sb, sc = blocks["scaled"]
@@ -627,18 +636,18 @@ def run_ours(args):
         out = {"status": st2.status.value, "iterations": st2.iterations, "restarts": st2.restarts,
                "pdhg_wall_s": wall2, "ruiz_s": t_ruiz, "ruiz_passes": info.applied_iterations,
                "total_s": t_ruiz + wall2,
-               "ruiz_phases_s": dict(eng.ruiz.last_timings) if world == 1 else blocks.get("ruiz_phases"),
+               "ruiz_phases_s": dict(eng.ruiz.last_timings) if not sharded else blocks.get("ruiz_phases"),
                "reference_iterations": _reference_ttk_iterations(),
                "note": "device Ruiz (bit-identical to transform.py:35-77) + run_pdhg to eps_rel=1e-4"
                        + (f", sharded over {world} GPUs (Ruiz once on rank 0's GPU, blocks to "
-                          f"/dev/shm)" if world > 1 else "")}
-        if args.ttk_unscaled and world == 1:
+                          f"/dev/shm)" if sharded else "")}
+        if args.ttk_unscaled and not sharded:
             pt3, st3 = eng.run_pdhg(inst, T.PdhgParams(eps_rel=1e-4, time_limit_s=args.ttk_limit), gpu=opts)
             out["unscaled"] = {"status": st3.status.value, "iterations": st3.iterations,
                                "restarts": st3.restarts, "wall_s": st3.wall_seconds}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not sharded and not args.no_cpu:
         cs = cpu_sample(inst, steps=args.cpu_steps)
         cpu = _cpu_baseline(cs, m, n, nnz)
         if "time_to_1e4_s" not in cpu and out is not None and out.get("status") == "Optimal":
@@ -648,12 +657,12 @@ def run_ours(args):
                                             "reference's sampled seconds per iteration (the reference's "
                                             "own count, once tests/golden/run_config4_s1.json exists)"}
     rss_max = _host_rss_gb()
-    if world > 1:
+    if sharded:
         t = torch.tensor([rss_max], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         rss_max = float(t.item())
     if rank != 0:
-        if world > 1:
+        if sharded:
             dist.destroy_process_group()
         return 0
     line = {
@@ -665,7 +674,7 @@ def run_ours(args):
                                     ("xe / y pushed to peers by the step epilogues (symmetric memory, "
                                      "NVLink stores) + stream barrier" if args.comm == "peer" else
                                      "NCCL all-gather of xe and y per iteration"))
-                                   if world > 1 else "1 GPU"),
+                                   if sharded else "1 GPU"),
                    "kernel_layout": layout_name},
         "roofline": roofline,
         "period_breakdown": breakdown,
@@ -689,7 +698,7 @@ def run_ours(args):
         "host_rss_gb_max_over_ranks": rss_max,
     }
     print(json.dumps(line))
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
     return 0
 
@@ -703,6 +712,8 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--seed", type=int, default=4)
     ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the multi-GPU (sharded, NCCL) path even on one GPU (smoke test)")
     ap.add_argument("--e2e-reps", type=int, default=3, help="public-API calls for e2e (median reported)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ttk", action=argparse.BooleanOptionalAction, default=True,
