@@ -6,7 +6,7 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
 //        tools/gather4_lab.cu -o tools/gather4_lab -lcuda
-//   tools/gather4_lab [m=5000000] [W=40] [reps=20]
+//   tools/gather4_lab [m=5000000] [W=40] [reps=20] [n/m=2] [all]
 //
 // Matrix: m rows x n = 2m columns, every row W entries (sorted by column):
 // 70 % within +-50k of column 2i (wrapped), 30 % uniform -- config 4's
@@ -244,6 +244,74 @@ __global__ void __launch_bounds__(NW * 32) k_g4(const __grid_constant__ CUtensor
   y[sl * 32 + lane] = acc;
 }
 
+// ----------------------------------------------------------------- TMA-bulk stream
+// The matrix stream (values, indices) of each warp's slice arrives by
+// cp.async.bulk into a per-warp double-buffered ring (kU entry columns per
+// stage: 32*kU*12 bytes), lanes read it from shared memory; the gathers stay
+// LDG.  Does taking the stream's 0.375 sectors per entry off the L1 miss path
+// speed up the gather-bound loop?
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   saddr(dst)), "l"(src), "r"(bytes), "r"(saddr(bar)) : "memory");
+}
+
+template <int kU, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) k_tma_stream(int m, int W, const int* __restrict__ col,
+                                                             const double* __restrict__ val,
+                                                             const double* __restrict__ x, double* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int kVal = 32 * kU * 8, kCol = 32 * kU * 4, kStage = kVal + kCol;
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* ring = smem + (size_t)wib * 2 * kStage;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)NW * 2 * kStage) + wib * 2;
+  if (lane == 0) {
+    mbar_init(bars, 1);
+    mbar_init(bars + 1, 1);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const long long sl = (long long)blockIdx.x * NW + wib;
+  if (sl * 32 >= m) return;
+  const long long base = sl * 32 * W;
+  const int nch = (W + kU - 1) / kU;
+  auto issue = [&](int ch, int st) {
+    if (lane == 0) {
+      const int k0 = ch * kU, cols = min(kU, W - k0);
+      mbar_expect_tx(bars + st, (uint32_t)(cols * 32 * 12));
+      bulk_g2s(ring + st * kStage, val + base + 32LL * k0, (uint32_t)(cols * 32 * 8), bars + st);
+      bulk_g2s(ring + st * kStage + kVal, col + base + 32LL * k0, (uint32_t)(cols * 32 * 4), bars + st);
+    }
+  };
+  issue(0, 0);
+  if (nch > 1) issue(1, 1);
+  double acc = 0.0;
+  uint32_t ph0 = 0, ph1 = 0;
+  for (int ch = 0; ch < nch; ++ch) {
+    const int st = ch & 1;
+    mbar_wait(bars + st, st ? ph1 : ph0);
+    if (st) ph1 ^= 1; else ph0 ^= 1;
+    const double* sv = reinterpret_cast<const double*>(ring + st * kStage);
+    const int* sc = reinterpret_cast<const int*>(ring + st * kStage + kVal);
+    const int cols = min(kU, W - ch * kU);
+    double av[kU], xv[kU];
+    int jv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const bool on = u < cols;
+      av[u] = on ? sv[u * 32 + lane] : 0.0;
+      jv[u] = on ? sc[u * 32 + lane] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) xv[u] = jv[u] >= 0 ? __ldg(x + jv[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (jv[u] >= 0) acc = fma(av[u], xv[u], acc);
+    __syncwarp();
+    if (ch + 2 < nch) issue(ch + 2, st);
+  }
+  y[sl * 32 + lane] = acc;
+}
+
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -289,7 +357,8 @@ int main(int argc, char** argv) {
   const int m = argc > 1 ? atoi(argv[1]) : 5000000;
   const int W = argc > 2 ? atoi(argv[2]) : 40;
   const int reps = argc > 3 ? atoi(argv[3]) : 20;
-  const long long n = 2LL * m;
+  const int ratio = argc > 4 ? atoi(argv[4]) : 2;  // n = ratio * m (x footprint 8n bytes)
+  const long long n = (long long)ratio * m;
   const long long nnz = (long long)m * W;
   if (m % 32 || W % 4 || W > 64) {
     fprintf(stderr, "m %% 32 == 0, W %% 4 == 0, W <= 64\n");
@@ -310,7 +379,7 @@ int main(int argc, char** argv) {
   CK(cudaDeviceSynchronize());
   std::vector<double> h0(m), h1(m);
   const double alg = 12.0 * nnz + 8.0 * n + 8.0 * m;  // stream + compulsory x + y
-  printf("{\"m\": %d, \"n\": %lld, \"W\": %d, \"nnz\": %lld}\n", m, n, W, nnz);
+  printf("{\"m\": %d, \"n\": %lld, \"W\": %d, \"nnz\": %lld, \"x_MB\": %lld}\n", m, n, W, nnz, n * 8 / 1000000);
   auto report = [&](const char* name, float ms, bool check) {
     bool same = true;
     if (check) {
@@ -346,14 +415,32 @@ int main(int argc, char** argv) {
     snprintf(nm, sizeof nm, "%s_S%d_NW%d_occ%d", name, S, NW, nb);
     report(nm, tt, true);
   };
+  auto run_ts = [&](auto kern, int kU, int NW, const char* name) {
+    const size_t sm = (size_t)NW * 2 * (32 * kU * 12) + (size_t)NW * 2 * 8;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const unsigned g = (unsigned)((m / 32 + NW - 1) / NW);
+    CK(cudaMemset(y1, 0, (size_t)m * 8));
+    float tt = time_it([&] { kern<<<g, NW * 32, sm>>>(m, W, col, val, x, y1); }, reps);
+    int nb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, NW * 32, sm));
+    char nm[96];
+    snprintf(nm, sizeof nm, "%s_U%d_NW%d_occ%d", name, kU, NW, nb);
+    report(nm, tt, true);
+  };
+  if (argc > 5) {  // TMA-bulk stream variants (measured: slower)
+    run_ts(k_tma_stream<10, 8, 3>, 10, 8, "tma_stream");
+    run_ts(k_tma_stream<10, 4, 6>, 10, 4, "tma_stream");
+    run_ts(k_tma_stream<8, 8, 4>, 8, 8, "tma_stream");
+    run_ts(k_tma_stream<4, 8, 6>, 4, 8, "tma_stream");
+    run_ts(k_tma_stream<4, 16, 3>, 4, 16, "tma_stream");
+  }
+  if (argc > 5) {  // gather4 variants (measured: slower)
   run_g4(k_g4<4, 4, 8>, tm4, 4, 4, 8, "g4_32");
   run_g4(k_g4<4, 8, 8>, tm4, 4, 8, 8, "g4_32");
   run_g4(k_g4<4, 4, 4>, tm4, 4, 4, 4, "g4_32");
   run_g4(k_g4<4, 8, 4>, tm4, 4, 8, 4, "g4_32");
-  run_g4(k_g4<2, 4, 8>, tm2, 2, 4, 8, "g4_16");
-  run_g4(k_g4<2, 8, 8>, tm2, 2, 8, 8, "g4_16");
-  run_g4(k_g4<2, 12, 8>, tm2, 2, 12, 8, "g4_16");
-  run_g4(k_g4<2, 8, 4>, tm2, 2, 8, 4, "g4_16");
+  (void)tm2;  // 16-byte rows: the 64-byte smem destinations violate TMA's 128-byte alignment
+  }
   // ldg again (clock drift check)
   t = time_it([&] { k_ldg<10><<<gw, 256>>>(m, W, col, val, x, y1); }, reps);
   report("ldg_u10_again", t, true);

@@ -85,9 +85,15 @@ def main():
             "lab_A_spmv_u10": lab_ms("A", 0, 10),
             "lab_A_spmv_u6": lab_ms("A", 0, 6),
             "lab_A_spmv_epi_u10": lab_ms("A", 1, 10),
+            "lab_A_tail_10_2": lab_ms("A", 2, 10),
+            "lab_A_tail_10_4": lab_ms("A", 3, 10),
+            "lab_A_tail_8_2": lab_ms("A", 4, 10),
+            "lab_A_tail_6_2": lab_ms("A", 5, 10),
             "product_primal": round(d.time_kernel(0, args.reps, st, st), 4),
             "lab_At_spmv_u6": lab_ms("At", 0, 6),
             "lab_At_spmv_u10": lab_ms("At", 0, 10),
+            "lab_At_tail_6_2": lab_ms("At", 5, 10),
+            "lab_At_tail_8_2": lab_ms("At", 4, 10),
             "clock": subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader"],
                                     capture_output=True, text=True).stdout.strip(),
         }
