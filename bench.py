@@ -69,12 +69,16 @@ def _cpu_model() -> str:
 
 def _reference_ttk_iterations():
     """Iterations the REAL reference needed to reach 1e-4 on this instance
-    (tests/golden/run_config4_s1.json, oracle/make_golden_runs.py), or None."""
-    f = ROOT / "tests" / "golden" / "run_config4_s1.json"
-    try:
-        return int(json.loads(f.read_text())["iterations"])
-    except Exception:
-        return None
+    (tests/golden/run_config4_s1[_nolimit].json, oracle/make_golden_runs.py;
+    only a run that reached Optimal counts), or None."""
+    for name in ("run_config4_s1_nolimit.json", "run_config4_s1.json"):
+        try:
+            r = json.loads((ROOT / "tests" / "golden" / name).read_text())
+            if r.get("status") == "Optimal":
+                return int(r["iterations"])
+        except Exception:
+            continue
+    return None
 
 
 def _env_rank():
@@ -275,7 +279,7 @@ def _cpu_baseline(cs: dict, m: int, n: int, nnz: int) -> dict:
     if ref_its:
         out["time_to_1e4_s"] = {"value": ref_its * cs["per_iter_s"], "iterations": ref_its,
                                 "note": "extrapolated: iterations the real reference took to reach 1e-4 "
-                                        "on this instance (tests/golden/run_config4_s1.json) x the "
+                                        "on this instance (tests/golden/run_config4_s1_nolimit.json) x the "
                                         "sampled seconds per iteration"}
     return out
 
@@ -655,7 +659,7 @@ def run_ours(args):
             cpu["time_to_1e4_s"] = {"value": its * cs["per_iter_s"], "iterations": its,
                                     "note": "extrapolated: this run's GPU iteration count to 1e-4 x the "
                                             "reference's sampled seconds per iteration (the reference's "
-                                            "own count, once tests/golden/run_config4_s1.json exists)"}
+                                            "own count, once tests/golden/run_config4_s1_nolimit.json exists)"}
     rss_max = _host_rss_gb()
     if sharded:
         t = torch.tensor([rss_max], dtype=torch.float64, device="cuda")
