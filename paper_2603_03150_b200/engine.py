@@ -81,6 +81,12 @@ class GpuOptions:
                      sell_max_pad and at most row_order_max_tail of whose entries sit
                      in rows longer than 4x the mean (lane-per-row slices run a long
                      row on one lane: config 2's power-law rows stay on CSR-vector).
+    row_order_first: with row_order: rows longer than this many entries come first
+                     (window by window, longest first), then the rest -- the long
+                     slices start at the head of the grid, so no window's long slices
+                     are left running after the rest has drained (config 4's dual
+                     SpMV 0.889 -> 0.789 ms, tools/rowlen_lab.cu).  0 = plain windows;
+                     -1 = every log2 length class in turn, longest first.
     sell_sort:       "auto" | "on" | "off" -- order each slice's rows by length (lanes
                      active in a round form a prefix, so fetched sectors are full):
                      config 4's A' reads 3.55 instead of 3.85 GB per primal step (period
@@ -127,6 +133,7 @@ class GpuOptions:
     row_order: str = "auto"
     row_order_window: int = 65536
     row_order_max_tail: float = 0.15
+    row_order_first: int = 32
     check_dot: bool = True
 
 
@@ -277,7 +284,8 @@ class DeviceLp:
                     lanes0 = int(opts.a_lanes) or auto_lanes(nnz, m)
                     H0 = int(opts.heavy_threshold) or heavy_threshold(lanes0)
                     if _want_row_order(torch, opts, self.a_ptr, nnz, H0):
-                        self._renumber_rows(torch, dev, m, nnz, int(opts.row_order_window))
+                        self._renumber_rows(torch, dev, m, nnz, int(opts.row_order_window),
+                                            int(opts.row_order_first))
                 sptr = self.stream.cuda_stream
                 tmp = None
                 if At is None:
@@ -401,7 +409,7 @@ class DeviceLp:
         self._fin = weakref.finalize(self, self.lib.pdhg_ctx_destroy, ctx)
         self._scal = (C.c_double * (2 * N.NQ))()
 
-    def _renumber_rows(self, torch, dev, m: int, nnz: int, window: int):
+    def _renumber_rows(self, torch, dev, m: int, nnz: int, window: int, first: int = 0):
         """Renumber A's rows by decreasing length inside windows of `window` rows
         (stable): new row r = old row row_perm[r].  A, b are permuted on the
         device; y-space results are mapped back through row_inv."""
@@ -409,6 +417,18 @@ class DeviceLp:
         top = int(lens.max()) + 1
         win = torch.arange(m, device=dev, dtype=torch.int64) // max(1, window)
         key = win * (top + 1) + (top - lens)
+        first = int(first)
+        if first != 0:
+            # long rows first: their slices start at the head of the grid instead
+            # of at every window's head, where the last windows' long slices
+            # were still running after everything else had drained (config 4's
+            # dual step: 0.889 -> 0.789-0.795 ms, tools/rowlen_lab.cu)
+            if first > 0:
+                group = (lens <= first).to(torch.int64)            # 0: longer than `first`
+            else:                                                  # log2 length classes, longest first
+                cls = torch.floor(torch.log2(lens.clamp(min=1).to(torch.float64))).to(torch.int64)
+                group = int(cls.max()) - cls
+            key = group * (int(win.max()) + 1) * (top + 1) + key
         perm = torch.sort(key, stable=True).indices
         new_ptr = torch.zeros(m + 1, dtype=torch.int32, device=dev)
         new_ptr[1:] = torch.cumsum(lens[perm], 0).to(torch.int32)

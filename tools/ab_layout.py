@@ -22,6 +22,16 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 VARIANTS = {
     "natural": dict(row_order="natural"),
     "rows": dict(row_order="length"),
+    "rows_plain": dict(row_order="length", row_order_first=0),
+    "rows_first64": dict(row_order="length", row_order_first=64),
+    "rows_first32": dict(row_order="length", row_order_first=32),
+    "rows_classes": dict(row_order="length", row_order_first=-1),
+    "rows_first48": dict(row_order="length", row_order_first=48),
+    "rows_first24": dict(row_order="length", row_order_first=24),
+    # experiment build only (PDHG_B200_LIB=tools/_libs/libpdhg_b200_exp.so): L2 persisting windows
+    "rows_l2x": dict(row_order="length", l2_persist=2),
+    "rows_l2y": dict(row_order="length", l2_persist=1),
+    "rows_l2xy": dict(row_order="length", l2_persist=3),
     "rows_csr": dict(row_order="length", sell="off"),
     "csr": dict(row_order="natural", sell="off"),
 }
@@ -50,6 +60,8 @@ def main():
         d.run_period(64, 0, devs[nm][1], devs[nm][1], 0.0)   # capture the graph
     torch.cuda.synchronize()
     res = {nm: [] for nm in names}
+    res_chk = {nm: [] for nm in names}
+    from paper_2603_03150_b200 import _native as N
     clocks = []
     for r in range(args.rounds):
         for nm in names:
@@ -61,10 +73,17 @@ def main():
             e1.record(d.stream)
             torch.cuda.synchronize()
             res[nm].append(e0.elapsed_time(e1) / (3 * 64))
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(d.stream)
+            d.check(N.PT_CUR, N.PT_AVG)
+            c1.record(d.stream)
+            torch.cuda.synchronize()
+            res_chk[nm].append(c0.elapsed_time(c1))
         q = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader"],
                            capture_output=True, text=True).stdout.strip()
         clocks.append(q)
-    out = {nm: {"ms_per_iter_median": statistics.median(v), "all": v} for nm, v in res.items()}
+    out = {nm: {"ms_per_iter_median": statistics.median(v), "check_ms_median": statistics.median(res_chk[nm]),
+                "all": v} for nm, v in res.items()}
     out["clocks"] = clocks
     print(json.dumps(out, indent=1))
 
