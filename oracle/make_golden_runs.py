@@ -11,8 +11,10 @@ objectives at full size without the reference:
     ... python oracle/make_golden_runs.py config4 1.0 nolimit
 
 The third argument ``nolimit`` passes ``time_limit_s=1e9`` (the reference's
-default of 10,000 s, pdhg.py:36, stops config 2 at ~48k and config 4 at ~7k
-iterations on one core) and writes ``run_<config>_s<scale>_nolimit.json``.
+default of 10,000 s, pdhg.py:36, stops config 2 at ~48k and config 4 at ~3.5k
+iterations on one core) and writes ``run_<config>_s<scale>_nolimit.json``;
+``tl=SECONDS`` passes that limit and writes ``run_<config>_s<scale>_tl<SECONDS>.json``
+(config 4 needs ~2.8 s per iteration on one core: ~10 h to 1e-4).
 """
 
 from __future__ import annotations
@@ -33,7 +35,7 @@ import hybridlp  # noqa: E402
 from paper_2603_03150_b200.instances import config1_general, config3_general  # noqa: E402
 
 
-def main(which: str, scale: float = 1.0, nolimit: bool = False):
+def main(which: str, scale: float = 1.0, limit: str = ""):
     t0 = time.perf_counter()
     if which in ("config2", "config4"):   # built directly in standard form
         from paper_2603_03150_b200 import instances
@@ -57,7 +59,13 @@ def main(which: str, scale: float = 1.0, nolimit: bool = False):
         return orig_score(pp, x, y)
 
     hybridlp.pdhg._score = score
-    params = hybridlp.PdhgParams(eps_rel=1e-4, time_limit_s=1e9) if nolimit else hybridlp.PdhgParams(eps_rel=1e-4)
+    if limit == "nolimit":
+        params, suffix = hybridlp.PdhgParams(eps_rel=1e-4, time_limit_s=1e9), "_nolimit"
+    elif limit.startswith("tl="):
+        tl = float(limit[3:])
+        params, suffix = hybridlp.PdhgParams(eps_rel=1e-4, time_limit_s=tl), f"_tl{tl:g}"
+    else:
+        params, suffix = hybridlp.PdhgParams(eps_rel=1e-4), ""
     pt, st = hybridlp.run_pdhg(s, params)
     t3 = time.perf_counter()
     term = st.termination
@@ -72,11 +80,10 @@ def main(which: str, scale: float = 1.0, nolimit: bool = False):
         "numpy": np.__version__, "threads": "OPENBLAS_NUM_THREADS=1",
         "time_limit_s": params.time_limit_s,
     }
-    path = ROOT / "tests" / "golden" / f"run_{which}_s{scale:g}{'_nolimit' if nolimit else ''}.json"
+    path = ROOT / "tests" / "golden" / f"run_{which}_s{scale:g}{suffix}.json"
     path.write_text(json.dumps(out, indent=1))
     print(json.dumps(out))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 1.0,
-         len(sys.argv) > 3 and sys.argv[3] == "nolimit")
+    main(sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 1.0, sys.argv[3] if len(sys.argv) > 3 else "")

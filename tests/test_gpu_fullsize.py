@@ -111,11 +111,13 @@ def test_full_size_against_reference(eng, name):
 def _run_goldens(name):
     """The real reference's full runs of this instance: with its default
     time limit (10,000 s, pdhg.py:36 -- config 2 stops on it at 48,381
-    iterations on one core) and, when generated, without it (``_nolimit``)."""
+    iterations on one core), with a longer one (``_tl<seconds>``) and, when
+    generated, without one (``_nolimit``)."""
     import json
 
-    out = [json.loads(f.read_text()) for f in (GOLDEN / f"run_{name}_s1.json", GOLDEN / f"run_{name}_s1_nolimit.json")
-           if f.exists()]
+    files = [GOLDEN / f"run_{name}_s1.json", GOLDEN / f"run_{name}_s1_nolimit.json",
+             *sorted(GOLDEN.glob(f"run_{name}_s1_tl*.json"))]
+    out = [json.loads(f.read_text()) for f in files if f.exists()]
     if not out:
         pytest.skip(f"run_{name}_s1*.json not generated (oracle/make_golden_runs.py {name})")
     return out
