@@ -441,6 +441,32 @@ int main(int argc, char** argv) {
   run_g4(k_g4<4, 8, 4>, tm4, 4, 8, 4, "g4_32");
   (void)tm2;  // 16-byte rows: the 64-byte smem destinations violate TMA's 128-byte alignment
   }
+  // sustained (power-capped) interleaved A/B: blocks of 200 launches of each,
+  // 8 rounds, after a 2 s warm-up at full load
+  if (argc > 6) {
+    auto blk = [&](auto f, int k) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a);
+      for (int i = 0; i < k; ++i) f();
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      return ms / k;
+    };
+    auto f0 = [&] { k_ldg<10><<<gw, 256>>>(m, W, col, val, x, y1); };
+    auto f1 = [&] { k_ldg128<3><<<gw, 256>>>(m, W, reinterpret_cast<int4*>(colq), valp, x, y1); };
+    auto f2 = [&] { k_ldg128<2><<<gw, 256>>>(m, W, reinterpret_cast<int4*>(colq), valp, x, y1); };
+    blk(f0, 2500);
+    for (int r = 0; r < 8; ++r) {
+      const float a0 = blk(f0, 200), a1 = blk(f1, 200), a2 = blk(f2, 200);
+      printf("{\"sustained_round\": %d, \"ldg_u10_ms\": %.4f, \"ldg128_q3_ms\": %.4f, \"ldg128_q2_ms\": %.4f}\n", r, a0,
+             a1, a2);
+      fflush(stdout);
+    }
+  }
   // ldg again (clock drift check)
   t = time_it([&] { k_ldg<10><<<gw, 256>>>(m, W, col, val, x, y1); }, reps);
   report("ldg_u10_again", t, true);
