@@ -29,7 +29,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from . import hostio
+from . import hostio, streams
 from .lp_types import resolve
 
 _WEIGHT_CLIP = (1e-4, 1e4)  # pdhg.py:28
@@ -212,6 +212,17 @@ def _want_row_order(torch, opts, ptr, nnz: int, H: int) -> bool:
     return _slice_pad(torch, ptr, H) > opts.sell_max_pad
 
 
+def _close_ctx(lib, ctx, stream) -> None:
+    """DeviceLp finalizer: destroy the context; a pooled stream is drained
+    (its queued work may still read this layout, whose blocks are about to go
+    back to the allocator) and returned to the pool."""
+    if stream is not None:
+        stream.synchronize()
+    lib.pdhg_ctx_destroy(ctx)
+    if stream is not None:
+        streams.release(stream)
+
+
 def _as_csr(A):
     import scipy.sparse as sp
 
@@ -266,7 +277,10 @@ class DeviceLp:
         self.at_nnz = int(At.nnz) if At is not None else nnz
         self.m_full, self.n_full, self.y_off, self.x_off = m_full, n_full, y_off, x_off
         with torch.cuda.device(dev):
-            self.stream = stream if stream is not None else torch.cuda.Stream(dev)
+            # pooled: the next context on this device reuses the stream and so the
+            # caching allocator's blocks of this one (paper_2603_03150_b200/streams.py)
+            self.stream = stream if stream is not None else streams.acquire(dev)
+            own_stream = stream is None
             with torch.cuda.stream(self.stream):
                 t = lambda a, dt: hostio.h2d(a, dt, dev)
                 if device_arrays is not None:
@@ -280,12 +294,16 @@ class DeviceLp:
                 self.stream.synchronize()
                 t_up = time.monotonic()
                 self.row_perm = self.row_inv = None
+                t_rs = t_rn = t_up
                 if shard is None and m > 1:
                     lanes0 = int(opts.a_lanes) or auto_lanes(nnz, m)
                     H0 = int(opts.heavy_threshold) or heavy_threshold(lanes0)
-                    if _want_row_order(torch, opts, self.a_ptr, nnz, H0):
+                    want = _want_row_order(torch, opts, self.a_ptr, nnz, H0)
+                    t_rs = t_rn = time.monotonic()
+                    if want:
                         self._renumber_rows(torch, dev, m, nnz, int(opts.row_order_window),
                                             int(opts.row_order_first))
+                        t_rn = time.monotonic()
                 sptr = self.stream.cuda_stream
                 tmp = None
                 if At is None:
@@ -304,6 +322,7 @@ class DeviceLp:
                     self.at_val = t(At.data, np.float64)
                 self.stream.synchronize()
                 t_tr = time.monotonic()
+                t_tr0 = t_rn
                 self.a_lanes = int(opts.a_lanes) or auto_lanes(nnz, m)
                 self.at_lanes = int(opts.at_lanes) or auto_lanes(self.at_nnz, n)
                 H = int(opts.heavy_threshold) or heavy_threshold(self.a_lanes)
@@ -313,6 +332,7 @@ class DeviceLp:
                 self.at_heavy = torch.nonzero((self.at_ptr[1:] - self.at_ptr[:-1]) > Ht).flatten().to(torch.int32)
                 self.a_medium, la = _medium_list(torch, self.a_ptr, self.a_lanes, H, opts.medium_per_lane)
                 self.at_medium, lt = _medium_list(torch, self.at_ptr, self.at_lanes, Ht, opts.medium_per_lane)
+                t_lists = time.monotonic()
                 self.light_max = (la, lt)
                 self.psr_info = {}
                 self._psr = {}
@@ -404,9 +424,10 @@ class DeviceLp:
                               and self.lib.pdhg_check_dot_enable(ctx, 1) == 0)
         t_end = time.monotonic()
         self.timings = {"upload_s": t_up - t_start, "layout_s": t_end - t_up,
-                        "layout_detail": {"transpose_s": t_tr - t_up, "psr_sell_s": t_sell - t_tr,
-                                          "ctx_s": t_end - t_sell}}
-        self._fin = weakref.finalize(self, self.lib.pdhg_ctx_destroy, ctx)
+                        "layout_detail": {"row_order_choice_s": t_rs - t_up, "renumber_s": t_rn - t_rs,
+                                          "transpose_s": t_tr - t_tr0, "row_lists_s": t_lists - t_tr,
+                                          "psr_sell_s": t_sell - t_lists, "ctx_s": t_end - t_sell}}
+        self._fin = weakref.finalize(self, _close_ctx, self.lib, ctx, self.stream if own_stream else None)
         self._scal = (C.c_double * (2 * N.NQ))()
 
     def _renumber_rows(self, torch, dev, m: int, nnz: int, window: int, first: int = 0):

@@ -29,7 +29,7 @@ import weakref
 import numpy as np
 
 from . import _native as N
-from . import hostio
+from . import hostio, streams
 from .lp_types import resolve
 
 _lock = threading.Lock()
@@ -123,8 +123,7 @@ def unscale_point(s, pt_scaled, *, gpu=None):
     torch, dev = _torch_dev(gpu)
     lib = N.load()
     n, m = np.asarray(pt_scaled.x).size, np.asarray(pt_scaled.y).size
-    stream = torch.cuda.Stream(dev)
-    with torch.cuda.device(dev), torch.cuda.stream(stream):
+    with streams.Borrowed(dev) as stream, torch.cuda.device(dev), torch.cuda.stream(stream):
         rs, cs = _up(torch, dev, s.row_scale), _up(torch, dev, s.col_scale)
         xs, ys, zs = (_up(torch, dev, v) for v in (pt_scaled.x, pt_scaled.y, pt_scaled.z))
         x, y, z = (torch.empty(max(k, 1), dtype=torch.float64, device=dev) for k in (n, m, n))
@@ -143,8 +142,7 @@ def restrict_point(g, fmap, pt, *, gpu=None):
     torch, dev = _torch_dev(gpu)
     lib = N.load()
     n, m = fmap.n_general, fmap.m_general
-    stream = torch.cuda.Stream(dev)
-    with torch.cuda.device(dev), torch.cuda.stream(stream):
+    with streams.Borrowed(dev) as stream, torch.cuda.device(dev), torch.cuda.stream(stream):
         G = _dev_csr(g, torch, dev, stream)
         xs = _up(torch, dev, pt.x)
         pos, neg = _up(torch, dev, fmap.pos_col, np.int32), _up(torch, dev, fmap.neg_col, np.int32)
@@ -204,8 +202,7 @@ def lift_point(g, p, fmap, x, y, *, gpu=None):
             raise T.InvalidModelError(f"expected array of length {k}, got {v.size}")
     torch, dev = _torch_dev(gpu)
     lib = N.load()
-    stream = torch.cuda.Stream(dev)
-    with torch.cuda.device(dev), torch.cuda.stream(stream):
+    with streams.Borrowed(dev) as stream, torch.cuda.device(dev), torch.cuda.stream(stream):
         G, P = _dev_csr(g, torch, dev, stream), _dev_csr(p, torch, dev, stream)
         xs, ys, zs, _, _ = _lift_device(lib, torch, dev, stream, g, G, P, p, fmap, x, y)
         ns, ms = fmap.n_std, fmap.m_std
@@ -240,8 +237,7 @@ def violation_summary(p, pt, *, gpu=None):
             f"point dims ({x.size}, {y.size}, {z.size}) do not match model ({n}, {m})")
     torch, dev = _torch_dev(gpu)
     lib = N.load()
-    stream = torch.cuda.Stream(dev)
-    with torch.cuda.device(dev), torch.cuda.stream(stream):
+    with streams.Borrowed(dev) as stream, torch.cuda.device(dev), torch.cuda.stream(stream):
         P = _dev_csr(p, torch, dev, stream)
         u = lambda v: _up(torch, dev, v if v.size else np.zeros(1))
         return _violation(T, lib, stream, P, u(np.asarray(p.b, dtype=float)),
@@ -262,8 +258,7 @@ def evaluate_general_point(g, x, y, *, gpu=None):
             raise T.InvalidModelError(f"expected array of length {k}, got {v.size}")
     torch, dev = _torch_dev(gpu)
     lib = N.load()
-    stream = torch.cuda.Stream(dev)
-    with torch.cuda.device(dev), torch.cuda.stream(stream):
+    with streams.Borrowed(dev) as stream, torch.cuda.device(dev), torch.cuda.stream(stream):
         G, P = _dev_csr(g, torch, dev, stream), _dev_csr(p, torch, dev, stream)
         xs, ys, zs, b, c = _lift_device(lib, torch, dev, stream, g, G, P, p, fmap, x, y)
         return _violation(T, lib, stream, P, b, c, xs, ys, zs)
@@ -305,8 +300,7 @@ def mu_target(x, z, n: int, mu_min: float, *, gpu=None) -> float:
         raise T.InvalidModelError("x and z must both have length n >= 1")
     torch, dev = _torch_dev(gpu)
     lib = N.load()
-    stream = torch.cuda.Stream(dev)
-    with torch.cuda.device(dev), torch.cuda.stream(stream):
+    with streams.Borrowed(dev) as stream, torch.cuda.device(dev), torch.cuda.stream(stream):
         a, b = _up(torch, dev, x.ravel()), _up(torch, dev, z.ravel())
         tb = lib.pdhg_dot_tmp_bytes()
         tmp = torch.empty(tb, dtype=torch.uint8, device=dev)
@@ -323,8 +317,7 @@ def center_toward_target(x, z, mu: float, alpha_min: float, delta_max: float, *,
     torch, dev = _torch_dev(gpu)
     lib = N.load()
     n = x.size
-    stream = torch.cuda.Stream(dev)
-    with torch.cuda.device(dev), torch.cuda.stream(stream):
+    with streams.Borrowed(dev) as stream, torch.cuda.device(dev), torch.cuda.stream(stream):
         xd, zd = _up(torch, dev, x if n else np.zeros(1)), _up(torch, dev, z if n else np.zeros(1))
         xo, zo = torch.empty_like(xd), torch.empty_like(zd)
         N.check(lib.pdhg_center_toward_target(n, xd.data_ptr(), zd.data_ptr(), float(mu), float(alpha_min),

@@ -19,7 +19,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from . import _native as N
-from . import hostio
+from . import hostio, streams
 
 
 last_timings: dict = {}   # phase -> seconds of the latest ruiz_equilibrate call
@@ -79,8 +79,7 @@ def ruiz_equilibrate(p, max_iters: int = 20, tol: float = 1e-2, *, gpu=None, reg
     lib = N.load()
     opts = gpu or GpuOptions()
     dev = torch.device("cuda", torch.cuda.current_device() if opts.device is None else opts.device)
-    stream = torch.cuda.Stream(dev)
-    with torch.cuda.device(dev), torch.cuda.stream(stream):
+    with streams.Borrowed(dev) as stream, torch.cuda.device(dev), torch.cuda.stream(stream):
         from .stdform import device_csr
 
         t = time.perf_counter()
@@ -138,8 +137,11 @@ def ruiz_equilibrate(p, max_iters: int = 20, tol: float = 1e-2, *, gpu=None, reg
     tm["assemble_s"] = time.perf_counter() - t
     t = time.perf_counter()
     if register_layout:
+        # its own pooled stream: the arrays' producer work is complete (the
+        # downloads above synchronised the Ruiz stream), and the context drains
+        # its stream before the arrays go back to the allocator
         lay = DeviceLp(scaled.A, scaled.b, scaled.c, opts,
-                       device_arrays=None if dropped else (ptr, col, val), stream=stream)
+                       device_arrays=None if dropped else (ptr, col, val))
         _cache_register(scaled, lay, opts)
         torch.cuda.synchronize(dev)
     tm["layout_s"] = time.perf_counter() - t
