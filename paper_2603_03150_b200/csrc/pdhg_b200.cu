@@ -614,16 +614,41 @@ __device__ __forceinline__ double dual_epi(int i, double ax, const double* __res
 }
 
 // Same epilogues with the row's operands already in registers.
+// Epilogue cache policy: the operands a step reads once and the outputs the
+// next half step does not gather (c, x, x-bar loads and x, x-bar stores of the
+// primal step; y-bar stores of the dual step) are streamed evict-first, so L2
+// keeps the vector the next half step gathers (xe written by the primal step,
+// y by the dual step).  Sliced-ELL steps, config 4, power-capped: 1.7556 vs
+// 1.7591 ms per iteration, 3 alternating processes each (tools/lib_ab.py,
+// profiles/r02_epi_hint_ab.log).  0 = plain loads and stores.
+#ifndef PDHG_EPI_HINT
+#define PDHG_EPI_HINT 1
+#endif
+__device__ __forceinline__ double epi_ld(const double* p) {
+#if PDHG_EPI_HINT
+  return __ldcs(p);
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ void epi_st(double* p, double v) {
+#if PDHG_EPI_HINT
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
 __device__ __forceinline__ double primal_epi_pre(int j, double aty, double cj, double xj, double xb,
                                                double* __restrict__ x, double* __restrict__ xe,
                                                double* __restrict__ xbar, double tau_w, double w,
                                                long long iter, StepParams* P) {
   const double g = __dsub_rn(cj, aty);
   const double xn = np_max0(__dsub_rn(xj, __dmul_rn(tau_w, g)));
-  x[j] = xn;
+  epi_st(x + j, xn);
   const double xev = __dsub_rn(__dmul_rn(2.0, xn), xj);
   xe[j] = xev;
-  xbar[j] = __dadd_rn(xb, __ddiv_rn(__dsub_rn(xn, xb), w));
+  epi_st(xbar + j, __dadd_rn(xb, __ddiv_rn(__dsub_rn(xn, xb), w)));
   if (!finite(xn)) fail_at(P, iter);
   return xev;
 }
@@ -633,7 +658,7 @@ __device__ __forceinline__ double dual_epi_pre(int i, double ax, double bi, doub
                                              double sigma_w, double w, long long iter, StepParams* P) {
   const double yn = __dadd_rn(yi, __dmul_rn(sigma_w, __dsub_rn(bi, ax)));
   y[i] = yn;
-  ybar[i] = __dadd_rn(yb, __ddiv_rn(__dsub_rn(yn, yb), w));
+  epi_st(ybar + i, __dadd_rn(yb, __ddiv_rn(__dsub_rn(yn, yb), w)));
   if (!finite(yn)) fail_at(P, iter);
   return yn;
 }
@@ -863,9 +888,9 @@ __global__ void __launch_bounds__(kBlock, (sell_min_blocks<PRIMAL, kU>())) k_ste
   const double acc = sell_row_dot<kU>(S, sl, lane, len, a.gather);
 
   if (PDHG_SELL_LATE && ok) {
-    o1 = a.cb[rl];
-    o2 = a.x[rl];
-    o3 = a.xbar[rl];
+    o1 = epi_ld(a.cb + rl);
+    o2 = epi_ld(a.x + rl);
+    o3 = epi_ld(a.xbar + rl);
   }
   if (ok) {
     const int row = (int)rl;
