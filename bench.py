@@ -556,6 +556,10 @@ def run_ours(args):
                 # 40/80 MB vector is a 32 B L2 sector, so L1TEX / L2-slice throughput, not DRAM,
                 # caps the step kernels
                 "binding_units_pct_ncu": units,
+                # the same kernel's frac at the clock ncu ran it (no power cap; informational --
+                # `frac` above is the in-sequence, power-capped one this run measured)
+                "frac_at_ncu_clock": (ab[top] / (units["time_us"] * 1e-6) / 1e9 / peak
+                                      if units and units.get("time_us") else None),
                 "iteration_gbs": (ab["iter"] + ab["check"] / CHECK_EVERY) / (iter_ms * 1e-3) / 1e9}
     # the timing leg's device memory goes back to torch's caching allocator
     # (not to the driver): the e2e call below reuses it, as repeated calls in
