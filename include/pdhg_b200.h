@@ -178,8 +178,9 @@ int pdhg_ctx_destroy(pdhg_ctx* ctx);
  * Replaces scipy csr_matvec behind `p.A @ x` and `p.at_y(y)` (lp_core.py:140-142). */
 int pdhg_spmv(pdhg_ctx* ctx, int transpose, const double* in, double* out);
 
-/* Power iteration on A'A (estimate_opnorm, pdhg.py:80-109).  v0 (host, n)
- * is the caller's normalised start vector (numpy default_rng(seed), pdhg.py:89-91). */
+/* Power iteration on A'A (estimate_opnorm, pdhg.py:80-109).  v0 (n doubles,
+ * host or device memory) is the caller's normalised start vector (numpy
+ * default_rng(seed), pdhg.py:89-91), in the context's column order. */
 int pdhg_opnorm(pdhg_ctx* ctx, const double* v0_host, double tol, int32_t max_iters,
                 double* lam_out, int32_t* iters_out);
 

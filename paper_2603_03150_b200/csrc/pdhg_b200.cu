@@ -2339,7 +2339,9 @@ int pdhg_opnorm(pdhg_ctx* c, const double* v0_host, double tol, int32_t max_iter
   if (c->mf != c->prob.m || c->nf != c->prob.n)
     return fail(PDHG_ERR_STATE, "pdhg_opnorm is single-shard; sharded hosts drive the power iteration");
   const int n = c->prob.n;
-  CUDA_TRY(cudaMemcpyAsync(c->tn1, v0_host, (size_t)n * 8, cudaMemcpyHostToDevice, c->stream));
+  // host or device pointer (UVA): the engine hands a device copy already in
+  // the context's (renumbered) column order
+  CUDA_TRY(cudaMemcpyAsync(c->tn1, v0_host, (size_t)n * 8, cudaMemcpyDefault, c->stream));
   double lam = 0.0;
   int it = 0;
   int rc;

@@ -81,6 +81,15 @@ class GpuOptions:
                      sell_max_pad and at most row_order_max_tail of whose entries sit
                      in rows longer than 4x the mean (lane-per-row slices run a long
                      row on one lane: config 2's power-law rows stay on CSR-vector).
+    col_order:       "auto" | "length" | "natural" -- the same for A's columns (the
+                     variables: c, x, z; the rows of A'), so the primal step's sliced
+                     ELL of A' runs without padding (config 4's A': 1.49x slice-sorted
+                     in natural order; -4.4 % per primal SpMV at the power cap,
+                     tools/primal_pad_lab.cu).  A's entries keep their order inside
+                     each row (only their column labels change) and A' rows keep
+                     theirs, so every step's sums are the unrenumbered ones; x and z
+                     are mapped back on download.  auto: whenever row_order applies.
+    col_order_first: columns longer than this come first (as row_order_first).
     row_order_first: with row_order: rows longer than this many entries come first
                      (window by window, longest first), then the rest -- the long
                      slices start at the head of the grid, so no window's long slices
@@ -134,6 +143,8 @@ class GpuOptions:
     row_order_window: int = 65536
     row_order_max_tail: float = 0.15
     row_order_first: int = 32
+    col_order: str = "auto"
+    col_order_first: int = 24
     check_dot: bool = True
 
 
@@ -210,6 +221,29 @@ def _want_row_order(torch, opts, ptr, nnz: int, H: int) -> bool:
     if tail > opts.row_order_max_tail:
         return False
     return _slice_pad(torch, ptr, H) > opts.sell_max_pad
+
+
+def _length_order(torch, dev, lens, window: int, first: int):
+    """New -> old index order of a row renumbering: decreasing length inside
+    windows of `window` rows (stable); with first > 0 the rows longer than
+    `first` come first (window by window), then the rest -- their slices start
+    at the head of the grid instead of at every window's head, where the last
+    windows' long slices were still running after everything else had drained
+    (config 4's dual step: 0.889 -> 0.789-0.795 ms, tools/rowlen_lab.cu);
+    first < 0: every log2 length class in turn, longest first."""
+    k = lens.numel()
+    top = int(lens.max()) + 1 if k else 1
+    win = torch.arange(k, device=dev, dtype=torch.int64) // max(1, window)
+    key = win * (top + 1) + (top - lens)
+    first = int(first)
+    if first != 0 and k:
+        if first > 0:
+            group = (lens <= first).to(torch.int64)            # 0: longer than `first`
+        else:
+            cls = torch.floor(torch.log2(lens.clamp(min=1).to(torch.float64))).to(torch.int64)
+            group = int(cls.max()) - cls
+        key = group * (int(win.max()) + 1) * (top + 1) + key
+    return torch.sort(key, stable=True).indices
 
 
 def _close_ctx(lib, ctx, stream) -> None:
@@ -294,6 +328,8 @@ class DeviceLp:
                 self.stream.synchronize()
                 t_up = time.monotonic()
                 self.row_perm = self.row_inv = None
+                self.col_perm = self.col_inv = None
+                self._col_perm_host = None
                 t_rs = t_rn = t_up
                 if shard is None and m > 1:
                     lanes0 = int(opts.a_lanes) or auto_lanes(nnz, m)
@@ -303,7 +339,10 @@ class DeviceLp:
                     if want:
                         self._renumber_rows(torch, dev, m, nnz, int(opts.row_order_window),
                                             int(opts.row_order_first))
-                        t_rn = time.monotonic()
+                    if opts.col_order == "length" or (opts.col_order == "auto" and want):
+                        self._renumber_cols(torch, dev, n, nnz, int(opts.row_order_window),
+                                            int(opts.col_order_first))
+                    t_rn = time.monotonic()
                 sptr = self.stream.cuda_stream
                 tmp = None
                 if At is None:
@@ -435,22 +474,7 @@ class DeviceLp:
         (stable): new row r = old row row_perm[r].  A, b are permuted on the
         device; y-space results are mapped back through row_inv."""
         lens = (self.a_ptr[1:] - self.a_ptr[:-1]).to(torch.int64)
-        top = int(lens.max()) + 1
-        win = torch.arange(m, device=dev, dtype=torch.int64) // max(1, window)
-        key = win * (top + 1) + (top - lens)
-        first = int(first)
-        if first != 0:
-            # long rows first: their slices start at the head of the grid instead
-            # of at every window's head, where the last windows' long slices
-            # were still running after everything else had drained (config 4's
-            # dual step: 0.889 -> 0.789-0.795 ms, tools/rowlen_lab.cu)
-            if first > 0:
-                group = (lens <= first).to(torch.int64)            # 0: longer than `first`
-            else:                                                  # log2 length classes, longest first
-                cls = torch.floor(torch.log2(lens.clamp(min=1).to(torch.float64))).to(torch.int64)
-                group = int(cls.max()) - cls
-            key = group * (int(win.max()) + 1) * (top + 1) + key
-        perm = torch.sort(key, stable=True).indices
+        perm = _length_order(torch, dev, lens, window, first)
         new_ptr = torch.zeros(m + 1, dtype=torch.int32, device=dev)
         new_ptr[1:] = torch.cumsum(lens[perm], 0).to(torch.int32)
         new_col = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
@@ -466,6 +490,25 @@ class DeviceLp:
         self.a_ptr, self.a_col, self.a_val = new_ptr, new_col, new_val
         self.row_perm, self.row_inv = perm, inv
         self._row_perm_host = None      # host copy made on first use (spmv gates only)
+
+    def _renumber_cols(self, torch, dev, n: int, nnz: int, window: int, first: int = 0):
+        """Renumber A's columns (the rows of A', built next by the transpose) by
+        decreasing length, as _renumber_rows does for A's rows: new column j =
+        old column col_perm[j].  A's entries are relabelled in place of order
+        (each row keeps its entry sequence), c is permuted; x-space results
+        are mapped back through col_inv."""
+        col = self.a_col[:nnz]
+        lens = torch.bincount(col, minlength=n).to(torch.int64)
+        perm = _length_order(torch, dev, lens, window, first)
+        inv = torch.empty_like(perm)
+        inv[perm] = torch.arange(n, device=dev, dtype=torch.int64)
+        inv32 = inv.to(torch.int32)
+        new_col = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        torch.index_select(inv32, 0, col, out=new_col[:nnz])
+        self.c = self.c[perm].contiguous()
+        self.stream.synchronize()
+        self.a_col = new_col
+        self.col_perm, self.col_inv = perm, inv
 
     def _build_sell(self, torch, dev, key, rows, nnz, ptr, col, val, H, opts):
         """Plan + fill the sliced-ELL layout of one operator on the device (or None)."""
@@ -563,8 +606,16 @@ class DeviceLp:
     def opnorm(self, v0: np.ndarray, tol: float = 1e-4, max_iters: int = 100) -> float:
         v0 = np.ascontiguousarray(v0, dtype=np.float64)
         lam, its = C.c_double(), C.c_int32()
-        N.check(self.lib.pdhg_opnorm(self.ctx, v0.ctypes.data, tol, max_iters,
-                                     C.byref(lam), C.byref(its)))
+        if self.col_perm is None:
+            N.check(self.lib.pdhg_opnorm(self.ctx, v0.ctypes.data, tol, max_iters,
+                                         C.byref(lam), C.byref(its)))
+        else:   # renumbered columns: the start vector permuted on the device
+            torch = _torch()
+            with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+                vd = hostio.h2d(v0, np.float64, self.device).index_select(0, self.col_perm)
+                N.check(self.lib.pdhg_opnorm(self.ctx, vd.data_ptr(), tol, max_iters,
+                                             C.byref(lam), C.byref(its)))
+        self.opnorm_iterations = int(its.value)
         return float(lam.value)
 
     def reset(self):
@@ -614,13 +665,29 @@ class DeviceLp:
         base = self.ws.data_ptr()
         view = lambda ptr, k: self.ws[ptr - base:ptr - base + 8 * k].view(torch.float64)
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
-            x = hostio.d2h(view(px.value, self.n_full))
+            xv = view(px.value, self.n_full)
+            if self.col_perm is not None:     # renumbered variables -> the caller's order
+                xv = xv.index_select(0, self.col_inv)
+            x = hostio.d2h(xv)
             yv = view(py.value, self.m_full)
             if self.row_perm is not None:     # renumbered constraints -> the caller's order
                 yv = yv.index_select(0, self.row_inv)
             y = hostio.d2h(yv)
-            z = hostio.d2h(view(pz.value, self.n_full)) if want_z else None
+            z = None
+            if want_z:
+                zv = view(pz.value, self.n_full)
+                if self.col_perm is not None:
+                    zv = zv.index_select(0, self.col_inv)
+                z = hostio.d2h(zv)
         return x, y, z
+
+    def _to_cols(self, v: np.ndarray) -> np.ndarray:
+        """An x-space host vector in the context's (renumbered) column order."""
+        if self.col_perm is None:
+            return v
+        if self._col_perm_host is None:
+            self._col_perm_host = self.col_perm.cpu().numpy()
+        return v[self._col_perm_host]
 
     def spmv(self, v: np.ndarray, transpose: bool = False) -> np.ndarray:
         """A @ v or A' @ v through the device SpMV (the 1e-12 parity gate)."""
@@ -630,12 +697,16 @@ class DeviceLp:
             if self._row_perm_host is None:
                 self._row_perm_host = self.row_perm.cpu().numpy()
             v = np.ascontiguousarray(v[self._row_perm_host])
+        if not transpose:
+            v = np.ascontiguousarray(self._to_cols(v))
         with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
             vin = torch.from_numpy(v).to(self.device)
             out = torch.empty(self.n if transpose else self.m, dtype=torch.float64, device=self.device)
             N.check(self.lib.pdhg_spmv(self.ctx, 1 if transpose else 0, vin.data_ptr(), out.data_ptr()))
             if not transpose and self.row_perm is not None:
                 out = out.index_select(0, self.row_inv)
+            if transpose and self.col_perm is not None:
+                out = out.index_select(0, self.col_inv)
             self.stream.synchronize()
             return out.cpu().numpy()
 
@@ -908,6 +979,8 @@ def _run(T, dev: DeviceLp, p, params, seed, opts, t0, v0_future=None):
         opnorm = dev.opnorm(v, tol=1e-4, max_iters=100)
     step = 1.0 / (1.05 * opnorm)                               # pdhg.py:119
     tm["opnorm_s"] = time.monotonic() - t_op
+    if getattr(dev, "opnorm_iterations", None) is not None and opts.opnorm is None:
+        tm["opnorm_iterations"] = dev.opnorm_iterations
     t_it = time.monotonic()
     dev.reset()
     tau = sigma = step

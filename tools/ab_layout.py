@@ -23,6 +23,7 @@ VARIANTS = {
     "natural": dict(row_order="natural"),
     "rows": dict(row_order="length"),
     "rows_plain": dict(row_order="length", row_order_first=0),
+    "rows_nocol": dict(row_order="length", col_order="natural"),
     "rows_first64": dict(row_order="length", row_order_first=64),
     "rows_first32": dict(row_order="length", row_order_first=32),
     "rows_classes": dict(row_order="length", row_order_first=-1),
