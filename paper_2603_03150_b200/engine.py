@@ -144,7 +144,7 @@ class GpuOptions:
     row_order_max_tail: float = 0.15
     row_order_first: int = 32
     col_order: str = "auto"
-    col_order_first: int = 24
+    col_order_first: int = 32
     check_dot: bool = True
 
 
@@ -534,8 +534,8 @@ class DeviceLp:
         sval = torch.empty(max(slots.value, 1), dtype=torch.float64, device=dev)
         perm = inv = None
         sort = opts.sell_sort if isinstance(opts.sell_sort, str) else ("on" if opts.sell_sort else "off")
-        if key == "A" and self.row_perm is not None:
-            sort = "off"     # already ordered by length (row_order)
+        if (key == "A" and self.row_perm is not None) or (key == "At" and self.col_perm is not None):
+            sort = "off"     # already ordered by length (row_order / col_order)
         if sort == "on" or (sort == "auto" and nnz / rows >= 12):
             perm = torch.empty(ns * 32, dtype=torch.uint8, device=dev)
             inv = torch.empty(ns * 32, dtype=torch.uint8, device=dev)

@@ -24,6 +24,9 @@ VARIANTS = {
     "rows": dict(row_order="length"),
     "rows_plain": dict(row_order="length", row_order_first=0),
     "rows_nocol": dict(row_order="length", col_order="natural"),
+    "rows_col0": dict(row_order="length", col_order_first=0),
+    "rows_col16": dict(row_order="length", col_order_first=16),
+    "rows_col32": dict(row_order="length", col_order_first=32),
     "rows_first64": dict(row_order="length", row_order_first=64),
     "rows_first32": dict(row_order="length", row_order_first=32),
     "rows_classes": dict(row_order="length", row_order_first=-1),
@@ -65,7 +68,10 @@ def main():
     from paper_2603_03150_b200 import _native as N
     clocks = []
     for r in range(args.rounds):
-        for nm in names:
+        # rotate the order every round: the variant timed first after the previous
+        # round sees a different power/clock transition than the others
+        order = names[r % len(names):] + names[:r % len(names)]
+        for nm in order:
             d, st = devs[nm]
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(d.stream)
