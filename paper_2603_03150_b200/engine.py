@@ -90,6 +90,9 @@ class GpuOptions:
                      theirs, so every step's sums are the unrenumbered ones; x and z
                      are mapped back on download.  auto: whenever row_order applies.
     col_order_first: columns longer than this come first (as row_order_first).
+    row_order_window: rows (and columns) per renumbering window: 16k measured best
+                     on config 4 (per period, rotated A/B: 16k 112.7, 32k 113.0,
+                     8k 113.1, 64k 113.9, 256k 115.6 ms; profiles/r02_ab_window*.log).
     row_order_first: with row_order: rows longer than this many entries come first
                      (window by window, longest first), then the rest -- the long
                      slices start at the head of the grid, so no window's long slices
@@ -140,7 +143,7 @@ class GpuOptions:
     sell_min_nnz: int = 5_000_000
     sell_sort: str = "auto"
     row_order: str = "auto"
-    row_order_window: int = 65536
+    row_order_window: int = 16384
     row_order_max_tail: float = 0.15
     row_order_first: int = 32
     col_order: str = "auto"

@@ -25,9 +25,16 @@ VARIANTS = {
     "rows_plain": dict(row_order="length", row_order_first=0),
     "rows_nocol": dict(row_order="length", col_order="natural"),
     "rows_col0": dict(row_order="length", col_order_first=0),
+    "rows_colclasses": dict(row_order="length", col_order_first=-1),
+    "rows_w16k": dict(row_order="length", row_order_window=16384),
+    "rows_w4k": dict(row_order="length", row_order_window=4096),
+    "rows_w8k": dict(row_order="length", row_order_window=8192),
+    "rows_w32k": dict(row_order="length", row_order_window=32768),
+    "rows_w256k": dict(row_order="length", row_order_window=262144),
     "rows_col16": dict(row_order="length", col_order_first=16),
     "rows_col32": dict(row_order="length", col_order_first=32),
     "rows_first64": dict(row_order="length", row_order_first=64),
+    "rows_first16": dict(row_order="length", row_order_first=16),
     "rows_first32": dict(row_order="length", row_order_first=32),
     "rows_classes": dict(row_order="length", row_order_first=-1),
     "rows_first48": dict(row_order="length", row_order_first=48),
