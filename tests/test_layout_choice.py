@@ -44,3 +44,40 @@ def test_slice_pad_of_sorted_rows_is_one():
     order = np.argsort(-lens, kind="stable")
     sorted_ptr = torch.from_numpy(np.concatenate([[0], np.cumsum(lens[order])]).astype(np.int64))
     assert _slice_pad(torch, sorted_ptr, 512) < 1.05
+
+
+def test_length_order_long_first_windows():
+    """_length_order (the row / column renumbering): a permutation; rows longer
+    than `first` come first, window by window; inside each group and window
+    by decreasing length, ties in the original order (stable)."""
+    from paper_2603_03150_b200.engine import _length_order
+
+    rng = np.random.default_rng(7)
+    lens = torch.from_numpy(rng.integers(0, 80, 1000).astype(np.int64))
+    W, first = 64, 32
+    perm = _length_order(torch, "cpu", lens, W, first).numpy()
+    L = lens.numpy()
+    assert sorted(perm.tolist()) == list(range(1000))
+    longs = L[perm] > first
+    k = int(longs.sum())
+    assert longs[:k].all() and not longs[k:].any()
+    for part in (perm[:k], perm[k:]):
+        win = part // W
+        assert np.all(np.diff(win) >= 0)                       # window by window
+        for w in np.unique(win):
+            idx = part[win == w]
+            lw = L[idx]
+            assert np.all(np.diff(lw) <= 0)                     # longest first
+            for v in np.unique(lw):                             # stable among ties
+                same = idx[lw == v]
+                assert np.all(np.diff(same) > 0)
+
+
+def test_length_order_plain_windows_and_classes():
+    from paper_2603_03150_b200.engine import _length_order
+
+    lens = torch.tensor([3, 9, 1, 9, 5, 2, 40, 7], dtype=torch.int64)
+    # plain windows of 4: [9, 9, 3, 1] then [40, 7, 5, 2]
+    assert _length_order(torch, "cpu", lens, 4, 0).tolist() == [1, 3, 0, 2, 6, 7, 4, 5]
+    # log2 classes, longest class first, one window: 40 | 9 9 | 5 7 | 3 2 | 1
+    assert _length_order(torch, "cpu", lens, 8, -1).tolist() == [6, 1, 3, 7, 4, 0, 5, 2]
