@@ -334,15 +334,17 @@ class DeviceLp:
                 self.col_perm = self.col_inv = None
                 self._col_perm_host = None
                 t_rs = t_rn = t_up
-                if shard is None and m > 1:
-                    lanes0 = int(opts.a_lanes) or auto_lanes(nnz, m)
-                    H0 = int(opts.heavy_threshold) or heavy_threshold(lanes0)
-                    want = _want_row_order(torch, opts, self.a_ptr, nnz, H0)
+                if shard is None:
+                    want = False
+                    if m > 1:
+                        lanes0 = int(opts.a_lanes) or auto_lanes(nnz, m)
+                        H0 = int(opts.heavy_threshold) or heavy_threshold(lanes0)
+                        want = _want_row_order(torch, opts, self.a_ptr, nnz, H0)
                     t_rs = t_rn = time.monotonic()
                     if want:
                         self._renumber_rows(torch, dev, m, nnz, int(opts.row_order_window),
                                             int(opts.row_order_first))
-                    if opts.col_order == "length" or (opts.col_order == "auto" and want):
+                    if n > 1 and (opts.col_order == "length" or (opts.col_order == "auto" and want)):
                         self._renumber_cols(torch, dev, n, nnz, int(opts.row_order_window),
                                             int(opts.col_order_first))
                     t_rn = time.monotonic()
