@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PDHG_ABI_VERSION 4
+#define PDHG_ABI_VERSION 5
 
 /* Error codes. */
 #define PDHG_OK 0
@@ -228,6 +228,20 @@ int pdhg_check_device(pdhg_ctx* ctx, int32_t npts, const int32_t* specs);
  * pdhg_step after _score (pdhg.py:142, 201-204). */
 int pdhg_check_dot_enable(pdhg_ctx* ctx, int32_t on);
 int pdhg_use_check_dot(pdhg_ctx* ctx, int32_t slot);
+
+/* Check fused into the steps.  With check_fuse enabled (needs the sliced-ELL
+ * layouts of A and A' and one unsharded GPU, else PDHG_ERR_STATE), a
+ * pdhg_run_period_check of >= 2 iterations whose points are exactly (CUR,
+ * AVG) runs its last iteration with the check's A side inside it: the primal
+ * step stores (xe, x, avg_x) per column as one 32-byte quad, the dual step
+ * gathers the quads -- one pass over A for the step's A xe (pdhg.py:143) and
+ * the check's A x, A avg_x (lp_core.py:436 for both points of pdhg.py:201-202)
+ * -- and leaves each row's two primal residuals for the check, which
+ * accumulates them in the separate A-side kernel's exact order: iterates and
+ * check scalars are bit for bit those of the unfused path.  Since ABI 5 the
+ * workspace holds the quads and residual pairs (32 bytes per column and 16
+ * per row more than ABI 4's). */
+int pdhg_check_fuse_enable(pdhg_ctx* ctx, int32_t on);
 
 /* Restart at point `which` (CUR or AVG): x, y, avg_x, avg_y <- that point
  * (pdhg.py:235-238). */

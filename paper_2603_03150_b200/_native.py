@@ -37,7 +37,7 @@ EXPORTS = (
     "pdhg_sell_tmp_bytes", "pdhg_sell_plan", "pdhg_sell_fill", "pdhg_sell_sort", "pdhg_set_peers",
     "pdhg_run_period_check", "pdhg_center_toward_target", "pdhg_dot_tmp_bytes", "pdhg_dot",
     "pdhg_permute_rows", "pdhg_features", "pdhg_half_step_pass", "pdhg_debug_oob",
-    "pdhg_check_dot_enable", "pdhg_use_check_dot",
+    "pdhg_check_dot_enable", "pdhg_use_check_dot", "pdhg_check_fuse_enable",
 )
 
 VEC = {name: i for i, name in enumerate(
@@ -105,7 +105,7 @@ def _sig(lib, name, restype, *argtypes):
     f.argtypes = list(argtypes)
 
 
-ABI_VERSION = 4   # include/pdhg_b200.h PDHG_ABI_VERSION
+ABI_VERSION = 5   # include/pdhg_b200.h PDHG_ABI_VERSION
 
 
 def load():
@@ -183,6 +183,7 @@ def load():
         _sig(lib, "pdhg_features", C.c_int)
         _sig(lib, "pdhg_check_dot_enable", C.c_int, vp, i32)
         _sig(lib, "pdhg_use_check_dot", C.c_int, vp, i32)
+        _sig(lib, "pdhg_check_fuse_enable", C.c_int, vp, i32)
         _sig(lib, "pdhg_half_step_pass", C.c_int, vp, i32, i32, i32)
         _sig(lib, "pdhg_debug_oob", C.c_int, P(i64), P(i64), P(i64))
         _sig(lib, "pdhg_violation", C.c_int, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,

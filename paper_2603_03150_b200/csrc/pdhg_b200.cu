@@ -846,7 +846,46 @@ __device__ __forceinline__ double sell_row_dot(const SellSet& S, long long sl, i
 template <bool PRIMAL, int kU>
 constexpr int sell_min_blocks() { return (!PRIMAL && kU > PDHG_SELL_U_LONG) ? 6 : PDHG_SELL_MINB; }
 
-template <bool PRIMAL, int kU>
+// ---------------------------------------------- check fused into the steps
+// The last iteration of a period that ends at a two-point check (CUR, AVG):
+// the primal step writes (xe, x, avg_x) of every column as one 32-byte quad
+// instead of xe alone, and the dual step gathers the quad -- one 32-byte
+// sector per entry, like its 8-byte xe gather -- so one pass over A gives
+// the step's A xe and the check's A x and A avg_x (pdhg.py:143 and
+// lp_core.py:436 for both points of pdhg.py:201-202).  The dual step stores
+// each row's primal residuals b - A x, b - A avg_x; k_check_primal_fold then
+// accumulates them in k_check_primal_sell's exact order, so the check's
+// scalars are bit for bit those of the separate A-side pass it replaces.
+struct __align__(32) Quad {
+  double e, x, a, pad;  // xe, x, avg_x of one column
+};
+
+__device__ __forceinline__ void st_quad(Quad* p, double e, double x, double a) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(e), "d"(x), "d"(a), "d"(0.0)
+               : "memory");
+}
+
+__device__ __forceinline__ void ld_quad(const Quad* p, double& e, double& x, double& a) {
+  double pad;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(e), "=d"(x), "=d"(a), "=d"(pad) : "l"(p));
+}
+
+// primal_epi_pre with the quad store in place of the xe store
+__device__ __forceinline__ void primal_epi_quad(int j, double aty, double cj, double xj, double xb,
+                                                double* __restrict__ x, Quad* __restrict__ q,
+                                                double* __restrict__ xbar, double tau_w, double w,
+                                                long long iter, StepParams* P) {
+  const double g = __dsub_rn(cj, aty);
+  const double xn = np_max0(__dsub_rn(xj, __dmul_rn(tau_w, g)));
+  epi_st(x + j, xn);
+  const double xev = __dsub_rn(__dmul_rn(2.0, xn), xj);
+  const double xbn = __dadd_rn(xb, __ddiv_rn(__dsub_rn(xn, xb), w));
+  epi_st(xbar + j, xbn);
+  st_quad(q + j, xev, xn, xbn);
+  if (!finite(xn)) fail_at(P, iter);
+}
+
+template <bool PRIMAL, int kU, bool QUAD = false>
 __global__ void __launch_bounds__(kBlock, (sell_min_blocks<PRIMAL, kU>())) k_step_sell(StepArgs a, SellSet S, int j_in_period) {
   __shared__ double red[kWarps];
   pdl_enter();
@@ -863,7 +902,10 @@ __global__ void __launch_bounds__(kBlock, (sell_min_blocks<PRIMAL, kU>())) k_ste
     row_dot<kBlock, 1>(a.rs, s, e, threadIdx.x, xin, acc);
     const double d = block_sum(acc[0], red);
     if (threadIdx.x == 0) {
-      if (PRIMAL) bcast(P, 0, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
+      if constexpr (PRIMAL && QUAD)
+        primal_epi_quad(row, d, a.cb[row], a.x[row], a.xbar[row], a.x, reinterpret_cast<Quad*>(a.xe), a.xbar,
+                        step, w, iter, P);
+      else if (PRIMAL) bcast(P, 0, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
       else bcast(P, 1, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
     }
     return;
@@ -894,8 +936,115 @@ __global__ void __launch_bounds__(kBlock, (sell_min_blocks<PRIMAL, kU>())) k_ste
   }
   if (ok) {
     const int row = (int)rl;
-    if (PRIMAL) bcast(P, 0, row, primal_epi_pre(row, acc, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
+    if constexpr (PRIMAL && QUAD)
+      primal_epi_quad(row, acc, o1, o2, o3, a.x, reinterpret_cast<Quad*>(a.xe), a.xbar, step, w, iter, P);
+    else if (PRIMAL) bcast(P, 0, row, primal_epi_pre(row, acc, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
     else bcast(P, 1, row, dual_epi_pre(row, acc, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
+  }
+}
+
+// The dual step of a check-fused iteration over the sliced ELL of A: the
+// step's fma chain over xe (bitwise the k_step_sell<false> result) plus the
+// check's chains over x and avg_x (bitwise k_check_primal_sell's), all from
+// one quad gather per entry.  a.gather = the quads, a.partial = each row's
+// residual pair (b - A x, b - A avg_x), indexed by row.
+#ifndef PDHG_FUSE_U
+#define PDHG_FUSE_U 4
+#endif
+#ifndef PDHG_FUSE_MINB
+#define PDHG_FUSE_MINB 4
+#endif
+template <int V>
+__device__ __forceinline__ void row_dot_quad(const RowSet& A, int s, int e, int lane, const Quad* __restrict__ q,
+                                             double* acc) {
+  constexpr int kU = V >= 16 ? PDHG_ROW_U16 : 2;   // row_dot's entry order: k, k+V, k+2V, ...
+  acc[0] = acc[1] = acc[2] = 0.0;
+  for (int k = s + lane; k < e; k += kU * V) {
+    double av[kU], ev[kU], xv[kU], mv[kU];
+    int j[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int kk = k + u * V;
+      av[u] = kk < e ? ld_stream(A.val + CHK(kk, A.nnz)) : 0.0;
+      j[u] = kk < e ? ld_stream(A.col + CHK(kk, A.nnz)) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      ev[u] = xv[u] = mv[u] = 0.0;
+      if (j[u] >= 0) ld_quad(q + CHK(j[u], A.ncols), ev[u], xv[u], mv[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (j[u] >= 0) {
+        acc[0] = fma(av[u], ev[u], acc[0]);
+        acc[1] = fma(av[u], xv[u], acc[1]);
+        acc[2] = fma(av[u], mv[u], acc[2]);
+      }
+  }
+}
+
+template <int kU>
+__global__ void __launch_bounds__(kBlock, PDHG_FUSE_MINB) k_step_sell_chk(StepArgs a, SellSet S, int j_in_period) {
+  __shared__ double red[kWarps];
+  pdl_enter();
+  StepParams* P = a.P;
+  const long long iter = P->iter0 + j_in_period + 1;
+  if (P->fail_iter < iter) return;
+  const double w = P->w0 + (double)(j_in_period + 1);
+  const double step = P->sigma_w;
+  const Quad* __restrict__ q = reinterpret_cast<const Quad*>(a.gather);
+  double2* __restrict__ res = reinterpret_cast<double2*>(a.partial);
+  if ((int)blockIdx.x < a.rs.n_heavy) {
+    const int row = a.rs.heavy[blockIdx.x];
+    double acc[3], d[3];
+    row_dot_quad<kBlock>(a.rs, a.rs.ptr[row], a.rs.ptr[row + 1], threadIdx.x, q, acc);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) d[r] = block_sum(acc[r], red);
+    if (threadIdx.x == 0) {
+      const double bi = a.cb[row];
+      dual_epi_pre(row, d[0], bi, a.x[row], a.xbar[row], a.x, a.xbar, step, w, iter, P);
+      res[row] = make_double2(__dsub_rn(bi, d[1]), __dsub_rn(bi, d[2]));
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const long long sl = ((long long)(blockIdx.x - a.rs.n_heavy) * kBlock + threadIdx.x) >> 5;
+  if (sl >= S.nslices) return;  // warp-uniform
+  const long long rl = sl * 32 + (S.perm ? S.perm[sl * 32 + lane] : lane);
+  const bool in_range = rl < a.rs.rows;
+  int len = in_range ? a.rs.ptr[rl + 1] - a.rs.ptr[rl] : 0;
+  const bool ok = in_range && len <= a.rs.heavy_threshold;
+  if (!ok) len = 0;
+  const int width = S.width[sl];
+  const long long base = S.sptr[sl] + lane;
+  double de = 0.0, dx = 0.0, da = 0.0;   // sell_row_dot's / sell_row_dot_pair's chains
+  for (int k = 0; k < width; k += kU) {
+    double av[kU], ev[kU], xv[kU], mv[kU];
+    int jv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const bool on = k + u < len;
+      av[u] = on ? ld_stream(S.val + CHK(base + 32LL * (k + u), S.nslots)) : 0.0;
+      jv[u] = on ? ld_stream(S.col + CHK(base + 32LL * (k + u), S.nslots)) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      ev[u] = xv[u] = mv[u] = 0.0;
+      if (jv[u] >= 0) ld_quad(q + CHK(jv[u], S.ncols), ev[u], xv[u], mv[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (jv[u] >= 0) {
+        de = fma(av[u], ev[u], de);
+        dx = fma(av[u], xv[u], dx);
+        da = fma(av[u], mv[u], da);
+      }
+  }
+  if (ok) {
+    const int row = (int)rl;
+    const double bi = epi_ld(a.cb + rl);
+    dual_epi_pre(row, de, bi, epi_ld(a.x + rl), epi_ld(a.xbar + rl), a.x, a.xbar, step, w, iter, P);
+    res[rl] = make_double2(__dsub_rn(bi, dx), __dsub_rn(bi, da));
   }
 }
 
@@ -1664,6 +1813,52 @@ __global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_primal_sell(Ro
   }
 }
 
+// The A side of a check-fused two-point check: k_check_primal_sell's loops
+// and row terms over the residual pairs the fused dual step stored (res[i] =
+// (b - A x, b - A avg_x) of row i), so every per-thread chain and block
+// reduction -- and with them the scalars -- are bitwise that kernel's.
+__global__ void __launch_bounds__(kBlock, PDHG_CHECK_BPS) k_check_primal_fold(RowSet rs, SellSet S,
+                                                                          const double* __restrict__ b,
+                                                                          CheckPts pts,
+                                                                          const double2* __restrict__ res,
+                                                                          double* __restrict__ partials) {
+  __shared__ double red[kWarps];
+  double rp2[2] = {0.0, 0.0}, rpmax[2] = {0.0, 0.0}, by[2] = {0.0, 0.0};
+  auto row_terms = [&](long long i) {
+    const double bi = b[i];
+    const double2 rr = res[i];
+    const double r2[2] = {rr.x, rr.y};
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const double r = r2[p];
+      rp2[p] = fma(r, r, rp2[p]);
+      rpmax[p] = nan_max(fabs(r), rpmax[p]);
+      by[p] = fma(bi, pts.y[p][i], by[p]);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int h = blockIdx.x; h < rs.n_heavy; h += gridDim.x) row_terms(rs.heavy[h]);
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * kWarps;
+  for (long long sl = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5; sl < S.nslices; sl += warps) {
+    const long long rl = sell_row(S, sl, lane);
+    const int len = rl < rs.rows ? rs.ptr[rl + 1] - rs.ptr[rl] : -1;
+    if (len >= 0 && len <= rs.heavy_threshold) row_terms(rl);
+  }
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const double t0 = block_sum(rp2[p], red);
+    const double t1 = block_max(rpmax[p], red);
+    const double t2 = block_sum(by[p], red);
+    if (threadIdx.x == 0) {
+      double* o = partials + (size_t)blockIdx.x * kMaxQ + p * PDHG_NQ;
+      o[PDHG_Q_RP2] = t0;
+      o[PDHG_Q_RPMAX] = t1;
+      o[PDHG_Q_BY] = t2;
+    }
+  }
+}
+
 // Row relabelling of a CSR matrix (warp per new row): new row r is old row
 // perm[r]; new_ptr must already hold the scanned lengths.  Entries keep their
 // order inside each row.
@@ -1863,6 +2058,14 @@ struct pdhg_ctx {
   bool check_dot = false;  // enabled for this context
   bool dots_ready = false; // px holds the last two-point check's A'y pairs
   int first_dot = -1;      // armed: the next period's first primal step uses px[.].{x,y}
+  // check fused into the last iteration of a period (pdhg_check_fuse_enable):
+  // pq = (xe, x, avg_x) quads written by that iteration's primal step, pr = the
+  // residual pairs its dual step leaves for k_check_primal_fold
+  void* pq = nullptr;
+  double2* pr = nullptr;
+  bool check_fuse = false;  // enabled for this context
+  bool fuse_next = false;   // the next launch_period fuses its last iteration
+  bool fuse_ready = false;  // pr holds the residuals of the current (x, y) and average
 };
 
 namespace {
@@ -1886,6 +2089,7 @@ size_t carve_bytes(int32_t m, int32_t n) {
   b += align_up(64 * 8 + 256);
   b += align_up(sizeof(StepParams) + 256);
   b += align_up((size_t)n * 16 + 256) + align_up((size_t)m * 16 + 256);  // px, py
+  b += align_up((size_t)n * 32 + 256) + align_up((size_t)m * 16 + 256);  // pq, pr
   return b;
 }
 
@@ -1983,31 +2187,60 @@ int launch_primal_from_dot(pdhg_ctx* c, int slot, int j) {
                    (const double2*)(c->px + c->xo), slot, j);
 }
 
+// The half steps of the last iteration of a check-fused period (sliced ELL
+// of A and A', one GPU): the primal step writes the (xe, x, avg_x) quads, the
+// dual step gathers them and leaves the check's residual pairs in pr.
+int launch_step_fused(pdhg_ctx* c, bool primal, int j) {
+  StepArgs a = step_args(c, primal);
+  const SellSet& S = c->sell[primal ? 1 : 0];
+  const int grid = a.rs.n_heavy + (int)(((long long)S.nslices * 32 + kBlock - 1) / kBlock);
+  if (grid == 0) return 0;
+  if (primal) {
+    a.xe = reinterpret_cast<double*>(c->pq);
+    return S.u_long ? launch_ex(c, k_step_sell<true, PDHG_SELL_U_LONG, true>, dim3(grid), dim3(kBlock), 0, nullptr,
+                                0, a, S, j)
+                    : launch_ex(c, k_step_sell<true, PDHG_SELL_U, true>, dim3(grid), dim3(kBlock), 0, nullptr, 0,
+                                a, S, j);
+  }
+  a.gather = reinterpret_cast<const double*>(c->pq);
+  a.partial = reinterpret_cast<double*>(c->pr);
+  return launch_ex(c, k_step_sell_chk<PDHG_FUSE_U>, dim3(grid), dim3(kBlock), 0, nullptr, 0, a, S, j);
+}
+
 int launch_period(pdhg_ctx* c, int iters) {
   // an armed check-dot slot is consumed by this period (or dropped)
   const int first = c->first_dot;
   c->first_dot = -1;
   c->dots_ready = false;
+  // a check-fused period needs a last iteration other than the first
+  const bool fuse = c->fuse_next && iters >= 2 && c->coop_grid == 0;
+  c->fuse_next = false;
+  c->fuse_ready = false;
   if (iters <= 0) return 0;
   if (c->coop_grid > 0) return launch_period_persistent(c, iters);
   int rc = 0;
-  auto primal0 = [&](int j) { return (j == 0 && first >= 0) ? launch_primal_from_dot(c, first, 0)
-                                                            : launch_step(c, true, j); };
+  auto half = [&](bool primal, int j) {
+    if (fuse && j == iters - 1) return launch_step_fused(c, primal, j);
+    if (primal && j == 0 && first >= 0) return launch_primal_from_dot(c, first, 0);
+    return launch_step(c, primal, j);
+  };
   if (c->period_direct) {
     for (int j = 0; j < iters && !rc; ++j) {
-      rc = primal0(j);
-      if (!rc) rc = launch_step(c, false, j);
+      rc = half(true, j);
+      if (!rc) rc = half(false, j);
     }
+    if (!rc) c->fuse_ready = fuse;
     return rc;
   }
-  const int key = iters + (first + 1) * (1 << 28);  // graphs per (length, first step)
+  // graphs per (length, first step, fused check)
+  const int key = iters + (first + 1) * (1 << 28) + (fuse ? (1 << 30) : 0);
   auto it = c->graphs.find(key);
   if (it == c->graphs.end()) {
     cudaGraph_t g;
     CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     for (int j = 0; j < iters && !rc; ++j) {
-      rc = primal0(j);
-      if (!rc) rc = launch_step(c, false, j);
+      rc = half(true, j);
+      if (!rc) rc = half(false, j);
     }
     cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
     if (rc) return rc;
@@ -2018,6 +2251,7 @@ int launch_period(pdhg_ctx* c, int iters) {
     it = c->graphs.emplace(key, ex).first;
   }
   CUDA_TRY(cudaGraphLaunch(it->second, c->stream));
+  c->fuse_ready = fuse;
   return 0;
 }
 
@@ -2218,6 +2452,8 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
   c->P = cv.take<StepParams>(1);
   c->px = cv.take<double2>(n);
   c->py = cv.take<double2>(m);
+  c->pq = cv.take<Quad>(n);
+  c->pr = cv.take<double2>(m);
   if ((prob->a_nsplit > 1 && !prob->a_split) || (prob->at_nsplit > 1 && !prob->at_split)) {
     delete c;
     return fail(PDHG_ERR_ARG, "split step without split points");
@@ -2379,6 +2615,7 @@ int pdhg_reset(pdhg_ctx* c) {
   const size_t nb = (size_t)c->nf * 8, mb = (size_t)c->mf * 8;
   c->first_dot = -1;
   c->dots_ready = false;
+  c->fuse_ready = false;
   CUDA_TRY(cudaMemsetAsync(c->x, 0, nb, c->stream));
   CUDA_TRY(cudaMemsetAsync(c->xe, 0, nb, c->stream));
   CUDA_TRY(cudaMemsetAsync(c->xbar, 0, nb, c->stream));
@@ -2429,6 +2666,7 @@ int pdhg_run_period_check(pdhg_ctx* c, int32_t iters, int64_t iter0, double tau_
   h.iter0 = iter0;
   h.fail_iter = LLONG_MAX;
   CUDA_TRY(cudaMemcpyAsync(c->P, c->P_host, sizeof(StepParams), cudaMemcpyHostToDevice, c->stream));
+  c->fuse_next = c->check_fuse && npts == 2 && specs[0] == PDHG_PT_CUR && specs[1] == PDHG_PT_AVG;
   int rc = launch_period(c, iters);
   if (rc) return rc;
   if (npts > 0) {
@@ -2459,6 +2697,9 @@ int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
     pd.zin[p] = (specs[p] & PDHG_SPEC_BEST_Z) ? c->zbest + c->xo : nullptr;
     pd.zout[p] = nullptr;
   }
+  // the period just run fused this check's A side into its last dual step
+  const bool fused = c->fuse_ready && npts == 2 && specs[0] == PDHG_PT_CUR && specs[1] == PDHG_PT_AVG;
+  c->fuse_ready = false;
   if (npts == 2 && PDHG_CHECK_PAIR) {
     // interleave the two points' gathered vectors (full padded length: the
     // check gathers by global index): 0.5 GB of copies on config 4 buys one
@@ -2466,7 +2707,7 @@ int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
     const double *x0, *y0, *x1, *y1;
     point_xy(c, specs[0], &x0, &y0);
     point_xy(c, specs[1], &x1, &y1);
-    k_pair<<<kCheckBlocks, kBlock, 0, c->stream>>>(x0, x1, c->px, c->nf);
+    if (!fused) k_pair<<<kCheckBlocks, kBlock, 0, c->stream>>>(x0, x1, c->px, c->nf);
     k_pair<<<kCheckBlocks, kBlock, 0, c->stream>>>(y0, y1, c->py, c->mf);
     pp.pair = c->px;
     pd.pair = c->py;
@@ -2479,7 +2720,11 @@ int pdhg_check_device(pdhg_ctx* c, int32_t npts, const int32_t* specs) {
   c->dots_ready = false;
   CUDA_TRY(cudaMemsetAsync(c->partials, 0, (size_t)kCheckBlocks * kMaxQ * 8, c->stream));
   int rc = 0;
-  if (pp.pair && c->has_sell[0] && PDHG_CHECK_SELL) {
+  if (fused) {
+    k_check_primal_fold<<<kCheckBlocks, kBlock, 0, c->stream>>>(c->A, c->sell[0], c->prob.b, pp, c->pr,
+                                                                c->partials);
+    CUDA_TRY(cudaGetLastError());
+  } else if (pp.pair && c->has_sell[0] && PDHG_CHECK_SELL) {
     if (c->sell[0].u_long)
       k_check_primal_sell<PDHG_SELL_U_LONG><<<kCheckBlocks, kBlock, 0, c->stream>>>(c->A, c->sell[0], c->prob.b,
                                                                                   pp, c->partials);
@@ -2530,6 +2775,23 @@ int pdhg_check_dot_enable(pdhg_ctx* c, int32_t on) {
   return 0;
 }
 
+int pdhg_check_fuse_enable(pdhg_ctx* c, int32_t on) {
+  CTX_DEVICE_GUARD(c);
+  if (!c) return fail(PDHG_ERR_ARG, "null ctx");
+  c->fuse_next = c->fuse_ready = false;
+  if (!on) {
+    c->check_fuse = false;
+    return 0;
+  }
+  // both steps on sliced ELL, one unsharded GPU, graph or direct periods
+  if (!c->has_sell[0] || !c->has_sell[1] || !PDHG_CHECK_SELL || !PDHG_CHECK_PAIR || c->npeers[0] > 0 ||
+      c->npeers[1] > 0 || c->has_psr[0] || c->has_psr[1] || c->coop_grid > 0 || c->prob.a_nsplit > 1 ||
+      c->prob.at_nsplit > 1 || c->xo != 0 || c->yo != 0 || c->mf != c->prob.m || c->nf != c->prob.n)
+    return fail(PDHG_ERR_STATE, "check_fuse: needs the sliced-ELL layouts of A and A' on one GPU");
+  c->check_fuse = true;
+  return 0;
+}
+
 int pdhg_use_check_dot(pdhg_ctx* c, int32_t slot) {
   CTX_DEVICE_GUARD(c);
   if (!c || slot < 0 || slot > 1) return fail(PDHG_ERR_ARG, "use_check_dot: bad argument");
@@ -2556,6 +2818,7 @@ int pdhg_restart(pdhg_ctx* c, int32_t which) {
   CTX_DEVICE_GUARD(c);
   if (!c) return fail(PDHG_ERR_ARG, "null ctx");
   const size_t nb = (size_t)c->nf * 8, mb = (size_t)c->mf * 8;
+  c->fuse_ready = false;
   if (which == PDHG_PT_CUR) {
     CUDA_TRY(cudaMemcpyAsync(c->xbar, c->x, nb, cudaMemcpyDeviceToDevice, c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->ybar, c->y, mb, cudaMemcpyDeviceToDevice, c->stream));
@@ -2692,6 +2955,7 @@ int pdhg_half_step_pass(pdhg_ctx* c, int32_t primal, int32_t j, int32_t pass) {
 int pdhg_set_peers(pdhg_ctx* c, int32_t which, const double* const* peers_dev, int32_t npeers) {
   CTX_DEVICE_GUARD(c);
   if (c && which == 0 && npeers > 0) { c->check_dot = false; c->first_dot = -1; c->dots_ready = false; }
+  if (c && which <= 1 && npeers > 0) c->check_fuse = c->fuse_next = c->fuse_ready = false;
   if (!c || which < 0 || which > 2 || npeers < 0 || (npeers > 0 && !peers_dev))
     return fail(PDHG_ERR_ARG, "set_peers: bad argument");
   if (which == 2) {  // peers' fail words (pdhg_vector(peer, PDHG_VEC_FAILWORD))

@@ -118,6 +118,11 @@ class GpuOptions:
                      (pdhg_use_check_dot; bit-identical iterates).  Applies when A' has a
                      sliced-ELL layout, unsharded: config 4 skips one of the 64 primal
                      SpMVs of every period.
+    check_fuse:      run the two-point check's A side inside the last iteration of each
+                     period (pdhg_check_fuse_enable): one pass over A gives the dual step's
+                     A xe and the check's A x, A avg_x from (xe, x, avg_x) quads; bitwise
+                     the same iterates and check scalars.  Applies when A and A' both have
+                     sliced-ELL layouts, unsharded (config 4).
     """
 
     device: int | None = None
@@ -149,6 +154,7 @@ class GpuOptions:
     col_order: str = "auto"
     col_order_first: int = 32
     check_dot: bool = True
+    check_fuse: bool = True
 
 
 def auto_lanes(nnz: int, rows: int) -> int:
@@ -466,6 +472,9 @@ class DeviceLp:
         # check -> first primal step reuse (sliced ELL of A', one GPU)
         self.check_dot = bool(opts.check_dot and shard is None and p.at_sell
                               and self.lib.pdhg_check_dot_enable(ctx, 1) == 0)
+        # two-point check's A side fused into each period's last dual step
+        self.check_fuse = bool(opts.check_fuse and shard is None and p.a_sell and p.at_sell
+                               and self.lib.pdhg_check_fuse_enable(ctx, 1) == 0)
         t_end = time.monotonic()
         self.timings = {"upload_s": t_up - t_start, "layout_s": t_end - t_up,
                         "layout_detail": {"row_order_choice_s": t_rs - t_up, "renumber_s": t_rn - t_rs,
