@@ -447,6 +447,7 @@ def run_ours(args):
     # next period's first primal step when nothing restarts (check_dot)
     reuse = (lambda: dev.use_check_dot(0)) if getattr(dev, "check_dot", False) else (lambda: None)
     period = getattr(dev, "run_period_check", None)
+    check_fused = bool(period is not None and getattr(dev, "check_fuse", False))
     for _ in range(args.warmup):   # the timed loop's own calls (graphs captured here)
         if period is not None:
             period(CHECK_EVERY, it, step, step, float(it), N.PT_CUR, N.PT_AVG)
@@ -506,7 +507,7 @@ def run_ours(args):
                                "and around the two-point check (run_period + check, 2 host syncs)"}
         if period is not None:
             breakdown["period_check_ms"] = statistics.median(e[0].elapsed_time(e[1]) for e in pc)
-            breakdown["check_fused"] = bool(getattr(dev, "check_fuse", False))
+            breakdown["check_fused"] = check_fused
             breakdown["method"] += ("; period_check_ms: 3 more periods through the product's "
                                     "run_period_check (check_fused: its A side inside the last dual step)")
     if sharded:
@@ -714,9 +715,11 @@ def run_ours(args):
         "clocks": clk.summary(),
         # per step: 2 step kernels per iteration (4 with the split steps of the
         # overlapped multi-GPU schedule) + the check's k_pair x2,
-        # k_check_primal(_sell), k_check_dual(_sell), k_reduce (ncu launch list)
+        # k_check_primal(_sell), k_check_dual(_sell), k_reduce; with the fused
+        # check k_pair (y), k_check_primal_fold, k_check_dual_sell, k_reduce
+        # (ncu launch list, profiles/r02_fa_launches.csv)
         "gpu_launches": args.steps * ((4 if comm_info and comm_info["overlap"] != "off" else 2)
-                                      * CHECK_EVERY + 5),
+                                      * CHECK_EVERY + (4 if check_fused else 5)),
         "setup_s": t_setup,
         "time_to_1e4": out,
         "multi_gpu": comm_info,

@@ -584,6 +584,32 @@ __device__ __forceinline__ void bcast_if(const StepParams* P, int k, int row, do
 
 // ------------------------------------------------------------------- steps
 
+// L2 policy of the vectors the next half step gathers (xe from the primal
+// step, y from the dual step): 0 = plain stores; PDHG_XE_LAST: xe stored
+// with an L2 evict_last policy; PDHG_Y_EF: y stored evict-first.
+#ifndef PDHG_XE_LAST
+#define PDHG_XE_LAST 0
+#endif
+#ifndef PDHG_Y_EF
+#define PDHG_Y_EF 0
+#endif
+__device__ __forceinline__ void st_xe(double* p, double v) {
+#if PDHG_XE_LAST
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+#else
+  *p = v;
+#endif
+}
+__device__ __forceinline__ void st_y(double* p, double v) {
+#if PDHG_Y_EF
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
 // Epilogue of the primal step for row j of A' (= column j of A).
 __device__ __forceinline__ double primal_epi(int j, double aty, const double* __restrict__ c,
                                            double* __restrict__ x, double* __restrict__ xe,
@@ -595,7 +621,7 @@ __device__ __forceinline__ double primal_epi(int j, double aty, const double* __
   const double xb = xbar[j];
   x[j] = xn;
   const double xev = __dsub_rn(__dmul_rn(2.0, xn), xj);       // 2 x+ - x
-  xe[j] = xev;
+  st_xe(xe + j, xev);
   xbar[j] = __dadd_rn(xb, __ddiv_rn(__dsub_rn(xn, xb), w));    // avg += (x+ - avg)/w
   if (!finite(xn)) fail_at(P, iter);
   return xev;
@@ -607,7 +633,7 @@ __device__ __forceinline__ double dual_epi(int i, double ax, const double* __res
   const double yi = y[i];
   const double yn = __dadd_rn(yi, __dmul_rn(sigma_w, __dsub_rn(b[i], ax)));
   const double yb = ybar[i];
-  y[i] = yn;
+  st_y(y + i, yn);
   ybar[i] = __dadd_rn(yb, __ddiv_rn(__dsub_rn(yn, yb), w));
   if (!finite(yn)) fail_at(P, iter);
   return yn;
@@ -647,7 +673,7 @@ __device__ __forceinline__ double primal_epi_pre(int j, double aty, double cj, d
   const double xn = np_max0(__dsub_rn(xj, __dmul_rn(tau_w, g)));
   epi_st(x + j, xn);
   const double xev = __dsub_rn(__dmul_rn(2.0, xn), xj);
-  xe[j] = xev;
+  st_xe(xe + j, xev);
   epi_st(xbar + j, __dadd_rn(xb, __ddiv_rn(__dsub_rn(xn, xb), w)));
   if (!finite(xn)) fail_at(P, iter);
   return xev;
@@ -657,7 +683,7 @@ __device__ __forceinline__ double dual_epi_pre(int i, double ax, double bi, doub
                                              double* __restrict__ y, double* __restrict__ ybar,
                                              double sigma_w, double w, long long iter, StepParams* P) {
   const double yn = __dadd_rn(yi, __dmul_rn(sigma_w, __dsub_rn(bi, ax)));
-  y[i] = yn;
+  st_y(y + i, yn);
   epi_st(ybar + i, __dadd_rn(yb, __ddiv_rn(__dsub_rn(yn, yb), w)));
   if (!finite(yn)) fail_at(P, iter);
   return yn;
@@ -865,9 +891,22 @@ __device__ __forceinline__ void st_quad(Quad* p, double e, double x, double a) {
                : "memory");
 }
 
+// 0: one 256-bit load; 1: two 128-bit loads of the same sector; 2: one
+// 256-bit load that does not allocate in L1
+#ifndef PDHG_QUAD_LD
+#define PDHG_QUAD_LD 0
+#endif
 __device__ __forceinline__ void ld_quad(const Quad* p, double& e, double& x, double& a) {
   double pad;
+#if PDHG_QUAD_LD == 1
+  asm("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(e), "=d"(x) : "l"(p));
+  asm("ld.global.nc.f64 %0, [%1+16];" : "=d"(a) : "l"(p));
+  (void)pad;
+#elif PDHG_QUAD_LD == 2
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(e), "=d"(x), "=d"(a), "=d"(pad) : "l"(p));
+#else
   asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(e), "=d"(x), "=d"(a), "=d"(pad) : "l"(p));
+#endif
 }
 
 // primal_epi_pre with the quad store in place of the xe store
