@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define PDHG_ABI_VERSION 5
+#define PDHG_ABI_VERSION 6
 
 /* Error codes. */
 #define PDHG_OK 0
@@ -152,6 +152,17 @@ typedef struct pdhg_problem {
    * slices overlaps pass 0 (pdhg_half_step_pass). */
   int32_t at_nsplit;
   const int32_t* at_split;
+  /* Optional sliced-ELL layouts of the two passes of a split step (with
+   * a_nsplit / at_nsplit = 2): part 0 = each row's first segment (sharded:
+   * its local-slot entries), part 1 = the rest, as two CSR matrices
+   * (a_part_ptr[h] their row pointers) laid out by pdhg_sell_plan/fill.
+   * Rows longer than the heavy threshold are left out of both parts (length
+   * 0) and run whole, block per row, in pass 1.  NULL = the CSR-vector split
+   * kernels over a_split / at_split. */
+  const pdhg_sell* a_sell_part[2];
+  const int32_t* a_part_ptr[2];
+  const pdhg_sell* at_sell_part[2];
+  const int32_t* at_part_ptr[2];
 } pdhg_problem;
 
 typedef struct pdhg_ctx pdhg_ctx;

@@ -88,6 +88,8 @@ class Problem(C.Structure):
         ("a_n_medium", C.c_int32), ("at_n_medium", C.c_int32),
         ("a_medium", C.c_void_p), ("at_medium", C.c_void_p),
         ("at_nsplit", C.c_int32), ("at_split", C.c_void_p),
+        ("a_sell_part", C.c_void_p * 2), ("a_part_ptr", C.c_void_p * 2),
+        ("at_sell_part", C.c_void_p * 2), ("at_part_ptr", C.c_void_p * 2),
     ]
 
 
@@ -105,7 +107,7 @@ def _sig(lib, name, restype, *argtypes):
     f.argtypes = list(argtypes)
 
 
-ABI_VERSION = 5   # include/pdhg_b200.h PDHG_ABI_VERSION
+ABI_VERSION = 6   # include/pdhg_b200.h PDHG_ABI_VERSION
 
 
 def load():

@@ -1288,6 +1288,74 @@ __global__ void __launch_bounds__(kBlock) k_step_split(StepArgs a, int j_in_peri
   else bcast(P, 1, row, dual_epi_pre(row, d, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
 }
 
+// One pass of a split half step over the sliced ELL of that pass's part of
+// every row (sharded local-first blocks: part 0 = the entries whose columns
+// are this shard's own slots, part 1 = the rest).  Pass 0
+// runs each light row's chain over its part-0 entries and parks it in
+// a.partial; pass 1 continues the same chain over the part-1 entries (so a
+// row's sum is one sequential fma chain over its local-first entry order)
+// and runs the epilogue; heavy rows are in neither part and run whole, block
+// per row, in pass 1.  pptr: the part's CSR row pointers (per-row lengths).
+template <bool PRIMAL, int kU, int PASS>
+__global__ void __launch_bounds__(kBlock, (sell_min_blocks<PRIMAL, kU>())) k_step_sell_pass(StepArgs a, SellSet S,
+                                                                                        const int* __restrict__ pptr,
+                                                                                        int j_in_period) {
+  __shared__ double red[kWarps];
+  pdl_enter();
+  StepParams* P = a.P;
+  const long long iter = P->iter0 + j_in_period + 1;
+  if (P->fail_iter < iter) return;
+  const double w = P->w0 + (double)(j_in_period + 1);
+  const double step = PRIMAL ? P->tau_w : P->sigma_w;
+  const int nh = PASS == 1 ? a.rs.n_heavy : 0;
+  if ((int)blockIdx.x < nh) {
+    const double* xin[1] = {a.gather};
+    const int row = a.rs.heavy[blockIdx.x];
+    double acc[1];
+    row_dot<kBlock, 1>(a.rs, a.rs.ptr[row], a.rs.ptr[row + 1], threadIdx.x, xin, acc);
+    const double d = block_sum(acc[0], red);
+    if (threadIdx.x == 0) {
+      if (PRIMAL) bcast(P, 0, row, primal_epi(row, d, a.cb, a.x, a.xe, a.xbar, step, w, iter, P));
+      else bcast(P, 1, row, dual_epi(row, d, a.cb, a.x, a.xbar, step, w, iter, P));
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const long long sl = ((long long)(blockIdx.x - nh) * kBlock + threadIdx.x) >> 5;
+  if (sl >= S.nslices) return;  // warp-uniform
+  const long long rl = sell_row(S, sl, lane);
+  const bool in_range = rl < a.rs.rows;
+  const bool ok = in_range && a.rs.ptr[rl + 1] - a.rs.ptr[rl] <= a.rs.heavy_threshold;
+  const int len = ok ? pptr[rl + 1] - pptr[rl] : 0;
+  double acc = (PASS == 1 && ok) ? a.partial[rl] : 0.0;
+  const int width = S.width[sl];
+  const long long base = S.sptr[sl] + lane;
+  for (int k = 0; k < width; k += kU) {
+    double av[kU], xv[kU];
+    int jv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const bool on = k + u < len;
+      av[u] = on ? ld_stream(S.val + CHK(base + 32LL * (k + u), S.nslots)) : 0.0;
+      jv[u] = on ? ld_stream(S.col + CHK(base + 32LL * (k + u), S.nslots)) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) xv[u] = jv[u] >= 0 ? ld_gather(a.gather + CHK(jv[u], S.ncols)) : 0.0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (jv[u] >= 0) acc = fma(av[u], xv[u], acc);
+  }
+  if (!ok) return;
+  if (PASS == 0) {
+    a.partial[rl] = acc;
+    return;
+  }
+  const int row = (int)rl;
+  const double o1 = epi_ld(a.cb + rl), o2 = epi_ld(a.x + rl), o3 = epi_ld(a.xbar + rl);
+  if (PRIMAL) bcast(P, 0, row, primal_epi_pre(row, acc, o1, o2, o3, a.x, a.xe, a.xbar, step, w, iter, P));
+  else bcast(P, 1, row, dual_epi_pre(row, acc, o1, o2, o3, a.x, a.xbar, step, w, iter, P));
+}
+
 #if PDHG_EXPERIMENTAL  // PSR step
 // PSR step: persistent CTAs (one per SM) walk row blocks; the SpMV lands in
 // shared memory (psr::block_spmv), then the same epilogue as k_step.
@@ -2080,6 +2148,9 @@ struct pdhg_ctx {
   bool has_psr[2];     // [0] = A (dual), [1] = A' (primal)
   bool has_sell[2];    // same indexing
   SellSet sell[2];
+  bool has_sellp[2];   // split steps over sliced-ELL parts (pdhg_problem a_sell_part / at_sell_part)
+  SellSet sellp[2][2];
+  const int* pptr[2][2];
 #if PDHG_EXPERIMENTAL
   psr::Layout psr_l[2];
   size_t psr_smem[2];
@@ -2324,6 +2395,30 @@ int launch_step_pass(pdhg_ctx* c, bool primal, int j, int pass) {
   // written through pointers offset to its slice
   StepArgs a = step_args(c, primal);
   const int nsplit = primal ? c->prob.at_nsplit : c->prob.a_nsplit;
+  if (nsplit > 1 && c->has_sellp[primal ? 1 : 0]) {  // sliced-ELL parts, 2 passes
+    const int k = primal ? 1 : 0;
+    a.partial = primal ? c->tn2 : c->tm2;
+    const int p0 = pass < 0 ? 0 : pass, p1 = pass < 0 ? 2 : std::min(pass + 1, 2);
+    for (int h = p0; h < p1; ++h) {
+      const SellSet& S = c->sellp[k][h];
+      const int nh = h == 1 ? a.rs.n_heavy : 0;
+      const int grid = nh + (int)(((long long)S.nslices * 32 + kBlock - 1) / kBlock);
+      if (grid == 0) continue;
+      int rc;
+      if (h == 0)
+        rc = primal ? launch_ex(c, k_step_sell_pass<true, PDHG_SELL_U, 0>, dim3(grid), dim3(kBlock), 0, nullptr, 0,
+                                a, S, c->pptr[k][0], j)
+                    : launch_ex(c, k_step_sell_pass<false, PDHG_SELL_U, 0>, dim3(grid), dim3(kBlock), 0, nullptr,
+                                0, a, S, c->pptr[k][0], j);
+      else
+        rc = primal ? launch_ex(c, k_step_sell_pass<true, PDHG_SELL_U, 1>, dim3(grid), dim3(kBlock), 0, nullptr, 0,
+                                a, S, c->pptr[k][1], j)
+                    : launch_ex(c, k_step_sell_pass<false, PDHG_SELL_U, 1>, dim3(grid), dim3(kBlock), 0, nullptr,
+                                0, a, S, c->pptr[k][1], j);
+      if (rc) return rc;
+    }
+    return 0;
+  }
   if (nsplit > 1 && !c->has_psr[primal ? 1 : 0]) {
     a.split = primal ? c->prob.at_split : c->prob.a_split;
     a.nsplit = nsplit;
@@ -2539,6 +2634,27 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
       c->sell[k].u_long = q->rows > 0 && ops_nnz >= (long long)PDHG_SELL_U_MEAN * q->rows;
       c->sell[k].ncols = k == 0 ? c->A.ncols : c->At.ncols;
       c->sell[k].nslots = q->nslots > 0 ? q->nslots : 0x7fffffffffffffffLL;
+    }
+  }
+  for (int k = 0; k < 2; ++k) {  // split steps' sliced-ELL parts
+    const pdhg_sell* const* qs = k == 0 ? prob->a_sell_part : prob->at_sell_part;
+    const int32_t* const* pp = k == 0 ? prob->a_part_ptr : prob->at_part_ptr;
+    const int nsplit = k == 0 ? prob->a_nsplit : prob->at_nsplit;
+    c->has_sellp[k] = qs[0] != nullptr || qs[1] != nullptr;
+    if (!c->has_sellp[k]) continue;
+    const int rows = k == 0 ? prob->m : prob->n;
+    for (int h = 0; h < 2; ++h) {
+      const pdhg_sell* q = qs[h];
+      if (nsplit != 2 || !q || !pp[h] || q->rows != rows || q->nslices != (rows + 31) / 32 || !q->sptr ||
+          !q->width) {
+        delete c;
+        return fail(PDHG_ERR_ARG, "split-step sell parts need 2 passes and match the operator");
+      }
+      c->sellp[k][h] = SellSet{q->rows, q->nslices, reinterpret_cast<const long long*>(q->sptr), q->width,
+                               q->col, q->val, q->perm};
+      c->sellp[k][h].ncols = k == 0 ? c->A.ncols : c->At.ncols;
+      c->sellp[k][h].nslots = q->nslots > 0 ? q->nslots : 0x7fffffffffffffffLL;
+      c->pptr[k][h] = pp[h];
     }
   }
 #if PDHG_EXPERIMENTAL

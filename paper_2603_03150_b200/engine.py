@@ -20,6 +20,7 @@ Differences from the reference, all documented in DESIGN.md:
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import math
 import threading
 import time
@@ -416,6 +417,15 @@ class DeviceLp:
                     self._sell[key] = None if (self._psr[key] or pers in ("tiny", "on")
                                                or self.split_local[key] is not None) else \
                         self._build_sell(torch, dev, key, rows, nz, ptr, col, val, Hk, opts)
+                # split steps (overlapped multi-GPU schedule) over sliced-ELL parts:
+                # part 0 = each row's local-slot entries, part 1 = the rest
+                self._sell_part = {"A": None, "At": None}
+                for key, rows, ptr, col, val, Hk in (
+                        ("A", m, self.a_ptr, self.a_col, self.a_val, H),
+                        ("At", n, self.at_ptr, self.at_col, self.at_val, Ht)):
+                    if self.split_local[key] is not None and opts.sell != "off" and rows > 0:
+                        self._sell_part[key] = self._build_sell_parts(torch, dev, key, rows, ptr, col, val,
+                                                                      self.split_local[key], Hk, opts)
                 self.stream.synchronize()
                 t_sell = time.monotonic()
                 self.a_split = None
@@ -464,6 +474,13 @@ class DeviceLp:
             p.a_nsplit, p.a_split = 2, self.split_local["A"].data_ptr()
         if self.split_local["At"] is not None:
             p.at_nsplit, p.at_split = 2, self.split_local["At"].data_ptr()
+        for key, fs, fp in (("A", "a_sell_part", "a_part_ptr"), ("At", "at_sell_part", "at_part_ptr")):
+            parts = self._sell_part.get(key)
+            if parts is not None:
+                sells, keep = parts
+                for h in range(2):
+                    getattr(p, fs)[h] = C.addressof(sells[h])
+                    getattr(p, fp)[h] = keep[h][0].data_ptr()
         self._prob = p
         ctx = C.c_void_p()
         N.check(self.lib.pdhg_ctx_create(C.byref(p), self.ws.data_ptr(), ws_bytes,
@@ -567,6 +584,36 @@ class DeviceLp:
         self.sell_info[key]["used"] = True
         self.sell_info[key]["sorted"] = perm is not None
         return (d, (width, sp, scol, sval, perm))
+
+    def _build_sell_parts(self, torch, dev, key, rows, ptr, col, val, split, H, opts):
+        """Sliced-ELL layouts of the two passes of a split step: each row's
+        entries [ptr, split) and [split, ptr+1) as two CSR matrices on the
+        device, heavy rows (> H entries, run whole in pass 1) left out of
+        both, each laid out by _build_sell.  -> ([Sell, Sell], keep-alive)."""
+        i64 = torch.int64
+        full = (ptr[1:] - ptr[:-1]).to(i64)
+        light = full <= H
+        starts = (ptr[:-1].to(i64), split.to(i64))
+        lens = (torch.where(light, split.to(i64) - starts[0], 0),
+                torch.where(light, ptr[1:].to(i64) - starts[1], 0))
+        sub = dataclasses.replace(opts, sell="on")   # the parts' pad / mean do not gate them
+        sells, keep = [], []
+        for h in range(2):
+            ln = lens[h]
+            pp = torch.zeros(rows + 1, dtype=i64, device=dev)
+            torch.cumsum(ln, 0, out=pp[1:])
+            nz = int(pp[-1].item())
+            rid = torch.repeat_interleave(torch.arange(rows, device=dev), ln)
+            idx = starts[h][rid] + (torch.arange(nz, device=dev) - pp[:-1][rid])
+            pcol = col[idx].contiguous()
+            pval = val[idx].contiguous()
+            p32 = pp.to(torch.int32)
+            built = self._build_sell(torch, dev, f"{key}.part{h}", rows, max(nz, 1), p32, pcol, pval, H, sub)
+            if built is None:
+                return None
+            sells.append(built[0])
+            keep.append((p32, built[1]))
+        return sells, keep
 
     def _build_psr(self, torch, dev, key, rows, cols, nnz, ptr, col, val, H, opts):
         """Plan + build the PSR layout of one operator on the device (or None)."""

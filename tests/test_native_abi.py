@@ -44,7 +44,7 @@ def test_every_declared_symbol_is_exported(lib):
 def test_abi_version_and_error_channel(lib):
     from paper_2603_03150_b200 import _native
 
-    assert lib.pdhg_abi_version() == _native.ABI_VERSION == 5
+    assert lib.pdhg_abi_version() == _native.ABI_VERSION == 6
     assert isinstance(lib.pdhg_last_error(), bytes)
 
 
