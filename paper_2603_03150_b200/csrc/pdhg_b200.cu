@@ -2404,17 +2404,32 @@ int launch_step_pass(pdhg_ctx* c, bool primal, int j, int pass) {
       const int nh = h == 1 ? a.rs.n_heavy : 0;
       const int grid = nh + (int)(((long long)S.nslices * 32 + kBlock - 1) / kBlock);
       if (grid == 0) continue;
+      // entries in flight as the unsplit sliced-ELL steps (long rows: 6 primal, 10 dual)
+      const int* pp = c->pptr[k][h];
       int rc;
-      if (h == 0)
-        rc = primal ? launch_ex(c, k_step_sell_pass<true, PDHG_SELL_U, 0>, dim3(grid), dim3(kBlock), 0, nullptr, 0,
-                                a, S, c->pptr[k][0], j)
-                    : launch_ex(c, k_step_sell_pass<false, PDHG_SELL_U, 0>, dim3(grid), dim3(kBlock), 0, nullptr,
-                                0, a, S, c->pptr[k][0], j);
-      else
-        rc = primal ? launch_ex(c, k_step_sell_pass<true, PDHG_SELL_U, 1>, dim3(grid), dim3(kBlock), 0, nullptr, 0,
-                                a, S, c->pptr[k][1], j)
-                    : launch_ex(c, k_step_sell_pass<false, PDHG_SELL_U, 1>, dim3(grid), dim3(kBlock), 0, nullptr,
-                                0, a, S, c->pptr[k][1], j);
+      if (S.u_long) {
+        if (h == 0)
+          rc = primal ? launch_ex(c, k_step_sell_pass<true, PDHG_SELL_U_LONG, 0>, dim3(grid), dim3(kBlock), 0,
+                                  nullptr, 0, a, S, pp, j)
+                      : launch_ex(c, k_step_sell_pass<false, PDHG_SELL_U_DUAL, 0>, dim3(grid), dim3(kBlock), 0,
+                                  nullptr, 0, a, S, pp, j);
+        else
+          rc = primal ? launch_ex(c, k_step_sell_pass<true, PDHG_SELL_U_LONG, 1>, dim3(grid), dim3(kBlock), 0,
+                                  nullptr, 0, a, S, pp, j)
+                      : launch_ex(c, k_step_sell_pass<false, PDHG_SELL_U_DUAL, 1>, dim3(grid), dim3(kBlock), 0,
+                                  nullptr, 0, a, S, pp, j);
+      } else {
+        if (h == 0)
+          rc = primal ? launch_ex(c, k_step_sell_pass<true, PDHG_SELL_U, 0>, dim3(grid), dim3(kBlock), 0, nullptr,
+                                  0, a, S, pp, j)
+                      : launch_ex(c, k_step_sell_pass<false, PDHG_SELL_U, 0>, dim3(grid), dim3(kBlock), 0, nullptr,
+                                  0, a, S, pp, j);
+        else
+          rc = primal ? launch_ex(c, k_step_sell_pass<true, PDHG_SELL_U, 1>, dim3(grid), dim3(kBlock), 0, nullptr,
+                                  0, a, S, pp, j)
+                      : launch_ex(c, k_step_sell_pass<false, PDHG_SELL_U, 1>, dim3(grid), dim3(kBlock), 0, nullptr,
+                                  0, a, S, pp, j);
+      }
       if (rc) return rc;
     }
     return 0;
@@ -2652,6 +2667,8 @@ int pdhg_ctx_create(const pdhg_problem* prob, void* workspace, size_t workspace_
       }
       c->sellp[k][h] = SellSet{q->rows, q->nslices, reinterpret_cast<const long long*>(q->sptr), q->width,
                                q->col, q->val, q->perm};
+      const long long ops_nnz = k == 0 ? prob->nnz : (prob->at_nnz > 0 ? prob->at_nnz : prob->nnz);
+      c->sellp[k][h].u_long = rows > 0 && ops_nnz >= (long long)PDHG_SELL_U_MEAN * rows;  // as sell[k]
       c->sellp[k][h].ncols = k == 0 ? c->A.ncols : c->At.ncols;
       c->sellp[k][h].nslots = q->nslots > 0 ? q->nslots : 0x7fffffffffffffffLL;
       c->pptr[k][h] = pp[h];

@@ -589,14 +589,18 @@ class DeviceLp:
         """Sliced-ELL layouts of the two passes of a split step: each row's
         entries [ptr, split) and [split, ptr+1) as two CSR matrices on the
         device, heavy rows (> H entries, run whole in pass 1) left out of
-        both, each laid out by _build_sell.  -> ([Sell, Sell], keep-alive)."""
+        both, each laid out by _build_sell.  -> ([Sell, Sell], keep-alive), or
+        None when either part's sliced ELL is rejected (slice padding beyond
+        sell_max_pad under sell="auto")."""
         i64 = torch.int64
         full = (ptr[1:] - ptr[:-1]).to(i64)
         light = full <= H
         starts = (ptr[:-1].to(i64), split.to(i64))
         lens = (torch.where(light, split.to(i64) - starts[0], 0),
                 torch.where(light, ptr[1:].to(i64) - starts[1], 0))
-        sub = dataclasses.replace(opts, sell="on")   # the parts' pad / mean do not gate them
+        # "auto": only the slice-padding gate applies (a part whose long rows
+        # pad its slices beyond sell_max_pad keeps the CSR-vector split kernels)
+        sub = dataclasses.replace(opts, sell_min_nnz=0) if opts.sell == "auto" else opts
         sells, keep = [], []
         for h in range(2):
             ln = lens[h]

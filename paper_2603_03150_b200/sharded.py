@@ -105,10 +105,37 @@ class ShardBlock:
     at_nloc: np.ndarray | None = None
 
 
-class ShardPlan:
-    """Equal-nnz row and column partition of A over G shards, with padded slots."""
+def block_length_order(lens: np.ndarray, rcut: np.ndarray, window: int) -> np.ndarray:
+    """New position -> old row: inside every row block [rcut[g], rcut[g+1]),
+    rows by decreasing length within windows of `window` rows (stable), the
+    single-GPU renumbering's plain-window form (engine._length_order with
+    first = 0) applied per shard, so every block keeps its rows and with them
+    its band of local columns."""
+    order = np.arange(lens.size, dtype=np.int64)
+    for g in range(rcut.size - 1):
+        r0, r1 = int(rcut[g]), int(rcut[g + 1])
+        if r1 - r0 < 2:
+            continue
+        ln = lens[r0:r1].astype(np.int64)
+        top = int(ln.max()) + 1
+        key = (np.arange(r1 - r0, dtype=np.int64) // max(1, int(window))) * (top + 1) + (top - ln)
+        order[r0:r1] = r0 + np.argsort(key, kind="stable")
+    return order
 
-    def __init__(self, A, G: int):
+
+class ShardPlan:
+    """Equal-nnz row and column partition of A over G shards, with padded slots.
+
+    ``row_window`` > 0: inside each row block the constraints are renumbered
+    by decreasing length in windows of that many rows (block_length_order) --
+    the block's slot k holds original row rorder[r_g + k], yslot maps every
+    original row to its slot, so the A' blocks (indexed by slot), the
+    all-gathers and the result download (y = slots[yslot]) follow without
+    further change.  Each row's entries and each A' row's entry order are
+    unchanged, so the steps' sums are those of the unrenumbered plan; the
+    sliced-ELL slices of A's blocks lose their long-row padding."""
+
+    def __init__(self, A, G: int, row_window: int = 0):
         A = sp.csr_matrix(A)
         self.G = int(G)
         self.m, self.n = A.shape
@@ -126,6 +153,12 @@ class ShardPlan:
         cg = np.repeat(np.arange(self.G), np.diff(self.ccut))
         self.yslot = (rg * self.maxR + np.arange(self.m) - self.rcut[rg]).astype(np.int64)
         self.xslot = (cg * self.maxC + np.arange(self.n) - self.ccut[cg]).astype(np.int64)
+        self.row_window = int(row_window)
+        self.rorder = None
+        if self.row_window > 0:
+            self.rorder = block_length_order(np.diff(A.indptr), self.rcut, self.row_window)
+            slots = self.yslot.copy()
+            self.yslot[self.rorder] = slots          # the row at new position p takes p's slot
 
     def block(self, g: int, A, b, c, local_first: bool = False) -> ShardBlock:
         """Shard g's rows of A and of A' (slot-indexed).  ``local_first``: each
@@ -134,7 +167,8 @@ class ShardPlan:
         A = A if sp.isspmatrix_csr(A) else sp.csr_matrix(A)
         r0, r1 = int(self.rcut[g]), int(self.rcut[g + 1])
         c0, c1 = int(self.ccut[g]), int(self.ccut[g + 1])
-        Ar = A[r0:r1]
+        rows = slice(r0, r1) if self.rorder is None else self.rorder[r0:r1]
+        Ar = A[rows]
         Ag = sp.csr_matrix((Ar.data, self.xslot[Ar.indices].astype(np.int32), Ar.indptr),
                            shape=(r1 - r0, self.n_full))
         # CSC of A once per plan (column blocks are then contiguous ranges) =
@@ -146,7 +180,7 @@ class ShardPlan:
         Atg = sp.csr_matrix((Acsc.data[s0:s1], self.yslot[Acsc.indices[s0:s1]].astype(np.int32),
                              (Acsc.indptr[c0:c1 + 1] - s0).astype(Acsc.indptr.dtype)),
                             shape=(c1 - c0, self.m_full))
-        blk = ShardBlock(g, Ag, Atg, np.asarray(b, float)[r0:r1], np.asarray(c, float)[c0:c1],
+        blk = ShardBlock(g, Ag, Atg, np.asarray(b, float)[rows], np.asarray(c, float)[c0:c1],
                          self.m_full, self.n_full, g * self.maxR, g * self.maxC)
         if local_first:
             blk.A, blk.a_nloc = _local_first(Ag, g * self.maxC, (g + 1) * self.maxC)
@@ -612,6 +646,22 @@ def _to_like(a: np.ndarray, like):
 # ----------------------------------------------------------- entry points
 
 
+def shard_row_window(opts, A) -> int:
+    """ShardPlan's row_window for GpuOptions.row_order: "length" -> the
+    renumbering window, "natural" -> 0, "auto" -> the window when A's rows
+    average >= sell_max_mean entries (long, lognormal-tailed rows whose
+    sliced-ELL slices the renumbering un-pads; config 4), else 0."""
+    if opts is None:
+        from .engine import GpuOptions
+
+        opts = GpuOptions()
+    if opts.row_order == "natural" or A.shape[0] == 0:
+        return 0
+    if opts.row_order == "length" or A.nnz / A.shape[0] >= opts.sell_max_mean:
+        return int(opts.row_order_window)
+    return 0
+
+
 def build_sharded(p, G: int, comm_kind: str = "loopback", opts=None, group=None, overlap: str = "auto"):
     """ShardedDevice for StandardLp ``p`` over G shards of CUDA contexts.
 
@@ -630,7 +680,7 @@ def build_sharded(p, G: int, comm_kind: str = "loopback", opts=None, group=None,
     split = overlap in ("on", "serial") and comm_kind in ("loopback", "torch")
     if not split:
         overlap = "off"
-    plan = ShardPlan(p.A, G)
+    plan = ShardPlan(p.A, G, row_window=shard_row_window(opts, p.A))
     if comm_kind in ("loopback", "loopback_fused"):
         comm = LoopbackComm(plan, fused=comm_kind == "loopback_fused")
         dev = torch.device("cuda", torch.cuda.current_device() if opts.device is None else opts.device)

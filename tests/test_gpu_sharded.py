@@ -302,14 +302,15 @@ def test_overlap_sell_parts_match_csr_split(eng, G, name):
     from paper_2603_03150_b200.sharded import build_sharded, run_pdhg_sharded
 
     gm = load_golden(name)
-    dev = build_sharded(gm, G, comm_kind="loopback", overlap="on")
+    on = eng.GpuOptions(sell="on")
+    dev = build_sharded(gm, G, comm_kind="loopback", overlap="on", opts=on)
     assert all(s._sell_part["A"] is not None and s._sell_part["At"] is not None for s in dev.shards)
     assert all(s._sell_part["A"] is None for s in
                build_sharded(gm, G, comm_kind="loopback", overlap="on",
                              opts=eng.GpuOptions(sell="off")).shards)
     T = eng.types()
     params = T.PdhgParams(eps_rel=1e-4)
-    pa, sa = run_pdhg_sharded(gm, params, G=G, gpu=eng.GpuOptions(), comm_kind="loopback", overlap="on")
+    pa, sa = run_pdhg_sharded(gm, params, G=G, gpu=on, comm_kind="loopback", overlap="on")
     pb, sb = run_pdhg_sharded(gm, params, G=G, gpu=eng.GpuOptions(sell="off"), comm_kind="loopback",
                               overlap="on")
     assert (sa.status, sa.iterations, sa.restarts) == (sb.status, sb.iterations, sb.restarts)
@@ -337,6 +338,12 @@ def test_overlap_config4_instance_matches_single_gpu(eng):
     params = T.PdhgParams(eps_rel=1e-12, max_kkt_passes=256)
     pa, _ = run_pdhg_sharded(p, params, G=4, comm_kind="loopback", overlap="serial")
     pb, _ = run_pdhg_sharded(p, params, G=4, comm_kind="loopback", overlap="on")
+    assert pa.x.tobytes() == pb.x.tobytes() and pa.y.tobytes() == pb.y.tobytes()
+    # the same with both operators' split steps forced onto sliced-ELL parts
+    # (heavy rows of A whole in pass 1)
+    on = eng.GpuOptions(sell="on")
+    pa, _ = run_pdhg_sharded(p, params, G=4, gpu=on, comm_kind="loopback", overlap="serial")
+    pb, _ = run_pdhg_sharded(p, params, G=4, gpu=on, comm_kind="loopback", overlap="on")
     assert pa.x.tobytes() == pb.x.tobytes() and pa.y.tobytes() == pb.y.tobytes()
     plan = ShardPlan(p.A, 4)
     blk = plan.block(1, p.A, p.b, p.c, local_first=True)

@@ -515,3 +515,42 @@ def test_gloo_failure_stops_every_rank(overlap):
     for (rank, *_, xbs, ybs), sh in zip(res, shards):
         assert xbs == pytest.approx(float(sh.v["xbar"].sum()), rel=1e-12, abs=1e-300, nan_ok=True)
         assert ybs == pytest.approx(float(sh.v["ybar"].sum()), rel=1e-12, abs=1e-300, nan_ok=True)
+
+
+@pytest.mark.parametrize("G", [1, 2, 3])
+def test_plan_row_window_renumbers_inside_blocks(G):
+    """ShardPlan(row_window=...): every block keeps its rows, ordered by
+    decreasing length inside each window; yslot maps each original row to its
+    slot, so the blocks (and their A' column indices) reassemble A exactly."""
+    from paper_2603_03150_b200.instances import config4
+
+    A = config4(0.001, seed=4).A
+    w = 64
+    plan = ShardPlan(A, G, row_window=w)
+    base = ShardPlan(A, G)
+    assert np.array_equal(plan.rcut, base.rcut) and plan.m_full == base.m_full
+    lens = np.diff(A.indptr)
+    inv_y = np.full(plan.m_full, -1)
+    inv_y[plan.yslot] = np.arange(A.shape[0])
+    inv_x = np.full(plan.n_full, -1)
+    inv_x[plan.xslot] = np.arange(A.shape[1])
+    rows, cols, vals, trows, tcols, tvals = [], [], [], [], [], []
+    for g in range(G):
+        blk = plan.block(g, A, np.arange(A.shape[0], dtype=float), np.zeros(A.shape[1]))
+        r0, r1 = plan.rcut[g], plan.rcut[g + 1]
+        orig = inv_y[g * plan.maxR + np.arange(r1 - r0)]
+        assert sorted(orig) == list(range(r0, r1))                 # the block keeps its rows
+        np.testing.assert_array_equal(blk.b, orig.astype(float))    # b follows the rows
+        bl = lens[orig]
+        for k0 in range(0, r1 - r0, w):
+            assert np.all(np.diff(bl[k0:k0 + w]) <= 0)              # decreasing inside a window
+        Ab = blk.A.tocoo()
+        rows.append(orig[Ab.row]); cols.append(inv_x[Ab.col]); vals.append(Ab.data)
+        At = blk.At.tocoo()                                          # rows: columns c0.. of A
+        trows.append(plan.ccut[g] + At.row)
+        tcols.append(inv_y[At.col])
+        tvals.append(At.data)
+    R = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=A.shape)
+    assert (R != A).nnz == 0
+    T = sp.csr_matrix((np.concatenate(tvals), (np.concatenate(tcols), np.concatenate(trows))), shape=A.shape)
+    assert (T != A).nnz == 0
