@@ -64,8 +64,10 @@ def main():
     names = {}
     for d in launches:
         name = d.get("Kernel Name", "")
-        m = re.search(r"(k_step\w*)<(\w+)", name)
-        if not m:
+        # the ordinary step kernels only (not the check-fused last iteration's
+        # k_step_sell_chk / quad-writing k_step_sell<1, U, 1>)
+        m = re.search(r"(k_step(?:_sell)?)<(\w+)(?:, (\w+))?(?:, (\w+))?>", name)
+        if not m or m.group(4) == "1":
             continue
         key = "primal" if m.group(2) in ("1", "true") else "dual"
         groups[key].append(d)
