@@ -317,7 +317,7 @@ def _shard_blocks(args, world: int, rank: int, local: int, eng, opts) -> dict:
     import torch
     import torch.distributed as dist
 
-    from paper_2603_03150_b200.sharded import ShardPlan, load_block, save_block, shard_row_window
+    from paper_2603_03150_b200.sharded import ShardPlan, load_block, save_block, shard_windows
 
     need = 2 * 30e9 * max(args.scale, 0.01)          # both models' blocks (~24 B/entry + vectors)
     root = Path("/dev/shm")
@@ -338,7 +338,8 @@ def _shard_blocks(args, world: int, rank: int, local: int, eng, opts) -> dict:
                 torch.cuda.synchronize()
                 meta[0] = {"ruiz_s": time.perf_counter() - t0, "ruiz_passes": info.applied_iterations,
                            "ruiz_phases": dict(eng.ruiz.last_timings)}
-            plan = ShardPlan(model.A, world, row_window=shard_row_window(opts, model.A))
+            rw, cw = shard_windows(opts, model.A)
+            plan = ShardPlan(model.A, world, row_window=rw, col_window=cw)
             for g in range(world):
                 save_block(shm / f"{tag}_{g}.npz", plan,
                            plan.block(g, model.A, model.b, model.c, local_first=True), model.b, model.c)

@@ -133,9 +133,12 @@ class ShardPlan:
     all-gathers and the result download (y = slots[yslot]) follow without
     further change.  Each row's entries and each A' row's entry order are
     unchanged, so the steps' sums are those of the unrenumbered plan; the
-    sliced-ELL slices of A's blocks lose their long-row padding."""
+    sliced-ELL slices of A's blocks lose their long-row padding.
+    ``col_window`` > 0: the same for the variables inside each column block
+    (A' rows; corder / xslot), which also carries the power iteration's start
+    vector and the x / z download."""
 
-    def __init__(self, A, G: int, row_window: int = 0):
+    def __init__(self, A, G: int, row_window: int = 0, col_window: int = 0):
         A = sp.csr_matrix(A)
         self.G = int(G)
         self.m, self.n = A.shape
@@ -159,6 +162,12 @@ class ShardPlan:
             self.rorder = block_length_order(np.diff(A.indptr), self.rcut, self.row_window)
             slots = self.yslot.copy()
             self.yslot[self.rorder] = slots          # the row at new position p takes p's slot
+        self.col_window = int(col_window)
+        self.corder = None
+        if self.col_window > 0:
+            self.corder = block_length_order(col_counts, self.ccut, self.col_window)
+            slots = self.xslot.copy()
+            self.xslot[self.corder] = slots
 
     def block(self, g: int, A, b, c, local_first: bool = False) -> ShardBlock:
         """Shard g's rows of A and of A' (slot-indexed).  ``local_first``: each
@@ -176,11 +185,18 @@ class ShardPlan:
         if getattr(self, "_csc_of", None) is not A:
             self._csc, self._csc_of = A.tocsc(), A
         Acsc = self._csc
-        s0, s1 = int(Acsc.indptr[c0]), int(Acsc.indptr[c1])
-        Atg = sp.csr_matrix((Acsc.data[s0:s1], self.yslot[Acsc.indices[s0:s1]].astype(np.int32),
-                             (Acsc.indptr[c0:c1 + 1] - s0).astype(Acsc.indptr.dtype)),
-                            shape=(c1 - c0, self.m_full))
-        blk = ShardBlock(g, Ag, Atg, np.asarray(b, float)[rows], np.asarray(c, float)[c0:c1],
+        if self.corder is None:
+            s0, s1 = int(Acsc.indptr[c0]), int(Acsc.indptr[c1])
+            Atg = sp.csr_matrix((Acsc.data[s0:s1], self.yslot[Acsc.indices[s0:s1]].astype(np.int32),
+                                 (Acsc.indptr[c0:c1 + 1] - s0).astype(Acsc.indptr.dtype)),
+                                shape=(c1 - c0, self.m_full))
+            cols = slice(c0, c1)
+        else:   # renumbered variables: the block's columns in corder (each keeps its entry order)
+            cols = self.corder[c0:c1]
+            sub = Acsc[:, cols]
+            Atg = sp.csr_matrix((sub.data, self.yslot[sub.indices].astype(np.int32), sub.indptr),
+                                shape=(c1 - c0, self.m_full))
+        blk = ShardBlock(g, Ag, Atg, np.asarray(b, float)[rows], np.asarray(c, float)[cols],
                          self.m_full, self.n_full, g * self.maxR, g * self.maxC)
         if local_first:
             blk.A, blk.a_nloc = _local_first(Ag, g * self.maxC, (g + 1) * self.maxC)
@@ -646,20 +662,22 @@ def _to_like(a: np.ndarray, like):
 # ----------------------------------------------------------- entry points
 
 
-def shard_row_window(opts, A) -> int:
-    """ShardPlan's row_window for GpuOptions.row_order: "length" -> the
-    renumbering window, "natural" -> 0, "auto" -> the window when A's rows
-    average >= sell_max_mean entries (long, lognormal-tailed rows whose
-    sliced-ELL slices the renumbering un-pads; config 4), else 0."""
+def shard_windows(opts, A) -> tuple[int, int]:
+    """ShardPlan's (row_window, col_window) for GpuOptions.row_order /
+    col_order: "length" -> the renumbering window, "natural" -> 0, "auto" ->
+    the window when A's rows average >= sell_max_mean entries (long,
+    lognormal-tailed rows whose sliced-ELL slices the renumbering un-pads;
+    config 4), else 0 -- the variables follow the constraints' choice, as on
+    one GPU."""
     if opts is None:
         from .engine import GpuOptions
 
         opts = GpuOptions()
-    if opts.row_order == "natural" or A.shape[0] == 0:
-        return 0
-    if opts.row_order == "length" or A.nnz / A.shape[0] >= opts.sell_max_mean:
-        return int(opts.row_order_window)
-    return 0
+    auto = A.shape[0] > 0 and A.nnz / A.shape[0] >= opts.sell_max_mean
+    win = int(opts.row_order_window)
+    rw = win if opts.row_order == "length" or (opts.row_order == "auto" and auto) else 0
+    cw = win if opts.col_order == "length" or (opts.col_order == "auto" and rw > 0) else 0
+    return rw, cw
 
 
 def build_sharded(p, G: int, comm_kind: str = "loopback", opts=None, group=None, overlap: str = "auto"):
@@ -680,7 +698,8 @@ def build_sharded(p, G: int, comm_kind: str = "loopback", opts=None, group=None,
     split = overlap in ("on", "serial") and comm_kind in ("loopback", "torch")
     if not split:
         overlap = "off"
-    plan = ShardPlan(p.A, G, row_window=shard_row_window(opts, p.A))
+    rw, cw = shard_windows(opts, p.A)
+    plan = ShardPlan(p.A, G, row_window=rw, col_window=cw)
     if comm_kind in ("loopback", "loopback_fused"):
         comm = LoopbackComm(plan, fused=comm_kind == "loopback_fused")
         dev = torch.device("cuda", torch.cuda.current_device() if opts.device is None else opts.device)

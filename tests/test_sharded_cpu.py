@@ -519,14 +519,15 @@ def test_gloo_failure_stops_every_rank(overlap):
 
 @pytest.mark.parametrize("G", [1, 2, 3])
 def test_plan_row_window_renumbers_inside_blocks(G):
-    """ShardPlan(row_window=...): every block keeps its rows, ordered by
-    decreasing length inside each window; yslot maps each original row to its
-    slot, so the blocks (and their A' column indices) reassemble A exactly."""
+    """ShardPlan(row_window=..., col_window=...): every block keeps its rows
+    and columns, each ordered by decreasing length inside each window; yslot /
+    xslot map the originals to their slots, so the blocks reassemble A and A'
+    exactly."""
     from paper_2603_03150_b200.instances import config4
 
     A = config4(0.001, seed=4).A
     w = 64
-    plan = ShardPlan(A, G, row_window=w)
+    plan = ShardPlan(A, G, row_window=w, col_window=w)
     base = ShardPlan(A, G)
     assert np.array_equal(plan.rcut, base.rcut) and plan.m_full == base.m_full
     lens = np.diff(A.indptr)
@@ -536,7 +537,7 @@ def test_plan_row_window_renumbers_inside_blocks(G):
     inv_x[plan.xslot] = np.arange(A.shape[1])
     rows, cols, vals, trows, tcols, tvals = [], [], [], [], [], []
     for g in range(G):
-        blk = plan.block(g, A, np.arange(A.shape[0], dtype=float), np.zeros(A.shape[1]))
+        blk = plan.block(g, A, np.arange(A.shape[0], dtype=float), np.arange(A.shape[1], dtype=float))
         r0, r1 = plan.rcut[g], plan.rcut[g + 1]
         orig = inv_y[g * plan.maxR + np.arange(r1 - r0)]
         assert sorted(orig) == list(range(r0, r1))                 # the block keeps its rows
@@ -546,8 +547,16 @@ def test_plan_row_window_renumbers_inside_blocks(G):
             assert np.all(np.diff(bl[k0:k0 + w]) <= 0)              # decreasing inside a window
         Ab = blk.A.tocoo()
         rows.append(orig[Ab.row]); cols.append(inv_x[Ab.col]); vals.append(Ab.data)
-        At = blk.At.tocoo()                                          # rows: columns c0.. of A
-        trows.append(plan.ccut[g] + At.row)
+        c0, c1 = plan.ccut[g], plan.ccut[g + 1]
+        ocol = inv_x[g * plan.maxC + np.arange(c1 - c0)]
+        assert sorted(ocol) == list(range(c0, c1))                  # the block keeps its columns
+        np.testing.assert_array_equal(blk.c, ocol.astype(float))    # c follows them
+        cl = np.diff(blk.At.indptr)
+        np.testing.assert_array_equal(cl, np.bincount(A.indices, minlength=A.shape[1])[ocol])
+        for k0 in range(0, c1 - c0, w):
+            assert np.all(np.diff(cl[k0:k0 + w]) <= 0)
+        At = blk.At.tocoo()                                          # rows: the block's columns
+        trows.append(ocol[At.row])
         tcols.append(inv_y[At.col])
         tvals.append(At.data)
     R = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=A.shape)
