@@ -338,8 +338,8 @@ def _shard_blocks(args, world: int, rank: int, local: int, eng, opts) -> dict:
                 torch.cuda.synchronize()
                 meta[0] = {"ruiz_s": time.perf_counter() - t0, "ruiz_passes": info.applied_iterations,
                            "ruiz_phases": dict(eng.ruiz.last_timings)}
-            rw, cw = shard_windows(opts, model.A)
-            plan = ShardPlan(model.A, world, row_window=rw, col_window=cw)
+            rw, cw, first = shard_windows(opts, model.A)
+            plan = ShardPlan(model.A, world, row_window=rw, col_window=cw, first=first)
             for g in range(world):
                 save_block(shm / f"{tag}_{g}.npz", plan,
                            plan.block(g, model.A, model.b, model.c, local_first=True), model.b, model.c)

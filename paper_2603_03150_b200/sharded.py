@@ -105,12 +105,13 @@ class ShardBlock:
     at_nloc: np.ndarray | None = None
 
 
-def block_length_order(lens: np.ndarray, rcut: np.ndarray, window: int) -> np.ndarray:
+def block_length_order(lens: np.ndarray, rcut: np.ndarray, window: int, first: int = 0) -> np.ndarray:
     """New position -> old row: inside every row block [rcut[g], rcut[g+1]),
-    rows by decreasing length within windows of `window` rows (stable), the
-    single-GPU renumbering's plain-window form (engine._length_order with
-    first = 0) applied per shard, so every block keeps its rows and with them
-    its band of local columns."""
+    rows by decreasing length within windows of `window` rows (stable) --
+    the single-GPU renumbering (engine._length_order) applied per shard, so
+    every block keeps its rows and with them its band of local columns; with
+    first > 0 the block's rows longer than `first` come first (window by
+    window), then the rest."""
     order = np.arange(lens.size, dtype=np.int64)
     for g in range(rcut.size - 1):
         r0, r1 = int(rcut[g]), int(rcut[g + 1])
@@ -118,7 +119,10 @@ def block_length_order(lens: np.ndarray, rcut: np.ndarray, window: int) -> np.nd
             continue
         ln = lens[r0:r1].astype(np.int64)
         top = int(ln.max()) + 1
-        key = (np.arange(r1 - r0, dtype=np.int64) // max(1, int(window))) * (top + 1) + (top - ln)
+        win = np.arange(r1 - r0, dtype=np.int64) // max(1, int(window))
+        key = win * (top + 1) + (top - ln)
+        if first > 0:
+            key = (ln <= first).astype(np.int64) * (int(win[-1]) + 1) * (top + 1) + key
         order[r0:r1] = r0 + np.argsort(key, kind="stable")
     return order
 
@@ -134,11 +138,13 @@ class ShardPlan:
     further change.  Each row's entries and each A' row's entry order are
     unchanged, so the steps' sums are those of the unrenumbered plan; the
     sliced-ELL slices of A's blocks lose their long-row padding.
+    ``first`` > 0: inside each block, the rows / variables longer than
+    that come first (window by window), as the single-GPU renumbering does.
     ``col_window`` > 0: the same for the variables inside each column block
     (A' rows; corder / xslot), which also carries the power iteration's start
     vector and the x / z download."""
 
-    def __init__(self, A, G: int, row_window: int = 0, col_window: int = 0):
+    def __init__(self, A, G: int, row_window: int = 0, col_window: int = 0, first: int = 0):
         A = sp.csr_matrix(A)
         self.G = int(G)
         self.m, self.n = A.shape
@@ -159,13 +165,13 @@ class ShardPlan:
         self.row_window = int(row_window)
         self.rorder = None
         if self.row_window > 0:
-            self.rorder = block_length_order(np.diff(A.indptr), self.rcut, self.row_window)
+            self.rorder = block_length_order(np.diff(A.indptr), self.rcut, self.row_window, first)
             slots = self.yslot.copy()
             self.yslot[self.rorder] = slots          # the row at new position p takes p's slot
         self.col_window = int(col_window)
         self.corder = None
         if self.col_window > 0:
-            self.corder = block_length_order(col_counts, self.ccut, self.col_window)
+            self.corder = block_length_order(col_counts, self.ccut, self.col_window, first)
             slots = self.xslot.copy()
             self.xslot[self.corder] = slots
 
@@ -662,8 +668,8 @@ def _to_like(a: np.ndarray, like):
 # ----------------------------------------------------------- entry points
 
 
-def shard_windows(opts, A) -> tuple[int, int]:
-    """ShardPlan's (row_window, col_window) for GpuOptions.row_order /
+def shard_windows(opts, A) -> tuple[int, int, int]:
+    """ShardPlan's (row_window, col_window, first) for GpuOptions.row_order /
     col_order: "length" -> the renumbering window, "natural" -> 0, "auto" ->
     the window when A's rows average >= sell_max_mean entries (long,
     lognormal-tailed rows whose sliced-ELL slices the renumbering un-pads;
@@ -677,7 +683,7 @@ def shard_windows(opts, A) -> tuple[int, int]:
     win = int(opts.row_order_window)
     rw = win if opts.row_order == "length" or (opts.row_order == "auto" and auto) else 0
     cw = win if opts.col_order == "length" or (opts.col_order == "auto" and rw > 0) else 0
-    return rw, cw
+    return rw, cw, int(opts.row_order_first)
 
 
 def build_sharded(p, G: int, comm_kind: str = "loopback", opts=None, group=None, overlap: str = "auto"):
@@ -698,8 +704,8 @@ def build_sharded(p, G: int, comm_kind: str = "loopback", opts=None, group=None,
     split = overlap in ("on", "serial") and comm_kind in ("loopback", "torch")
     if not split:
         overlap = "off"
-    rw, cw = shard_windows(opts, p.A)
-    plan = ShardPlan(p.A, G, row_window=rw, col_window=cw)
+    rw, cw, first = shard_windows(opts, p.A)
+    plan = ShardPlan(p.A, G, row_window=rw, col_window=cw, first=first)
     if comm_kind in ("loopback", "loopback_fused"):
         comm = LoopbackComm(plan, fused=comm_kind == "loopback_fused")
         dev = torch.device("cuda", torch.cuda.current_device() if opts.device is None else opts.device)

@@ -517,8 +517,9 @@ def test_gloo_failure_stops_every_rank(overlap):
         assert ybs == pytest.approx(float(sh.v["ybar"].sum()), rel=1e-12, abs=1e-300, nan_ok=True)
 
 
+@pytest.mark.parametrize("first", [0, 32])
 @pytest.mark.parametrize("G", [1, 2, 3])
-def test_plan_row_window_renumbers_inside_blocks(G):
+def test_plan_row_window_renumbers_inside_blocks(G, first):
     """ShardPlan(row_window=..., col_window=...): every block keeps its rows
     and columns, each ordered by decreasing length inside each window; yslot /
     xslot map the originals to their slots, so the blocks reassemble A and A'
@@ -527,7 +528,7 @@ def test_plan_row_window_renumbers_inside_blocks(G):
 
     A = config4(0.001, seed=4).A
     w = 64
-    plan = ShardPlan(A, G, row_window=w, col_window=w)
+    plan = ShardPlan(A, G, row_window=w, col_window=w, first=first)
     base = ShardPlan(A, G)
     assert np.array_equal(plan.rcut, base.rcut) and plan.m_full == base.m_full
     lens = np.diff(A.indptr)
@@ -543,8 +544,7 @@ def test_plan_row_window_renumbers_inside_blocks(G):
         assert sorted(orig) == list(range(r0, r1))                 # the block keeps its rows
         np.testing.assert_array_equal(blk.b, orig.astype(float))    # b follows the rows
         bl = lens[orig]
-        for k0 in range(0, r1 - r0, w):
-            assert np.all(np.diff(bl[k0:k0 + w]) <= 0)              # decreasing inside a window
+        _check_length_order(bl, lens[r0:r1], w, first)
         Ab = blk.A.tocoo()
         rows.append(orig[Ab.row]); cols.append(inv_x[Ab.col]); vals.append(Ab.data)
         c0, c1 = plan.ccut[g], plan.ccut[g + 1]
@@ -552,9 +552,9 @@ def test_plan_row_window_renumbers_inside_blocks(G):
         assert sorted(ocol) == list(range(c0, c1))                  # the block keeps its columns
         np.testing.assert_array_equal(blk.c, ocol.astype(float))    # c follows them
         cl = np.diff(blk.At.indptr)
-        np.testing.assert_array_equal(cl, np.bincount(A.indices, minlength=A.shape[1])[ocol])
-        for k0 in range(0, c1 - c0, w):
-            assert np.all(np.diff(cl[k0:k0 + w]) <= 0)
+        counts = np.bincount(A.indices, minlength=A.shape[1])
+        np.testing.assert_array_equal(cl, counts[ocol])
+        _check_length_order(cl, counts[c0:c1], w, first)
         At = blk.At.tocoo()                                          # rows: the block's columns
         trows.append(ocol[At.row])
         tcols.append(inv_y[At.col])
@@ -563,3 +563,20 @@ def test_plan_row_window_renumbers_inside_blocks(G):
     assert (R != A).nnz == 0
     T = sp.csr_matrix((np.concatenate(tvals), (np.concatenate(tcols), np.concatenate(trows))), shape=A.shape)
     assert (T != A).nnz == 0
+
+
+def _check_length_order(new_lens, old_lens, w, first):
+    """new_lens (block order after renumbering) against the block's natural
+    lengths: with first = 0, decreasing inside every window of w; with
+    first > 0, the long rows (> first) of every window first, each group
+    keeping windows in order and decreasing length inside each window."""
+    win = np.arange(old_lens.size) // w
+    groups = [np.ones(old_lens.size, bool)] if first <= 0 else [old_lens > first, old_lens <= first]
+    pos = 0
+    for gmask in groups:
+        for k in range(int(win[-1]) + 1 if old_lens.size else 0):
+            sel = old_lens[gmask & (win == k)]
+            got = new_lens[pos:pos + sel.size]
+            np.testing.assert_array_equal(got, np.sort(sel)[::-1])
+            pos += sel.size
+    assert pos == old_lens.size
