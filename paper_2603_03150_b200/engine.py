@@ -124,6 +124,10 @@ class GpuOptions:
                      A xe and the check's A x, A avg_x from (xe, x, avg_x) quads; bitwise
                      the same iterates and check scalars.  Applies when A and A' both have
                      sliced-ELL layouts, unsharded (config 4).
+    split_full_sell: shards with split steps (overlapped multi-GPU schedule) also lay
+                     out their whole rows in sliced ELL (when the padding gate passes),
+                     for the two-point check and the power iteration; the split steps
+                     run over their own part layouts either way.
     """
 
     device: int | None = None
@@ -156,6 +160,7 @@ class GpuOptions:
     col_order_first: int = 32
     check_dot: bool = True
     check_fuse: bool = True
+    split_full_sell: bool = True
 
 
 def auto_lanes(nnz: int, rows: int) -> int:
@@ -415,7 +420,8 @@ class DeviceLp:
                         ("A", m, nnz, self.a_ptr, self.a_col, self.a_val, H),
                         ("At", n, self.at_nnz, self.at_ptr, self.at_col, self.at_val, Ht)):
                     self._sell[key] = None if (self._psr[key] or pers in ("tiny", "on")
-                                               or self.split_local[key] is not None) else \
+                                               or (self.split_local[key] is not None
+                                                   and not opts.split_full_sell)) else \
                         self._build_sell(torch, dev, key, rows, nz, ptr, col, val, Hk, opts)
                 # split steps (overlapped multi-GPU schedule) over sliced-ELL parts:
                 # part 0 = each row's local-slot entries, part 1 = the rest
