@@ -586,10 +586,10 @@ def run_ours(args):
     def _op_layout(key, lanes):
         if getattr(kdev, "_psr", {}).get(key):
             return "psr"
-        if getattr(kdev, "_sell", {}).get(key):
-            return "sliced-ELL"
         if getattr(kdev, "_sell_part", {}).get(key):
             return "sliced-ELL split (pass 0 local-slot entries, pass 1 the rest)"
+        if getattr(kdev, "_sell", {}).get(key):
+            return "sliced-ELL"
         split = getattr(kdev, "split_local", {}).get(key) is not None
         return f"csr-vector ({lanes} lanes/row)" + (" split" if split else "")
 
