@@ -144,3 +144,19 @@ def test_check_fuse_enabled_only_where_it_applies(eng):
     assert not eng.DeviceLp(gm.A, gm.b, gm.c, eng.GpuOptions(cache_layout=False, sell="off")).check_fuse
     assert not eng.DeviceLp(gm.A, gm.b, gm.c,
                             eng.GpuOptions(cache_layout=False, sell="on", check_fuse=False)).check_fuse
+
+
+@pytest.mark.parametrize("check_every", [64, 5])
+def test_check_fuse_numerical_failure(eng, check_every):
+    """A model whose x overflows at iteration 335 (pdhg.py:194-196): inside a
+    fused period (check_every 64) and in the fused last iteration itself
+    (check_every 5: the period 331-335 ends there) -- the failure exit, its
+    best point and z are bitwise those of the unfused path."""
+    from test_sharded_cpu import failing_block_model
+
+    p = failing_block_model()
+    params = eng.types().PdhgParams(eps_rel=1e-6, max_kkt_passes=500, check_every=check_every)
+    on = _run(eng, p, params, True, sell="on")
+    off = _run(eng, p, params, False, sell="on")
+    assert on[1].status.value == "NumericalFailure" and on[1].iterations == 335
+    _same(on, off)
